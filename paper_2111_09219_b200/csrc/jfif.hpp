@@ -1,0 +1,53 @@
+// Host-side JFIF header parsing and table setup: everything the reference's
+// parse() does (parser.hpp:264-347) up to the first entropy-coded byte.  The
+// scan itself (extract_scan + unstuff, parser.hpp:238-258, bitstream.hpp:56-76)
+// is left to the GPU (kernel K0), so the host never walks the scan bytes.
+#pragma once
+
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "pjg_internal.h"
+
+namespace pjg {
+
+struct HuffSpec {
+    std::array<uint8_t, 16> counts{};
+    std::vector<uint8_t> symbols;
+    bool present = false;
+};
+
+struct Component {
+    uint8_t id = 0, h = 1, v = 1, tq = 0, td = 0, ta = 0;
+};
+
+struct Header {
+    int32_t status = kOk;
+    std::string message;
+    uint32_t width = 0, height = 0;
+    std::vector<Component> comps;
+    uint32_t h_max = 1, v_max = 1, mcus_x = 0, mcus_y = 0, dpm = 0;
+    std::vector<uint8_t> du_seq;
+    std::array<std::array<uint16_t, 64>, 4> quant{};
+    std::array<bool, 4> quant_present{};
+    std::array<HuffSpec, 4> dc, ac;
+    size_t scan_start = 0;  // offset of the first entropy-coded byte
+    int32_t table_status = kOk;  // build_table error, reported after the scan checks
+
+    uint64_t total_dus() const { return uint64_t(mcus_x) * mcus_y * dpm; }
+    uint32_t comp_width(size_t c) const { return (width * comps[c].h + h_max - 1) / h_max; }
+    uint32_t comp_height(size_t c) const { return (height * comps[c].v + v_max - 1) / v_max; }
+};
+
+// Parses markers up to and including SOS.  Never throws; errors land in
+// Header::status with the reference's Errc (parser.hpp error sites).
+Header parse_header(const uint8_t* data, size_t size);
+
+// build_table validation (huffman.hpp:60-93) + device two-level table.
+// Returns kOk or the reference's error (OversubscribedCode / MalformedHeader).
+int32_t build_dev_huff(const HuffSpec& spec, DevHuff* out);
+
+}  // namespace pjg

@@ -1,0 +1,867 @@
+// C-ABI (include/pjg.h) and host orchestration of the fully-on-GPU decode.
+//
+// Host work per batch is the reference's header walk (parser.hpp:264-347
+// minus the scan), Huffman/quant table setup (huffman.hpp:60-93) and the
+// layout plan; then ONE H2D of the compressed bytes (plus one of a small
+// descriptor blob) and six stream-ordered kernels (K0, K1, K1c, K2, K3, K4).
+// No host synchronisation between kernels; no CPU fallback anywhere: if the
+// device path fails the call fails.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/pjg.h"
+#include "jfif.hpp"
+#include "pjg_internal.h"
+
+using namespace pjg;
+
+namespace {
+
+constexpr uint32_t kNumEvents = PJG_NUM_STAGES + 1;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    bool zero = false;  // zero-fill on (re)allocation (lookback flag arrays)
+
+    cudaError_t ensure(size_t n) {
+        if (n <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n + n / 4, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) return e;
+        cap = want;
+        if (zero) e = cudaMemset(p, 0, want);
+        return e;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct HostBuf {  // pinned
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap && p) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(n + n / 4, 4096);
+        cudaError_t e = cudaMallocHost(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct pjg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint32_t epoch = 0;
+    bool busy = false;
+    double basis[64];
+    cudaEvent_t ev[kNumEvents] = {};
+    DevBuf raw, ubuf, meta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out,
+        counters, k0_flag, k0_agg, k2_flag, k2_agg, stats;
+    HostBuf stage, meta_host, status_host;
+};
+
+struct pjg_batch {
+    pjg_ctx* ctx = nullptr;
+    pjg_config cfg{};
+    size_t n = 0;
+    std::vector<const uint8_t*> files;
+    std::vector<size_t> sizes;
+    std::vector<Header> hdr;
+    std::vector<ImgDesc> desc;
+    std::vector<int32_t> host_status;
+    std::vector<pjg_image_info> info;
+    // raw layout
+    const uint8_t* raw_src = nullptr;  // contiguous user region, or ctx->stage
+    size_t raw_bytes = 0;
+    bool packed = false;
+    // meta blob layout (offsets into ctx->meta)
+    size_t m_desc = 0, m_state = 0, m_huff = 0, m_quant = 0, m_basis = 0, m_k0 = 0, m_tile = 0,
+           m_sub = 0, m_total = 0;
+    uint32_t n_huff = 0, n_quant = 0;
+    uint32_t k0_tiles = 0, k4_tiles = 0, k1_ctas = 0, k2_tiles = 0;
+    uint64_t total_subs = 0, total_dus = 0, out_bytes = 0;
+    Params prm{};
+    bool uploaded = false, decoded = false, synced = false;
+    std::vector<ImgState> dev_state;  // fetched at synchronize
+    double stage_ms[PJG_NUM_STAGES] = {};
+    unsigned long long stats[kNumStats] = {};
+};
+
+namespace {
+
+int fail(pjg_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    return code;
+}
+
+int cuda_fail(pjg_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, PJG_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(call, where)                                          \
+    do {                                                         \
+        cudaError_t e__ = (call);                                \
+        if (e__ != cudaSuccess) return cuda_fail(ctx, e__, where); \
+    } while (0)
+
+uint64_t out_bytes_for(const Header& h, uint32_t mode) {
+    if (h.comps.empty()) return 0;
+    if (mode == PJG_OUT_RGB) return uint64_t(h.width) * h.height * (h.comps.size() == 3 ? 3 : 1);
+    if (mode == PJG_OUT_GRAY) return uint64_t(h.comp_width(0)) * h.comp_height(0);
+    uint64_t s = 0;
+    for (size_t c = 0; c < h.comps.size(); ++c) s += uint64_t(h.comp_width(c)) * h.comp_height(c);
+    return s;
+}
+
+void fill_info(const Header& h, uint32_t mode, size_t compressed, pjg_image_info* info) {
+    std::memset(info, 0, sizeof(*info));
+    info->compressed_bytes = compressed;
+    if (h.status != kOk && h.comps.empty()) return;
+    info->width = h.width;
+    info->height = h.height;
+    info->num_components = uint32_t(h.comps.size());
+    for (size_t c = 0; c < h.comps.size() && c < 3; ++c) {
+        info->plane_width[c] = h.comp_width(c);
+        info->plane_height[c] = h.comp_height(c);
+    }
+    info->h_max = h.h_max;
+    info->v_max = h.v_max;
+    info->mcus_x = h.mcus_x;
+    info->mcus_y = h.mcus_y;
+    info->data_units = h.total_dus();
+    info->channels = mode == PJG_OUT_RGB ? (h.comps.size() == 3 ? 3 : 1)
+                                         : (mode == PJG_OUT_GRAY ? 1 : uint32_t(h.comps.size()));
+    info->output_bytes = out_bytes_for(h, mode);
+}
+
+bool validate_cfg(pjg_ctx* ctx, const pjg_config* cfg, int* st) {
+    // partition() validation (parallel_decode.hpp:50-62)
+    if (!cfg || cfg->subsequence_bits == 0 || cfg->subsequence_bits % 32 != 0 ||
+        cfg->sequence_length_b == 0) {
+        *st = fail(ctx, PJG_CONSISTENCY_FAILURE,
+                   "subsequence_bits must be a positive multiple of 32 and sequence_length_b >= 1");
+        return false;
+    }
+    if (cfg->output > PJG_OUT_GRAY) {
+        *st = fail(ctx, PJG_INVALID_ARGUMENT, "bad output kind");
+        return false;
+    }
+    return true;
+}
+
+void parallel_memcpy(uint8_t* dst, const std::vector<std::pair<const uint8_t*, size_t>>& src,
+                     const std::vector<size_t>& dst_off) {
+    size_t total = 0;
+    for (auto& s : src) total += s.second;
+    unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (total < (8u << 20) || hw == 1) {
+        for (size_t i = 0; i < src.size(); ++i) std::memcpy(dst + dst_off[i], src[i].first, src[i].second);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned w = 0; w < hw; ++w)
+        th.emplace_back([&, w] {
+            for (size_t i = w; i < src.size(); i += hw) std::memcpy(dst + dst_off[i], src[i].first, src[i].second);
+        });
+    for (auto& t : th) t.join();
+}
+
+}  // namespace
+
+// ====================================================================== API
+extern "C" {
+
+const char* pjg_status_name(int s) {
+    switch (s) {
+        case PJG_OK: return "Ok";
+        case PJG_MALFORMED_STUFFING: return "MalformedStuffing";
+        case PJG_EMPTY_SCAN: return "EmptyScan";
+        case PJG_OUT_OF_BITS: return "OutOfBits";
+        case PJG_UNSUPPORTED_FEATURE: return "UnsupportedFeature";
+        case PJG_MALFORMED_HEADER: return "MalformedHeader";
+        case PJG_MISSING_TABLE: return "MissingTable";
+        case PJG_OVERSUBSCRIBED_CODE: return "OversubscribedCode";
+        case PJG_INVALID_CODE: return "InvalidCode";
+        case PJG_CONSISTENCY_FAILURE: return "ConsistencyFailure";
+        case PJG_EMPTY_CORPUS: return "EmptyCorpus";
+        case PJG_IO_ERROR: return "IoError";
+        case PJG_CUDA_ERROR: return "CudaError";
+        case PJG_INVALID_ARGUMENT: return "InvalidArgument";
+        case PJG_CAPACITY: return "Capacity";
+        case PJG_NOT_DECODED: return "NotDecoded";
+    }
+    return "Unknown";
+}
+
+void pjg_default_config(pjg_config* cfg) {
+    cfg->subsequence_bits = 1024;
+    cfg->sequence_length_b = 256;
+    cfg->output = PJG_OUT_PLANES;
+}
+
+int pjg_ctx_create(int device, pjg_ctx** out) {
+    if (!out) return PJG_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto c = std::make_unique<pjg_ctx>();
+    pjg_ctx* ctx = c.get();
+    c->device = device;
+    CU(cudaSetDevice(device), "cudaSetDevice");
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : c->ev) CU(cudaEventCreate(&e), "cudaEventCreate");
+    c->k0_flag.zero = c->k2_flag.zero = c->k1_flag.zero = true;
+    // IdctBasis (transform.hpp:93-108): the same host libm expression.
+    for (int u = 0; u < 8; ++u) {
+        double cu = u == 0 ? 1.0 / std::sqrt(2.0) : 1.0;
+        for (int x = 0; x < 8; ++x) c->basis[u * 8 + x] = 0.5 * cu * std::cos((2 * x + 1) * u * M_PI / 16.0);
+    }
+    *out = c.release();
+    return PJG_OK;
+}
+
+void pjg_ctx_destroy(pjg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&c->raw, &c->ubuf, &c->meta, &c->ent, &c->dcs, &c->off, &c->cap, &c->pred,
+                      &c->cta_end, &c->cta_start, &c->k1_flag, &c->coef, &c->out, &c->counters,
+                      &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats})
+        b->release();
+    c->stage.release();
+    c->meta_host.release();
+    c->status_host.release();
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* pjg_last_error(const pjg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+void* pjg_ctx_stream(pjg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int pjg_inspect(const uint8_t* file, size_t size, uint32_t output, pjg_image_info* info) {
+    if (!file || !info) return PJG_INVALID_ARGUMENT;
+    Header h = parse_header(file, size);
+    fill_info(h, output, size, info);
+    return h.status;
+}
+
+int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const size_t* sizes,
+                     const pjg_config* cfg, pjg_batch** out) {
+    if (!ctx || !out || (n && (!files || !sizes))) return PJG_INVALID_ARGUMENT;
+    *out = nullptr;
+    int st = 0;
+    if (!validate_cfg(ctx, cfg, &st)) return st;
+    if (ctx->busy) return fail(ctx, PJG_INVALID_ARGUMENT, "one live batch per context");
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    auto b = std::make_unique<pjg_batch>();
+    b->ctx = ctx;
+    b->cfg = *cfg;
+    b->n = n;
+    b->files.assign(files, files + n);
+    b->sizes.assign(sizes, sizes + n);
+    b->hdr.resize(n);
+    b->desc.resize(n);
+    b->host_status.assign(n, 0);
+    b->info.resize(n);
+
+    // ---- host header parse (parallel for large batches)
+    {
+        unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        auto body = [&](size_t lo, size_t step) {
+            for (size_t i = lo; i < n; i += step) b->hdr[i] = parse_header(files[i], sizes[i]);
+        };
+        if (n >= 256 && hw > 1) {
+            std::vector<std::thread> th;
+            for (unsigned w = 0; w < hw; ++w) th.emplace_back(body, w, hw);
+            for (auto& t : th) t.join();
+        } else {
+            body(0, 1);
+        }
+    }
+    // ---- tables: dedupe by content
+    std::map<std::vector<uint8_t>, uint32_t> huff_ids, quant_ids;
+    std::vector<DevHuff> huffs;
+    std::vector<std::array<uint16_t, 64>> quants;
+    auto huff_id = [&](const HuffSpec& s) -> uint32_t {
+        std::vector<uint8_t> key(s.counts.begin(), s.counts.end());
+        key.insert(key.end(), s.symbols.begin(), s.symbols.end());
+        auto it = huff_ids.find(key);
+        if (it != huff_ids.end()) return it->second;
+        DevHuff d;
+        build_dev_huff(s, &d);
+        huffs.push_back(d);
+        uint32_t id = uint32_t(huffs.size() - 1);
+        huff_ids.emplace(std::move(key), id);
+        return id;
+    };
+    static const uint8_t kZz2R[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
+                                      12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
+                                      35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
+                                      58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+    auto quant_id = [&](const std::array<uint16_t, 64>& q) -> uint32_t {
+        std::vector<uint8_t> key(reinterpret_cast<const uint8_t*>(q.data()),
+                                 reinterpret_cast<const uint8_t*>(q.data()) + 128);
+        auto it = quant_ids.find(key);
+        if (it != quant_ids.end()) return it->second;
+        std::array<uint16_t, 64> r{};
+        for (int z = 0; z < 64; ++z) r[kZz2R[z]] = q[z];  // raster order
+        quants.push_back(r);
+        uint32_t id = uint32_t(quants.size() - 1);
+        quant_ids.emplace(std::move(key), id);
+        return id;
+    };
+
+    // ---- layout plan
+    const uint64_t sb = cfg->subsequence_bits;
+    uint64_t sub = 0, du = 0, outb = 0;
+    uint32_t k0t = 0, k4t = 0;
+    std::vector<uint32_t> k0_first(n + 1), tile_first(n + 1);
+    std::vector<uint64_t> sub_first(n + 1);
+    // raw extent: contiguous user region or pack
+    const uint8_t* lo = nullptr;
+    const uint8_t* hi = nullptr;
+    uint64_t raw_sum = 0;
+    for (size_t i = 0; i < n; ++i) {
+        Header& h = b->hdr[i];
+        fill_info(h, cfg->output, sizes[i], &b->info[i]);
+        if (h.status != kOk) continue;
+        size_t rl = sizes[i] - h.scan_start;
+        if (rl == 0) {  // extract_scan of nothing → unstuff throws EmptyScan
+            h.status = kEmptyScan;
+            continue;
+        }
+        const uint8_t* s = files[i] + h.scan_start;
+        if (!lo || s < lo) lo = s;
+        if (!hi || s + rl > hi) hi = s + rl;
+        raw_sum += rl;
+    }
+    b->packed = !(lo && uint64_t(hi - lo) <= raw_sum + raw_sum / 2 + (1u << 20));
+    uint64_t pack_off = 0;
+    std::vector<std::pair<const uint8_t*, size_t>> pk_src;
+    std::vector<size_t> pk_dst;
+    for (size_t i = 0; i < n; ++i) {
+        Header& h = b->hdr[i];
+        ImgDesc& d = b->desc[i];
+        std::memset(&d, 0, sizeof(d));
+        k0_first[i] = k0t;
+        tile_first[i] = k4t;
+        sub_first[i] = sub;
+        d.sub_first = sub;
+        d.du_first = du;
+        d.out_mode = cfg->output;
+        d.out_off = outb;
+        b->host_status[i] = h.status;
+        if (h.status != kOk) continue;
+        const size_t rl = sizes[i] - h.scan_start;
+        if (b->packed) {
+            d.raw_off = pack_off;
+            pk_src.emplace_back(files[i] + h.scan_start, rl);
+            pk_dst.push_back(pack_off);
+            pack_off = align_up(pack_off + rl, 16);
+        } else {
+            d.raw_off = uint64_t(files[i] + h.scan_start - lo);
+        }
+        d.raw_len = rl;
+        d.deferred = h.table_status;
+        d.width = h.width;
+        d.height = h.height;
+        d.mcus_x = h.mcus_x;
+        d.mcus_y = h.mcus_y;
+        d.ncomp = uint32_t(h.comps.size());
+        d.dpm = h.dpm;
+        d.h_max = h.h_max;
+        d.v_max = h.v_max;
+        uint32_t seen[4] = {0, 0, 0, 0};
+        for (uint32_t s = 0; s < h.dpm; ++s) {
+            uint32_t c = h.du_seq[s];
+            d.du_comp |= uint64_t(c) << (4 * s);
+            d.du_kslot |= uint64_t(seen[c]++) << (4 * s);
+        }
+        for (size_t c = 0; c < h.comps.size(); ++c) {
+            d.comp_h[c] = h.comps[c].h;
+            d.comp_v[c] = h.comps[c].v;
+            d.plane_w[c] = h.comp_width(c);
+            d.plane_h[c] = h.comp_height(c);
+            if (h.table_status == kOk) {
+                d.dc_tab[c] = uint16_t(huff_id(h.dc[h.comps[c].td]));
+                d.ac_tab[c] = uint16_t(huff_id(h.ac[h.comps[c].ta]));
+            }
+            d.q_tab[c] = uint16_t(quant_id(h.quant[h.comps[c].tq]));
+        }
+        // K0 tiles always run (scan checks precede table errors)
+        k0t += uint32_t((rl + kK0Tile - 1) / kK0Tile);
+        if (h.table_status != kOk) continue;
+        d.sub_count = (uint64_t(rl) * 8 + sb - 1) / sb;
+        d.expected = h.total_dus() * 64;
+        d.mcus_per_tile = uint16_t(std::max<uint32_t>(1, kK4MaxBlocks / h.dpm));
+        d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
+        sub += d.sub_count;
+        du += h.total_dus();
+        k4t += d.tiles_x * h.mcus_y;
+        outb = align_up(outb + out_bytes_for(h, cfg->output), 256);
+    }
+    k0_first[n] = k0t;
+    tile_first[n] = k4t;
+    sub_first[n] = sub;
+    if (huffs.empty()) huffs.emplace_back();  // keep pointers valid
+    if (quants.empty()) quants.emplace_back();
+    b->n_huff = uint32_t(huffs.size());
+    b->n_quant = uint32_t(quants.size());
+    b->k0_tiles = k0t;
+    b->k4_tiles = k4t;
+    b->total_subs = sub;
+    b->total_dus = du;
+    b->out_bytes = outb;
+    b->k1_ctas = uint32_t((sub + kK1Threads - 1) / kK1Threads);
+    b->k2_tiles = uint32_t((sub + kK2Threads - 1) / kK2Threads);
+
+    // ---- raw bytes: user region or pinned staging
+    if (b->packed) {
+        CU(ctx->stage.ensure(pack_off + 64), "cudaMallocHost(stage)");
+        parallel_memcpy(static_cast<uint8_t*>(ctx->stage.p), pk_src, pk_dst);
+        b->raw_src = static_cast<const uint8_t*>(ctx->stage.p);
+        b->raw_bytes = pack_off;
+    } else {
+        b->raw_src = lo;
+        b->raw_bytes = lo ? uint64_t(hi - lo) : 0;
+    }
+
+    // ---- meta blob
+    size_t o = 0;
+    b->m_desc = o;
+    o = align_up(o + n * sizeof(ImgDesc), 16);
+    b->m_state = o;
+    o = align_up(o + n * sizeof(ImgState), 16);
+    b->m_huff = o;
+    o = align_up(o + huffs.size() * sizeof(DevHuff), 16);
+    b->m_quant = o;
+    o = align_up(o + quants.size() * 128, 16);
+    b->m_basis = o;
+    o = align_up(o + 64 * sizeof(double), 16);
+    b->m_k0 = o;
+    o = align_up(o + (n + 1) * 4, 16);
+    b->m_tile = o;
+    o = align_up(o + (n + 1) * 4, 16);
+    b->m_sub = o;
+    o = align_up(o + (n + 1) * 8, 16);
+    b->m_total = o;
+    CU(ctx->meta_host.ensure(o), "cudaMallocHost(meta)");
+    uint8_t* mh = static_cast<uint8_t*>(ctx->meta_host.p);
+    std::memcpy(mh + b->m_desc, b->desc.data(), n * sizeof(ImgDesc));
+    for (size_t i = 0; i < n; ++i) {
+        ImgState s{};
+        s.status = b->hdr[i].status;
+        std::memcpy(mh + b->m_state + i * sizeof(ImgState), &s, sizeof(s));
+    }
+    std::memcpy(mh + b->m_huff, huffs.data(), huffs.size() * sizeof(DevHuff));
+    std::memcpy(mh + b->m_quant, quants.data(), quants.size() * 128);
+    std::memcpy(mh + b->m_basis, ctx->basis, 64 * sizeof(double));
+    std::memcpy(mh + b->m_k0, k0_first.data(), (n + 1) * 4);
+    std::memcpy(mh + b->m_tile, tile_first.data(), (n + 1) * 4);
+    std::memcpy(mh + b->m_sub, sub_first.data(), (n + 1) * 8);
+
+    // ---- device reservation
+    CU(ctx->meta.ensure(o), "cudaMalloc(meta)");
+    CU(ctx->raw.ensure(b->raw_bytes + 64), "cudaMalloc(raw)");
+    CU(ctx->ubuf.ensure(b->raw_bytes + 64), "cudaMalloc(ubuf)");
+    const size_t subs = std::max<uint64_t>(sub, 1);
+    CU(ctx->ent.ensure(subs * sizeof(Entry)), "cudaMalloc(ent)");
+    CU(ctx->dcs.ensure(subs * sizeof(DcSums)), "cudaMalloc(dcs)");
+    CU(ctx->off.ensure(subs * 8), "cudaMalloc(off)");
+    CU(ctx->cap.ensure(subs * 4), "cudaMalloc(cap)");
+    CU(ctx->pred.ensure(subs * sizeof(DcSums)), "cudaMalloc(pred)");
+    CU(ctx->cta_end.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_end)");
+    CU(ctx->cta_start.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_start)");
+    CU(ctx->k1_flag.ensure((b->k1_ctas + 1) * 4), "cudaMalloc(k1_flag)");
+    CU(ctx->coef.ensure(std::max<uint64_t>(du, 1) * 128), "cudaMalloc(coef)");
+    CU(ctx->out.ensure(std::max<uint64_t>(outb, 1)), "cudaMalloc(out)");
+    CU(ctx->counters.ensure(kNumCounters * 4), "cudaMalloc(counters)");
+    CU(ctx->stats.ensure(kNumStats * 8), "cudaMalloc(stats)");
+    CU(ctx->k0_flag.ensure((k0t + 1) * 4), "cudaMalloc(k0_flag)");
+    CU(ctx->k0_agg.ensure((k0t + 1) * 32), "cudaMalloc(k0_agg)");
+    CU(ctx->k2_flag.ensure((b->k2_tiles + 1) * 4), "cudaMalloc(k2_flag)");
+    CU(ctx->k2_agg.ensure((b->k2_tiles + 1) * 64), "cudaMalloc(k2_agg)");
+    CU(ctx->status_host.ensure(n * sizeof(ImgState) + 64 + kNumStats * 8), "cudaMallocHost(status)");
+
+    // ---- kernel parameters
+    Params& p = b->prm;
+    uint8_t* md = ctx->meta.as<uint8_t>();
+    p.img = reinterpret_cast<const ImgDesc*>(md + b->m_desc);
+    p.ist = reinterpret_cast<ImgState*>(md + b->m_state);
+    p.n_img = uint32_t(n);
+    p.huff = reinterpret_cast<const DevHuff*>(md + b->m_huff);
+    p.quant_raster = reinterpret_cast<const uint16_t*>(md + b->m_quant);
+    p.basis = reinterpret_cast<const double*>(md + b->m_basis);
+    p.raw = ctx->raw.as<uint8_t>();
+    p.ubuf = ctx->ubuf.as<uint8_t>();
+    p.k0_first = reinterpret_cast<const uint32_t*>(md + b->m_k0);
+    p.k0_tiles = k0t;
+    p.k1_ctas = b->k1_ctas;
+    p.sb = sb;
+    p.sub_first = reinterpret_cast<const uint64_t*>(md + b->m_sub);
+    p.total_subs = sub;
+    p.ent = ctx->ent.as<Entry>();
+    p.dcs = ctx->dcs.as<DcSums>();
+    p.off = ctx->off.as<uint64_t>();
+    p.cap = ctx->cap.as<uint32_t>();
+    p.pred = ctx->pred.as<DcSums>();
+    p.cta_end = ctx->cta_end.as<Entry>();
+    p.cta_start = ctx->cta_start.as<Entry>();
+    p.k1_flag = ctx->k1_flag.as<uint32_t>();
+    p.k2_tiles = b->k2_tiles;
+    p.k4_tiles = k4t;
+    p.tile_first = reinterpret_cast<const uint32_t*>(md + b->m_tile);
+    p.coef = ctx->coef.as<int16_t>();
+    p.out = ctx->out.as<uint8_t>();
+    p.counters = ctx->counters.as<uint32_t>();
+    p.k0_flag = ctx->k0_flag.as<uint32_t>();
+    p.k0_agg = ctx->k0_agg.as<uint64_t>();
+    p.k2_flag = ctx->k2_flag.as<uint32_t>();
+    p.k2_agg = ctx->k2_agg.as<uint64_t>();
+    p.stats = ctx->stats.as<unsigned long long>();
+
+    ctx->busy = true;
+    *out = b.release();
+    return PJG_OK;
+}
+
+int pjg_batch_upload(pjg_batch* b) {
+    if (!b) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CU(cudaEventRecord(ctx->ev[0], ctx->stream), "cudaEventRecord");
+    if (b->raw_bytes)
+        CU(cudaMemcpyAsync(ctx->raw.p, b->raw_src, b->raw_bytes, cudaMemcpyHostToDevice, ctx->stream),
+           "H2D raw");
+    CU(cudaMemcpyAsync(ctx->meta.p, ctx->meta_host.p, b->m_total, cudaMemcpyHostToDevice, ctx->stream),
+       "H2D meta");
+    CU(cudaEventRecord(ctx->ev[1], ctx->stream), "cudaEventRecord");
+    b->uploaded = true;
+    return PJG_OK;
+}
+
+int pjg_batch_decode(pjg_batch* b) {
+    if (!b) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    if (!b->uploaded) return fail(ctx, PJG_INVALID_ARGUMENT, "batch not uploaded");
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = ctx->stream;
+    // status words are re-initialised so decode can be re-run on the same upload
+    {
+        uint8_t* mh = static_cast<uint8_t*>(ctx->meta_host.p);
+        CU(cudaMemcpyAsync(ctx->meta.as<uint8_t>() + b->m_state, mh + b->m_state, b->n * sizeof(ImgState),
+                           cudaMemcpyHostToDevice, s),
+           "H2D status");
+    }
+    CU(cudaMemsetAsync(ctx->counters.p, 0, kNumCounters * 4, s), "memset counters");
+    CU(cudaMemsetAsync(ctx->stats.p, 0, kNumStats * 8, s), "memset stats");
+    b->prm.epoch = ++ctx->epoch;
+    CU(cudaEventRecord(ctx->ev[2], s), "ev");
+    launch_k0_unstuff(b->prm, s);
+    CU(cudaEventRecord(ctx->ev[3], s), "ev");
+    launch_k1_sync(b->prm, s);
+    launch_k1c_fixup(b->prm, s);
+    CU(cudaEventRecord(ctx->ev[4], s), "ev");
+    launch_k2_scan(b->prm, s);
+    CU(cudaEventRecord(ctx->ev[5], s), "ev");
+    launch_k3_write(b->prm, s);
+    CU(cudaEventRecord(ctx->ev[6], s), "ev");
+    launch_k4_transform(b->prm, s);
+    CU(cudaGetLastError(), "kernel launch");
+    CU(cudaEventRecord(ctx->ev[7], s), "ev");
+    // statuses + stats back (small)
+    uint8_t* sh = static_cast<uint8_t*>(ctx->status_host.p);
+    CU(cudaMemcpyAsync(sh, ctx->meta.as<uint8_t>() + b->m_state, b->n * sizeof(ImgState),
+                       cudaMemcpyDeviceToHost, s),
+       "D2H status");
+    CU(cudaMemcpyAsync(sh + align_up(b->n * sizeof(ImgState), 16), ctx->stats.p, kNumStats * 8,
+                       cudaMemcpyDeviceToHost, s),
+       "D2H stats");
+    b->decoded = true;
+    b->synced = false;
+    return PJG_OK;
+}
+
+int pjg_batch_synchronize(pjg_batch* b, int32_t* statuses) {
+    if (!b) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    if (!b->decoded) return fail(ctx, PJG_NOT_DECODED, "batch not decoded");
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CU(cudaStreamSynchronize(ctx->stream), "decode");
+    if (!b->synced) {
+        b->dev_state.resize(b->n);
+        const uint8_t* sh = static_cast<const uint8_t*>(ctx->status_host.p);
+        std::memcpy(b->dev_state.data(), sh, b->n * sizeof(ImgState));
+        std::memcpy(b->stats, sh + align_up(b->n * sizeof(ImgState), 16), sizeof(b->stats));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+        b->stage_ms[PJG_STAGE_UPLOAD] = ms;
+        for (int k = 0; k < 5; ++k) {
+            cudaEventElapsedTime(&ms, ctx->ev[2 + k], ctx->ev[3 + k]);
+            b->stage_ms[PJG_STAGE_UNSTUFF + k] = ms;
+        }
+        b->synced = true;
+    }
+    if (statuses)
+        for (size_t i = 0; i < b->n; ++i) statuses[i] = b->dev_state[i].status;
+    return PJG_OK;
+}
+
+int pjg_batch_download(pjg_batch* b, uint8_t* const* outs, const size_t* caps) {
+    if (!b || !outs) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    int st = pjg_batch_synchronize(b, nullptr);
+    if (st) return st;
+    cudaEvent_t e0 = ctx->ev[0], e1 = ctx->ev[1];
+    CU(cudaEventRecord(e0, ctx->stream), "ev");
+    for (size_t i = 0; i < b->n; ++i) {
+        if (!outs[i] || b->dev_state[i].status != 0) continue;
+        uint64_t nb = b->info[i].output_bytes;
+        if (caps && caps[i] < nb) return fail(ctx, PJG_CAPACITY, "output buffer too small");
+        CU(cudaMemcpyAsync(outs[i], ctx->out.as<uint8_t>() + b->desc[i].out_off, nb, cudaMemcpyDeviceToHost,
+                           ctx->stream),
+           "D2H out");
+    }
+    CU(cudaEventRecord(e1, ctx->stream), "ev");
+    CU(cudaStreamSynchronize(ctx->stream), "D2H");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    b->stage_ms[PJG_STAGE_DOWNLOAD] = ms;
+    return PJG_OK;
+}
+
+int pjg_batch_info(const pjg_batch* b, size_t i, pjg_image_info* info) {
+    if (!b || i >= b->n || !info) return PJG_INVALID_ARGUMENT;
+    *info = b->info[i];
+    return b->host_status[i];
+}
+
+const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i) {
+    if (!b || i >= b->n) return nullptr;
+    return b->ctx->out.as<uint8_t>() + b->desc[i].out_off;
+}
+
+uint64_t pjg_batch_output_bytes(const pjg_batch* b) { return b ? b->out_bytes : 0; }
+
+int pjg_batch_stage_times(const pjg_batch* b, double* ms) {
+    if (!b || !ms) return PJG_INVALID_ARGUMENT;
+    for (int k = 0; k < PJG_NUM_STAGES; ++k) ms[k] = b->stage_ms[k];
+    return PJG_OK;
+}
+
+int pjg_batch_sync_stats(const pjg_batch* b, uint64_t* stats) {
+    if (!b || !stats) return PJG_INVALID_ARGUMENT;
+    stats[0] = b->stats[kStatRoundsSum];
+    stats[1] = b->stats[kStatRoundsMax];
+    stats[2] = b->stats[kStatInterHops];
+    stats[3] = b->stats[kStatFixPasses];
+    return PJG_OK;
+}
+
+void pjg_batch_destroy(pjg_batch* b) {
+    if (!b) return;
+    if (b->ctx) {
+        cudaSetDevice(b->ctx->device);
+        cudaStreamSynchronize(b->ctx->stream);
+        b->ctx->busy = false;
+    }
+    delete b;
+}
+
+int pjg_batch_dump_coefficients(const pjg_batch* b, size_t i, int pre_dc_zigzag, int16_t* out, size_t count) {
+    if (!b || i >= b->n || !out) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    const Header& h = b->hdr[i];
+    uint64_t nco = h.total_dus() * 64;
+    if (count < nco) return fail(ctx, PJG_CAPACITY, "coefficient buffer too small");
+    if (b->host_status[i] != 0) return b->host_status[i];
+    CU(cudaStreamSynchronize(ctx->stream), "sync");
+    std::vector<int16_t> raster(nco);
+    CU(cudaMemcpy(raster.data(), ctx->coef.as<int16_t>() + b->desc[i].du_first * 64, nco * 2,
+                  cudaMemcpyDeviceToHost),
+       "D2H coef");
+    if (!pre_dc_zigzag) {
+        std::memcpy(out, raster.data(), nco * 2);
+        return PJG_OK;
+    }
+    static const uint8_t kZz2R[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
+                                      12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
+                                      35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
+                                      58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+    const uint64_t dus = h.total_dus();
+    int32_t last[3] = {0, 0, 0};
+    bool seen[3] = {false, false, false};
+    for (uint64_t d = 0; d < dus; ++d) {
+        const int16_t* r = raster.data() + d * 64;
+        int16_t* z = out + d * 64;
+        for (int k = 0; k < 64; ++k) z[k] = r[kZz2R[k]];
+        unsigned comp = h.du_seq[d % h.dpm];
+        int32_t abs_dc = z[0];
+        // inverse of dc_prefix_sum (transform.hpp:56-74), exact mod 2^16
+        if (seen[comp]) z[0] = int16_t(uint16_t(abs_dc - last[comp]));
+        seen[comp] = true;
+        last[comp] = abs_dc;
+    }
+    return PJG_OK;
+}
+
+int pjg_batch_dump_sync_states(const pjg_batch* b, size_t i, pjg_sync_entry* out, size_t cap, size_t* n_out) {
+    if (!b || i >= b->n || !n_out) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    int st = pjg_batch_synchronize(const_cast<pjg_batch*>(b), nullptr);
+    if (st) return st;
+    if (b->host_status[i] != 0) return b->host_status[i];
+    const uint64_t L = b->dev_state[i].bit_length;
+    const uint64_t N = (L + b->cfg.subsequence_bits - 1) / b->cfg.subsequence_bits;
+    *n_out = N;
+    if (!out) return PJG_OK;
+    if (cap < N) return fail(ctx, PJG_CAPACITY, "sync state buffer too small");
+    std::vector<Entry> ents(N);
+    std::vector<uint32_t> caps(N);
+    const uint64_t g0 = b->desc[i].sub_first;
+    if (N) {
+        CU(cudaMemcpy(ents.data(), ctx->ent.as<Entry>() + g0, N * sizeof(Entry), cudaMemcpyDeviceToHost), "D2H ent");
+        CU(cudaMemcpy(caps.data(), ctx->cap.as<uint32_t>() + g0, N * 4, cudaMemcpyDeviceToHost), "D2H cap");
+    }
+    for (uint64_t k = 0; k < N; ++k) {
+        out[k].p = ents[k].p;
+        out[k].n = caps[k];
+        out[k].c = czd_c(ents[k].czd);
+        out[k].z = czd_z(ents[k].czd);
+        out[k].divergent = czd_div(ents[k].czd) ? 1 : 0;
+        out[k].pad = 0;
+    }
+    return PJG_OK;
+}
+
+int pjg_batch_dump_segment(const pjg_batch* b, size_t i, uint8_t* out, size_t cap, size_t* n_out) {
+    if (!b || i >= b->n || !n_out) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    int st = pjg_batch_synchronize(const_cast<pjg_batch*>(b), nullptr);
+    if (st) return st;
+    if (b->host_status[i] != 0) return b->host_status[i];
+    const uint64_t bytes = b->dev_state[i].bit_length / 8;
+    *n_out = bytes;
+    if (!out) return PJG_OK;
+    if (cap < bytes) return fail(ctx, PJG_CAPACITY, "segment buffer too small");
+    if (bytes)
+        CU(cudaMemcpy(out, ctx->ubuf.as<uint8_t>() + b->desc[i].raw_off, bytes, cudaMemcpyDeviceToHost),
+           "D2H segment");
+    return PJG_OK;
+}
+
+int pjg_decode_batch(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const size_t* sizes,
+                     const pjg_config* cfg, pjg_image_info* infos, uint8_t* const* outs,
+                     const size_t* out_caps, int32_t* statuses) {
+    if (!ctx) return PJG_INVALID_ARGUMENT;
+    pjg_batch* b = nullptr;
+    int st = pjg_batch_create(ctx, n, files, sizes, cfg, &b);
+    if (st) return st;
+    std::unique_ptr<pjg_batch, void (*)(pjg_batch*)> guard(b, pjg_batch_destroy);
+    if ((st = pjg_batch_upload(b))) return st;
+    if ((st = pjg_batch_decode(b))) return st;
+    if ((st = pjg_batch_synchronize(b, statuses))) return st;
+    if (infos)
+        for (size_t i = 0; i < n; ++i) infos[i] = b->info[i];
+    if (outs && (st = pjg_batch_download(b, outs, out_caps))) return st;
+    return PJG_OK;
+}
+
+int pjg_decode(pjg_ctx* ctx, const uint8_t* file, size_t size, const pjg_config* cfg, pjg_image_info* info,
+               uint8_t* out, size_t out_capacity) {
+    int32_t status = 0;
+    pjg_image_info tmp;
+    uint8_t* outs[1] = {out};
+    size_t caps[1] = {out_capacity};
+    int st = pjg_decode_batch(ctx, 1, &file, &size, cfg, info ? info : &tmp, out ? outs : nullptr, caps, &status);
+    if (st) return st;
+    if (status) {
+        if (ctx) ctx->err = pjg_status_name(status);
+        return status;
+    }
+    return PJG_OK;
+}
+
+int pjg_upsample_and_convert(pjg_ctx* ctx, uint32_t width, uint32_t height, uint32_t nplanes,
+                             const uint32_t* plane_w, const uint32_t* plane_h, const uint8_t* const* planes,
+                             uint8_t* out_rgb) {
+    if (!ctx || !plane_w || !plane_h || !planes || !out_rgb || nplanes < 1 || nplanes > 3)
+        return PJG_INVALID_ARGUMENT;
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const uint64_t npx = uint64_t(width) * height;
+    if (nplanes == 1) {  // grayscale passthrough (pipeline.hpp:171-176)
+        for (uint32_t r = 0; r < height; ++r) std::memcpy(out_rgb + uint64_t(r) * width, planes[0] + uint64_t(r) * plane_w[0], width);
+        return PJG_OK;
+    }
+    if (nplanes != 3) return fail(ctx, PJG_INVALID_ARGUMENT, "upsample_and_convert needs 1 or 3 planes");
+    uint64_t sz[3], tot = 0;
+    for (int c = 0; c < 3; ++c) {
+        sz[c] = uint64_t(plane_w[c]) * plane_h[c];
+        tot += align_up(sz[c], 256);
+    }
+    DevBuf tmp;
+    CU(tmp.ensure(tot + npx * 3), "cudaMalloc(tmp)");
+    uint8_t* d = tmp.as<uint8_t>();
+    uint8_t* dp[3];
+    uint64_t o = 0;
+    for (int c = 0; c < 3; ++c) {
+        dp[c] = d + o;
+        CU(cudaMemcpyAsync(dp[c], planes[c], sz[c], cudaMemcpyHostToDevice, ctx->stream), "H2D planes");
+        o += align_up(sz[c], 256);
+    }
+    launch_k5_color(dp[0], dp[1], dp[2], width, height, plane_w[0], plane_w[1], plane_h[1], plane_w[2], plane_h[2],
+                    d + o, ctx->stream);
+    CU(cudaGetLastError(), "k5 launch");
+    CU(cudaMemcpyAsync(out_rgb, d + o, npx * 3, cudaMemcpyDeviceToHost, ctx->stream), "D2H rgb");
+    CU(cudaStreamSynchronize(ctx->stream), "colour");
+    tmp.release();
+    return PJG_OK;
+}
+
+int pjg_debug_huff_decode(const uint8_t* counts16, const uint8_t* symbols, size_t nsym, const uint16_t* windows,
+                          size_t nwin, uint32_t* out) {
+    HuffSpec s;
+    std::memcpy(s.counts.data(), counts16, 16);
+    s.symbols.assign(symbols, symbols + nsym);
+    s.present = true;
+    DevHuff d;
+    int32_t st = build_dev_huff(s, &d);
+    if (st) return -st;
+    for (size_t i = 0; i < nwin; ++i) out[i] = huff_lookup(d, windows[i]);
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+// Internal layout shared by the host planner (pjg_api.cu, jfif.cpp) and the
+// sm_100a kernels (kernels.cu).  Not part of the public C-ABI (include/pjg.h).
+#pragma once
+
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define PJG_HD __host__ __device__ __forceinline__
+#else
+#define PJG_HD inline
+#endif
+
+namespace pjg {
+
+// ---------------------------------------------------------------- status --
+// Mirrors pjpeg::Errc (reference common.hpp:26-38); C-ABI value = ordinal+1.
+enum Status : int32_t {
+    kOk = 0,
+    kMalformedStuffing = 1,
+    kEmptyScan = 2,
+    kOutOfBits = 3,
+    kUnsupportedFeature = 4,
+    kMalformedHeader = 5,
+    kMissingTable = 6,
+    kOversubscribedCode = 7,
+    kInvalidCode = 8,
+    kConsistencyFailure = 9,
+    kEmptyCorpus = 10,
+    kIoError = 11,
+};
+
+// ------------------------------------------------------- Huffman tables --
+// Two-level canonical decoder reproducing the reference's flat 2^maxlen LUT
+// (huffman.hpp:60-93, 113-130) bit for bit: a 9-bit primary table resolves
+// codes of length <= 9; longer codes walk per-length maxcode (Annex F.2.2.3).
+constexpr int kPrimaryBits = 9;
+
+struct DevHuff {
+    uint16_t lut[1 << kPrimaryBits];  // (length << 8) | symbol; length 0 = unresolved
+    int32_t maxcode[18];              // per length 1..16 ([17] unused), -1 when no code has that length
+    int32_t valoff[18];               // symbol index = code + valoff[len]
+    uint8_t symbols[256];
+    uint32_t maxlen;                  // reference HuffmanTable::max_code_length
+    uint32_t pad[3];
+};
+static_assert(sizeof(DevHuff) % 16 == 0, "DevHuff must stay 16-byte aligned");
+
+// Decodes one codeword from the top 16 bits of `w16` (MSB first).  Returns
+// (length << 8) | symbol, or 0 when no code matches the first maxlen bits —
+// the reference's `e.length == 0`.
+PJG_HD uint32_t huff_lookup(const DevHuff& t, uint32_t w16) {
+    uint32_t e = t.lut[w16 >> (16 - kPrimaryBits)];
+    if (e != 0) return e;
+    for (uint32_t len = kPrimaryBits + 1; len <= t.maxlen; ++len) {
+        int32_t code = int32_t(w16 >> (16 - len));
+        if (code <= t.maxcode[len]) return (len << 8) | t.symbols[code + t.valoff[len]];
+    }
+    return 0;
+}
+
+// -------------------------------------------------------------- images --
+constexpr int kMaxSlots = 10;  // data units per MCU (4:2:0 → 6)
+
+struct ImgDesc {
+    // input: the raw bytes following the SOS header, in the batch's raw buffer
+    uint64_t raw_off;      // byte offset of the first scan byte (== unstuffed offset)
+    uint64_t raw_len;      // bytes from the first scan byte to the end of the file
+    // geometry (parser.hpp:56-85)
+    uint32_t width, height;
+    uint32_t mcus_x, mcus_y;
+    uint32_t ncomp, dpm, h_max, v_max;
+    uint32_t comp_h[3], comp_v[3];
+    uint32_t plane_w[3], plane_h[3];
+    uint64_t du_comp;      // slot -> component, 4 bits per slot
+    uint64_t du_kslot;     // slot -> index of that unit within its component, 4 bits per slot
+    uint16_t dc_tab[3], ac_tab[3], q_tab[3];
+    uint16_t mcus_per_tile;  // K4 tile width in MCUs
+    // partition / layout
+    uint64_t sub_first;    // first global subsequence
+    uint64_t sub_count;    // allocated subsequences (upper bound from raw_len)
+    uint64_t du_first;     // first data unit in the batch coefficient buffer
+    uint64_t out_off;      // byte offset of this image in the batch output buffer
+    uint64_t expected;     // 64 * total data units (parallel_decode.hpp:341)
+    uint32_t out_mode;     // pjg_output_kind
+    int32_t deferred;      // build_table error, applied after K0's scan checks
+    uint32_t tiles_x;      // K4 tiles per MCU row
+    uint32_t pad1;
+};
+
+// Per-image results written by the device.
+struct ImgState {
+    uint64_t bit_length;   // 8 * unstuffed bytes (bitstream.hpp:74), written by K0
+    int32_t status;        // first error (Status), 0 = ok
+    uint32_t inter_hops;   // inter-sequence overflow hops (diagnostics)
+};
+
+// ----------------------------------------------------------- sync state --
+// One s_info entry (parallel_decode.hpp:64-84): state after the last symbol
+// owned by a subsequence.  czd packs c (bits 0-3), z (bits 4-10) and the
+// divergence flag (bit 15); n is the coefficient-slot count.
+struct Entry {
+    uint64_t p;
+    uint32_t n;
+    uint32_t czd;
+};
+static_assert(sizeof(Entry) == 16, "Entry layout");
+
+constexpr uint32_t kDivBit = 0x8000u;
+constexpr uint32_t kBoundaryBit = 0x4000u;  // cta_start only: CTA starts mid-image
+
+PJG_HD uint32_t pack_czd(uint32_t c, uint32_t z, bool div) {
+    return c | (z << 4) | (div ? kDivBit : 0u);
+}
+PJG_HD uint32_t czd_c(uint32_t v) { return v & 15u; }
+PJG_HD uint32_t czd_z(uint32_t v) { return (v >> 4) & 127u; }
+PJG_HD bool czd_div(uint32_t v) { return (v & kDivBit) != 0; }
+// sync_equal (parallel_decode.hpp:81-84): divergence flag, p, c, z; n ignored.
+PJG_HD bool sync_equal(uint64_t pa, uint32_t ca, uint64_t pb, uint32_t cb) {
+    return pa == pb && ((ca ^ cb) & (kDivBit | 0x7FFu)) == 0;
+}
+
+// Per-subsequence DC-difference sums, one 16-bit lane per component
+// (dc_prefix_sum accumulates in int32 and stores int16: transform.hpp:56-74,
+// so only the sum mod 2^16 matters).  lanes 0,1 in lo; lane 2 in hi.
+struct DcSums {
+    uint32_t lo, hi;
+};
+
+// ------------------------------------------------------------- params --
+constexpr int kK0Threads = 256;
+constexpr int kK0BytesPerThread = 16;
+constexpr int kK0Tile = kK0Threads * kK0BytesPerThread;  // 4096 raw bytes per tile
+constexpr int kK1Threads = 128;                          // subsequences per K1 CTA
+constexpr int kK2Threads = 256;
+constexpr int kK3Threads = 128;
+constexpr int kK4Threads = 256;
+constexpr int kK4MaxBlocks = 48;                         // data units per K4 tile
+
+struct Params {
+    // batch
+    const ImgDesc* img;
+    ImgState* ist;
+    uint32_t n_img;
+    uint32_t epoch;
+    const DevHuff* huff;
+    const uint16_t* quant_raster;  // 64 uint16 per table, RASTER order
+    const double* basis;           // 64 doubles, basis[u][x] (host std::cos)
+    // raw & unstuffed scan
+    const uint8_t* raw;
+    uint8_t* ubuf;
+    // K0 tiles
+    const uint32_t* k0_first;      // n_img + 1 prefix
+    uint32_t k0_tiles;
+    uint32_t k1_ctas;
+    // subsequences
+    uint64_t sb;                   // subsequence_bits
+    const uint64_t* sub_first;     // n_img + 1 prefix
+    uint64_t total_subs;
+    Entry* ent;
+    DcSums* dcs;
+    uint64_t* off;                 // trimmed exclusive offsets (slots)
+    uint32_t* cap;                 // trimmed counts
+    DcSums* pred;                  // DC predictor at the start of each subsequence
+    Entry* cta_end;                // K1: each CTA's last entry after intra sync
+    Entry* cta_start;              // K1: start state each CTA's inter overflow used
+    uint32_t* k1_flag;
+    uint32_t k2_tiles;
+    uint32_t k4_tiles;
+    // K4
+    const uint32_t* tile_first;    // n_img + 1 prefix of K4 tiles
+    int16_t* coef;                 // 64 int16 per data unit, raster order, absolute DC
+    uint8_t* out;
+    // lookback scratch
+    uint32_t* counters;            // tickets (reset per run)
+    uint32_t* k0_flag;
+    uint64_t* k0_agg;              // 4 x uint64 per tile: aggregate (cnt, mk), inclusive (cnt, mk)
+    uint32_t* k2_flag;
+    uint64_t* k2_agg;              // 4 x uint64 per tile: aggregate (n|head, dc), inclusive (n, dc)
+    // stats
+    unsigned long long* stats;     // see StatIndex
+};
+
+enum Counter { kTicketK0 = 0, kTicketK1 = 1, kTicketK2 = 2, kNumCounters = 8 };
+enum StatIndex {
+    kStatRoundsSum = 0,    // intra rounds summed over K1 CTAs
+    kStatRoundsMax = 1,
+    kStatInterHops = 2,    // subsequences decoded by inter-CTA overflows
+    kStatFixPasses = 3,    // K1c passes that found work
+    kStatSymbols = 4,      // reserved
+    kNumStats = 8
+};
+
+// Kernel launchers (kernels.cu).  All are stream-ordered, no host syncs.
+void launch_k0_unstuff(const Params& p, void* stream);
+void launch_k1_sync(const Params& p, void* stream);
+void launch_k1c_fixup(const Params& p, void* stream);
+void launch_k2_scan(const Params& p, void* stream);
+void launch_k3_write(const Params& p, void* stream);
+void launch_k4_transform(const Params& p, void* stream);
+void launch_k5_color(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, uint32_t W, uint32_t H,
+                     uint32_t pw0, uint32_t pw1, uint32_t ph1, uint32_t pw2, uint32_t ph2, uint8_t* out,
+                     void* stream);
+
+}  // namespace pjg

@@ -1,0 +1,20 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); parity tests through the C-ABI")
+
+
+@pytest.fixture(scope="session")
+def decoder():
+    import paper_2111_09219_b200 as pj
+    d = pj.Decoder(0)
+    yield d
+    d.close()

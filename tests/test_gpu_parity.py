@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference.
+
+The reference itself (oracle/_ref, pjpeg headers compiled in place) is the
+checker here; tests/test_oracle.py separately pins my C restatement against it.
+Bar: bit-exact coefficients, sync states, planes and RGB.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import Orc, Ref
+from tests.corpus import acceptance_corpus, ref_jpeg
+
+pj = pytest.importorskip("paper_2111_09219_b200")
+
+pytestmark = pytest.mark.gpu
+
+
+def _rgb(buf, inf):
+    ch = inf.channels
+    pix = buf[: inf.width * inf.height * ch]
+    return pix.reshape(inf.height, inf.width, ch) if ch == 3 else pix.reshape(inf.height, inf.width)
+
+
+def _check_file(b, i, data, sb, rgb_mode=True):
+    """coefficients, sync states and output of image i against the reference."""
+    coeffs, ents, meta = Ref.entropy(data, sb=sb, b=4)
+    got = b.coefficients(i, pre_dc_zigzag=True)
+    assert np.array_equal(got, coeffs), "entropy-stage coefficients differ"
+    st = b.sync_states(i)
+    assert st.shape[0] == ents.shape[0] == int(meta[0])
+    # trimmed n per subsequence is unique (true decomposition) → exact
+    assert np.array_equal(st[:, 1], ents[:, 1]), "trimmed n differs"
+    # (p, c, z) at every boundary the oracle trace marks valid (test_parallel_decode.cpp:205-227)
+    N = st.shape[0]
+    bnd = np.arange(1, N, dtype=np.uint64) * sb
+    states, valid, _, _ = Ref.trace(data, bnd)
+    for k in range(N - 1):
+        if valid[k]:
+            assert st[k, 0] == states[k, 0] and st[k, 2] == states[k, 2] and st[k, 3] == states[k, 3], k
+
+
+def test_acceptance_corpus_rgb_bit_exact(decoder):
+    corpus = acceptance_corpus()
+    files = [f for _, f in corpus]
+    with decoder.batch(files, pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved) as b:
+        st = b.run()
+        assert (st == 0).all(), st
+        outs = b.download()
+        for i, ((w, h, q, s), f) in enumerate(corpus):
+            ref = Ref.decode(f, rgb=True)
+            assert ref.status == 0
+            got = _rgb(outs[i], b.infos[i])
+            assert got.shape == ref.data.shape, (w, h, q, s)
+            assert np.array_equal(got, ref.data), (w, h, q, s, int((got != ref.data).sum()))
+
+
+@pytest.mark.parametrize("sb", [128, 256, 1024, 4096])
+def test_acceptance_corpus_entropy_and_states(decoder, sb):
+    corpus = acceptance_corpus()
+    files = [f for _, f in corpus]
+    with decoder.batch(files, pj.DecodeConfig(subsequence_bits=sb), pj.OutputColorspace.YCbCrPlanes) as b:
+        st = b.run()
+        assert (st == 0).all(), st
+        outs = b.download()
+        for i, (_, f) in enumerate(corpus):
+            _check_file(b, i, f, sb)
+            ref = Ref.decode(f, rgb=False)
+            assert np.array_equal(outs[i][: ref.data.size], ref.data)
+
+
+@pytest.mark.parametrize("shape", [(512, 512, 85, "444", 1), (500, 375, 75, "420", 1000),
+                                   (1023, 769, 90, "420", 5), (333, 257, 95, "422", 6),
+                                   (801, 601, 60, "gray", 7)])
+def test_config_shapes_bit_exact(decoder, shape):
+    w, h, q, s, seed = shape
+    f = ref_jpeg(w, h, seed, q, s)
+    with decoder.batch([f], pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved) as b:
+        st = b.run()
+        assert st[0] == 0
+        got = _rgb(b.download()[0], b.infos[0])
+        _check_file(b, 0, f, 1024)
+    ref = Ref.decode(f, rgb=True)
+    assert np.array_equal(got, ref.data)
+
+
+def test_decode_single_planes_and_errors(decoder):
+    f = ref_jpeg(80, 60, 10, 80, "420")
+    res = pj.decode_single(f)
+    assert len(res.planes.planes) == 3
+    assert res.planes.planes[0].samples.shape == (60, 80)
+    assert res.planes.planes[1].samples.shape == (30, 40)
+    assert res.compressed_bytes == len(f)
+    ref = Ref.decode(f, rgb=False)
+    assert np.array_equal(np.concatenate([p.samples.reshape(-1) for p in res.planes.planes]), ref.data)
+    with pytest.raises(pj.Error) as ei:
+        pj.decode_single(bytes([0xDE, 0xAD, 0xBE, 0xEF]))
+    assert ei.value.code == pj.Errc.MalformedHeader
+
+
+def test_decode_batch_isolates_failures(decoder):
+    # test_pipeline.cpp:38-54
+    good1 = ref_jpeg(32, 32, 20, 70, "444")
+    good2 = ref_jpeg(24, 16, 21, 70, "gray")
+    truncated = good1[:10]
+    garbage = bytes([0xDE, 0xAD, 0xBE, 0xEF])
+    out = pj.decode_batch([good1, truncated, good2, garbage])
+    assert isinstance(out[0], pj.DecodeSuccess)
+    assert isinstance(out[1], pj.DecodeFailure)
+    assert isinstance(out[2], pj.DecodeSuccess)
+    assert isinstance(out[3], pj.DecodeFailure)
+    assert out[3].code == pj.Errc.MalformedHeader
+    for o, f in ((out[0], good1), (out[2], good2)):
+        assert pj.planes_checksum(o.planes) == pj.planes_checksum(
+            pj.ImagePlanes(o.planes.width, o.planes.height, 1, 1,
+                           [pj.Plane(p.width, p.height, p.samples) for p in o.planes.planes]))
+        ref = Ref.decode(f, rgb=False)
+        assert np.array_equal(np.concatenate([p.samples.reshape(-1) for p in o.planes.planes]), ref.data)
+
+
+def test_error_codes_match_reference(decoder):
+    base = ref_jpeg(64, 48, 3, 75, "420")
+    cases = {
+        "trunc_header": base[:40],
+        "garbage": bytes([0xDE, 0xAD, 0xBE, 0xEF]),
+        "no_soi": b"\x00" + base[1:],
+        "scan_cut": base[: len(base) // 2],
+        "empty_scan": None,
+    }
+    # empty scan: SOS header immediately followed by EOI
+    sos = base.index(b"\xff\xda")
+    ln = (base[sos + 2] << 8) | base[sos + 3]
+    cases["empty_scan"] = base[: sos + 2 + ln] + b"\xff\xd9"
+    # RST marker inside the scan → UnsupportedFeature (parser.hpp:249-250)
+    scan0 = sos + 2 + ln
+    cases["rst_in_scan"] = base[: scan0 + 20] + b"\xff\xd0" + base[scan0 + 20:]
+    files = list(cases.values())
+    with decoder.batch(files, pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved) as b:
+        st = b.run()
+    for (name, f), s in zip(cases.items(), st):
+        ref = Ref.decode(f, rgb=True)
+        if ref.status == 0:
+            assert s == 0, name
+        else:
+            assert s != 0, name
+            if name != "scan_cut":  # mid-scan truncation: both fail; the stage may differ
+                assert s == ref.status, (name, s, ref.status)
+
+
+def test_upsample_and_convert_kats(decoder):
+    # test_pipeline.cpp:122-165
+    P = pj.Plane
+    planes = pj.ImagePlanes(8, 8, 1, 1, [P(8, 8, np.full((8, 8), 200, np.uint8)),
+                                        P(8, 8, np.full((8, 8), 128, np.uint8)),
+                                        P(8, 8, np.full((8, 8), 128, np.uint8))])
+    out = pj.upsample_and_convert(planes)
+    assert out.channels == 3 and (out.pixels == 200).all()
+    planes = pj.ImagePlanes(4, 2, 2, 2, [P(4, 2, np.full((2, 4), 128, np.uint8)),
+                                        P(2, 1, np.array([[128, 255]], np.uint8)),
+                                        P(2, 1, np.array([[128, 128]], np.uint8))])
+    out = pj.upsample_and_convert(planes).pixels
+    assert list(out[0, 0]) == [128, 128, 128] and list(out[1, 1]) == [128, 128, 128]
+    assert out[0, 2, 2] == 255 and out[1, 3, 2] == 255 and out[0, 2, 1] < 100
+    # random planes vs the reference, all three channels
+    rng = np.random.default_rng(3)
+    for (W, H) in [(17, 9), (64, 48), (33, 31)]:
+        pl = [P(W, H, rng.integers(0, 256, (H, W), dtype=np.uint8)),
+              P((W + 1) // 2, (H + 1) // 2, rng.integers(0, 256, ((H + 1) // 2, (W + 1) // 2), dtype=np.uint8)),
+              P((W + 1) // 2, (H + 1) // 2, rng.integers(0, 256, ((H + 1) // 2, (W + 1) // 2), dtype=np.uint8))]
+        got = pj.upsample_and_convert(pj.ImagePlanes(W, H, 2, 2, pl)).pixels
+        ref = Ref.upsample_and_convert(W, H, [p.samples for p in pl])
+        assert np.array_equal(got, ref)
+
+
+def test_restatement_agrees_on_gpu_box():
+    """Sanity on the GPU box: the C restatement still matches the reference."""
+    f = ref_jpeg(97, 33, 7, 90, "420")
+    assert np.array_equal(Orc.decode(f).data, Ref.decode(f).data)
