@@ -1,0 +1,367 @@
+#!/usr/bin/env python3
+"""Benchmark: JPEG decode GB/s (RGB out) & images/s on B200 vs the CPU reference.
+
+Workload (BASELINE.json configs[2], the batch the metric's 1/2/4/8-GPU scaling
+is quoted on): 4096 synthetic 500x375 4:2:0 q75 baseline JPEGs per GPU
+(weak scaling: every rank decodes its own 4096-image batch, no collective on
+the data path).  ``--config`` selects the other BASELINE shapes.
+
+One step = one full batch decode: K0 unstuff -> K1 sync -> K1c fix-up ->
+K2 scan -> K3 write -> K4 IDCT+upsample+RGB, inputs already resident in HBM
+(``value``), RGB left in HBM.  ``e2e`` = the same batch through the C-ABI
+from pinned HOST JPEG bytes to pinned HOST RGB: header parse + H2D + decode +
+D2H inside the timed region.
+
+``--impl reference`` times the reference's own CPU decoder (pjpeg headers
+compiled in place: oracle/_ref, decode_batch + upsample_and_convert) on a
+bounded sample of the same workload with all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n images, w, h, quality, sampling, restart_interval)
+    "1": (1, 512, 512, 85, "444", 0),
+    "2": (1, 3840, 2160, 90, "420", 0),
+    "3": (4096, 500, 375, 75, "420", 0),
+    "4": (1, 16384, 16384, 95, "444", 0),
+    "5": (1, 8192, 8192, 75, "420", 0),
+}
+CONFIG_NAMES = {
+    "1": "single 512x512 4:4:4 q85",
+    "2": "single 3840x2160 4:2:0 q90",
+    "3": "batch 4096 x 500x375 4:2:0 q75 per GPU",
+    "4": "single 16384x16384 4:4:4 q95",
+    "5": "single 8192x8192 4:2:0 q75",
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_corpus(cfg_key, rank, pinned=True):
+    from paper_2111_09219_b200.synth import synth_batch
+    n, w, h, q, s, ri = CONFIGS[cfg_key]
+    blob, offs, sizes = synth_batch(n, w, h, 100000 * (rank + 1), q, s, ri)
+    if pinned:
+        import torch
+        pb = torch.empty(blob.size + 64, dtype=torch.uint8).pin_memory()
+        pn = pb.numpy()
+        pn[: blob.size] = blob
+        return pb, pn[: blob.size], offs, sizes
+    return None, blob, offs, sizes
+
+
+def cpu_reference_sample(blob, offs, sizes, target_s, threads):
+    """Reference decode_batch + upsample_and_convert on a bounded sample."""
+    from oracle.oracle import Ref
+    files = [blob[o: o + s].tobytes() for o, s in zip(offs, sizes)]
+    n_all = len(files)
+    # calibrate on a small prefix, then size the sample for ~target_s seconds
+    k = min(n_all, max(1, threads))
+    t0 = time.perf_counter()
+    st, outs = Ref.decode_batch_rgb(files[:k], threads)
+    dt = time.perf_counter() - t0
+    assert (st == 0).all(), st
+    per = dt / k
+    m = int(min(n_all, max(k, target_s / max(per, 1e-9))))
+    sample = [files[i % n_all] for i in range(m)] if n_all > 1 else files
+    t0 = time.perf_counter()
+    reps = 0
+    rgb_bytes = 0
+    while True:
+        st, outs = Ref.decode_batch_rgb(sample, threads)
+        assert (st == 0).all()
+        rgb_bytes += sum(o.size for o in outs)
+        reps += 1
+        if time.perf_counter() - t0 >= target_s * 0.5 or n_all == 1 and reps >= 1:
+            break
+    el = time.perf_counter() - t0
+    nimg = reps * len(sample)
+    return {"gbs": rgb_bytes / el / 1e9, "img_s": nimg / el, "seconds": el, "images": nimg,
+            "sample": f"{len(sample)} of {n_all} images x {reps} reps"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle.oracle import Ref
+    threads = Ref.hardware_concurrency()
+    _, blob, offs, sizes = make_corpus(args.config, 0, pinned=False)
+    n, w, h, q, s, _ = CONFIGS[args.config]
+    target = 6.0 if args.config in ("1", "2", "3") else 60.0
+    for _ in range(args.warmup):
+        cpu_reference_sample(blob, offs, sizes[:], 1.0, threads)
+    vals = []
+    for _ in range(args.steps):
+        r = cpu_reference_sample(blob, offs, sizes, target / max(1, args.steps) * 2, threads)
+        vals.append(r)
+    gbs = float(np.mean([v["gbs"] for v in vals]))
+    ims = float(np.mean([v["img_s"] for v in vals]))
+    rec = {
+        "impl": "reference", "metric": "JPEG decode GB/s (RGB out)", "value": round(gbs, 4), "unit": "GB/s",
+        "images_per_s": round(ims, 2), "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * float(np.mean([v["seconds"] for v in vals])), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8 in / f64 IDCT+colour / u8 out",
+        "data": "synthetic", "config": {"workload": CONFIG_NAMES[args.config], "images": n, "width": w, "height": h,
+                                        "quality": q, "sampling": s},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": vals[-1]["sample"]},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(rec), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pjg", choices=["pjg", "reference"])
+    ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
+    ap.add_argument("--sb", type=int, default=1024, help="subsequence_bits")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--check", action="store_true", help="verify a few images against the reference")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_2111_09219_b200 as pj
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    n, w, h, q, s, _ = CONFIGS[args.config]
+    pinned_t, blob, offs, sizes = make_corpus(args.config, rank)
+    dec = pj.Decoder(local)
+    cfg = pj.DecodeConfig(subsequence_bits=args.sb)
+    out_kind = pj.OutputColorspace.RGBInterleaved
+    stream = torch.cuda.ExternalStream(dec.stream(), device=torch.device("cuda", local))
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
+
+    # ---------------- device-resident timing (value) ----------------------
+    b = dec.batch((blob, offs, sizes), cfg, out_kind)
+    b.upload()
+    st = b.decode().synchronize()
+    assert (st == 0).all(), f"decode failed: {np.unique(st)}"
+    rgb_bytes = sum(int(i.output_bytes) for i in b.infos)
+    dus = sum(int(i.data_units) for i in b.infos)
+    comp_bytes = int(sum(sizes))
+    if args.check:
+        from oracle.oracle import Ref
+        outs = b.download()
+        for i in list(range(min(4, n))) + ([n - 1] if n > 4 else []):
+            f = blob[offs[i]: offs[i] + sizes[i]].tobytes()
+            ref = Ref.decode(f, rgb=True)
+            assert np.array_equal(outs[i][: ref.data.size], ref.data.reshape(-1)), f"mismatch image {i}"
+        print(f"# check: {min(4, n) + (1 if n > 4 else 0)} images bit-exact vs reference", file=sys.stderr)
+
+    def one_step():
+        with torch.cuda.stream(stream):
+            flush_buf.zero_()  # untimed L2 flush
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        b.decode()
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        b.synchronize()
+        return e0.elapsed_time(e1), b.stage_times()
+
+    for _ in range(args.warmup):
+        one_step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    step_ms, stages = [], []
+    for _ in range(args.steps):
+        ms, stt = one_step()
+        step_ms.append(ms)
+        stages.append(stt)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    sync_stats = b.sync_stats()
+    tot_ms = float(np.sum(step_ms))
+    if dist:
+        t = torch.tensor([tot_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = world * rgb_bytes / (ms_per_step / 1e3) / 1e9
+    img_s = world * n / (ms_per_step / 1e3)
+    st_mean = {k: float(np.mean([getattr(x, k) for x in stages])) for k in
+               ("unstuff", "sync", "scan", "write", "idct")}
+    b.close()
+
+    # ---------------- end-to-end through the C-ABI with host buffers ------
+    host_out = torch.empty(rgb_bytes + n * 256 + 4096, dtype=torch.uint8).pin_memory()
+    host_ptr = host_out.data_ptr()
+    e2e_ms = []
+    h2d = d2h = 0
+
+    def e2e_step():
+        t0 = time.perf_counter()
+        bb = dec.batch((blob, offs, sizes), cfg, out_kind)  # host header parse + plan
+        bb.upload()
+        bb.decode()
+        bb.download_all(host_ptr, host_out.numel())
+        stt = bb.synchronize()
+        t1 = time.perf_counter()
+        ob = bb.output_bytes()
+        bb.close()
+        assert (stt == 0).all()
+        return (t1 - t0) * 1e3, ob
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    if dist:
+        dist.barrier()
+    for _ in range(args.steps):
+        ms, ob = e2e_step()
+        e2e_ms.append(ms)
+        d2h = ob
+    h2d = comp_bytes
+    e2e_tot = float(np.sum(e2e_ms))
+    if dist:
+        t = torch.tensor([e2e_tot], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_tot = float(t.item())
+    e2e_val = world * rgb_bytes / (e2e_tot / args.steps / 1e3) / 1e9
+
+    # ---------------- roofline of the dominant HBM-bound stage (K4) -------
+    peak, peak_kind = load_peaks()
+    k4_bytes = dus * 128 + rgb_bytes  # int16 coefficient read + RGB write
+    k4_ms = st_mean["idct"]
+    achieved = k4_bytes / (k4_ms / 1e3) / 1e9
+    dominant = max(st_mean, key=st_mean.get)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle.oracle import Ref
+            threads = Ref.hardware_concurrency()
+            r = cpu_reference_sample(blob, offs, sizes, 10.0 if args.config in ("1", "2", "3") else 30.0, threads)
+            cpu = {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                   "images_per_s": round(r["img_s"], 2), "sample": r["sample"]}
+        except Exception as ex:  # pragma: no cover
+            cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        rec = {
+            "metric": "JPEG decode GB/s (RGB out)", "value": round(value, 3), "unit": "GB/s",
+            "images_per_s": round(img_s, 1), "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8 in / f64 IDCT+colour / u8 out", "data": "synthetic",
+            "config": {"workload": CONFIG_NAMES[args.config], "images_per_gpu": n, "width": w, "height": h,
+                       "quality": q, "sampling": s, "subsequence_bits": args.sb,
+                       "compressed_bytes_per_gpu": comp_bytes, "rgb_bytes_per_gpu": rgb_bytes,
+                       "l2": "flushed between steps (256 MB write, untimed)"},
+            "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_tot / args.steps, 3),
+                    "path": "pjg_batch_create+upload+decode+download_all (pinned host in/out)"},
+            "roofline": {"bound": "hbm", "kernel": "k4_transform", "achieved": round(achieved, 1),
+                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_kind": peak_kind, "algorithmic_bytes": k4_bytes},
+            "stages_ms": {k: round(v, 4) for k, v in st_mean.items()},
+            "dominant_stage": dominant,
+            "sync": sync_stats,
+            "compressed_mb_per_s": round(world * comp_bytes / (ms_per_step / 1e3) / 1e6, 1),
+            "gpu_launches": 6 * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(rec), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    dec.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

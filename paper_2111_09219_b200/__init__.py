@@ -182,6 +182,9 @@ def lib():
                 getattr(L, fn).argtypes = [C.c_void_p]
             L.pjg_batch_synchronize.argtypes = [C.c_void_p, C.c_void_p]
             L.pjg_batch_download.argtypes = [C.c_void_p, C.POINTER(u8p), C.POINTER(C.c_size_t)]
+            L.pjg_batch_download_all.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+            L.pjg_batch_output_offset.argtypes = [C.c_void_p, C.c_size_t]
+            L.pjg_batch_output_offset.restype = C.c_uint64
             L.pjg_batch_info.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(_Info)]
             L.pjg_batch_device_output.argtypes = [C.c_void_p, C.c_size_t]
             L.pjg_batch_output_bytes.argtypes = [C.c_void_p]
@@ -208,7 +211,7 @@ EXPORTED_SYMBOLS = [
     "pjg_ctx_create", "pjg_ctx_destroy", "pjg_last_error", "pjg_status_name", "pjg_default_config",
     "pjg_ctx_stream", "pjg_inspect", "pjg_decode", "pjg_decode_batch", "pjg_batch_create",
     "pjg_batch_upload", "pjg_batch_decode", "pjg_batch_synchronize", "pjg_batch_download",
-    "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_output_bytes", "pjg_batch_stage_times",
+    "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_download_all", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
     "pjg_batch_sync_stats", "pjg_batch_destroy", "pjg_batch_dump_coefficients",
     "pjg_batch_dump_sync_states", "pjg_batch_dump_segment", "pjg_upsample_and_convert",
     "pjg_debug_huff_decode",
@@ -334,6 +337,13 @@ class Batch:
         caps = (C.c_size_t * self.n)(*[o.size for o in outs])
         self._check(lib().pjg_batch_download(self._h, ptrs, caps))
         return outs
+
+    def download_all(self, host_ptr: int, cap: int):
+        """One D2H of the whole batch output into host memory at host_ptr."""
+        self._check(lib().pjg_batch_download_all(self._h, C.c_void_p(host_ptr), cap))
+
+    def output_offset(self, i) -> int:
+        return int(lib().pjg_batch_output_offset(self._h, i))
 
     def stage_times(self) -> StageTimings:
         ms = (C.c_double * 7)()

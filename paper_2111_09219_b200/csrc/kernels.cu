@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "pjg_internal.h"
 
 namespace pjg {
@@ -897,185 +899,508 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
 }
 
 // ============================================ K4: IDCT + upsample + RGB ====
-// One CTA per tile of `mcus_per_tile` MCUs of one MCU row (<= 48 data units).
-//  1. load + dequantise coefficients into smem (int32, raster)
-//  2. IDCT: thread per (data unit, column y); exact FP64 in the reference's
-//     summation order; samples into per-component smem planes
-//  3. crop + chroma replication + FP64 YCbCr->RGB, stores to the output
-__global__ void __launch_bounds__(kK4Threads) k4_transform(Params P) {
-    __shared__ __align__(16) int32_t s_F[kK4MaxBlocks * 64];
-    __shared__ __align__(16) uint8_t s_pl[kK4MaxBlocks * 64];
-    __shared__ double s_basis[64];
-    __shared__ uint8_t s_rows[kK4MaxBlocks];
-    __shared__ uint16_t s_cmap[2][384];
-    __shared__ uint8_t s_rmap[2][16];
+// One CTA (384 threads) per tile of `mcus_per_tile` MCUs of one MCU row
+// (<= 48 data units, so one thread per (data unit, column)).
+//
+// Exactness strategy (reference transform.hpp:114-142, pipeline.hpp:190-197
+// are IEEE double):
+//  * IDCT: FP32 FMA separable sum with a rigorous per-block error bound
+//    |r32 - r64| <= 18.1 u S, S <= max|b|^2 * sum|F| (u = 2^-24).  A sample
+//    whose FP32 value lies farther than that bound from a rounding boundary
+//    (x.5) rounds identically to the reference double; the rest (~0.1-0.3%)
+//    are recomputed exactly in FP64 in the reference's summation order.
+//    Blocks whose coefficients are not exact in FP32 take the FP64 path.
+//  * Colour: Y is an integer, so lround(Y + t) = Y + round(t) unless t is an
+//    exact half-integer in real arithmetic (FP64 rounding then decides).
+//    round(t) is computed exactly in integers per chroma sample
+//    (1.402, 0.344136, 0.714136, 1.772 are decimal); exact ties are detected
+//    in integers and only those pixels are evaluated in FP64.
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float + kMagic rounds to an integer
+constexpr int kMagicBits = 0x4B400000;
 
-    const int tid = threadIdx.x;
-    const uint32_t t = blockIdx.x;
-    const uint32_t k = find_seg(P.tile_first, P.n_img, t);
-    if (P.ist[k].status != 0) return;
-    const ImgDesc& D = P.img[k];
-    const uint32_t lt = t - P.tile_first[k];
-    const uint32_t my = lt / D.tiles_x, tx = lt % D.tiles_x;
+__device__ __forceinline__ int round_div_away(int n, int d) {
+    return n >= 0 ? (n + d / 2) / d : -((-n + d / 2) / d);
+}
+
+// packed per-chroma-sample offsets: oR, oG, oB biased by 512 in 10-bit
+// fields, bit 30 = an exact real tie somewhere (FP64 replay needed)
+__device__ __forceinline__ uint32_t chroma_word(int Cb, int Cr) {
+    const int cb = Cb - 128, cr = Cr - 128;
+    const int nR = 1402 * cr, nB = 1772 * cb, nG = -(344136 * cb + 714136 * cr);
+    const bool tie = (abs(nR) % 1000 == 500) | (abs(nB) % 1000 == 500) | (abs(nG) % 1000000 == 500000);
+    const int oR = round_div_away(nR, 1000), oB = round_div_away(nB, 1000), oG = round_div_away(nG, 1000000);
+    return uint32_t(oR + 512) | (uint32_t(oG + 512) << 10) | (uint32_t(oB + 512) << 20) | (tie ? (1u << 30) : 0u);
+}
+
+__device__ __forceinline__ uint32_t pack4_sat(int a0, int a1, int a2, int a3) {
+    uint32_t t, d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(t) : "r"(a3), "r"(a2), "r"(0));
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a1), "r"(a0), "r"(t));
+    return d;
+}
+
+// exact FP64 replay of one sample (reference order, zero terms skipped):
+// walks the nonzero rows / coefficients of the data unit via bit masks.
+__device__ __noinline__ int idct_sample_fp64(const float* F, bool big, uint32_t rows, const uint8_t* nz,
+                                             const double* b64, int x, int y) {
+    const int32_t* Fi = reinterpret_cast<const int32_t*>(F);
+    double s = 0.0;
+    while (rows) {
+        const int u = __ffs(rows) - 1;
+        rows &= rows - 1;
+        uint32_t m = nz[u];
+        double t = 0.0;
+        while (m) {
+            const int v = __ffs(m) - 1;
+            m &= m - 1;
+            const double f = big ? double(Fi[u * 8 + v]) : double(F[u * 8 + v]);
+            t = __dadd_rn(t, __dmul_rn(b64[v * 8 + y], f));
+        }
+        s = __dadd_rn(s, __dmul_rn(b64[u * 8 + x], t));
+    }
+    return lround_away(s) + 128;
+}
+
+__device__ __noinline__ void rgb_fp64(int Y, int Cb, int Cr, int& R, int& G, int& B) {
+    const double Yd = double(Y);
+    const int cb = Cb - 128, cr = Cr - 128;
+    R = lround_away(__dadd_rn(Yd, __dmul_rn(1.402, double(cr))));
+    G = lround_away(__dsub_rn(__dsub_rn(Yd, __dmul_rn(0.344136, double(cb))), __dmul_rn(0.714136, double(cr))));
+    B = lround_away(__dadd_rn(Yd, __dmul_rn(1.772, double(cb))));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on an mbarrier (UBLKCP)
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Per-tile geometry, computed by one thread and shared through smem.
+struct TileInfo {
+    uint32_t k;  // image
+    uint32_t my, mx0, nm, nblk;
+    uint32_t valid;
+    uint64_t du0;
+    // plane geometry inside the tile (row stride padded by 4 bytes against bank conflicts)
+    uint32_t pw_t[3], pst[3], poff[3];
+    uint32_t X0, Y0, cols, rws;
+    uint32_t rgb;
+};
+
+// Tiles of one CTA are a contiguous range, so the image index only walks
+// forward; kend caches tile_first[kc + 1].
+__device__ __forceinline__ void tile_info(const Params& P, uint32_t t, uint32_t& kc, uint32_t& kend,
+                                          TileInfo& ti) {
+    while (t >= kend) {
+        ++kc;
+        kend = P.tile_first[kc + 1];
+    }
+    const ImgDesc& D = P.img[kc];
+    const uint32_t lt = t - P.tile_first[kc];
     const uint32_t MT = D.mcus_per_tile;
-    const uint32_t mx0 = tx * MT;
-    const uint32_t nm = min(MT, D.mcus_x - mx0);
-    const uint32_t dpm = D.dpm;
-    const uint32_t nblk = nm * dpm;
-    const uint64_t du0 = D.du_first + (uint64_t(my) * D.mcus_x + mx0) * dpm;
-
-    if (tid < 64) s_basis[tid] = P.basis[tid];
-    // 1. load 8 coefficients per 16-byte chunk, dequantise with the raster table
-    const int4* src = reinterpret_cast<const int4*>(P.coef + du0 * 64);
-    for (uint32_t ch = tid; ch < nblk * 8; ch += kK4Threads) {
-        const uint32_t blk = ch >> 3, slot = blk % dpm;
-        const uint32_t comp = uint32_t(D.du_comp >> (4 * slot)) & 15u;
-        const uint16_t* q = P.quant_raster + 64u * D.q_tab[comp] + (ch & 7) * 8;
-        int4 v = __ldcs(src + ch);
-        const int16_t* c16 = reinterpret_cast<const int16_t*>(&v);
-        int32_t* d = s_F + ch * 8;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) d[j] = int32_t(c16[j]) * int32_t(__ldg(q + j));
+    ti.k = kc;
+    ti.my = lt / D.tiles_x;
+    ti.mx0 = (lt % D.tiles_x) * MT;
+    ti.nm = min(MT, D.mcus_x - ti.mx0);
+    ti.nblk = ti.nm * D.dpm;
+    ti.du0 = D.du_first + (uint64_t(ti.my) * D.mcus_x + ti.mx0) * D.dpm;
+    ti.valid = P.ist[kc].status == 0;
+    uint32_t acc = 0;
+    for (uint32_t c = 0; c < 3; ++c) {
+        const bool has = c < D.ncomp;
+        ti.pw_t[c] = has ? MT * D.comp_h[c] * 8 : 0;
+        ti.pst[c] = ti.pw_t[c] + 4;
+        ti.poff[c] = acc;
+        acc += has ? ti.pst[c] * D.comp_v[c] * 8 : 0;
     }
-    __syncthreads();
-    if (tid < int(nblk)) {
-        uint32_t m = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int4* r = reinterpret_cast<const int4*>(s_F + tid * 64 + u * 8);
-            int4 a = r[0], b = r[1];
-            if ((a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w) != 0) m |= 1u << u;
-        }
-        s_rows[tid] = uint8_t(m);
-    }
-    // plane geometry inside the tile
-    uint32_t pw_t[3], poff[3];
-    {
-        uint32_t acc = 0;
-        for (uint32_t c = 0; c < 3; ++c) {
-            pw_t[c] = c < D.ncomp ? MT * D.comp_h[c] * 8 : 0;
-            poff[c] = acc;
-            acc += c < D.ncomp ? pw_t[c] * D.comp_v[c] * 8 : 0;
-        }
-    }
-    __syncthreads();
-    // 2. IDCT (transform.hpp:114-142): column pass tmp[u][y] = sum_v basis[v][y]*F[u][v],
-    // row pass out[x][y] = sum_u basis[u][x]*tmp[u][y], both ascending, zero terms skipped.
-    for (uint32_t it = tid; it < nblk * 8; it += kK4Threads) {
-        const uint32_t blk = it >> 3, y = it & 7;
-        const uint32_t rows = s_rows[blk];
-        const int32_t* F = s_F + blk * 64;
-        double tmp[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            double s = 0.0;
-            if (rows & (1u << u)) {
-#pragma unroll
-                for (int v = 0; v < 8; ++v) {
-                    int32_t f = F[u * 8 + v];
-                    if (f != 0) s = __dadd_rn(s, __dmul_rn(s_basis[v * 8 + y], double(f)));
-                }
-            }
-            tmp[u] = s;
-        }
-        const uint32_t slot = blk % dpm, m = blk / dpm;
-        const uint32_t comp = uint32_t(D.du_comp >> (4 * slot)) & 15u;
-        const uint32_t kk = uint32_t(D.du_kslot >> (4 * slot)) & 15u;
-        const uint32_t ch = D.comp_h[comp];
-        const uint32_t bx = kk % ch, by = kk / ch;
-        uint8_t* pl = s_pl + poff[comp] + (by * 8) * pw_t[comp] + (m * ch + bx) * 8 + y;
-#pragma unroll
-        for (int x = 0; x < 8; ++x) {
-            double s = 0.0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (rows & (1u << u)) s = __dadd_rn(s, __dmul_rn(s_basis[u * 8 + x], tmp[u]));
-            pl[x * pw_t[comp]] = uint8_t(clamp_u8(lround_away(s) + 128));
-        }
-    }
-    // 3. output
     const uint32_t mcu_w = 8 * D.h_max, mcu_h = 8 * D.v_max;
-    const uint32_t X0 = mx0 * mcu_w, Y0 = my * mcu_h;
-    const uint32_t W = D.width, H = D.height;
-    const uint32_t cols = min(nm * mcu_w, W - X0), rws = min(mcu_h, H - Y0);
-    const bool rgb = D.out_mode == 1 && D.ncomp == 3;
-    if (rgb) {
-        // chroma sample index maps (pipeline.hpp:182-187), tile-local
-        for (uint32_t c = 1; c < 3; ++c) {
-            const uint32_t pw = D.plane_w[c], ph = D.plane_h[c];
-            const uint32_t cx0 = mx0 * D.comp_h[c] * 8, cy0 = my * D.comp_v[c] * 8;
-            for (uint32_t x = tid; x < cols; x += kK4Threads) {
-                uint32_t sx = uint32_t(min64(uint64_t(X0 + x) * pw / W, pw - 1));
-                s_cmap[c - 1][x] = uint16_t(sx - cx0);
-            }
-            if (tid < int(rws)) {
-                uint32_t sy = uint32_t(min64(uint64_t(Y0 + tid) * ph / H, ph - 1));
-                s_rmap[c - 1][tid] = uint8_t(sy - cy0);
-            }
-        }
+    ti.X0 = ti.mx0 * mcu_w;
+    ti.Y0 = ti.my * mcu_h;
+    ti.cols = min(ti.nm * mcu_w, D.width - ti.X0);
+    ti.rws = min(mcu_h, D.height - ti.Y0);
+    ti.rgb = D.out_mode == 1 && D.ncomp == 3;
+}
+
+// packed offsets of one chroma sample: oR, oG, oB biased by 512 in 10-bit
+// fields; bit 30 flags an exact real tie (FP64 replay).  round(k*c) is taken
+// in integers on biased-positive values (divisions by constants).
+__device__ __forceinline__ uint32_t chroma_word2(uint32_t Cb, uint32_t Cr) {
+    const int cb = int(Cb) - 128, cr = int(Cr) - 128;
+    const uint32_t mR = uint32_t(1402 * cr + 500 + 200000);
+    const uint32_t mB = uint32_t(1772 * cb + 500 + 300000);
+    const uint32_t mG = uint32_t(-(344136 * cb + 714136 * cr) + 500000 + 200000000);
+    const uint32_t qR = mR / 1000u, qB = mB / 1000u, qG = mG / 1000000u;
+    const bool tie = (mB - qB * 1000u == 0) | (mG - qG * 1000000u == 0) | (mR - qR * 1000u == 0);
+    // oX + 512 = q - bias + 512
+    return (qR + 312u) | ((qG + 312u) << 10) | ((qB + 212u) << 20) | (tie ? (1u << 30) : 0u);
+}
+
+// one row of 4 pixels: Y bytes in y4, chroma words w0..w3
+__device__ __forceinline__ void emit_rgb4(uint8_t* dst, bool fast, uint32_t npx, uint32_t y4, const uint32_t w[4],
+                                          const uint8_t* cbrow, const uint8_t* crrow, const uint32_t cx[4]) {
+    int R[4], G[4], B[4];
+    uint32_t tie = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int Yv = int((y4 >> (8 * q)) & 0xFFu) - 512;
+        R[q] = Yv + int(w[q] & 1023u);
+        G[q] = Yv + int((w[q] >> 10) & 1023u);
+        B[q] = Yv + int((w[q] >> 20) & 1023u);
+        tie |= (w[q] >> 30) << q;
     }
-    __syncthreads();
-    if (rgb) {
-        // FP64 YCbCr->RGB exactly as pipeline.hpp:190-197
-        const uint32_t groups = (cols + 3) >> 2;
-        uint8_t* obase = P.out + D.out_off;
-        for (uint32_t it = tid; it < rws * groups; it += kK4Threads) {
-            const uint32_t r = it / groups, gx = (it % groups) * 4;
-            const uint32_t npx = min(4u, cols - gx);
-            uint32_t pk[3] = {0, 0, 0};
-            const uint8_t* yrow = s_pl + poff[0] + r * pw_t[0];
-            const uint8_t* cbrow = s_pl + poff[1] + s_rmap[0][r] * pw_t[1];
-            const uint8_t* crrow = s_pl + poff[2] + s_rmap[1][r] * pw_t[2];
-            uint8_t px[12];
+    if (tie) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (q < int(npx)) {
-                    const uint32_t x = gx + q;
-                    const double Yd = double(yrow[x]);
-                    const int cb = int(cbrow[s_cmap[0][x]]) - 128;
-                    const int cr = int(crrow[s_cmap[1][x]]) - 128;
-                    const int R = lround_away(__dadd_rn(Yd, __dmul_rn(1.402, double(cr))));
-                    const int G = lround_away(__dsub_rn(__dsub_rn(Yd, __dmul_rn(0.344136, double(cb))),
-                                                        __dmul_rn(0.714136, double(cr))));
-                    const int B = lround_away(__dadd_rn(Yd, __dmul_rn(1.772, double(cb))));
-                    px[3 * q + 0] = uint8_t(clamp_u8(R));
-                    px[3 * q + 1] = uint8_t(clamp_u8(G));
-                    px[3 * q + 2] = uint8_t(clamp_u8(B));
-                }
-            }
-            uint8_t* dst = obase + (uint64_t(Y0 + r) * W + X0 + gx) * 3;
-            if (npx == 4 && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
-#pragma unroll
-                for (int w = 0; w < 3; ++w)
-                    pk[w] = uint32_t(px[4 * w]) | (uint32_t(px[4 * w + 1]) << 8) |
-                            (uint32_t(px[4 * w + 2]) << 16) | (uint32_t(px[4 * w + 3]) << 24);
-                uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-                d32[0] = pk[0];
-                d32[1] = pk[1];
-                d32[2] = pk[2];
-            } else {
-                for (uint32_t q = 0; q < npx * 3; ++q) dst[q] = px[q];
-            }
-        }
+        for (int q = 0; q < 4; ++q)
+            if ((tie & (1u << q)) && q < int(npx))
+                rgb_fp64(int((y4 >> (8 * q)) & 0xFFu), cbrow[cx[q]], crrow[cx[q]], R[q], G[q], B[q]);
+    }
+    const uint32_t r4 = pack4_sat(R[0], R[1], R[2], R[3]);
+    const uint32_t g4 = pack4_sat(G[0], G[1], G[2], G[3]);
+    const uint32_t b4 = pack4_sat(B[0], B[1], B[2], B[3]);
+    const uint32_t t0 = __byte_perm(r4, g4, 0x5140);                            // R0 G0 R1 G1
+    const uint32_t t1 = __byte_perm(r4, g4, 0x7362);                            // R2 G2 R3 G3
+    const uint32_t o0 = __byte_perm(t0, b4, 0x2410);                            // R0 G0 B0 R1
+    const uint32_t o1 = __byte_perm(__byte_perm(t0, b4, 0x0053), t1, 0x5410);  // G1 B1 R2 G2
+    const uint32_t o2 = __byte_perm(t1, b4, 0x7326);                            // B2 R3 G3 B3
+    if (fast) {
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+        d32[0] = o0;
+        d32[1] = o1;
+        d32[2] = o2;
     } else {
-        // planes (extract_planes, transform.hpp:165-211) — or the Y plane only
-        // for grayscale output / single-component images
-        const uint32_t nplanes = (D.out_mode == 0) ? D.ncomp : 1;
-        uint64_t plane_base = D.out_off;
-        for (uint32_t c = 0; c < nplanes; ++c) {
-            const uint32_t pw = D.plane_w[c], ph = D.plane_h[c];
-            const uint32_t cx0 = mx0 * D.comp_h[c] * 8, cy0 = my * D.comp_v[c] * 8;
-            const uint32_t ccols = cx0 < pw ? min(pw_t[c] * nm / MT, pw - cx0) : 0;
-            const uint32_t crows = cy0 < ph ? min(D.comp_v[c] * 8, ph - cy0) : 0;
-            for (uint32_t it = tid; it < crows * ccols; it += kK4Threads) {
-                const uint32_t r = it / ccols, x = it % ccols;
-                P.out[plane_base + uint64_t(cy0 + r) * pw + cx0 + x] = s_pl[poff[c] + r * pw_t[c] + x];
-            }
-            plane_base += uint64_t(pw) * ph;
+        for (uint32_t q = 0; q < npx * 3; ++q) {
+            const uint32_t wq = q < 4 ? o0 : (q < 8 ? o1 : o2);
+            dst[q] = uint8_t(wq >> (8 * (q & 3)));
         }
     }
 }
 
+// Persistent: grid = min(#tiles, SMs x resident CTAs); each CTA walks tiles
+// blockIdx.x, +gridDim.x, ...; the next tile's coefficients are prefetched by
+// a TMA bulk copy into the other staging buffer while this tile computes.
+__global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
+    constexpr int NB = kK4MaxBlocks;
+    constexpr int kPlaneBytes = NB * 64 + 3 * 16 * 4;
+    // max_x |basis[u][x]| rounded up: weights of the rigorous FP32 error bound
+    constexpr float kW[8] = {0.35356f, 0.4904f, 0.46195f, 0.4904f, 0.35356f, 0.4904f, 0.46195f, 0.4904f};
+    __shared__ __align__(128) int16_t s_raw[2][NB * 64];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ TileInfo s_ti[2];
+    __shared__ ImgDesc s_desc[2];
+    __shared__ __align__(16) float s_F[NB * 64];  // float, or int32 bits when big
+    __shared__ __align__(16) uint8_t s_pl[kPlaneBytes];
+    __shared__ __align__(16) float s_b32[64];
+    __shared__ __align__(16) double s_b64[64];
+    __shared__ __align__(8) uint16_t s_cmap[192 + 4];
+    __shared__ uint8_t s_rmap[16];
+    __shared__ uint8_t s_rows[NB];
+    __shared__ uint8_t s_nz[NB * 8];
+    __shared__ uint8_t s_big[NB];
+    __shared__ float s_lim[NB];
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    // this CTA's contiguous tile range
+    const uint32_t t_begin = uint32_t(uint64_t(P.k4_tiles) * blockIdx.x / gridDim.x);
+    const uint32_t t_end = uint32_t(uint64_t(P.k4_tiles) * (blockIdx.x + 1) / gridDim.x);
+    __shared__ uint32_t s_desc_k[2];
+    uint32_t kc = 0, kend = 0;  // thread 0's cached image index and its tile end
+    if (tid < 64) {
+        const double b = P.basis[tid];
+        s_b64[tid] = b;
+        s_b32[tid] = float(b);
+    }
+    if (tid == 0 && t_begin < t_end) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // first image of the range: binary search once
+        uint32_t lo = 0, hi = P.n_img;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (P.tile_first[mid] <= t_begin) lo = mid; else hi = mid;
+        }
+        kc = lo;
+        kend = P.tile_first[kc + 1];
+        tile_info(P, t_begin, kc, kend, s_ti[0]);
+        s_desc[0] = P.img[s_ti[0].k];
+        s_desc_k[0] = s_ti[0].k;
+        s_desc_k[1] = 0xFFFFFFFFu;
+        const uint32_t bytes = s_ti[0].nblk * 128;
+        mbar_expect_tx(&s_bar[0], bytes);
+        tma_load(s_raw[0], P.coef + s_ti[0].du0 * 64, bytes, &s_bar[0]);
+    }
+    for (uint32_t it = 0;; ++it) {
+        const uint32_t t = t_begin + it;
+        if (t >= t_end) break;
+        const uint32_t cb = it & 1;
+        __syncthreads();  // previous tile done with every buffer; s_ti/s_desc[cb] ready
+        if (tid == 0) {
+            const uint32_t tn = t + 1;
+            if (tn < t_end) {
+                TileInfo ti;
+                tile_info(P, tn, kc, kend, ti);
+                s_ti[cb ^ 1] = ti;
+                if (s_desc_k[cb ^ 1] != ti.k) {
+                    s_desc[cb ^ 1] = P.img[ti.k];
+                    s_desc_k[cb ^ 1] = ti.k;
+                }
+                const uint32_t bytes = ti.nblk * 128;
+                mbar_expect_tx(&s_bar[cb ^ 1], bytes);
+                tma_load(s_raw[cb ^ 1], P.coef + ti.du0 * 64, bytes, &s_bar[cb ^ 1]);
+            }
+        }
+        const TileInfo& ti = s_ti[cb];
+        const ImgDesc& D = s_desc[cb];
+        mbar_wait(&s_bar[cb], (it >> 1) & 1);
+        if (!ti.valid) continue;
+        const uint32_t nblk = ti.nblk, dpm = D.dpm;
+
+        // 1. dequantise: thread (data unit, coefficient row); the 8 lanes of a
+        //    data unit reduce its row mask, "big" flag and the weighted sum
+        //    S = sum_uv w_u w_v |F_uv| that bounds the FP32 error.
+        {
+            const uint32_t ch = tid;  // NB * 8 == kK4Threads
+            const bool act = ch < nblk * 8;
+            const uint32_t u = ch & 7;
+            uint32_t m = 0;
+            float S = 0.f;
+            int32_t d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (act) {
+                const uint32_t blk = ch >> 3, slot = blk % dpm;
+                const uint32_t comp = uint32_t(D.du_comp >> (4 * slot)) & 15u;
+                const uint4 q4 =
+                    __ldg(reinterpret_cast<const uint4*>(P.quant_raster + 64u * D.q_tab[comp] + u * 8));
+                const int4 v = *reinterpret_cast<const int4*>(s_raw[cb] + ch * 8);
+                const int16_t* c16 = reinterpret_cast<const int16_t*>(&v);
+                const uint16_t* q16 = reinterpret_cast<const uint16_t*>(&q4);
+                uint32_t rm = 0, big = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    d[j] = int32_t(c16[j]) * int32_t(q16[j]);
+                    const uint32_t a = uint32_t(abs(d[j]));
+                    rm |= a ? (1u << j) : 0u;
+                    big |= a >= (1u << 22) ? 1u : 0u;
+                    S = fmaf(kW[j], float(min(a, 1u << 22)), S);
+                }
+                s_nz[ch] = uint8_t(rm);
+                S *= kW[u];
+                m = (rm ? (1u << u) : 0u) | (big << 8);
+            }
+            m |= __shfl_xor_sync(0xFFFFFFFFu, m, 1);
+            m |= __shfl_xor_sync(0xFFFFFFFFu, m, 2);
+            m |= __shfl_xor_sync(0xFFFFFFFFu, m, 4);
+            S += __shfl_xor_sync(0xFFFFFFFFu, S, 1);
+            S += __shfl_xor_sync(0xFFFFFFFFu, S, 2);
+            S += __shfl_xor_sync(0xFFFFFFFFu, S, 4);
+            // whole data unit exact-FP64 when F is not exact in float or the
+            // sample magnitude (<= S) could leave the magic-rounding range
+            const bool blk_big = (m & 0x100u) || S >= 2097152.f;
+            if (act) {
+                float* dst = s_F + ch * 8;
+                if (!blk_big) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) dst[j] = __int_as_float(d[j] + kMagicBits) - kMagic;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) dst[j] = __int_as_float(d[j]);
+                }
+                if (u == 0) {
+                    const uint32_t blk = ch >> 3;
+                    s_rows[blk] = uint8_t(m);
+                    s_big[blk] = blk_big ? 1 : 0;
+                    // |r32 - r64| <= 18u S (+ FP64's own ~1e-15 S), u = 2^-24
+                    s_lim[blk] = 0.5f - (1.1e-6f * S + 2.0e-6f);
+                }
+            }
+            // chroma index maps (pipeline.hpp:182-187), tile-local; Cb and Cr
+            // share geometry (both 1x1 sampled, parser.hpp:209-212)
+            if (ti.rgb) {
+                const uint32_t pw = D.plane_w[1], ph = D.plane_h[1], W = D.width, H = D.height;
+                const uint32_t cx0 = ti.mx0 * D.comp_h[1] * 8, cy0 = ti.my * D.comp_v[1] * 8;
+                for (uint32_t x = tid; x < ti.cols; x += kK4Threads)
+                    s_cmap[x] = uint16_t(min((ti.X0 + x) * pw / W, pw - 1) - cx0);
+                if (tid < int(ti.rws)) s_rmap[tid] = uint8_t(min((ti.Y0 + tid) * ph / H, ph - 1) - cy0);
+            }
+        }
+        __syncthreads();
+        // 2. IDCT (transform.hpp:114-142): thread (data unit, column y)
+        {
+            const uint32_t blk = tid >> 3, y = tid & 7;
+            const bool act = blk < nblk;
+            const uint32_t rows = act ? s_rows[blk] : 0u;
+            const uint32_t urows = __reduce_or_sync(0xFFFFFFFFu, rows);
+            const bool big = act && s_big[blk];
+            uint32_t out[8];
+            const float* F = s_F + (act ? blk : 0) * 64;
+            if (!big) {
+                float bcol[8];
+#pragma unroll
+                for (int v = 0; v < 8; ++v) bcol[v] = s_b32[v * 8 + y];
+                float acc[8];
+#pragma unroll
+                for (int x = 0; x < 8; ++x) acc[x] = 0.f;
+#pragma unroll
+                for (int uu = 0; uu < 8; ++uu) {
+                    if (urows & (1u << uu)) {
+                        const float4 f0 = *reinterpret_cast<const float4*>(F + uu * 8);
+                        const float4 f1 = *reinterpret_cast<const float4*>(F + uu * 8 + 4);
+                        float tu = bcol[0] * f0.x;
+                        tu = fmaf(bcol[1], f0.y, tu);
+                        tu = fmaf(bcol[2], f0.z, tu);
+                        tu = fmaf(bcol[3], f0.w, tu);
+                        tu = fmaf(bcol[4], f1.x, tu);
+                        tu = fmaf(bcol[5], f1.y, tu);
+                        tu = fmaf(bcol[6], f1.z, tu);
+                        tu = fmaf(bcol[7], f1.w, tu);
+                        const float4 b0 = *reinterpret_cast<const float4*>(s_b32 + uu * 8);
+                        const float4 b1 = *reinterpret_cast<const float4*>(s_b32 + uu * 8 + 4);
+                        acc[0] = fmaf(b0.x, tu, acc[0]);
+                        acc[1] = fmaf(b0.y, tu, acc[1]);
+                        acc[2] = fmaf(b0.z, tu, acc[2]);
+                        acc[3] = fmaf(b0.w, tu, acc[3]);
+                        acc[4] = fmaf(b1.x, tu, acc[4]);
+                        acc[5] = fmaf(b1.y, tu, acc[5]);
+                        acc[6] = fmaf(b1.z, tu, acc[6]);
+                        acc[7] = fmaf(b1.w, tu, acc[7]);
+                    }
+                }
+                const float lim = act ? s_lim[blk] : 0.5f;
+                uint32_t unsafe = 0;
+#pragma unroll
+                for (int x = 0; x < 8; ++x) {
+                    const float v = acc[x] + kMagic;
+                    const float dd = acc[x] - (v - kMagic);
+                    if (fabsf(dd) > lim) unsafe |= 1u << x;
+                    out[x] = uint32_t(__float_as_int(v) - kMagicBits + 128);
+                }
+                if (unsafe) {
+#pragma unroll
+                    for (int x = 0; x < 8; ++x)
+                        if (unsafe & (1u << x))
+                            out[x] = uint32_t(idct_sample_fp64(F, false, rows, s_nz + blk * 8, s_b64, x, int(y)));
+                }
+            } else {
+#pragma unroll
+                for (int x = 0; x < 8; ++x)
+                    out[x] = uint32_t(idct_sample_fp64(F, true, rows, s_nz + blk * 8, s_b64, x, int(y)));
+            }
+            if (act) {
+                const uint32_t slot = blk % dpm, mm = blk / dpm;
+                const uint32_t comp = uint32_t(D.du_comp >> (4 * slot)) & 15u;
+                const uint32_t kk = uint32_t(D.du_kslot >> (4 * slot)) & 15u;
+                const uint32_t chh = D.comp_h[comp];
+                const uint32_t bx = kk % chh, by = kk / chh;
+                const uint32_t ps = comp == 0 ? ti.pst[0] : (comp == 1 ? ti.pst[1] : ti.pst[2]);
+                const uint32_t po = comp == 0 ? ti.poff[0] : (comp == 1 ? ti.poff[1] : ti.poff[2]);
+                uint8_t* pl = s_pl + po + (by * 8) * ps + (mm * chh + bx) * 8 + y;
+                const uint32_t lo = pack4_sat(int(out[0]), int(out[1]), int(out[2]), int(out[3]));
+                const uint32_t hi = pack4_sat(int(out[4]), int(out[5]), int(out[6]), int(out[7]));
+#pragma unroll
+                for (int x = 0; x < 4; ++x) pl[x * ps] = uint8_t(lo >> (8 * x));
+#pragma unroll
+                for (int x = 0; x < 4; ++x) pl[(x + 4) * ps] = uint8_t(hi >> (8 * x));
+            }
+        }
+        __syncthreads();
+        // 3. output
+        const uint32_t cols = ti.cols, rws = ti.rws, W = D.width;
+        if (ti.rgb) {
+            // thread = 4 pixels of one row (or of a row pair sharing a chroma
+            // row for 4:2:0); chroma offsets computed inline per chroma sample
+            const bool pair = D.v_max == 2;
+            const uint32_t nrow = pair ? (rws + 1) >> 1 : rws;
+            const uint32_t groups = (cols + 3) >> 2;
+            const uint32_t gsh = 32 - __clz(max(groups, 1u) - 1);  // groups rounded up to 2^gsh
+            uint8_t* obase = P.out + D.out_off;
+            const bool aligned = ((W & 3) == 0) && ((D.out_off & 3) == 0);
+            const uint8_t* ybase = s_pl + ti.poff[0];
+            const uint8_t* cbbase = s_pl + ti.poff[1];
+            const uint8_t* crbase = s_pl + ti.poff[2];
+            const uint32_t pst0 = ti.pst[0], pst1 = ti.pst[1];
+            for (uint32_t itg = tid; itg < (nrow << gsh); itg += kK4Threads) {
+                const uint32_t j = itg >> gsh, gxi = itg & ((1u << gsh) - 1);
+                if (gxi >= groups) continue;
+                const uint32_t gx = gxi * 4;
+                const uint32_t npx = min(4u, cols - gx);
+                const uint2 cm = *reinterpret_cast<const uint2*>(s_cmap + gx);
+                const uint32_t cx[4] = {cm.x & 0xFFFFu, cm.x >> 16, cm.y & 0xFFFFu, cm.y >> 16};
+                const uint32_t r0 = pair ? 2 * j : j;
+                uint32_t crow = s_rmap[r0];
+                const uint8_t* cbrow = cbbase + crow * pst1;
+                const uint8_t* crrow = crbase + crow * pst1;
+                uint32_t w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t c = q < int(npx) ? cx[q] : cx[0];
+                    if (q > 0 && c == cx[q - 1])
+                        w[q] = w[q - 1];
+                    else
+                        w[q] = chroma_word2(cbrow[c], crrow[c]);
+                }
+                const bool fast = npx == 4 && aligned;
+                emit_rgb4(obase + (uint64_t(ti.Y0 + r0) * W + ti.X0 + gx) * 3, fast, npx,
+                          *reinterpret_cast<const uint32_t*>(ybase + r0 * pst0 + gx), w, cbrow, crrow, cx);
+                if (pair && r0 + 1 < rws) {
+                    const uint32_t crow1 = s_rmap[r0 + 1];
+                    if (crow1 != crow) {
+                        crow = crow1;
+                        cbrow = cbbase + crow * pst1;
+                        crrow = crbase + crow * pst1;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t c = q < int(npx) ? cx[q] : cx[0];
+                            if (q > 0 && c == cx[q - 1])
+                                w[q] = w[q - 1];
+                            else
+                                w[q] = chroma_word2(cbrow[c], crrow[c]);
+                        }
+                    }
+                    emit_rgb4(obase + (uint64_t(ti.Y0 + r0 + 1) * W + ti.X0 + gx) * 3, fast, npx,
+                              *reinterpret_cast<const uint32_t*>(ybase + (r0 + 1) * pst0 + gx), w, cbrow, crrow,
+                              cx);
+                }
+            }
+        } else {
+            // planes (extract_planes, transform.hpp:165-211) — or the Y plane
+            // only for grayscale output / single-component images
+            const uint32_t nplanes = (D.out_mode == 0) ? D.ncomp : 1;
+            const uint32_t MT = D.mcus_per_tile;
+            uint64_t plane_base = D.out_off;
+#pragma unroll
+            for (uint32_t c = 0; c < 3; ++c) {
+                if (c >= nplanes) break;
+                const uint32_t pw = D.plane_w[c], ph = D.plane_h[c];
+                const uint32_t cx0 = ti.mx0 * D.comp_h[c] * 8, cy0 = ti.my * D.comp_v[c] * 8;
+                const uint32_t ccols = cx0 < pw ? min(ti.pw_t[c] * ti.nm / MT, pw - cx0) : 0;
+                const uint32_t crows = cy0 < ph ? min(D.comp_v[c] * 8, ph - cy0) : 0;
+                for (uint32_t e = tid; e < crows * ccols; e += kK4Threads) {
+                    const uint32_t r = e / ccols, x = e % ccols;
+                    P.out[plane_base + uint64_t(cy0 + r) * pw + cx0 + x] = s_pl[ti.poff[c] + r * ti.pst[c] + x];
+                }
+                plane_base += uint64_t(pw) * ph;
+            }
+        }
+    }
+}
 
 // ============================== K5: colour stage of host-provided planes ====
 // upsample_and_convert (pipeline.hpp:167-201) for the standalone C-ABI call;
@@ -1128,7 +1453,17 @@ void launch_k3_write(const Params& p, void* stream) {
                    (cudaStream_t)stream>>>(p);
 }
 void launch_k4_transform(const Params& p, void* stream) {
-    if (p.k4_tiles) k4_transform<<<p.k4_tiles, kK4Threads, 0, (cudaStream_t)stream>>>(p);
+    if (!p.k4_tiles) return;
+    static int grid_cap = 0;
+    if (!grid_cap) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_transform, kK4Threads, 0);
+        grid_cap = std::max(1, sms * std::max(per_sm, 1));
+    }
+    const unsigned grid = unsigned(std::min<uint64_t>(p.k4_tiles, uint64_t(grid_cap)));
+    k4_transform<<<grid, kK4Threads, 0, (cudaStream_t)stream>>>(p);
 }
 
 }  // namespace pjg

@@ -663,6 +663,29 @@ int pjg_batch_download(pjg_batch* b, uint8_t* const* outs, const size_t* caps) {
     return PJG_OK;
 }
 
+int pjg_batch_download_all(pjg_batch* b, void* host, size_t cap) {
+    if (!b || !host) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    if (cap < b->out_bytes) return fail(ctx, PJG_CAPACITY, "output buffer too small");
+    if (!b->decoded) return fail(ctx, PJG_NOT_DECODED, "batch not decoded");
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CU(cudaEventRecord(ctx->ev[0], ctx->stream), "ev");
+    if (b->out_bytes)
+        CU(cudaMemcpyAsync(host, ctx->out.p, b->out_bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H out");
+    CU(cudaEventRecord(ctx->ev[1], ctx->stream), "ev");
+    int st = pjg_batch_synchronize(b, nullptr);
+    if (st) return st;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    b->stage_ms[PJG_STAGE_DOWNLOAD] = ms;
+    return PJG_OK;
+}
+
+uint64_t pjg_batch_output_offset(const pjg_batch* b, size_t i) {
+    if (!b || i >= b->n) return 0;
+    return b->desc[i].out_off;
+}
+
 int pjg_batch_info(const pjg_batch* b, size_t i, pjg_image_info* info) {
     if (!b || i >= b->n || !info) return PJG_INVALID_ARGUMENT;
     *info = b->info[i];

@@ -133,8 +133,8 @@ constexpr int kK0Tile = kK0Threads * kK0BytesPerThread;  // 4096 raw bytes per t
 constexpr int kK1Threads = 128;                          // subsequences per K1 CTA
 constexpr int kK2Threads = 256;
 constexpr int kK3Threads = 128;
-constexpr int kK4Threads = 256;
-constexpr int kK4MaxBlocks = 48;                         // data units per K4 tile
+constexpr int kK4Threads = 192;
+constexpr int kK4MaxBlocks = 24;                         // data units per K4 tile
 
 struct Params {
     // batch
