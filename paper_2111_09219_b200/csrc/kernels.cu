@@ -899,38 +899,30 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
 }
 
 // ============================================ K4: IDCT + upsample + RGB ====
-// One CTA (384 threads) per tile of `mcus_per_tile` MCUs of one MCU row
-// (<= 48 data units, so one thread per (data unit, column)).
+// Warp-independent persistent kernel: every warp owns a contiguous range of
+// tiles (one MCU-row segment 32 pixels wide: <= 12 data units) and runs the
+// whole pipeline for a tile with only __syncwarp — no CTA barriers, so the
+// ~24 resident warps per SM hide each other's latency.  The next tile's
+// coefficients are prefetched into registers (3 x 16 B per lane) while the
+// current tile computes.
 //
-// Exactness strategy (reference transform.hpp:114-142, pipeline.hpp:190-197
-// are IEEE double):
-//  * IDCT: FP32 FMA separable sum with a rigorous per-block error bound
-//    |r32 - r64| <= 18.1 u S, S <= max|b|^2 * sum|F| (u = 2^-24).  A sample
-//    whose FP32 value lies farther than that bound from a rounding boundary
-//    (x.5) rounds identically to the reference double; the rest (~0.1-0.3%)
-//    are recomputed exactly in FP64 in the reference's summation order.
-//    Blocks whose coefficients are not exact in FP32 take the FP64 path.
-//  * Colour: Y is an integer, so lround(Y + t) = Y + round(t) unless t is an
-//    exact half-integer in real arithmetic (FP64 rounding then decides).
-//    round(t) is computed exactly in integers per chroma sample
-//    (1.402, 0.344136, 0.714136, 1.772 are decimal); exact ties are detected
-//    in integers and only those pixels are evaluated in FP64.
-constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: float + kMagic rounds to an integer
+//  1. dequantise (reference transform.hpp:146-161, int32 coef * Q) into a
+//     warp-private smem tile; per data unit: row mask and the weighted sum
+//     S = sum_uv w_u w_v |F_uv|
+//  2. IDCT, lane = (data unit, column y).  FP32 FMA separable sum with the
+//     rigorous bound |r32 - r64| <= 18u S (u = 2^-24); samples within that
+//     bound of a rounding boundary (x.5) are replayed exactly in FP64 in the
+//     reference's order (transform.hpp:114-142); DC-only units use the
+//     reference's two products fl(b0 * fl(b0 * F00)) directly.
+//  3. crop + chroma replication (pipeline.hpp:182-187, exact index maps) +
+//     YCbCr->RGB: Y integer => lround(Y + t) = Y + round(t) unless t is an
+//     exact real half-integer; round(t) and the tie test are exact integer
+//     arithmetic on the decimal coefficients, ties are replayed in FP64
+//     (pipeline.hpp:190-197).  Packed 12-byte stores per 4 pixels.
+constexpr float kM128 = 12583040.0f;  // 1.5 * 2^23 + 128: round(acc) + 128 in the low mantissa bits
 constexpr int kMagicBits = 0x4B400000;
-
-__device__ __forceinline__ int round_div_away(int n, int d) {
-    return n >= 0 ? (n + d / 2) / d : -((-n + d / 2) / d);
-}
-
-// packed per-chroma-sample offsets: oR, oG, oB biased by 512 in 10-bit
-// fields, bit 30 = an exact real tie somewhere (FP64 replay needed)
-__device__ __forceinline__ uint32_t chroma_word(int Cb, int Cr) {
-    const int cb = Cb - 128, cr = Cr - 128;
-    const int nR = 1402 * cr, nB = 1772 * cb, nG = -(344136 * cb + 714136 * cr);
-    const bool tie = (abs(nR) % 1000 == 500) | (abs(nB) % 1000 == 500) | (abs(nG) % 1000000 == 500000);
-    const int oR = round_div_away(nR, 1000), oB = round_div_away(nB, 1000), oG = round_div_away(nG, 1000000);
-    return uint32_t(oR + 512) | (uint32_t(oG + 512) << 10) | (uint32_t(oB + 512) << 20) | (tie ? (1u << 30) : 0u);
-}
+constexpr int kK4Warps = kK4Threads / 32;
+constexpr int kTileW = 32;  // pixels per tile row
 
 __device__ __forceinline__ uint32_t pack4_sat(int a0, int a1, int a2, int a3) {
     uint32_t t, d;
@@ -939,143 +931,191 @@ __device__ __forceinline__ uint32_t pack4_sat(int a0, int a1, int a2, int a3) {
     return d;
 }
 
-// exact FP64 replay of one sample (reference order, zero terms skipped):
-// walks the nonzero rows / coefficients of the data unit via bit masks.
-__device__ __noinline__ int idct_sample_fp64(const float* F, bool big, uint32_t rows, const uint8_t* nz,
-                                             const double* b64, int x, int y) {
+// Exact FP64 replay of the samples of column y selected by `mask` (reference
+// order, zero terms skipped: transform.hpp:114-142).  The column pass
+// tmp[u][y] is shared by all selected rows.  Returns the 8 clamped samples
+// packed in two words (unselected bytes are unspecified).
+__device__ __noinline__ uint2 idct_column_fp64(const float* F, bool big, uint32_t rows, const double* b64, int y,
+                                               uint32_t mask) {
     const int32_t* Fi = reinterpret_cast<const int32_t*>(F);
-    double s = 0.0;
-    while (rows) {
-        const int u = __ffs(rows) - 1;
-        rows &= rows - 1;
-        uint32_t m = nz[u];
+    double tmp[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
         double t = 0.0;
-        while (m) {
-            const int v = __ffs(m) - 1;
-            m &= m - 1;
-            const double f = big ? double(Fi[u * 8 + v]) : double(F[u * 8 + v]);
-            t = __dadd_rn(t, __dmul_rn(b64[v * 8 + y], f));
+        if (rows & (1u << u)) {
+            for (int v = 0; v < 8; ++v) {
+                const double f = big ? double(Fi[u * 8 + v]) : double(F[u * 8 + v]);
+                if (f != 0.0) t = __dadd_rn(t, __dmul_rn(b64[v * 8 + y], f));
+            }
         }
-        s = __dadd_rn(s, __dmul_rn(b64[u * 8 + x], t));
+        tmp[u] = t;
     }
-    return lround_away(s) + 128;
+    int o[8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+        o[x] = 0;
+        if (mask & (1u << x)) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (rows & (1u << u)) sacc = __dadd_rn(sacc, __dmul_rn(b64[u * 8 + x], tmp[u]));
+            o[x] = lround_away(sacc) + 128;
+        }
+    }
+    return make_uint2(pack4_sat(o[0], o[1], o[2], o[3]), pack4_sat(o[4], o[5], o[6], o[7]));
 }
 
-__device__ __noinline__ void rgb_fp64(int Y, int Cb, int Cr, int& R, int& G, int& B) {
+// exact FP64 colour of one pixel (pipeline.hpp:190-197): returns R | G << 8 | B << 16
+__device__ __noinline__ uint32_t rgb_fp64(int Y, int Cb, int Cr) {
     const double Yd = double(Y);
     const int cb = Cb - 128, cr = Cr - 128;
-    R = lround_away(__dadd_rn(Yd, __dmul_rn(1.402, double(cr))));
-    G = lround_away(__dsub_rn(__dsub_rn(Yd, __dmul_rn(0.344136, double(cb))), __dmul_rn(0.714136, double(cr))));
-    B = lround_away(__dadd_rn(Yd, __dmul_rn(1.772, double(cb))));
+    const int R = lround_away(__dadd_rn(Yd, __dmul_rn(1.402, double(cr))));
+    const int G = lround_away(__dsub_rn(__dsub_rn(Yd, __dmul_rn(0.344136, double(cb))), __dmul_rn(0.714136, double(cr))));
+    const int B = lround_away(__dadd_rn(Yd, __dmul_rn(1.772, double(cb))));
+    return pack4_sat(R, G, B, 0);
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-            smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-// TMA bulk copy global -> shared, completion counted on an mbarrier (UBLKCP)
-__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
-// Per-tile geometry, computed by one thread and shared through smem.
-struct TileInfo {
-    uint32_t k;  // image
-    uint32_t my, mx0, nm, nblk;
-    uint32_t valid;
-    uint64_t du0;
-    // plane geometry inside the tile (row stride padded by 4 bytes against bank conflicts)
-    uint32_t pw_t[3], pst[3], poff[3];
-    uint32_t X0, Y0, cols, rws;
-    uint32_t rgb;
+// Per-warp image cache: layout of the tile's data units in the warp's sample
+// planes, quantisers, and the descriptor fields the tile loop needs.
+struct __align__(16) WarpImg {
+    uint16_t q[3][64];  // raster-order quantiser per component
+    uint32_t pst[3], poff[3];
+    uint16_t boff[kK4MaxBlocks];  // plane byte offset of the unit's (0,0) sample
+    uint16_t bps[kK4MaxBlocks];   // plane row stride
+    uint8_t bcomp[kK4MaxBlocks];
+    uint32_t width, height, ncomp, h_max, v_max, rgb, out_mode;
+    uint32_t pw1, ph1, ch1, cv1;
+    uint32_t plane_w[3], plane_h[3], comp_h[3], comp_v[3];
+    uint64_t out_off;
 };
 
-// Tiles of one CTA are a contiguous range, so the image index only walks
-// forward; kend caches tile_first[kc + 1].
-__device__ __forceinline__ void tile_info(const Params& P, uint32_t t, uint32_t& kc, uint32_t& kend,
-                                          TileInfo& ti) {
-    while (t >= kend) {
-        ++kc;
-        kend = P.tile_first[kc + 1];
+// Tile walker state (warp-uniform; lives in the warp's smem).
+struct TileWalk {
+    uint32_t k, kend, tiles_x, MT, mcus_x, dpm, mcu_w, mcu_h, valid, my, tx;
+    uint64_t du_first;
+};
+
+struct WarpSmem {
+    float F[kK4MaxBlocks * 64];  // dequantised (float, or int32 bits when big)
+    uint8_t pl[1024];            // sample planes (row stride padded by 4)
+    WarpImg img;
+    uint16_t cmap[kTileW];
+    uint8_t rmap[16];
+    uint16_t rows[kK4MaxBlocks];  // row mask | big << 8 | dc-only << 9
+    float lim[kK4MaxBlocks];
+    TileWalk w;
+};
+
+// Warp-cooperative cache fill (runs at image changes only).
+__device__ __forceinline__ void fill_warp_img(const Params& P, uint32_t k, WarpImg& c, int lane) {
+    const ImgDesc& D = P.img[k];
+    const uint32_t MT = D.mcus_per_tile, ncomp = D.ncomp, dpm = D.dpm;
+    uint32_t pst[3], poff[3], acc = 0;
+#pragma unroll
+    for (uint32_t cc = 0; cc < 3; ++cc) {
+        const bool has = cc < ncomp;
+        pst[cc] = has ? MT * D.comp_h[cc] * 8 + 4 : 0;
+        poff[cc] = acc;
+        acc += has ? pst[cc] * D.comp_v[cc] * 8 : 0;
     }
-    const ImgDesc& D = P.img[kc];
-    const uint32_t lt = t - P.tile_first[kc];
-    const uint32_t MT = D.mcus_per_tile;
-    ti.k = kc;
-    ti.my = lt / D.tiles_x;
-    ti.mx0 = (lt % D.tiles_x) * MT;
-    ti.nm = min(MT, D.mcus_x - ti.mx0);
-    ti.nblk = ti.nm * D.dpm;
-    ti.du0 = D.du_first + (uint64_t(ti.my) * D.mcus_x + ti.mx0) * D.dpm;
-    ti.valid = P.ist[kc].status == 0;
-    uint32_t acc = 0;
-    for (uint32_t c = 0; c < 3; ++c) {
-        const bool has = c < D.ncomp;
-        ti.pw_t[c] = has ? MT * D.comp_h[c] * 8 : 0;
-        ti.pst[c] = ti.pw_t[c] + 4;
-        ti.poff[c] = acc;
-        acc += has ? ti.pst[c] * D.comp_v[c] * 8 : 0;
+    if (lane < 24) {  // 3 quantisers x 8 x 16 B
+        const uint32_t cc = lane >> 3;
+        if (cc < ncomp)
+            reinterpret_cast<uint4*>(c.q[cc])[lane & 7] =
+                __ldg(reinterpret_cast<const uint4*>(P.quant_raster + 64u * D.q_tab[cc]) + (lane & 7));
     }
-    const uint32_t mcu_w = 8 * D.h_max, mcu_h = 8 * D.v_max;
-    ti.X0 = ti.mx0 * mcu_w;
-    ti.Y0 = ti.my * mcu_h;
-    ti.cols = min(ti.nm * mcu_w, D.width - ti.X0);
-    ti.rws = min(mcu_h, D.height - ti.Y0);
-    ti.rgb = D.out_mode == 1 && D.ncomp == 3;
+    if (lane < int(MT * dpm) && lane < kK4MaxBlocks) {
+        const uint32_t blk = lane, slot = blk % dpm, m = blk / dpm;
+        const uint32_t comp = uint32_t(D.du_comp >> (4 * slot)) & 15u;
+        const uint32_t kk = uint32_t(D.du_kslot >> (4 * slot)) & 15u;
+        const uint32_t chh = D.comp_h[comp];
+        const uint32_t bx = kk % chh, by = kk / chh;
+        c.bcomp[blk] = uint8_t(comp);
+        c.bps[blk] = uint16_t(pst[comp]);
+        c.boff[blk] = uint16_t(poff[comp] + (by * 8) * pst[comp] + (m * chh + bx) * 8);
+    }
+    if (lane == 0) {
+        for (int cc = 0; cc < 3; ++cc) {
+            c.pst[cc] = pst[cc];
+            c.poff[cc] = poff[cc];
+            c.plane_w[cc] = D.plane_w[cc];
+            c.plane_h[cc] = D.plane_h[cc];
+            c.comp_h[cc] = D.comp_h[cc];
+            c.comp_v[cc] = D.comp_v[cc];
+        }
+        c.width = D.width;
+        c.height = D.height;
+        c.ncomp = ncomp;
+        c.h_max = D.h_max;
+        c.v_max = D.v_max;
+        c.out_mode = D.out_mode;
+        c.rgb = D.out_mode == 1 && ncomp == 3;
+        c.pw1 = D.plane_w[1];
+        c.ph1 = D.plane_h[1];
+        c.ch1 = D.comp_h[1];
+        c.cv1 = D.comp_v[1];
+        c.out_off = D.out_off;
+    }
+    __syncwarp();
 }
 
-// packed offsets of one chroma sample: oR, oG, oB biased by 512 in 10-bit
-// fields; bit 30 flags an exact real tie (FP64 replay).  round(k*c) is taken
-// in integers on biased-positive values (divisions by constants).
-__device__ __forceinline__ uint32_t chroma_word2(uint32_t Cb, uint32_t Cr) {
-    const int cb = int(Cb) - 128, cr = int(Cr) - 128;
-    const uint32_t mR = uint32_t(1402 * cr + 500 + 200000);
-    const uint32_t mB = uint32_t(1772 * cb + 500 + 300000);
-    const uint32_t mG = uint32_t(-(344136 * cb + 714136 * cr) + 500000 + 200000000);
-    const uint32_t qR = mR / 1000u, qB = mB / 1000u, qG = mG / 1000000u;
-    const bool tie = (mB - qB * 1000u == 0) | (mG - qG * 1000000u == 0) | (mR - qR * 1000u == 0);
-    // oX + 512 = q - bias + 512
-    return (qR + 312u) | ((qG + 312u) << 10) | ((qB + 212u) << 20) | (tie ? (1u << 30) : 0u);
+__device__ __forceinline__ void walk_enter_image(const Params& P, uint32_t t, TileWalk& w) {
+    while (P.tile_first[w.k + 1] <= t) ++w.k;
+    const ImgDesc& D = P.img[w.k];
+    w.kend = P.tile_first[w.k + 1];
+    w.tiles_x = D.tiles_x;
+    w.MT = D.mcus_per_tile;
+    w.mcus_x = D.mcus_x;
+    w.dpm = D.dpm;
+    w.mcu_w = 8 * D.h_max;
+    w.mcu_h = 8 * D.v_max;
+    w.du_first = D.du_first;
+    w.valid = P.ist[w.k].status == 0;
+    const uint32_t lt = t - P.tile_first[w.k];
+    w.my = lt / w.tiles_x;
+    w.tx = lt % w.tiles_x;
 }
 
-// one row of 4 pixels: Y bytes in y4, chroma words w0..w3
-__device__ __forceinline__ void emit_rgb4(uint8_t* dst, bool fast, uint32_t npx, uint32_t y4, const uint32_t w[4],
-                                          const uint8_t* cbrow, const uint8_t* crrow, const uint32_t cx[4]) {
-    int R[4], G[4], B[4];
-    uint32_t tie = 0;
+// colour LUT entries per chroma value (exact integers; see chroma_word)
+struct ColourLut {
+    uint32_t rb[256];   // (oR + 512) | tieR << 30 indexed by Cr  — and (oB + 512) << 20 | tieB << 30 by Cb
+    uint32_t bb[256];
+    int32_t ga[256];    // -344136 * cb + 500000 + 2e8
+    int32_t gb[256];    // -714136 * cr
+};
+
+__device__ __forceinline__ uint32_t chroma_word_lut(const ColourLut& L, uint32_t Cb, uint32_t Cr) {
+    const uint32_t mG = uint32_t(L.ga[Cb] + L.gb[Cr]);
+    const uint32_t qG = mG / 1000000u;
+    const uint32_t tieG = (mG - qG * 1000000u) == 0 ? (1u << 30) : 0u;
+    return L.rb[Cr] | L.bb[Cb] | ((qG + 312u) << 10) | tieG;
+}
+
+__device__ __forceinline__ void emit_rgb4(uint8_t* dst, bool fast, uint32_t npx, uint32_t y4, uint32_t w0,
+                                          uint32_t w1, uint32_t w2, uint32_t w3, const uint8_t* cbrow,
+                                          const uint8_t* crrow, uint32_t cx0, uint32_t cx1, uint32_t cx2,
+                                          uint32_t cx3) {
+    const int Y0 = int(y4 & 0xFFu) - 512, Y1 = int((y4 >> 8) & 0xFFu) - 512, Y2 = int((y4 >> 16) & 0xFFu) - 512,
+              Y3 = int(y4 >> 24) - 512;
+    uint32_t r4 = pack4_sat(Y0 + int(w0 & 1023u), Y1 + int(w1 & 1023u), Y2 + int(w2 & 1023u), Y3 + int(w3 & 1023u));
+    uint32_t g4 = pack4_sat(Y0 + int((w0 >> 10) & 1023u), Y1 + int((w1 >> 10) & 1023u),
+                            Y2 + int((w2 >> 10) & 1023u), Y3 + int((w3 >> 10) & 1023u));
+    uint32_t b4 = pack4_sat(Y0 + int((w0 >> 20) & 1023u), Y1 + int((w1 >> 20) & 1023u),
+                            Y2 + int((w2 >> 20) & 1023u), Y3 + int((w3 >> 20) & 1023u));
+    const uint32_t tie = ((w0 | w1 | w2 | w3) >> 30) & 1u;
+    if (tie) {  // exact real tie in some chroma sample: replay those pixels in FP64
+        const uint32_t ws[4] = {w0, w1, w2, w3}, cx[4] = {cx0, cx1, cx2, cx3};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int Yv = int((y4 >> (8 * q)) & 0xFFu) - 512;
-        R[q] = Yv + int(w[q] & 1023u);
-        G[q] = Yv + int((w[q] >> 10) & 1023u);
-        B[q] = Yv + int((w[q] >> 20) & 1023u);
-        tie |= (w[q] >> 30) << q;
+        for (int q = 0; q < 4; ++q) {
+            if ((ws[q] >> 30) & 1u) {
+                const uint32_t e = rgb_fp64(int((y4 >> (8 * q)) & 0xFFu), cbrow[cx[q]], crrow[cx[q]]);
+                const uint32_t sh = 8 * q, m = ~(0xFFu << sh);
+                r4 = (r4 & m) | ((e & 0xFFu) << sh);
+                g4 = (g4 & m) | (((e >> 8) & 0xFFu) << sh);
+                b4 = (b4 & m) | (((e >> 16) & 0xFFu) << sh);
+            }
+        }
     }
-    if (tie) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            if ((tie & (1u << q)) && q < int(npx))
-                rgb_fp64(int((y4 >> (8 * q)) & 0xFFu), cbrow[cx[q]], crrow[cx[q]], R[q], G[q], B[q]);
-    }
-    const uint32_t r4 = pack4_sat(R[0], R[1], R[2], R[3]);
-    const uint32_t g4 = pack4_sat(G[0], G[1], G[2], G[3]);
-    const uint32_t b4 = pack4_sat(B[0], B[1], B[2], B[3]);
     const uint32_t t0 = __byte_perm(r4, g4, 0x5140);                            // R0 G0 R1 G1
     const uint32_t t1 = __byte_perm(r4, g4, 0x7362);                            // R2 G2 R3 G3
     const uint32_t o0 = __byte_perm(t0, b4, 0x2410);                            // R0 G0 B0 R1
@@ -1094,311 +1134,328 @@ __device__ __forceinline__ void emit_rgb4(uint8_t* dst, bool fast, uint32_t npx,
     }
 }
 
-// Persistent: grid = min(#tiles, SMs x resident CTAs); each CTA walks tiles
-// blockIdx.x, +gridDim.x, ...; the next tile's coefficients are prefetched by
-// a TMA bulk copy into the other staging buffer while this tile computes.
 __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
-    constexpr int NB = kK4MaxBlocks;
-    constexpr int kPlaneBytes = NB * 64 + 3 * 16 * 4;
-    // max_x |basis[u][x]| rounded up: weights of the rigorous FP32 error bound
-    constexpr float kW[8] = {0.35356f, 0.4904f, 0.46195f, 0.4904f, 0.35356f, 0.4904f, 0.46195f, 0.4904f};
-    __shared__ __align__(128) int16_t s_raw[2][NB * 64];
-    __shared__ __align__(8) uint64_t s_bar[2];
-    __shared__ TileInfo s_ti[2];
-    __shared__ ImgDesc s_desc[2];
-    __shared__ __align__(16) float s_F[NB * 64];  // float, or int32 bits when big
-    __shared__ __align__(16) uint8_t s_pl[kPlaneBytes];
-    __shared__ __align__(16) float s_b32[64];
+    __shared__ __align__(16) WarpSmem s_w[kK4Warps];
+    __shared__ __align__(16) float s_b32[64];   // basis[u][x]
+    __shared__ __align__(16) float s_b32T[64];  // basis[v][y] at [y*8+v]
     __shared__ __align__(16) double s_b64[64];
-    __shared__ __align__(8) uint16_t s_cmap[192 + 4];
-    __shared__ uint8_t s_rmap[16];
-    __shared__ uint8_t s_rows[NB];
-    __shared__ uint8_t s_nz[NB * 8];
-    __shared__ uint8_t s_big[NB];
-    __shared__ float s_lim[NB];
+    __shared__ __align__(16) ColourLut s_lut;
 
-    const int tid = threadIdx.x, lane = tid & 31;
-    // this CTA's contiguous tile range
-    const uint32_t t_begin = uint32_t(uint64_t(P.k4_tiles) * blockIdx.x / gridDim.x);
-    const uint32_t t_end = uint32_t(uint64_t(P.k4_tiles) * (blockIdx.x + 1) / gridDim.x);
-    __shared__ uint32_t s_desc_k[2];
-    uint32_t kc = 0, kend = 0;  // thread 0's cached image index and its tile end
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 64) {
         const double b = P.basis[tid];
         s_b64[tid] = b;
         s_b32[tid] = float(b);
+        s_b32T[(tid & 7) * 8 + (tid >> 3)] = float(b);
     }
-    if (tid == 0 && t_begin < t_end) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        // first image of the range: binary search once
+    for (int c = tid; c < 256; c += kK4Threads) {
+        const int v = c - 128;
+        const uint32_t mR = uint32_t(1402 * v + 500 + 200000), mB = uint32_t(1772 * v + 500 + 300000);
+        const uint32_t qR = mR / 1000u, qB = mB / 1000u;
+        s_lut.rb[c] = (qR + 312u) | ((mR - qR * 1000u) == 0 ? (1u << 30) : 0u);
+        s_lut.bb[c] = ((qB + 212u) << 20) | ((mB - qB * 1000u) == 0 ? (1u << 30) : 0u);
+        s_lut.ga[c] = -344136 * v + 500000 + 200000000;
+        s_lut.gb[c] = -714136 * v;
+    }
+    __syncthreads();
+
+    WarpSmem& S = s_w[warp];
+    const uint32_t gw = blockIdx.x * kK4Warps + warp, nw = gridDim.x * kK4Warps;
+    const uint32_t t_begin = uint32_t(uint64_t(P.k4_tiles) * gw / nw);
+    const uint32_t t_end = uint32_t(uint64_t(P.k4_tiles) * (gw + 1) / nw);
+    if (t_begin >= t_end) return;
+
+    TileWalk& w = S.w;
+    if (lane == 0) {
         uint32_t lo = 0, hi = P.n_img;
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
-            if (P.tile_first[mid] <= t_begin) lo = mid; else hi = mid;
+            if (P.tile_first[mid] <= t_begin)
+                lo = mid;
+            else
+                hi = mid;
         }
-        kc = lo;
-        kend = P.tile_first[kc + 1];
-        tile_info(P, t_begin, kc, kend, s_ti[0]);
-        s_desc[0] = P.img[s_ti[0].k];
-        s_desc_k[0] = s_ti[0].k;
-        s_desc_k[1] = 0xFFFFFFFFu;
-        const uint32_t bytes = s_ti[0].nblk * 128;
-        mbar_expect_tx(&s_bar[0], bytes);
-        tma_load(s_raw[0], P.coef + s_ti[0].du0 * 64, bytes, &s_bar[0]);
+        w.k = lo;
+        walk_enter_image(P, t_begin, w);
     }
-    for (uint32_t it = 0;; ++it) {
-        const uint32_t t = t_begin + it;
-        if (t >= t_end) break;
-        const uint32_t cb = it & 1;
-        __syncthreads();  // previous tile done with every buffer; s_ti/s_desc[cb] ready
-        if (tid == 0) {
-            const uint32_t tn = t + 1;
-            if (tn < t_end) {
-                TileInfo ti;
-                tile_info(P, tn, kc, kend, ti);
-                s_ti[cb ^ 1] = ti;
-                if (s_desc_k[cb ^ 1] != ti.k) {
-                    s_desc[cb ^ 1] = P.img[ti.k];
-                    s_desc_k[cb ^ 1] = ti.k;
-                }
-                const uint32_t bytes = ti.nblk * 128;
-                mbar_expect_tx(&s_bar[cb ^ 1], bytes);
-                tma_load(s_raw[cb ^ 1], P.coef + ti.du0 * 64, bytes, &s_bar[cb ^ 1]);
+    __syncwarp();
+    uint32_t cached_k = 0xFFFFFFFFu;
+    // prefetch of the current tile: 3 x 16 B per lane (rows lane, lane+32, lane+64
+    // of the tile's units), issued one tile ahead
+    uint4 pf[3];
+    auto issue = [&](const TileWalk& tw) {
+        const uint32_t mx0 = tw.tx * tw.MT;
+        const uint32_t nblk = min(tw.MT, tw.mcus_x - mx0) * tw.dpm;
+        const int4* src = reinterpret_cast<const int4*>(
+            P.coef + (tw.du_first + (uint64_t(tw.my) * tw.mcus_x + mx0) * tw.dpm) * 64);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const uint32_t ch = lane + 32 * j;
+            pf[j] = make_uint4(0, 0, 0, 0);
+            if (tw.valid && ch < nblk * 8) {
+                const int4 v = __ldcs(src + ch);
+                pf[j] = make_uint4(uint32_t(v.x), uint32_t(v.y), uint32_t(v.z), uint32_t(v.w));
             }
         }
-        const TileInfo& ti = s_ti[cb];
-        const ImgDesc& D = s_desc[cb];
-        mbar_wait(&s_bar[cb], (it >> 1) & 1);
-        if (!ti.valid) continue;
-        const uint32_t nblk = ti.nblk, dpm = D.dpm;
+    };
+    issue(w);
+    for (uint32_t t = t_begin; t < t_end; ++t) {
+        const uint32_t cur_k = w.k, cur_my = w.my, cur_mx0 = w.tx * w.MT;
+        const uint32_t cur_nm = min(w.MT, w.mcus_x - cur_mx0);
+        const uint32_t cur_valid = w.valid, cur_mcuw = w.mcu_w, cur_mcuh = w.mcu_h;
+        const uint32_t nblk = cur_nm * w.dpm;
+        if (cur_valid && cached_k != cur_k) {
+            __syncwarp();
+            fill_warp_img(P, cur_k, S.img, lane);
+            cached_k = cur_k;
+        }
+        const WarpImg& I = S.img;
 
-        // 1. dequantise: thread (data unit, coefficient row); the 8 lanes of a
-        //    data unit reduce its row mask, "big" flag and the weighted sum
-        //    S = sum_uv w_u w_v |F_uv| that bounds the FP32 error.
-        {
-            const uint32_t ch = tid;  // NB * 8 == kK4Threads
+        // 1. dequantise the prefetched rows
+        if (cur_valid) {
+#pragma unroll 1
+        for (int j = 0; j < 3; ++j) {
+            const uint32_t ch = lane + 32 * j, blk = ch >> 3, u = ch & 7;
             const bool act = ch < nblk * 8;
-            const uint32_t u = ch & 7;
-            uint32_t m = 0;
-            float S = 0.f;
+            uint32_t m = 0, asum = 0;
             int32_t d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             if (act) {
-                const uint32_t blk = ch >> 3, slot = blk % dpm;
-                const uint32_t comp = uint32_t(D.du_comp >> (4 * slot)) & 15u;
-                const uint4 q4 =
-                    __ldg(reinterpret_cast<const uint4*>(P.quant_raster + 64u * D.q_tab[comp] + u * 8));
-                const int4 v = *reinterpret_cast<const int4*>(s_raw[cb] + ch * 8);
-                const int16_t* c16 = reinterpret_cast<const int16_t*>(&v);
-                const uint16_t* q16 = reinterpret_cast<const uint16_t*>(&q4);
-                uint32_t rm = 0, big = 0;
+                const uint4 rv = j == 0 ? pf[0] : (j == 1 ? pf[1] : pf[2]);
+                const uint4 qv = *reinterpret_cast<const uint4*>(I.q[I.bcomp[blk]] + u * 8);
+                const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
+                uint32_t ror = 0, aor = 0;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    d[j] = int32_t(c16[j]) * int32_t(q16[j]);
-                    const uint32_t a = uint32_t(abs(d[j]));
-                    rm |= a ? (1u << j) : 0u;
-                    big |= a >= (1u << 22) ? 1u : 0u;
-                    S = fmaf(kW[j], float(min(a, 1u << 22)), S);
+                for (int e = 0; e < 4; ++e) {
+                    d[2 * e] = int32_t(int16_t(rw[e] & 0xFFFFu)) * int32_t(qw[e] & 0xFFFFu);
+                    d[2 * e + 1] = (int32_t(rw[e]) >> 16) * int32_t(qw[e] >> 16);
+                    ror |= rw[e];
+                    const uint32_t a0 = uint32_t(abs(d[2 * e])), a1 = uint32_t(abs(d[2 * e + 1]));
+                    aor |= a0 | a1;
+                    asum += a0 + a1;  // cannot wrap unless some |d| >= 2^22 (then big)
                 }
-                s_nz[ch] = uint8_t(rm);
-                S *= kW[u];
-                m = (rm ? (1u << u) : 0u) | (big << 8);
+                // row mask bit, big flag, and (row 0 only) "a v > 0 coefficient"
+                m = (ror ? (1u << u) : 0u) | (aor >= (1u << 22) ? 0x100u : 0u) |
+                    ((u == 0 && ((rv.x >> 16) | rv.y | rv.z | rv.w) != 0u) ? 0x400u : 0u);
             }
+            const float wu = (u & 3) == 0 ? 0.35356f : ((u & 3) == 2 ? 0.46195f : 0.4904f);
+            float Ssum = float(asum) * (wu * 0.4904f);
             m |= __shfl_xor_sync(0xFFFFFFFFu, m, 1);
             m |= __shfl_xor_sync(0xFFFFFFFFu, m, 2);
             m |= __shfl_xor_sync(0xFFFFFFFFu, m, 4);
-            S += __shfl_xor_sync(0xFFFFFFFFu, S, 1);
-            S += __shfl_xor_sync(0xFFFFFFFFu, S, 2);
-            S += __shfl_xor_sync(0xFFFFFFFFu, S, 4);
-            // whole data unit exact-FP64 when F is not exact in float or the
-            // sample magnitude (<= S) could leave the magic-rounding range
-            const bool blk_big = (m & 0x100u) || S >= 2097152.f;
+            Ssum += __shfl_xor_sync(0xFFFFFFFFu, Ssum, 1);
+            Ssum += __shfl_xor_sync(0xFFFFFFFFu, Ssum, 2);
+            Ssum += __shfl_xor_sync(0xFFFFFFFFu, Ssum, 4);
+            const bool big = (m & 0x100u) || Ssum >= 2097152.f;
             if (act) {
-                float* dst = s_F + ch * 8;
-                if (!blk_big) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) dst[j] = __int_as_float(d[j] + kMagicBits) - kMagic;
+                float4* dst = reinterpret_cast<float4*>(S.F + ch * 8);
+                if (!big) {
+                    dst[0] = make_float4(float(d[0]), float(d[1]), float(d[2]), float(d[3]));
+                    dst[1] = make_float4(float(d[4]), float(d[5]), float(d[6]), float(d[7]));
                 } else {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) dst[j] = __int_as_float(d[j]);
+                    dst[0] = make_float4(__int_as_float(d[0]), __int_as_float(d[1]), __int_as_float(d[2]),
+                                         __int_as_float(d[3]));
+                    dst[1] = make_float4(__int_as_float(d[4]), __int_as_float(d[5]), __int_as_float(d[6]),
+                                         __int_as_float(d[7]));
                 }
                 if (u == 0) {
-                    const uint32_t blk = ch >> 3;
-                    s_rows[blk] = uint8_t(m);
-                    s_big[blk] = blk_big ? 1 : 0;
+                    const bool dconly = (m & 0xFEu) == 0 && !(m & 0x400u);
+                    S.rows[blk] = uint16_t((m & 0xFFu) | (big ? 0x100u : 0u) | (dconly ? 0x200u : 0u));
                     // |r32 - r64| <= 18u S (+ FP64's own ~1e-15 S), u = 2^-24
-                    s_lim[blk] = 0.5f - (1.1e-6f * S + 2.0e-6f);
+                    S.lim[blk] = 0.5f - (1.1e-6f * Ssum + 2.0e-6f);
                 }
             }
-            // chroma index maps (pipeline.hpp:182-187), tile-local; Cb and Cr
-            // share geometry (both 1x1 sampled, parser.hpp:209-212)
-            if (ti.rgb) {
-                const uint32_t pw = D.plane_w[1], ph = D.plane_h[1], W = D.width, H = D.height;
-                const uint32_t cx0 = ti.mx0 * D.comp_h[1] * 8, cy0 = ti.my * D.comp_v[1] * 8;
-                for (uint32_t x = tid; x < ti.cols; x += kK4Threads)
-                    s_cmap[x] = uint16_t(min((ti.X0 + x) * pw / W, pw - 1) - cx0);
-                if (tid < int(ti.rws)) s_rmap[tid] = uint8_t(min((ti.Y0 + tid) * ph / H, ph - 1) - cy0);
-            }
         }
-        __syncthreads();
-        // 2. IDCT (transform.hpp:114-142): thread (data unit, column y)
-        {
-            const uint32_t blk = tid >> 3, y = tid & 7;
+        }
+        // advance the walk and prefetch the next tile (in flight during 2 + 3)
+        if (t + 1 < t_end) {
+            __syncwarp();
+            if (lane == 0) {
+                if (++w.tx == w.tiles_x) {
+                    w.tx = 0;
+                    ++w.my;
+                }
+                if (t + 1 >= w.kend) {
+                    ++w.k;
+                    walk_enter_image(P, t + 1, w);
+                }
+            }
+            __syncwarp();
+            issue(w);
+        }
+        if (!cur_valid) continue;
+        // chroma index maps (pipeline.hpp:182-187), tile-local
+        const uint32_t X0 = cur_mx0 * cur_mcuw, Y0 = cur_my * cur_mcuh;
+        const uint32_t cols = min(cur_nm * cur_mcuw, I.width - X0), rws = min(cur_mcuh, I.height - Y0);
+        if (I.rgb) {
+            const uint32_t cx0 = cur_mx0 * I.ch1 * 8, cy0 = cur_my * I.cv1 * 8;
+            if (uint32_t(lane) < cols) S.cmap[lane] = uint16_t(min((X0 + lane) * I.pw1 / I.width, I.pw1 - 1) - cx0);
+            if (uint32_t(lane) < rws) S.rmap[lane] = uint8_t(min((Y0 + lane) * I.ph1 / I.height, I.ph1 - 1) - cy0);
+        }
+        __syncwarp();
+
+        // 2. IDCT: lane = (unit (lane>>3) + 4j, column y)
+        const uint32_t y = lane & 7;
+        const float4 bc0 = *reinterpret_cast<const float4*>(s_b32T + y * 8);
+        const float4 bc1 = *reinterpret_cast<const float4*>(s_b32T + y * 8 + 4);
+#pragma unroll 1
+        for (int j = 0; j < 3; ++j) {
+            const uint32_t blk = (lane >> 3) + 4 * j;
+            if (4 * uint32_t(j) >= nblk) break;  // warp-uniform
             const bool act = blk < nblk;
-            const uint32_t rows = act ? s_rows[blk] : 0u;
-            const uint32_t urows = __reduce_or_sync(0xFFFFFFFFu, rows);
-            const bool big = act && s_big[blk];
-            uint32_t out[8];
-            const float* F = s_F + (act ? blk : 0) * 64;
-            if (!big) {
-                float bcol[8];
+            const uint32_t rw = act ? S.rows[blk] : 0u;
+            const uint32_t rows = rw & 0xFFu;
+            const uint32_t urows = __reduce_or_sync(0xFFFFFFFFu, (rw & 0x200u) ? 0u : rows);
+            const float* F = S.F + (act ? blk : 0) * 64;
+            float acc[8];
 #pragma unroll
-                for (int v = 0; v < 8; ++v) bcol[v] = s_b32[v * 8 + y];
-                float acc[8];
+            for (int x = 0; x < 8; ++x) acc[x] = 0.f;
 #pragma unroll
-                for (int x = 0; x < 8; ++x) acc[x] = 0.f;
-#pragma unroll
-                for (int uu = 0; uu < 8; ++uu) {
-                    if (urows & (1u << uu)) {
-                        const float4 f0 = *reinterpret_cast<const float4*>(F + uu * 8);
-                        const float4 f1 = *reinterpret_cast<const float4*>(F + uu * 8 + 4);
-                        float tu = bcol[0] * f0.x;
-                        tu = fmaf(bcol[1], f0.y, tu);
-                        tu = fmaf(bcol[2], f0.z, tu);
-                        tu = fmaf(bcol[3], f0.w, tu);
-                        tu = fmaf(bcol[4], f1.x, tu);
-                        tu = fmaf(bcol[5], f1.y, tu);
-                        tu = fmaf(bcol[6], f1.z, tu);
-                        tu = fmaf(bcol[7], f1.w, tu);
-                        const float4 b0 = *reinterpret_cast<const float4*>(s_b32 + uu * 8);
-                        const float4 b1 = *reinterpret_cast<const float4*>(s_b32 + uu * 8 + 4);
-                        acc[0] = fmaf(b0.x, tu, acc[0]);
-                        acc[1] = fmaf(b0.y, tu, acc[1]);
-                        acc[2] = fmaf(b0.z, tu, acc[2]);
-                        acc[3] = fmaf(b0.w, tu, acc[3]);
-                        acc[4] = fmaf(b1.x, tu, acc[4]);
-                        acc[5] = fmaf(b1.y, tu, acc[5]);
-                        acc[6] = fmaf(b1.z, tu, acc[6]);
-                        acc[7] = fmaf(b1.w, tu, acc[7]);
-                    }
+            for (int uu = 0; uu < 8; ++uu) {
+                if (urows & (1u << uu)) {
+                    const float4 f0 = *reinterpret_cast<const float4*>(F + uu * 8);
+                    const float4 f1 = *reinterpret_cast<const float4*>(F + uu * 8 + 4);
+                    float tu = bc0.x * f0.x;
+                    tu = fmaf(bc0.y, f0.y, tu);
+                    tu = fmaf(bc0.z, f0.z, tu);
+                    tu = fmaf(bc0.w, f0.w, tu);
+                    tu = fmaf(bc1.x, f1.x, tu);
+                    tu = fmaf(bc1.y, f1.y, tu);
+                    tu = fmaf(bc1.z, f1.z, tu);
+                    tu = fmaf(bc1.w, f1.w, tu);
+                    const float4 b0 = *reinterpret_cast<const float4*>(s_b32 + uu * 8);
+                    const float4 b1 = *reinterpret_cast<const float4*>(s_b32 + uu * 8 + 4);
+                    acc[0] = fmaf(b0.x, tu, acc[0]);
+                    acc[1] = fmaf(b0.y, tu, acc[1]);
+                    acc[2] = fmaf(b0.z, tu, acc[2]);
+                    acc[3] = fmaf(b0.w, tu, acc[3]);
+                    acc[4] = fmaf(b1.x, tu, acc[4]);
+                    acc[5] = fmaf(b1.y, tu, acc[5]);
+                    acc[6] = fmaf(b1.z, tu, acc[6]);
+                    acc[7] = fmaf(b1.w, tu, acc[7]);
                 }
-                const float lim = act ? s_lim[blk] : 0.5f;
-                uint32_t unsafe = 0;
-#pragma unroll
-                for (int x = 0; x < 8; ++x) {
-                    const float v = acc[x] + kMagic;
-                    const float dd = acc[x] - (v - kMagic);
-                    if (fabsf(dd) > lim) unsafe |= 1u << x;
-                    out[x] = uint32_t(__float_as_int(v) - kMagicBits + 128);
-                }
-                if (unsafe) {
-#pragma unroll
-                    for (int x = 0; x < 8; ++x)
-                        if (unsafe & (1u << x))
-                            out[x] = uint32_t(idct_sample_fp64(F, false, rows, s_nz + blk * 8, s_b64, x, int(y)));
-                }
-            } else {
-#pragma unroll
-                for (int x = 0; x < 8; ++x)
-                    out[x] = uint32_t(idct_sample_fp64(F, true, rows, s_nz + blk * 8, s_b64, x, int(y)));
             }
+            int out[8];
+            float mx = 0.f;
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+                const float v = acc[x] + kM128;
+                mx = fmaxf(mx, fabsf(acc[x] - (v - kM128)));
+                out[x] = __float_as_int(v) - kMagicBits;
+            }
+            uint32_t lo = pack4_sat(out[0], out[1], out[2], out[3]);
+            uint32_t hi = pack4_sat(out[4], out[5], out[6], out[7]);
             if (act) {
-                const uint32_t slot = blk % dpm, mm = blk / dpm;
-                const uint32_t comp = uint32_t(D.du_comp >> (4 * slot)) & 15u;
-                const uint32_t kk = uint32_t(D.du_kslot >> (4 * slot)) & 15u;
-                const uint32_t chh = D.comp_h[comp];
-                const uint32_t bx = kk % chh, by = kk / chh;
-                const uint32_t ps = comp == 0 ? ti.pst[0] : (comp == 1 ? ti.pst[1] : ti.pst[2]);
-                const uint32_t po = comp == 0 ? ti.poff[0] : (comp == 1 ? ti.poff[1] : ti.poff[2]);
-                uint8_t* pl = s_pl + po + (by * 8) * ps + (mm * chh + bx) * 8 + y;
-                const uint32_t lo = pack4_sat(int(out[0]), int(out[1]), int(out[2]), int(out[3]));
-                const uint32_t hi = pack4_sat(int(out[4]), int(out[5]), int(out[6]), int(out[7]));
+                const bool big = rw & 0x100u;
+                if (rw & 0x200u) {
+                    // DC-only: fl(b0 * fl(b0 * F00)) for every sample, exactly the
+                    // reference's zero-skipped sums (ties at F00 = 8k+4 included)
+                    const double f00 = big ? double(reinterpret_cast<const int32_t*>(F)[0]) : double(F[0]);
+                    const int o = lround_away(__dmul_rn(s_b64[0], __dmul_rn(s_b64[0], f00))) + 128;
+                    lo = hi = pack4_sat(o, o, o, o);
+                } else if (big || mx > S.lim[blk]) {  // rare: FP64 for the samples near x.5
+                    const float lim = S.lim[blk];
+                    uint32_t mask = 0;
 #pragma unroll
-                for (int x = 0; x < 4; ++x) pl[x * ps] = uint8_t(lo >> (8 * x));
+                    for (int x = 0; x < 8; ++x) {
+                        const float v = acc[x] + kM128;
+                        if (big || fabsf(acc[x] - (v - kM128)) > lim) mask |= 1u << x;
+                    }
+                    const uint2 ex = idct_column_fp64(F, big, rows, s_b64, int(y), mask);
+                    uint32_t ml = 0, mh = 0;
 #pragma unroll
-                for (int x = 0; x < 4; ++x) pl[(x + 4) * ps] = uint8_t(hi >> (8 * x));
+                    for (int x = 0; x < 4; ++x) {
+                        if (mask & (1u << x)) ml |= 0xFFu << (8 * x);
+                        if (mask & (1u << (x + 4))) mh |= 0xFFu << (8 * x);
+                    }
+                    lo = (lo & ~ml) | (ex.x & ml);
+                    hi = (hi & ~mh) | (ex.y & mh);
+                }
+                const uint32_t ps = I.bps[blk];
+                uint8_t* pl = S.pl + I.boff[blk] + y;
+                pl[0] = uint8_t(lo);
+                pl[ps] = uint8_t(lo >> 8);
+                pl[2 * ps] = uint8_t(lo >> 16);
+                pl[3 * ps] = uint8_t(lo >> 24);
+                pl[4 * ps] = uint8_t(hi);
+                pl[5 * ps] = uint8_t(hi >> 8);
+                pl[6 * ps] = uint8_t(hi >> 16);
+                pl[7 * ps] = uint8_t(hi >> 24);
             }
         }
-        __syncthreads();
+        __syncwarp();
+
         // 3. output
-        const uint32_t cols = ti.cols, rws = ti.rws, W = D.width;
-        if (ti.rgb) {
-            // thread = 4 pixels of one row (or of a row pair sharing a chroma
-            // row for 4:2:0); chroma offsets computed inline per chroma sample
-            const bool pair = D.v_max == 2;
+        if (I.rgb) {
+            // lane item = 4 pixels of one row, or of a row pair sharing a
+            // chroma row (v_max == 2); 8 groups of 4 pixels per tile row
+            const bool pair = I.v_max == 2;
             const uint32_t nrow = pair ? (rws + 1) >> 1 : rws;
             const uint32_t groups = (cols + 3) >> 2;
-            const uint32_t gsh = 32 - __clz(max(groups, 1u) - 1);  // groups rounded up to 2^gsh
-            uint8_t* obase = P.out + D.out_off;
-            const bool aligned = ((W & 3) == 0) && ((D.out_off & 3) == 0);
-            const uint8_t* ybase = s_pl + ti.poff[0];
-            const uint8_t* cbbase = s_pl + ti.poff[1];
-            const uint8_t* crbase = s_pl + ti.poff[2];
-            const uint32_t pst0 = ti.pst[0], pst1 = ti.pst[1];
-            for (uint32_t itg = tid; itg < (nrow << gsh); itg += kK4Threads) {
-                const uint32_t j = itg >> gsh, gxi = itg & ((1u << gsh) - 1);
+            uint8_t* obase = P.out + I.out_off;
+            const uint32_t W = I.width;
+            const bool aligned = ((W & 3) == 0) && ((I.out_off & 3) == 0);
+            const uint8_t* ybase = S.pl + I.poff[0];
+            const uint8_t* cbbase = S.pl + I.poff[1];
+            const uint8_t* crbase = S.pl + I.poff[2];
+            const uint32_t pst0 = I.pst[0], pst1 = I.pst[1];
+            for (uint32_t itg = lane; itg < (nrow << 3); itg += 32) {
+                const uint32_t jr = itg >> 3, gxi = itg & 7;
                 if (gxi >= groups) continue;
                 const uint32_t gx = gxi * 4;
                 const uint32_t npx = min(4u, cols - gx);
-                const uint2 cm = *reinterpret_cast<const uint2*>(s_cmap + gx);
-                const uint32_t cx[4] = {cm.x & 0xFFFFu, cm.x >> 16, cm.y & 0xFFFFu, cm.y >> 16};
-                const uint32_t r0 = pair ? 2 * j : j;
-                uint32_t crow = s_rmap[r0];
+                const uint2 cm = *reinterpret_cast<const uint2*>(S.cmap + gx);
+                uint32_t cx0 = cm.x & 0xFFFFu, cx1 = cm.x >> 16, cx2 = cm.y & 0xFFFFu, cx3 = cm.y >> 16;
+                if (npx < 2) cx1 = cx0;
+                if (npx < 3) cx2 = cx1;
+                if (npx < 4) cx3 = cx2;
+                const uint32_t r0 = pair ? 2 * jr : jr;
+                uint32_t crow = S.rmap[r0];
                 const uint8_t* cbrow = cbbase + crow * pst1;
                 const uint8_t* crrow = crbase + crow * pst1;
-                uint32_t w[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t c = q < int(npx) ? cx[q] : cx[0];
-                    if (q > 0 && c == cx[q - 1])
-                        w[q] = w[q - 1];
-                    else
-                        w[q] = chroma_word2(cbrow[c], crrow[c]);
-                }
+                uint32_t w0 = chroma_word_lut(s_lut, cbrow[cx0], crrow[cx0]);
+                uint32_t w1 = cx1 == cx0 ? w0 : chroma_word_lut(s_lut, cbrow[cx1], crrow[cx1]);
+                uint32_t w2 = cx2 == cx1 ? w1 : chroma_word_lut(s_lut, cbrow[cx2], crrow[cx2]);
+                uint32_t w3 = cx3 == cx2 ? w2 : chroma_word_lut(s_lut, cbrow[cx3], crrow[cx3]);
                 const bool fast = npx == 4 && aligned;
-                emit_rgb4(obase + (uint64_t(ti.Y0 + r0) * W + ti.X0 + gx) * 3, fast, npx,
-                          *reinterpret_cast<const uint32_t*>(ybase + r0 * pst0 + gx), w, cbrow, crrow, cx);
+                emit_rgb4(obase + (uint64_t(Y0 + r0) * W + X0 + gx) * 3, fast, npx,
+                          *reinterpret_cast<const uint32_t*>(ybase + r0 * pst0 + gx), w0, w1, w2, w3, cbrow, crrow,
+                          cx0, cx1, cx2, cx3);
                 if (pair && r0 + 1 < rws) {
-                    const uint32_t crow1 = s_rmap[r0 + 1];
+                    const uint32_t crow1 = S.rmap[r0 + 1];
                     if (crow1 != crow) {
                         crow = crow1;
                         cbrow = cbbase + crow * pst1;
                         crrow = crbase + crow * pst1;
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const uint32_t c = q < int(npx) ? cx[q] : cx[0];
-                            if (q > 0 && c == cx[q - 1])
-                                w[q] = w[q - 1];
-                            else
-                                w[q] = chroma_word2(cbrow[c], crrow[c]);
-                        }
+                        w0 = chroma_word_lut(s_lut, cbrow[cx0], crrow[cx0]);
+                        w1 = cx1 == cx0 ? w0 : chroma_word_lut(s_lut, cbrow[cx1], crrow[cx1]);
+                        w2 = cx2 == cx1 ? w1 : chroma_word_lut(s_lut, cbrow[cx2], crrow[cx2]);
+                        w3 = cx3 == cx2 ? w2 : chroma_word_lut(s_lut, cbrow[cx3], crrow[cx3]);
                     }
-                    emit_rgb4(obase + (uint64_t(ti.Y0 + r0 + 1) * W + ti.X0 + gx) * 3, fast, npx,
-                              *reinterpret_cast<const uint32_t*>(ybase + (r0 + 1) * pst0 + gx), w, cbrow, crrow,
-                              cx);
+                    emit_rgb4(obase + (uint64_t(Y0 + r0 + 1) * W + X0 + gx) * 3, fast, npx,
+                              *reinterpret_cast<const uint32_t*>(ybase + (r0 + 1) * pst0 + gx), w0, w1, w2, w3,
+                              cbrow, crrow, cx0, cx1, cx2, cx3);
                 }
             }
         } else {
             // planes (extract_planes, transform.hpp:165-211) — or the Y plane
             // only for grayscale output / single-component images
-            const uint32_t nplanes = (D.out_mode == 0) ? D.ncomp : 1;
-            const uint32_t MT = D.mcus_per_tile;
-            uint64_t plane_base = D.out_off;
+            const uint32_t nplanes = (I.out_mode == 0) ? I.ncomp : 1;
+            uint64_t plane_base = I.out_off;
 #pragma unroll
             for (uint32_t c = 0; c < 3; ++c) {
                 if (c >= nplanes) break;
-                const uint32_t pw = D.plane_w[c], ph = D.plane_h[c];
-                const uint32_t cx0 = ti.mx0 * D.comp_h[c] * 8, cy0 = ti.my * D.comp_v[c] * 8;
-                const uint32_t ccols = cx0 < pw ? min(ti.pw_t[c] * ti.nm / MT, pw - cx0) : 0;
-                const uint32_t crows = cy0 < ph ? min(D.comp_v[c] * 8, ph - cy0) : 0;
-                for (uint32_t e = tid; e < crows * ccols; e += kK4Threads) {
+                const uint32_t pw = I.plane_w[c], ph = I.plane_h[c];
+                const uint32_t cx0 = cur_mx0 * I.comp_h[c] * 8, cy0 = cur_my * I.comp_v[c] * 8;
+                const uint32_t ccols = cx0 < pw ? min(cur_nm * I.comp_h[c] * 8, pw - cx0) : 0;
+                const uint32_t crows = cy0 < ph ? min(I.comp_v[c] * 8, ph - cy0) : 0;
+                for (uint32_t e = lane; e < crows * ccols; e += 32) {
                     const uint32_t r = e / ccols, x = e % ccols;
-                    P.out[plane_base + uint64_t(cy0 + r) * pw + cx0 + x] = s_pl[ti.poff[c] + r * ti.pst[c] + x];
+                    P.out[plane_base + uint64_t(cy0 + r) * pw + cx0 + x] = S.pl[I.poff[c] + r * I.pst[c] + x];
                 }
                 plane_base += uint64_t(pw) * ph;
             }
         }
+        __syncwarp();
     }
 }
 
@@ -1462,7 +1519,8 @@ void launch_k4_transform(const Params& p, void* stream) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_transform, kK4Threads, 0);
         grid_cap = std::max(1, sms * std::max(per_sm, 1));
     }
-    const unsigned grid = unsigned(std::min<uint64_t>(p.k4_tiles, uint64_t(grid_cap)));
+    const uint64_t want = (uint64_t(p.k4_tiles) + kK4Threads / 32 - 1) / (kK4Threads / 32);
+    const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(grid_cap)));
     k4_transform<<<grid, kK4Threads, 0, (cudaStream_t)stream>>>(p);
 }
 

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -426,7 +427,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         if (h.table_status != kOk) continue;
         d.sub_count = (uint64_t(rl) * 8 + sb - 1) / sb;
         d.expected = h.total_dus() * 64;
-        d.mcus_per_tile = uint16_t(std::max<uint32_t>(1, kK4MaxBlocks / h.dpm));
+        d.mcus_per_tile = uint16_t(32 / (8 * h.h_max));  // 32-pixel-wide warp tiles (<= 12 data units)
         d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
         sub += d.sub_count;
         du += h.total_dus();
@@ -552,6 +553,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.k2_flag = ctx->k2_flag.as<uint32_t>();
     p.k2_agg = ctx->k2_agg.as<uint64_t>();
     p.stats = ctx->stats.as<unsigned long long>();
+    p.debug = getenv("PJG_K4_DEBUG") ? uint32_t(atoi(getenv("PJG_K4_DEBUG"))) : 0u;
 
     ctx->busy = true;
     *out = b.release();

@@ -133,8 +133,8 @@ constexpr int kK0Tile = kK0Threads * kK0BytesPerThread;  // 4096 raw bytes per t
 constexpr int kK1Threads = 128;                          // subsequences per K1 CTA
 constexpr int kK2Threads = 256;
 constexpr int kK3Threads = 128;
-constexpr int kK4Threads = 192;
-constexpr int kK4MaxBlocks = 24;                         // data units per K4 tile
+constexpr int kK4Threads = 128;
+constexpr int kK4MaxBlocks = 12;                         // data units per K4 (warp) tile
 
 struct Params {
     // batch
@@ -178,6 +178,8 @@ struct Params {
     uint64_t* k2_agg;              // 4 x uint64 per tile: aggregate (n|head, dc), inclusive (n, dc)
     // stats
     unsigned long long* stats;     // see StatIndex
+    uint32_t debug;                // K4 ablation bits (PJG_K4_DEBUG), 0 in production
+    uint32_t pad3;
 };
 
 enum Counter { kTicketK0 = 0, kTicketK1 = 1, kTicketK2 = 2, kNumCounters = 8 };
