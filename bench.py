@@ -21,7 +21,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -58,61 +57,54 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled through NVML every 10 ms during
+    the timed region (the recipe's clocks line, B200_PROFILING.md)."""
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.reasons = set()
+        self.stop_evt = threading.Event()
+        self.max_mhz = None
+
+    def _run(self):
+        import pynvml as N
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
+        while not self.stop_evt.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for k, m in bits.items():
+                    if r & m:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.01)
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.t = None
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 9:
-                continue
-            try:
-                sm.append(float(p[1]))
-                mx = float(p[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not getattr(self, "t", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self.stop_evt.set()
+        self.t.join(timeout=2)
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    from paper_2111_09219_b200.dist import rank_env
+    return rank_env()
 
 
 def make_corpus(cfg_key, rank, pinned=True):
@@ -209,10 +201,9 @@ def main():
     import paper_2111_09219_b200 as pj
 
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2111_09219_b200 import dist as pdist
+    dist = pdist.init("nccl", local) if world > 1 else None
+    dev = torch.device("cuda", local)
 
     n, w, h, q, s, _ = CONFIGS[args.config]
     pinned_t, blob, offs, sizes = make_corpus(args.config, rank)
@@ -266,11 +257,7 @@ def main():
     torch.cuda.synchronize()
     clocks = clk.stop()
     sync_stats = b.sync_stats()
-    tot_ms = float(np.sum(step_ms))
-    if dist:
-        t = torch.tensor([tot_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot_ms = pdist.max_over_ranks(float(np.sum(step_ms)), dev)
     ms_per_step = tot_ms / args.steps
     value = world * rgb_bytes / (ms_per_step / 1e3) / 1e9
     img_s = world * n / (ms_per_step / 1e3)
@@ -306,11 +293,7 @@ def main():
         e2e_ms.append(ms)
         d2h = ob
     h2d = comp_bytes
-    e2e_tot = float(np.sum(e2e_ms))
-    if dist:
-        t = torch.tensor([e2e_tot], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_tot = float(t.item())
+    e2e_tot = pdist.max_over_ranks(float(np.sum(e2e_ms)), dev)
     e2e_val = world * rgb_bytes / (e2e_tot / args.steps / 1e3) / 1e9
 
     # ---------------- roofline of the dominant HBM-bound stage (K4) -------

@@ -419,3 +419,67 @@ def dc_prefix_inverse_zigzag(post_dc_raster: np.ndarray, du_seq) -> np.ndarray:
             out_dc[idx[1:]] = dc[idx[1:]] - dc[idx[:-1]]
     zz[:, 0] = ((out_dc + 32768) % 65536 - 32768).astype(np.int16)
     return zz.reshape(-1)
+
+
+def ref_huff_lut16(counts, symbols):
+    """Reference build_table LUT expanded to all 65536 16-bit windows."""
+    L = Ref.lib()
+    c = np.ascontiguousarray(counts, np.uint8)
+    s = np.ascontiguousarray(symbols, np.uint8) if len(symbols) else np.zeros(1, np.uint8)
+    out = np.zeros(65536, np.uint32)
+    ml = C.c_uint()
+    st = L.ref_huff_lut16(_ptr(c, u8p), _ptr(s, u8p), C.c_size_t(len(symbols)), _ptr(out, u32p), C.byref(ml))
+    return st, out, ml.value
+
+
+def ref_decode_symbols(dc, ac, bits: bytes, max_syms):
+    """decode_next_symbol over a raw bit string; dc/ac = (counts16, symbols)."""
+    L = Ref.lib()
+    dcc = np.ascontiguousarray(dc[0], np.uint8)
+    dcs = np.ascontiguousarray(dc[1], np.uint8)
+    acc = np.ascontiguousarray(ac[0], np.uint8)
+    acs = np.ascontiguousarray(ac[1], np.uint8)
+    b = np.frombuffer(bits, np.uint8)
+    rec = np.zeros(4 * max_syms, np.int64)
+    n = C.c_size_t()
+    st = L.ref_decode_symbols(_ptr(dcc, u8p), _ptr(dcs, u8p), C.c_size_t(dcs.size), _ptr(acc, u8p),
+                              _ptr(acs, u8p), C.c_size_t(acs.size), _ptr(b, u8p), C.c_size_t(b.size),
+                              C.c_size_t(max_syms), rec.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(n))
+    return st, rec[: 4 * n.value].reshape(-1, 4)
+
+
+def jfif_bytes(width, height, comps, quant, dc_specs, ac_specs, scan: bytes, dri=None, trailer=b"\xff\xd9"):
+    """Assembles a baseline JPEG from explicit parts (test fixtures such as the
+    reference's worked example, helpers.hpp:29-53).  comps: list of
+    (id, h, v, tq, td, ta); quant: {id: 64 zig-zag entries}; dc/ac_specs:
+    {id: (counts16, symbols)}."""
+    out = bytearray(b"\xff\xd8")
+    for tid, q in quant.items():
+        out += b"\xff\xdb" + (3 + 64).to_bytes(2, "big") + bytes([tid]) + bytes(q)
+    out += b"\xff\xc0" + (8 + 3 * len(comps)).to_bytes(2, "big") + bytes([8]) + height.to_bytes(2, "big") + \
+        width.to_bytes(2, "big") + bytes([len(comps)])
+    for (cid, h, v, tq, _, _) in comps:
+        out += bytes([cid, (h << 4) | v, tq])
+    for cls, specs in ((0, dc_specs), (1, ac_specs)):
+        for tid, (counts, syms) in specs.items():
+            out += b"\xff\xc4" + (3 + 16 + len(syms)).to_bytes(2, "big") + bytes([(cls << 4) | tid]) + \
+                bytes(counts) + bytes(syms)
+    if dri is not None:
+        out += b"\xff\xdd" + (4).to_bytes(2, "big") + dri.to_bytes(2, "big")
+    out += b"\xff\xda" + (6 + 2 * len(comps)).to_bytes(2, "big") + bytes([len(comps)])
+    for (cid, _, _, _, td, ta) in comps:
+        out += bytes([cid, (td << 4) | ta])
+    out += bytes([0, 63, 0]) + scan + trailer
+    return bytes(out)
+
+
+# The reference's worked example (tests/helpers.hpp:29-53): one grayscale data
+# unit, DC "0"->cat 0, "10"->cat 2; AC "00" EOB, "01" (0,1), "100" (0,2),
+# "1010" (2,1), "1011" (1,1); scan 98 49 59 DC.
+EXAMPLE_DC = ([1, 1] + [0] * 14, [0x00, 0x02])
+EXAMPLE_AC = ([0, 2, 1, 2] + [0] * 12, [0x00, 0x01, 0x02, 0x21, 0x11])
+EXAMPLE_SCAN = bytes([0x98, 0x49, 0x59, 0xDC])
+
+
+def example_jpeg(scan=EXAMPLE_SCAN):
+    return jfif_bytes(8, 8, [(1, 1, 1, 0, 0, 0)], {0: [1] * 64}, {0: EXAMPLE_DC}, {0: EXAMPLE_AC}, scan)

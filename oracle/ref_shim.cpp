@@ -352,4 +352,67 @@ int ref_decode_batch_rgb(const uint8_t* const* files, const size_t* sizes, size_
 
 unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
 
+// build_table (huffman.hpp:60-93) flat LUT, expanded to 16-bit windows:
+// out[w] = (length << 8) | symbol for the code matching the top bits of w,
+// 0 for an invalid prefix.  Returns the Errc+1 of build_table on failure.
+int ref_huff_lut16(const uint8_t* counts16, const uint8_t* symbols, size_t nsym, uint32_t* out,
+                   unsigned* maxlen) {
+    return guarded([&] {
+        pjpeg::HuffmanTableSpec spec;
+        for (int i = 0; i < 16; ++i) spec.counts[i] = counts16[i];
+        spec.symbols.assign(symbols, symbols + nsym);
+        spec.present = true;
+        pjpeg::HuffmanTable t = pjpeg::build_table(spec);
+        *maxlen = t.max_code_length;
+        for (uint32_t w = 0; w < 65536; ++w) {
+            const auto& e = t.lut[w >> (16 - t.max_code_length)];
+            out[w] = e.length ? ((uint32_t(e.length) << 8) | e.symbol) : 0u;
+        }
+        return 0;
+    });
+}
+
+// decode_next_symbol (huffman.hpp:137-175) over a bit string given as bytes
+// (bit_length = 8 * n): the first `max_syms` symbols with z tracking as the
+// reference test does (test_huffman.cpp:111-144).  Each record: start bit,
+// kind (0 coef, 1 EOB, 2 ZRL), run, coefficient.  Returns Errc+1 of the
+// first failing symbol (records written so far are kept in *count).
+int ref_decode_symbols(const uint8_t* dc_counts, const uint8_t* dc_syms, size_t n_dc,
+                       const uint8_t* ac_counts, const uint8_t* ac_syms, size_t n_ac,
+                       const uint8_t* bits, size_t nbytes, size_t max_syms, int64_t* rec,
+                       size_t* count) {
+    return guarded([&] {
+        pjpeg::HuffmanTableSpec d, a;
+        for (int i = 0; i < 16; ++i) {
+            d.counts[i] = dc_counts[i];
+            a.counts[i] = ac_counts[i];
+        }
+        d.symbols.assign(dc_syms, dc_syms + n_dc);
+        a.symbols.assign(ac_syms, ac_syms + n_ac);
+        d.cls = pjpeg::HuffmanTableSpec::Class::DC;
+        a.cls = pjpeg::HuffmanTableSpec::Class::AC;
+        pjpeg::HuffmanTable dt = pjpeg::build_table(d), at = pjpeg::build_table(a);
+        pjpeg::EntropySegment seg;
+        seg.data.assign(bits, bits + nbytes);
+        seg.bit_length = uint64_t(nbytes) * 8;
+        pjpeg::BitCursor cur(seg);
+        unsigned z = 0;
+        *count = 0;
+        for (size_t k = 0; k < max_syms; ++k) {
+            const uint64_t start = cur.position();
+            pjpeg::DecodedSymbol s = pjpeg::decode_next_symbol(cur, z, dt, at);
+            rec[4 * k + 0] = int64_t(start);
+            rec[4 * k + 1] = s.kind == pjpeg::DecodedSymbol::Kind::Coefficient ? 0
+                             : s.kind == pjpeg::DecodedSymbol::Kind::EOB       ? 1
+                                                                               : 2;
+            rec[4 * k + 2] = s.run_length;
+            rec[4 * k + 3] = s.coefficient;
+            *count = k + 1;
+            z += s.run_length + 1;
+            if (z >= 64 || s.kind == pjpeg::DecodedSymbol::Kind::EOB) z = 0;
+        }
+        return 0;
+    });
+}
+
 }  // extern "C"

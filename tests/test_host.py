@@ -1,0 +1,139 @@
+"""CPU: host side of the product — the C-ABI library loads and exports every
+symbol include/pjg.h declares, header parsing matches the reference, the
+device Huffman table format decodes every 16-bit window exactly like the
+reference's flat LUT, and decode calls without a GPU fail loudly."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2111_09219_b200 as pj
+from oracle.oracle import EXAMPLE_AC, EXAMPLE_DC, Ref, ref_huff_lut16
+from tests.corpus import ref_jpeg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "pjg.h")).read()
+    return sorted(set(re.findall(r"\b(pjg_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = pj.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) <= set(pj.EXPORTED_SYMBOLS) | set(syms)
+
+
+def test_status_names_match_errc():
+    for e in pj.Errc:
+        assert pj.lib().pjg_status_name(int(e) + 1).decode() == e.name
+
+
+def test_inspect_geometry_matches_reference():
+    for (w, h, q, s) in [(48, 48, 92, "444"), (97, 33, 75, "420"), (64, 48, 50, "422"), (31, 17, 20, "gray"),
+                         (500, 375, 75, "420")]:
+        f = ref_jpeg(w, h, 11, q, s)
+        g = Ref.parse_info(f)
+        info = pj.inspect(f)
+        assert info["status"] == 0
+        assert (info["width"], info["height"], info["components"]) == (g["width"], g["height"], g["ncomp"])
+        assert (info["mcus_x"], info["mcus_y"]) == (g["mcus_x"], g["mcus_y"])
+        assert info["data_units"] == g["dus"]
+        rgb = pj.inspect(f, pj.OutputColorspace.RGBInterleaved)
+        assert rgb["output_bytes"] == w * h * (1 if s == "gray" else 3)
+
+
+def test_header_error_codes_match_reference():
+    base = ref_jpeg(40, 24, 3, 75, "420")
+    sos = base.index(b"\xff\xda")
+    cases = {
+        "truncated": base[:10],
+        "garbage": bytes([0xDE, 0xAD, 0xBE, 0xEF]),
+        "progressive": base.replace(b"\xff\xc0", b"\xff\xc2", 1),
+        "no_soi": b"\x00" + base[1:],
+        "sos_cut": base[: sos + 5],
+    }
+    for name, f in cases.items():
+        want = Ref.decode(f).status
+        got = pj.inspect(f)["status"]
+        assert want != 0
+        assert got == want, (name, got, want)
+
+
+def annex_k_tables():
+    dcl = ([0, 1, 5, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0], list(range(12)))
+    dcc = ([0, 3, 1, 1, 1, 1, 1, 1, 1, 1, 1, 0, 0, 0, 0, 0], list(range(12)))
+    return [dcl, dcc, EXAMPLE_DC, EXAMPLE_AC]
+
+
+def random_canonical(rng):
+    # a random complete-or-incomplete canonical code (test_huffman.cpp:210-247)
+    counts = [0] * 16
+    left, code_space = int(rng.integers(1, 162)), 1
+    for L in range(16):
+        code_space *= 2
+        n = int(rng.integers(0, min(left, code_space - 1) + 1)) if L < 15 else min(left, code_space - 1)
+        counts[L] = n
+        code_space -= n
+        left -= n
+        if left == 0:
+            break
+    syms = list(rng.permutation(256)[: sum(counts)])
+    return counts, syms
+
+
+def test_two_level_huffman_table_equals_reference_flat_lut():
+    rng = np.random.default_rng(3)
+    tables = annex_k_tables() + [random_canonical(rng) for _ in range(60)]
+    # tables actually used by the reference encoder's files
+    windows = np.arange(65536, dtype=np.uint16)
+    for counts, syms in tables:
+        st, want, _ = ref_huff_lut16(counts, syms)
+        got = np.zeros(65536, np.uint32)
+        c = np.array(counts, np.uint8)
+        s = np.array(syms if syms else [0], np.uint8)
+        rc = pj.lib().pjg_debug_huff_decode(c.ctypes.data_as(pj.u8p), s.ctypes.data_as(pj.u8p), len(syms),
+                                            windows.ctypes.data_as(pj.C.POINTER(pj.C.c_uint16)), 65536,
+                                            got.ctypes.data_as(pj.C.POINTER(pj.C.c_uint32)))
+        if st:
+            assert rc == -st
+            continue
+        assert rc == 0
+        assert np.array_equal(got, want), (counts, syms[:8])
+
+
+def test_oversubscribed_table_rejected_like_reference():
+    counts = [3] + [0] * 15  # 3 codes of length 1
+    st, _, _ = ref_huff_lut16(counts, [1, 2, 3])
+    got = np.zeros(1, np.uint32)
+    w = np.zeros(1, np.uint16)
+    rc = pj.lib().pjg_debug_huff_decode(np.array(counts, np.uint8).ctypes.data_as(pj.u8p),
+                                        np.array([1, 2, 3], np.uint8).ctypes.data_as(pj.u8p), 3,
+                                        w.ctypes.data_as(pj.C.POINTER(pj.C.c_uint16)), 1,
+                                        got.ctypes.data_as(pj.C.POINTER(pj.C.c_uint32)))
+    assert st == int(pj.Errc.OversubscribedCode) + 1 and rc == -st
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(pj.Error):
+        pj.Decoder(0)
+    with pytest.raises(pj.Error):
+        pj.decode_single(ref_jpeg(16, 16, 1, 75, "444"))
+
+
+def test_synthetic_bench_corpus_is_valid_baseline_jpeg():
+    from paper_2111_09219_b200.synth import synth_batch
+    for (w, h, q, s) in [(500, 375, 75, "420"), (64, 64, 85, "444"), (40, 24, 95, "gray"), (48, 32, 50, "422")]:
+        blob, offs, sizes = synth_batch(3, w, h, 7, q, s)
+        for o, n in zip(offs, sizes):
+            f = blob[o: o + n].tobytes()
+            d = Ref.decode(f)
+            assert d.status == 0 and (d.width, d.height) == (w, h)
