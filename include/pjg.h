@@ -133,6 +133,9 @@ int pjg_batch_synchronize(pjg_batch* b, int32_t* statuses);
 int pjg_batch_download(pjg_batch* b, uint8_t* const* outs, const size_t* caps);
 /* One D2H of the whole batch output (image i at pjg_batch_output_offset(i)). */
 int pjg_batch_download_all(pjg_batch* b, void* host, size_t cap);
+/* Same, enqueued on the context stream without waiting (pinned host memory
+ * overlaps with other contexts' decode); pjg_batch_synchronize completes it. */
+int pjg_batch_download_all_async(pjg_batch* b, void* host, size_t cap);
 uint64_t pjg_batch_output_offset(const pjg_batch* b, size_t i);
 int pjg_batch_info(const pjg_batch* b, size_t i, pjg_image_info* info);
 const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i);

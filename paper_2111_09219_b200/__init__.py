@@ -183,6 +183,7 @@ def lib():
             L.pjg_batch_synchronize.argtypes = [C.c_void_p, C.c_void_p]
             L.pjg_batch_download.argtypes = [C.c_void_p, C.POINTER(u8p), C.POINTER(C.c_size_t)]
             L.pjg_batch_download_all.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
+            L.pjg_batch_download_all_async.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
             L.pjg_batch_output_offset.argtypes = [C.c_void_p, C.c_size_t]
             L.pjg_batch_output_offset.restype = C.c_uint64
             L.pjg_batch_info.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(_Info)]
@@ -211,7 +212,7 @@ EXPORTED_SYMBOLS = [
     "pjg_ctx_create", "pjg_ctx_destroy", "pjg_last_error", "pjg_status_name", "pjg_default_config",
     "pjg_ctx_stream", "pjg_inspect", "pjg_decode", "pjg_decode_batch", "pjg_batch_create",
     "pjg_batch_upload", "pjg_batch_decode", "pjg_batch_synchronize", "pjg_batch_download",
-    "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_download_all", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
+    "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_download_all", "pjg_batch_download_all_async", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
     "pjg_batch_sync_stats", "pjg_batch_destroy", "pjg_batch_dump_coefficients",
     "pjg_batch_dump_sync_states", "pjg_batch_dump_segment", "pjg_upsample_and_convert",
     "pjg_debug_huff_decode",
@@ -341,6 +342,10 @@ class Batch:
     def download_all(self, host_ptr: int, cap: int):
         """One D2H of the whole batch output into host memory at host_ptr."""
         self._check(lib().pjg_batch_download_all(self._h, C.c_void_p(host_ptr), cap))
+
+    def download_all_async(self, host_ptr: int, cap: int):
+        """Enqueue the batch output D2H on this context's stream (no wait)."""
+        self._check(lib().pjg_batch_download_all_async(self._h, C.c_void_p(host_ptr), cap))
 
     def output_offset(self, i) -> int:
         return int(lib().pjg_batch_output_offset(self._h, i))
@@ -528,3 +533,53 @@ def inspect(file_bytes, output=OutputColorspace.YCbCrPlanes) -> dict:
             "output_bytes": int(inf.output_bytes),
             "plane_dims": [(inf.plane_width[c], inf.plane_height[c])
                            for c in range(inf.num_components)]}
+
+
+def decode_to_host_pipelined(decoders, blob, offsets, sizes, host_ptr: int, host_cap: int,
+                             config: DecodeConfig | None = None, output=OutputColorspace.RGBInterleaved,
+                             chunk: int = 512):
+    """decode_batch into pinned host memory with copy/compute overlap.
+
+    The batch (files laid out contiguously in ``blob``) is cut into chunks of
+    ``chunk`` images that rotate over ``decoders`` (>= 2 contexts = 2 CUDA
+    streams): chunk i's D2H runs while chunk i+1 is parsed on the host,
+    uploaded and decoded.  Chunk outputs land back to back at ``host_ptr``.
+    Returns (statuses, [(first_image, batch_output_offset_base, Batch)...] is
+    not kept: returns statuses and per-chunk output byte offsets)."""
+    config = config or DecodeConfig()
+    n = len(sizes)
+    live = [None] * len(decoders)
+    statuses = np.zeros(n, np.int32)
+    chunk_base = []
+    base = 0
+    pending = []
+
+    def retire(slot):
+        b, lo = live[slot]
+        st = b.synchronize()
+        statuses[lo: lo + len(st)] = st
+        b.close()
+        live[slot] = None
+
+    for ci, lo in enumerate(range(0, n, chunk)):
+        hi = min(n, lo + chunk)
+        slot = ci % len(decoders)
+        if live[slot] is not None:
+            retire(slot)
+        b = decoders[slot].batch((blob, offsets[lo:hi], sizes[lo:hi]), config, output)
+        ob = b.output_bytes()
+        if base + ob > host_cap:
+            raise Error(int(Status_CAPACITY), "host buffer too small")
+        b.upload()
+        b.decode()
+        b.download_all_async(host_ptr + base, host_cap - base)
+        chunk_base.append(base)
+        base += ob
+        live[slot] = (b, lo)
+    for slot in range(len(decoders)):
+        if live[slot] is not None:
+            retire(slot)
+    return statuses, chunk_base, base
+
+
+Status_CAPACITY = 102

@@ -219,7 +219,7 @@ int32_t build_dev_huff(const HuffSpec& spec, DevHuff* out) {
     uint16_t codes[256];
     uint8_t lens[256];
     uint32_t maxlen = 0;
-    for (int len = 0; len <= 16; ++len) out->maxcode[len] = -1;
+    for (int len = 0; len <= 17; ++len) out->maxcode[len] = -1;
     for (uint32_t len = 1; len <= 16; ++len) {
         uint32_t n = spec.counts[len - 1];
         if (code + n > (1u << len)) return kOversubscribedCode;
@@ -247,6 +247,49 @@ int32_t build_dev_huff(const HuffSpec& spec, DevHuff* out) {
             out->lut[first + i] = uint16_t((uint32_t(lens[k]) << 8) | spec.symbols[k]);
     }
     return kOk;
+}
+
+// Fast table: decode_next_symbol (huffman.hpp:137-175) resolved for every
+// kFastBits window whose codeword AND magnitude bits both fit; symbols the
+// reference rejects (DC l > 11, AC l > 10, AC l == 0 with r not in {0, 15})
+// are left to the exact path so its error order is preserved.  `dc` selects
+// the class semantics the table is used with (DC at z == 0, AC otherwise).
+void build_fast(DevHuff* t, bool dc) {
+    for (uint32_t w = 0; w < (1u << kFastBits); ++w) {
+        const uint32_t e = huff_lookup(*t, w << (16 - kFastBits));
+        const uint32_t clen = e >> 8, sym = e & 255u;
+        uint32_t f = 0;
+        if (clen != 0 && clen <= uint32_t(kFastBits)) {
+            uint32_t l = 0, run = 0, kind = 0;
+            bool ok = true;
+            if (dc) {
+                l = sym;
+                ok = l <= 11;
+            } else {
+                run = sym >> 4;
+                l = sym & 15u;
+                if (l == 0) {
+                    if (run == 0)
+                        kind = 1;
+                    else if (run == 15)
+                        kind = 2;
+                    else
+                        ok = false;
+                } else if (l > 10) {
+                    ok = false;
+                }
+            }
+            if (ok && clen + l <= uint32_t(kFastBits)) {
+                int32_t v = 0;
+                if (l) {
+                    const uint32_t bits = (w >> (kFastBits - clen - l)) & ((1u << l) - 1);
+                    v = bits >= (1u << (l - 1)) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1);
+                }
+                f = (clen + l) | (run << 5) | (kind << 11) | (uint32_t(uint16_t(int16_t(v))) << 16);
+            }
+        }
+        t->fast[w] = f;
+    }
 }
 
 }  // namespace pjg

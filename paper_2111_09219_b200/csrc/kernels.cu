@@ -324,55 +324,68 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
         const DevHuff* t = z == 0 ? (comp == 0 ? ic.dc0 : (comp == 1 ? ic.dc1 : ic.dc2))
                                   : (comp == 0 ? ic.ac0 : (comp == 1 ? ic.ac1 : ic.ac2));
         const uint64_t avail = L - p;  // >= 1 inside the loop
-        uint32_t maxlen;
-        const uint32_t e = dev_lookup(t, uint32_t(acc >> 48), maxlen);
-        const uint32_t len = e >> 8, sym = e & 255u;
-        int32_t err = 0;
-        uint32_t l = 0, run = 0;
+        // fast path: code + magnitude resolved by one probe (valid symbols
+        // only, and only where all kFastBits window bits are real)
+        const uint32_t fe = __ldg(&t->fast[uint32_t(acc >> (64 - kFastBits))]);
+        uint32_t len, l = 0, run = 0;
         bool eob = false, coefk = false;
-        if (len == 0) {
-            err = avail < maxlen ? kOutOfBits : kInvalidCode;
-        } else if (len > avail) {
-            err = kOutOfBits;
-        } else if (z == 0) {
-            l = sym;
-            if (l > 11)
-                err = kInvalidCode;
-            else if (avail - len < l)
-                err = kOutOfBits;
-            coefk = true;
-        } else {
-            const uint32_t r = sym >> 4;
-            l = sym & 15u;
-            if (l == 0) {
-                if (r == 0) {
-                    eob = true;
-                    run = 63 - z;
-                } else if (r == 15) {
-                    run = 15;
-                } else {
-                    err = kInvalidCode;
-                }
-            } else if (l > 10) {
-                err = kInvalidCode;
-            } else if (avail - len < l) {
-                err = kOutOfBits;
-            } else {
-                run = r;
-                coefk = true;
-            }
-        }
-        if (err) {
-            s.div = true;
-            s.err = err;
-            break;
-        }
         int32_t coef = 0;
-        if (l) {
-            uint32_t bits = uint32_t((acc << len) >> (64 - l));
-            coef = bits >= (1u << (l - 1)) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1);
+        if ((fe & 31u) != 0 && avail >= 16) {
+            len = fe & 31u;  // code + magnitude bits
+            const uint32_t kind = fe & (3u << 11);
+            eob = kind == kFastEOB;
+            coefk = kind == 0;
+            run = eob ? 63 - z : ((fe >> 5) & 63u);
+            coef = int32_t(fe) >> 16;
+        } else {
+            uint32_t maxlen;
+            const uint32_t e = dev_lookup(t, uint32_t(acc >> 48), maxlen);
+            const uint32_t clen = e >> 8, sym = e & 255u;
+            int32_t err = 0;
+            if (clen == 0) {
+                err = avail < maxlen ? kOutOfBits : kInvalidCode;
+            } else if (clen > avail) {
+                err = kOutOfBits;
+            } else if (z == 0) {
+                l = sym;
+                if (l > 11)
+                    err = kInvalidCode;
+                else if (avail - clen < l)
+                    err = kOutOfBits;
+                coefk = true;
+            } else {
+                const uint32_t r = sym >> 4;
+                l = sym & 15u;
+                if (l == 0) {
+                    if (r == 0) {
+                        eob = true;
+                        run = 63 - z;
+                    } else if (r == 15) {
+                        run = 15;
+                    } else {
+                        err = kInvalidCode;
+                    }
+                } else if (l > 10) {
+                    err = kInvalidCode;
+                } else if (avail - clen < l) {
+                    err = kOutOfBits;
+                } else {
+                    run = r;
+                    coefk = true;
+                }
+            }
+            if (err) {
+                s.div = true;
+                s.err = err;
+                break;
+            }
+            if (l) {
+                const uint32_t bits = uint32_t((acc << clen) >> (64 - l));
+                coef = bits >= (1u << (l - 1)) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1);
+            }
+            len = clen + l;
         }
-        const uint32_t total = len + l;
+        const uint32_t total = len;
         const uint32_t step = run + 1;
         if (Sink::kWrite && n + step > cap) break;  // phantom tail past the true end
         if (z == 0) {

@@ -316,13 +316,15 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     std::map<std::vector<uint8_t>, uint32_t> huff_ids, quant_ids;
     std::vector<DevHuff> huffs;
     std::vector<std::array<uint16_t, 64>> quants;
-    auto huff_id = [&](const HuffSpec& s) -> uint32_t {
-        std::vector<uint8_t> key(s.counts.begin(), s.counts.end());
+    auto huff_id = [&](const HuffSpec& s, bool dc) -> uint32_t {
+        std::vector<uint8_t> key(1, dc ? 0 : 1);
+        key.insert(key.end(), s.counts.begin(), s.counts.end());
         key.insert(key.end(), s.symbols.begin(), s.symbols.end());
         auto it = huff_ids.find(key);
         if (it != huff_ids.end()) return it->second;
         DevHuff d;
         build_dev_huff(s, &d);
+        build_fast(&d, dc);
         huffs.push_back(d);
         uint32_t id = uint32_t(huffs.size() - 1);
         huff_ids.emplace(std::move(key), id);
@@ -417,8 +419,8 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
             d.plane_w[c] = h.comp_width(c);
             d.plane_h[c] = h.comp_height(c);
             if (h.table_status == kOk) {
-                d.dc_tab[c] = uint16_t(huff_id(h.dc[h.comps[c].td]));
-                d.ac_tab[c] = uint16_t(huff_id(h.ac[h.comps[c].ta]));
+                d.dc_tab[c] = uint16_t(huff_id(h.dc[h.comps[c].td], true));
+                d.ac_tab[c] = uint16_t(huff_id(h.ac[h.comps[c].ta], false));
             }
             d.q_tab[c] = uint16_t(quant_id(h.quant[h.comps[c].tq]));
         }
@@ -680,6 +682,17 @@ int pjg_batch_download_all(pjg_batch* b, void* host, size_t cap) {
     float ms = 0;
     cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
     b->stage_ms[PJG_STAGE_DOWNLOAD] = ms;
+    return PJG_OK;
+}
+
+int pjg_batch_download_all_async(pjg_batch* b, void* host, size_t cap) {
+    if (!b || !host) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    if (cap < b->out_bytes) return fail(ctx, PJG_CAPACITY, "output buffer too small");
+    if (!b->decoded) return fail(ctx, PJG_NOT_DECODED, "batch not decoded");
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (b->out_bytes)
+        CU(cudaMemcpyAsync(host, ctx->out.p, b->out_bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H out");
     return PJG_OK;
 }
 

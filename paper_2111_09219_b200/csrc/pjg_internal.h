@@ -35,7 +35,13 @@ enum Status : int32_t {
 // codes of length <= 9; longer codes walk per-length maxcode (Annex F.2.2.3).
 constexpr int kPrimaryBits = 9;
 
+constexpr int kFastBits = 11;
+// fast entry: bits 0-4 total length (code + magnitude, 0 = not fast), 5-10 run,
+// 11-12 kind (0 coefficient, 1 EOB, 2 ZRL), 16-31 coefficient (int16)
+constexpr uint32_t kFastEOB = 1u << 11, kFastZRL = 2u << 11;
+
 struct DevHuff {
+    uint32_t fast[1 << kFastBits];    // code + magnitude in one probe when both fit in kFastBits
     uint16_t lut[1 << kPrimaryBits];  // (length << 8) | symbol; length 0 = unresolved
     int32_t maxcode[18];              // per length 1..16 ([17] unused), -1 when no code has that length
     int32_t valoff[18];               // symbol index = code + valoff[len]
