@@ -810,32 +810,63 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
 // with a neighbouring subsequence write only the owned slots.
 constexpr int kBlkStride = 72;
 
+// Per data unit K3 also emits K4's metadata (it sees the few nonzero
+// coefficients as it decodes them; K4 would have to scan all 64):
+//   flags = nonzero-row mask | has-AC << 8 | big << 9, and
+//   S = sum over nonzero F of w_u w_v |F| (bounds |r| and the FP32 IDCT error).
+// Units split between two subsequences combine through atomics into the
+// buffer zeroed before K3.
+constexpr uint32_t kMetaNonDc = 1u << 8, kMetaBig = 1u << 9;
+
 struct BlockSink {
     static constexpr bool kWrite = true;
+    const uint8_t* zz2r; // zig-zag -> raster, in smem (lane-divergent index)
+    const float* wts;    // w_u * w_v per raster index, in smem
     int16_t* buf;        // this thread's smem block
     int16_t* coef;       // batch coefficient buffer
+    uint2* meta;         // batch per-unit metadata
     uint64_t du_first;   // image's first data unit
     uint64_t own_lo;     // owned slots [own_lo, own_hi) within the image
     uint64_t own_hi;
     uint64_t cur;        // current block (image-relative)
+    uint64_t du_comp;    // slot -> component nibbles
+    const uint16_t* q0;  // raster quantisers of components 0..2
+    const uint16_t* q1;
+    const uint16_t* q2;
+    const uint16_t* qc;  // quantiser of the current unit
+    uint32_t slot, dpm;
+    uint32_t mflags;     // metadata of the current unit (owned part)
+    float mS;
 
+    __device__ __forceinline__ void set_unit_comp() {
+        const uint32_t comp = uint32_t(du_comp >> (4 * slot)) & 15u;
+        qc = comp == 0 ? q0 : (comp == 1 ? q1 : q2);
+    }
     __device__ __forceinline__ void flush(uint64_t b) {
         const uint64_t lo = max(own_lo, b * 64), hi = min(own_hi, b * 64 + 64);
         int16_t* dst = coef + (du_first + b) * 64;
+        uint2* md = meta + du_first + b;
         if (lo == b * 64 && hi == b * 64 + 64) {
             const int4* s4 = reinterpret_cast<const int4*>(buf);
             int4* d4 = reinterpret_cast<int4*>(dst);
 #pragma unroll
             for (int q = 0; q < 8; ++q) d4[q] = s4[q];
+            *md = make_uint2(mflags, __float_as_uint(mS));
         } else {
             for (uint64_t sl = lo; sl < hi; ++sl) {
-                int r = c_zz2r[sl & 63];
+                int r = zz2r[sl & 63];
                 dst[r] = buf[r];
             }
+            if (mflags) atomicOr(&md->x, mflags);
+            if (mS != 0.f) atomicAdd(reinterpret_cast<float*>(&md->y), mS);
         }
         int4 zero = make_int4(0, 0, 0, 0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(buf)[q] = zero;
+        mflags = 0;
+        mS = 0.f;
+        slot = (slot + 1 == dpm) ? 0 : slot + 1;
+        set_unit_comp();
     }
     // slot relative to this subsequence's offset is passed as local index
     uint64_t base;       // own_lo
@@ -846,7 +877,14 @@ struct BlockSink {
             flush(cur);
             ++cur;
         }
-        buf[c_zz2r[s & 63]] = int16_t(v);
+        const uint32_t r = zz2r[s & 63];
+        buf[r] = int16_t(v);
+        if (int16_t(v) != 0) {
+            const int32_t F = int32_t(int16_t(v)) * int32_t(__ldg(qc + r));
+            const uint32_t a = uint32_t(abs(F));
+            mflags |= (1u << (r >> 3)) | (r ? kMetaNonDc : 0u) | (a >= (1u << 22) ? kMetaBig : 0u);
+            mS = fmaf(wts[r], float(a), mS);
+        }
     }
     __device__ __forceinline__ void finish() {
         if (own_hi <= own_lo) return;
@@ -860,7 +898,16 @@ struct BlockSink {
 
 __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
     __shared__ __align__(16) int16_t s_blk[kK3Threads * kBlkStride];
+    __shared__ uint8_t s_zz2r[64];
+    __shared__ float s_wts[64];
     const int tid = threadIdx.x;
+    if (tid < 64) {
+        // max_x |basis[u][x]| rounded up, product over (row, column)
+        const float w[8] = {0.35356f, 0.4904f, 0.46195f, 0.4904f, 0.35356f, 0.4904f, 0.46195f, 0.4904f};
+        s_zz2r[tid] = c_zz2r[tid];
+        s_wts[tid] = w[tid >> 3] * w[tid & 7];
+    }
+    __syncthreads();
     int16_t* buf = s_blk + tid * kBlkStride;
     {
         int4 zero = make_int4(0, 0, 0, 0);
@@ -895,6 +942,18 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
     s.dc2 = int16_t(pd.hi & 0xFFFFu);
     const uint64_t o = P.off[g];
     BlockSink sink;
+    sink.zz2r = s_zz2r;
+    sink.wts = s_wts;
+    sink.meta = P.meta;
+    sink.du_comp = D.du_comp;
+    sink.dpm = D.dpm;
+    sink.q0 = P.quant_raster + 64u * D.q_tab[0];
+    sink.q1 = P.quant_raster + 64u * D.q_tab[1];
+    sink.q2 = P.quant_raster + 64u * D.q_tab[2];
+    sink.slot = uint32_t((o >> 6) % D.dpm);
+    sink.set_unit_comp();
+    sink.mflags = 0;
+    sink.mS = 0.f;
     sink.buf = buf;
     sink.coef = P.coef;
     sink.du_first = D.du_first;
@@ -1196,11 +1255,14 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
     // prefetch of the current tile: 3 x 16 B per lane (rows lane, lane+32, lane+64
     // of the tile's units), issued one tile ahead
     uint4 pf[3];
+    uint2 pm;  // metadata of unit `lane` of the prefetched tile
     auto issue = [&](const TileWalk& tw) {
         const uint32_t mx0 = tw.tx * tw.MT;
         const uint32_t nblk = min(tw.MT, tw.mcus_x - mx0) * tw.dpm;
-        const int4* src = reinterpret_cast<const int4*>(
-            P.coef + (tw.du_first + (uint64_t(tw.my) * tw.mcus_x + mx0) * tw.dpm) * 64);
+        const uint64_t du0 = tw.du_first + (uint64_t(tw.my) * tw.mcus_x + mx0) * tw.dpm;
+        const int4* src = reinterpret_cast<const int4*>(P.coef + du0 * 64);
+        pm = make_uint2(0, 0);
+        if (tw.valid && uint32_t(lane) < nblk) pm = __ldcs(P.meta + du0 + lane);
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             const uint32_t ch = lane + 32 * j;
@@ -1224,60 +1286,49 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
         }
         const WarpImg& I = S.img;
 
-        // 1. dequantise the prefetched rows
+        // 1. dequantise the prefetched rows; row masks / bounds come from K3's
+        //    per-unit metadata (flags = rows | has-AC << 8 | big << 9, S)
         if (cur_valid) {
+            if (uint32_t(lane) < nblk) {
+                const float Sb = __uint_as_float(pm.y);
+                const bool big = (pm.x & kMetaBig) || Sb >= 2097152.f;
+                const bool dconly = (pm.x & 0xFFu) <= 1u && !(pm.x & kMetaNonDc);
+                S.rows[lane] = uint16_t((pm.x & 0xFFu) | (big ? 0x100u : 0u) | (dconly ? 0x200u : 0u));
+                // |r32 - r64| <= 18u S (+ FP64's own ~1e-15 S), u = 2^-24
+                S.lim[lane] = 0.5f - (1.1e-6f * Sb + 2.0e-6f);
+            }
 #pragma unroll 1
-        for (int j = 0; j < 3; ++j) {
-            const uint32_t ch = lane + 32 * j, blk = ch >> 3, u = ch & 7;
-            const bool act = ch < nblk * 8;
-            uint32_t m = 0, asum = 0;
-            int32_t d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            if (act) {
-                const uint4 rv = j == 0 ? pf[0] : (j == 1 ? pf[1] : pf[2]);
-                const uint4 qv = *reinterpret_cast<const uint4*>(I.q[I.bcomp[blk]] + u * 8);
-                const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
-                uint32_t ror = 0, aor = 0;
+            for (int j = 0; j < 3; ++j) {
+                const uint32_t ch = lane + 32 * j, blk = ch >> 3, u = ch & 7;
+                const uint32_t flags = __shfl_sync(0xFFFFFFFFu, pm.x, blk & 31);
+                const float Sb = __uint_as_float(__shfl_sync(0xFFFFFFFFu, pm.y, blk & 31));
+                if (ch < nblk * 8) {
+                    float4* dst = reinterpret_cast<float4*>(S.F + ch * 8);
+                    if (!((flags >> u) & 1u)) {
+                        dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    } else {
+                        const uint4 rv = j == 0 ? pf[0] : (j == 1 ? pf[1] : pf[2]);
+                        const uint4 qv = *reinterpret_cast<const uint4*>(I.q[I.bcomp[blk]] + u * 8);
+                        const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
+                        int32_t d[8];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    d[2 * e] = int32_t(int16_t(rw[e] & 0xFFFFu)) * int32_t(qw[e] & 0xFFFFu);
-                    d[2 * e + 1] = (int32_t(rw[e]) >> 16) * int32_t(qw[e] >> 16);
-                    ror |= rw[e];
-                    const uint32_t a0 = uint32_t(abs(d[2 * e])), a1 = uint32_t(abs(d[2 * e + 1]));
-                    aor |= a0 | a1;
-                    asum += a0 + a1;  // cannot wrap unless some |d| >= 2^22 (then big)
-                }
-                // row mask bit, big flag, and (row 0 only) "a v > 0 coefficient"
-                m = (ror ? (1u << u) : 0u) | (aor >= (1u << 22) ? 0x100u : 0u) |
-                    ((u == 0 && ((rv.x >> 16) | rv.y | rv.z | rv.w) != 0u) ? 0x400u : 0u);
-            }
-            const float wu = (u & 3) == 0 ? 0.35356f : ((u & 3) == 2 ? 0.46195f : 0.4904f);
-            float Ssum = float(asum) * (wu * 0.4904f);
-            m |= __shfl_xor_sync(0xFFFFFFFFu, m, 1);
-            m |= __shfl_xor_sync(0xFFFFFFFFu, m, 2);
-            m |= __shfl_xor_sync(0xFFFFFFFFu, m, 4);
-            Ssum += __shfl_xor_sync(0xFFFFFFFFu, Ssum, 1);
-            Ssum += __shfl_xor_sync(0xFFFFFFFFu, Ssum, 2);
-            Ssum += __shfl_xor_sync(0xFFFFFFFFu, Ssum, 4);
-            const bool big = (m & 0x100u) || Ssum >= 2097152.f;
-            if (act) {
-                float4* dst = reinterpret_cast<float4*>(S.F + ch * 8);
-                if (!big) {
-                    dst[0] = make_float4(float(d[0]), float(d[1]), float(d[2]), float(d[3]));
-                    dst[1] = make_float4(float(d[4]), float(d[5]), float(d[6]), float(d[7]));
-                } else {
-                    dst[0] = make_float4(__int_as_float(d[0]), __int_as_float(d[1]), __int_as_float(d[2]),
-                                         __int_as_float(d[3]));
-                    dst[1] = make_float4(__int_as_float(d[4]), __int_as_float(d[5]), __int_as_float(d[6]),
-                                         __int_as_float(d[7]));
-                }
-                if (u == 0) {
-                    const bool dconly = (m & 0xFEu) == 0 && !(m & 0x400u);
-                    S.rows[blk] = uint16_t((m & 0xFFu) | (big ? 0x100u : 0u) | (dconly ? 0x200u : 0u));
-                    // |r32 - r64| <= 18u S (+ FP64's own ~1e-15 S), u = 2^-24
-                    S.lim[blk] = 0.5f - (1.1e-6f * Ssum + 2.0e-6f);
+                        for (int e = 0; e < 4; ++e) {
+                            d[2 * e] = int32_t(int16_t(rw[e] & 0xFFFFu)) * int32_t(qw[e] & 0xFFFFu);
+                            d[2 * e + 1] = (int32_t(rw[e]) >> 16) * int32_t(qw[e] >> 16);
+                        }
+                        if (!((flags & kMetaBig) || Sb >= 2097152.f)) {
+                            dst[0] = make_float4(float(d[0]), float(d[1]), float(d[2]), float(d[3]));
+                            dst[1] = make_float4(float(d[4]), float(d[5]), float(d[6]), float(d[7]));
+                        } else {  // exact-FP64 unit: keep the int32 bits
+                            dst[0] = make_float4(__int_as_float(d[0]), __int_as_float(d[1]), __int_as_float(d[2]),
+                                                 __int_as_float(d[3]));
+                            dst[1] = make_float4(__int_as_float(d[4]), __int_as_float(d[5]), __int_as_float(d[6]),
+                                                 __int_as_float(d[7]));
+                        }
+                    }
                 }
             }
-        }
         }
         // advance the walk and prefetch the next tile (in flight during 2 + 3)
         if (t + 1 < t_end) {

@@ -89,7 +89,7 @@ struct pjg_ctx {
     bool busy = false;
     double basis[64];
     cudaEvent_t ev[kNumEvents] = {};
-    DevBuf raw, ubuf, meta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out,
+    DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out,
         counters, k0_flag, k0_agg, k2_flag, k2_agg, stats;
     HostBuf stage, meta_host, status_host;
 };
@@ -256,7 +256,7 @@ void pjg_ctx_destroy(pjg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    for (DevBuf* b : {&c->raw, &c->ubuf, &c->meta, &c->ent, &c->dcs, &c->off, &c->cap, &c->pred,
+    for (DevBuf* b : {&c->raw, &c->ubuf, &c->meta, &c->blkmeta, &c->ent, &c->dcs, &c->off, &c->cap, &c->pred,
                       &c->cta_end, &c->cta_start, &c->k1_flag, &c->coef, &c->out, &c->counters,
                       &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats})
         b->release();
@@ -510,6 +510,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     CU(ctx->cta_start.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_start)");
     CU(ctx->k1_flag.ensure((b->k1_ctas + 1) * 4), "cudaMalloc(k1_flag)");
     CU(ctx->coef.ensure(std::max<uint64_t>(du, 1) * 128), "cudaMalloc(coef)");
+    CU(ctx->blkmeta.ensure(std::max<uint64_t>(du, 1) * 8), "cudaMalloc(blkmeta)");
     CU(ctx->out.ensure(std::max<uint64_t>(outb, 1)), "cudaMalloc(out)");
     CU(ctx->counters.ensure(kNumCounters * 4), "cudaMalloc(counters)");
     CU(ctx->stats.ensure(kNumStats * 8), "cudaMalloc(stats)");
@@ -548,6 +549,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.k4_tiles = k4t;
     p.tile_first = reinterpret_cast<const uint32_t*>(md + b->m_tile);
     p.coef = ctx->coef.as<int16_t>();
+    p.meta = ctx->blkmeta.as<uint2>();
     p.out = ctx->out.as<uint8_t>();
     p.counters = ctx->counters.as<uint32_t>();
     p.k0_flag = ctx->k0_flag.as<uint32_t>();
@@ -601,6 +603,7 @@ int pjg_batch_decode(pjg_batch* b) {
     CU(cudaEventRecord(ctx->ev[4], s), "ev");
     launch_k2_scan(b->prm, s);
     CU(cudaEventRecord(ctx->ev[5], s), "ev");
+    if (b->total_dus) CU(cudaMemsetAsync(ctx->blkmeta.p, 0, b->total_dus * 8, s), "memset meta");
     launch_k3_write(b->prm, s);
     CU(cudaEventRecord(ctx->ev[6], s), "ev");
     launch_k4_transform(b->prm, s);

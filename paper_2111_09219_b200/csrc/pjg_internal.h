@@ -3,6 +3,11 @@
 #pragma once
 
 #include <stdint.h>
+#ifndef __CUDACC__
+struct uint2 { unsigned int x, y; };
+#else
+#include <vector_types.h>
+#endif
 
 #ifdef __CUDACC__
 #define PJG_HD __host__ __device__ __forceinline__
@@ -175,6 +180,7 @@ struct Params {
     // K4
     const uint32_t* tile_first;    // n_img + 1 prefix of K4 tiles
     int16_t* coef;                 // 64 int16 per data unit, raster order, absolute DC
+    uint2* meta;                   // per data unit: flags (row mask | has-AC | big), S (K3 -> K4)
     uint8_t* out;
     // lookback scratch
     uint32_t* counters;            // tickets (reset per run)
