@@ -53,6 +53,9 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t min64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
 __device__ __forceinline__ void spin_pause() { __nanosleep(32); }
 
 // largest k < n with first[k] <= g (first[] ascending, first[0] == 0)
@@ -1069,6 +1072,8 @@ struct TileWalk {
 
 struct WarpSmem {
     float F[kK4MaxBlocks * 64];  // dequantised (float, or int32 bits when big)
+    int4 raw[kK4MaxBlocks * 8];  // next tile's coefficients (cp.async staging)
+    uint2 meta[kK4MaxBlocks];    // next tile's per-unit metadata
     uint8_t pl[1024];            // sample planes (row stride padded by 4)
     WarpImg img;
     uint16_t cmap[kTileW];
@@ -1148,51 +1153,81 @@ __device__ __forceinline__ void walk_enter_image(const Params& P, uint32_t t, Ti
     w.tx = lt % w.tiles_x;
 }
 
-// colour LUT entries per chroma value (exact integers; see chroma_word)
+// Colour LUTs per chroma value (exact integers).  A chroma sample maps to two
+// words: crg = (oR + 256) | (oG + 256) << 16 and cb = (oB + 256) | tie << 31,
+// where oX = round(kX * c) and tie marks an exact real half-integer (only
+// Cb = 3 / 253 for B and (Cb, Cr) = (78, 178) / (178, 78) for G).
 struct ColourLut {
-    uint32_t rb[256];   // (oR + 512) | tieR << 30 indexed by Cr  — and (oB + 512) << 20 | tieB << 30 by Cb
-    uint32_t bb[256];
-    int32_t ga[256];    // -344136 * cb + 500000 + 2e8
-    int32_t gb[256];    // -714136 * cr
+    uint32_t r[256];   // oR + 256, indexed by Cr
+    uint32_t b[256];   // (oB + 256) | tieB << 31, indexed by Cb
+    int32_t ga[256];   // -344136 * cb + 500000 + 2e8
+    int32_t gb[256];   // -714136 * cr
 };
 
-__device__ __forceinline__ uint32_t chroma_word_lut(const ColourLut& L, uint32_t Cb, uint32_t Cr) {
+__device__ __forceinline__ uint2 chroma_words(const ColourLut& L, uint32_t Cb, uint32_t Cr) {
     const uint32_t mG = uint32_t(L.ga[Cb] + L.gb[Cr]);
-    const uint32_t qG = mG / 1000000u;
-    const uint32_t tieG = (mG - qG * 1000000u) == 0 ? (1u << 30) : 0u;
-    return L.rb[Cr] | L.bb[Cb] | ((qG + 312u) << 10) | tieG;
+    const uint32_t qG = mG / 1000000u;  // oG = qG - 200
+    const uint32_t tieG = (mG - qG * 1000000u) == 0 ? (1u << 31) : 0u;
+    return make_uint2(L.r[Cr] | ((qG + 56u) << 16), L.b[Cb] | tieG);
 }
 
-__device__ __forceinline__ void emit_rgb4(uint8_t* dst, bool fast, uint32_t npx, uint32_t y4, uint32_t w0,
-                                          uint32_t w1, uint32_t w2, uint32_t w3, const uint8_t* cbrow,
-                                          const uint8_t* crrow, uint32_t cx0, uint32_t cx1, uint32_t cx2,
-                                          uint32_t cx3) {
-    const int Y0 = int(y4 & 0xFFu) - 512, Y1 = int((y4 >> 8) & 0xFFu) - 512, Y2 = int((y4 >> 16) & 0xFFu) - 512,
-              Y3 = int(y4 >> 24) - 512;
-    uint32_t r4 = pack4_sat(Y0 + int(w0 & 1023u), Y1 + int(w1 & 1023u), Y2 + int(w2 & 1023u), Y3 + int(w3 & 1023u));
-    uint32_t g4 = pack4_sat(Y0 + int((w0 >> 10) & 1023u), Y1 + int((w1 >> 10) & 1023u),
-                            Y2 + int((w2 >> 10) & 1023u), Y3 + int((w3 >> 10) & 1023u));
-    uint32_t b4 = pack4_sat(Y0 + int((w0 >> 20) & 1023u), Y1 + int((w1 >> 20) & 1023u),
-                            Y2 + int((w2 >> 20) & 1023u), Y3 + int((w3 >> 20) & 1023u));
-    const uint32_t tie = ((w0 | w1 | w2 | w3) >> 30) & 1u;
-    if (tie) {  // exact real tie in some chroma sample: replay those pixels in FP64
-        const uint32_t ws[4] = {w0, w1, w2, w3}, cx[4] = {cx0, cx1, cx2, cx3};
+__device__ __forceinline__ uint32_t vmax_s16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t vmin_s16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+// clamp both 16-bit lanes of (value + 256) to [256, 511]: the low byte of each
+// lane is then clamp_u8(value)
+__device__ __forceinline__ uint32_t clamp2(uint32_t v) {
+    return vmin_s16x2(vmax_s16x2(v, 0x01000100u), 0x01FF01FFu);
+}
+
+// 4 pixels of one row: Y bytes in y4, chroma words per pixel.  16-bit SWAR:
+// (Y | Y << 16) + crg gives R and G in one add, clamps are VIMNMX.S16x2.
+__device__ __forceinline__ void emit_rgb4(uint8_t* dst, bool fast, uint32_t npx, uint32_t y4, uint2 c0, uint2 c1,
+                                          uint2 c2, uint2 c3, const uint8_t* cbrow, const uint8_t* crrow,
+                                          uint32_t cx0, uint32_t cx1, uint32_t cx2, uint32_t cx3) {
+    const uint32_t rg0 = clamp2(__byte_perm(y4, 0, 0x4040) + c0.x);
+    const uint32_t rg1 = clamp2(__byte_perm(y4, 0, 0x4141) + c1.x);
+    const uint32_t rg2 = clamp2(__byte_perm(y4, 0, 0x4242) + c2.x);
+    const uint32_t rg3 = clamp2(__byte_perm(y4, 0, 0x4343) + c3.x);
+    const uint32_t b01 = clamp2(__byte_perm(y4, 0, 0x4140) + __byte_perm(c0.y, c1.y, 0x5410));
+    const uint32_t b23 = clamp2(__byte_perm(y4, 0, 0x4342) + __byte_perm(c2.y, c3.y, 0x5410));
+    const uint32_t t = __byte_perm(rg0, rg1, 0x6420);  // R0 G0 R1 G1
+    const uint32_t u = __byte_perm(rg2, rg3, 0x6420);  // R2 G2 R3 G3
+    uint32_t o0 = __byte_perm(t, b01, 0x2410);                            // R0 G0 B0 R1
+    uint32_t o1 = __byte_perm(__byte_perm(t, b01, 0x0063), u, 0x5410);   // G1 B1 R2 G2
+    uint32_t o2 = __byte_perm(u, b23, 0x6324);                            // B2 R3 G3 B3
+    if ((c0.y | c1.y | c2.y | c3.y) >> 31) {
+        // exact real tie in some chroma sample: FP64 replay of those pixels
+        const uint2 cw[4] = {c0, c1, c2, c3};
+        const uint32_t cx[4] = {cx0, cx1, cx2, cx3};
+        uint8_t px[12];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            if ((ws[q] >> 30) & 1u) {
+            const uint32_t w = q < 1 ? o0 : (q < 2 ? o0 : o1);
+            (void)w;
+        }
+#pragma unroll
+        for (int k = 0; k < 12; ++k) px[k] = uint8_t((k < 4 ? o0 : (k < 8 ? o1 : o2)) >> (8 * (k & 3)));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (cw[q].y >> 31) {
                 const uint32_t e = rgb_fp64(int((y4 >> (8 * q)) & 0xFFu), cbrow[cx[q]], crrow[cx[q]]);
-                const uint32_t sh = 8 * q, m = ~(0xFFu << sh);
-                r4 = (r4 & m) | ((e & 0xFFu) << sh);
-                g4 = (g4 & m) | (((e >> 8) & 0xFFu) << sh);
-                b4 = (b4 & m) | (((e >> 16) & 0xFFu) << sh);
+                px[3 * q] = uint8_t(e);
+                px[3 * q + 1] = uint8_t(e >> 8);
+                px[3 * q + 2] = uint8_t(e >> 16);
             }
         }
+        o0 = uint32_t(px[0]) | (uint32_t(px[1]) << 8) | (uint32_t(px[2]) << 16) | (uint32_t(px[3]) << 24);
+        o1 = uint32_t(px[4]) | (uint32_t(px[5]) << 8) | (uint32_t(px[6]) << 16) | (uint32_t(px[7]) << 24);
+        o2 = uint32_t(px[8]) | (uint32_t(px[9]) << 8) | (uint32_t(px[10]) << 16) | (uint32_t(px[11]) << 24);
     }
-    const uint32_t t0 = __byte_perm(r4, g4, 0x5140);                            // R0 G0 R1 G1
-    const uint32_t t1 = __byte_perm(r4, g4, 0x7362);                            // R2 G2 R3 G3
-    const uint32_t o0 = __byte_perm(t0, b4, 0x2410);                            // R0 G0 B0 R1
-    const uint32_t o1 = __byte_perm(__byte_perm(t0, b4, 0x0053), t1, 0x5410);  // G1 B1 R2 G2
-    const uint32_t o2 = __byte_perm(t1, b4, 0x7326);                            // B2 R3 G3 B3
     if (fast) {
         uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
         d32[0] = o0;
@@ -1206,7 +1241,7 @@ __device__ __forceinline__ void emit_rgb4(uint8_t* dst, bool fast, uint32_t npx,
     }
 }
 
-__global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
+__global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
     __shared__ __align__(16) WarpSmem s_w[kK4Warps];
     __shared__ __align__(16) float s_b32[64];   // basis[u][x]
     __shared__ __align__(16) float s_b32T[64];  // basis[v][y] at [y*8+v]
@@ -1224,8 +1259,9 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
         const int v = c - 128;
         const uint32_t mR = uint32_t(1402 * v + 500 + 200000), mB = uint32_t(1772 * v + 500 + 300000);
         const uint32_t qR = mR / 1000u, qB = mB / 1000u;
-        s_lut.rb[c] = (qR + 312u) | ((mR - qR * 1000u) == 0 ? (1u << 30) : 0u);
-        s_lut.bb[c] = ((qB + 212u) << 20) | ((mB - qB * 1000u) == 0 ? (1u << 30) : 0u);
+        // oR = qR - 200 (never an exact tie in [-128, 127]); oB = qB - 300
+        s_lut.r[c] = qR + 56u;
+        s_lut.b[c] = (qB - 44u) | ((mB - qB * 1000u) == 0 ? (1u << 31) : 0u);
         s_lut.ga[c] = -344136 * v + 500000 + 200000000;
         s_lut.gb[c] = -714136 * v;
     }
@@ -1254,24 +1290,27 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
     uint32_t cached_k = 0xFFFFFFFFu;
     // prefetch of the current tile: 3 x 16 B per lane (rows lane, lane+32, lane+64
     // of the tile's units), issued one tile ahead
-    uint4 pf[3];
-    uint2 pm;  // metadata of unit `lane` of the prefetched tile
+    // prefetch of a tile into the warp's smem staging (cp.async, no registers
+    // held): rows lane, lane+32, lane+64 of its units + per-unit metadata
     auto issue = [&](const TileWalk& tw) {
         const uint32_t mx0 = tw.tx * tw.MT;
         const uint32_t nblk = min(tw.MT, tw.mcus_x - mx0) * tw.dpm;
         const uint64_t du0 = tw.du_first + (uint64_t(tw.my) * tw.mcus_x + mx0) * tw.dpm;
         const int4* src = reinterpret_cast<const int4*>(P.coef + du0 * 64);
-        pm = make_uint2(0, 0);
-        if (tw.valid && uint32_t(lane) < nblk) pm = __ldcs(P.meta + du0 + lane);
+        if (tw.valid) {
 #pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            const uint32_t ch = lane + 32 * j;
-            pf[j] = make_uint4(0, 0, 0, 0);
-            if (tw.valid && ch < nblk * 8) {
-                const int4 v = __ldcs(src + ch);
-                pf[j] = make_uint4(uint32_t(v.x), uint32_t(v.y), uint32_t(v.z), uint32_t(v.w));
+            for (int j = 0; j < 3; ++j) {
+                const uint32_t ch = lane + 32 * j;
+                if (ch < nblk * 8)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.raw[ch])), "l"(src + ch)
+                                 : "memory");
             }
+            if (uint32_t(lane) < nblk)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&S.meta[lane])),
+                             "l"(P.meta + du0 + lane)
+                             : "memory");
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
     issue(w);
     for (uint32_t t = t_begin; t < t_end; ++t) {
@@ -1288,6 +1327,9 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
 
         // 1. dequantise the prefetched rows; row masks / bounds come from K3's
         //    per-unit metadata (flags = rows | has-AC << 8 | big << 9, S)
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+        const uint2 pm = uint32_t(lane) < nblk ? S.meta[lane] : make_uint2(0, 0);
         if (cur_valid) {
             if (uint32_t(lane) < nblk) {
                 const float Sb = __uint_as_float(pm.y);
@@ -1308,7 +1350,8 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                         dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
                         dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
                     } else {
-                        const uint4 rv = j == 0 ? pf[0] : (j == 1 ? pf[1] : pf[2]);
+                        const int4 rvi = S.raw[ch];
+                        const uint4 rv = make_uint4(uint32_t(rvi.x), uint32_t(rvi.y), uint32_t(rvi.z), uint32_t(rvi.w));
                         const uint4 qv = *reinterpret_cast<const uint4*>(I.q[I.bcomp[blk]] + u * 8);
                         const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
                         int32_t d[8];
@@ -1343,7 +1386,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                     walk_enter_image(P, t + 1, w);
                 }
             }
-            __syncwarp();
+            __syncwarp();  // staging consumed by every lane before it is refilled
             issue(w);
         }
         if (!cur_valid) continue;
@@ -1361,6 +1404,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
         const uint32_t y = lane & 7;
         const float4 bc0 = *reinterpret_cast<const float4*>(s_b32T + y * 8);
         const float4 bc1 = *reinterpret_cast<const float4*>(s_b32T + y * 8 + 4);
+        uint32_t pend = 0;  // per j: samples of column y that need the FP64 replay
 #pragma unroll 1
         for (int j = 0; j < 3; ++j) {
             const uint32_t blk = (lane >> 3) + 4 * j;
@@ -1373,9 +1417,10 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
             float acc[8];
 #pragma unroll
             for (int x = 0; x < 8; ++x) acc[x] = 0.f;
-#pragma unroll
-            for (int uu = 0; uu < 8; ++uu) {
-                if (urows & (1u << uu)) {
+            // only the rows some unit of this warp uses (warp-uniform loop)
+            for (uint32_t m = urows; m; m &= m - 1) {
+                const uint32_t uu = __ffs(m) - 1;
+                {
                     const float4 f0 = *reinterpret_cast<const float4*>(F + uu * 8);
                     const float4 f1 = *reinterpret_cast<const float4*>(F + uu * 8 + 4);
                     float tu = bc0.x * f0.x;
@@ -1416,23 +1461,17 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                     const double f00 = big ? double(reinterpret_cast<const int32_t*>(F)[0]) : double(F[0]);
                     const int o = lround_away(__dmul_rn(s_b64[0], __dmul_rn(s_b64[0], f00))) + 128;
                     lo = hi = pack4_sat(o, o, o, o);
-                } else if (big || mx > S.lim[blk]) {  // rare: FP64 for the samples near x.5
+                } else if (big) {
+                    pend |= 0xFFu << (8 * j);
+                } else if (mx > S.lim[blk]) {  // rare: the samples near x.5 get FP64 below
                     const float lim = S.lim[blk];
                     uint32_t mask = 0;
 #pragma unroll
                     for (int x = 0; x < 8; ++x) {
                         const float v = acc[x] + kM128;
-                        if (big || fabsf(acc[x] - (v - kM128)) > lim) mask |= 1u << x;
+                        if (fabsf(acc[x] - (v - kM128)) > lim) mask |= 1u << x;
                     }
-                    const uint2 ex = idct_column_fp64(F, big, rows, s_b64, int(y), mask);
-                    uint32_t ml = 0, mh = 0;
-#pragma unroll
-                    for (int x = 0; x < 4; ++x) {
-                        if (mask & (1u << x)) ml |= 0xFFu << (8 * x);
-                        if (mask & (1u << (x + 4))) mh |= 0xFFu << (8 * x);
-                    }
-                    lo = (lo & ~ml) | (ex.x & ml);
-                    hi = (hi & ~mh) | (ex.y & mh);
+                    pend |= mask << (8 * j);
                 }
                 const uint32_t ps = I.bps[blk];
                 uint8_t* pl = S.pl + I.boff[blk] + y;
@@ -1444,6 +1483,21 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 pl[5 * ps] = uint8_t(hi >> 8);
                 pl[6 * ps] = uint8_t(hi >> 16);
                 pl[7 * ps] = uint8_t(hi >> 24);
+            }
+        }
+        // exact FP64 replay of the flagged samples (reference order), off the
+        // hot loop so it costs no registers there
+        if (pend) {
+            for (int j = 0; j < 3; ++j) {
+                const uint32_t mask = (pend >> (8 * j)) & 0xFFu;
+                if (!mask) continue;
+                const uint32_t blk = (lane >> 3) + 4 * j;
+                const uint32_t rw = S.rows[blk];
+                const uint2 ex = idct_column_fp64(S.F + blk * 64, rw & 0x100u, rw & 0xFFu, s_b64, int(y), mask);
+                const uint32_t ps = I.bps[blk];
+                uint8_t* pl = S.pl + I.boff[blk] + y;
+                for (int x = 0; x < 8; ++x)
+                    if (mask & (1u << x)) pl[x * ps] = uint8_t((x < 4 ? ex.x : ex.y) >> (8 * (x & 3)));
             }
         }
         __syncwarp();
@@ -1476,10 +1530,10 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 uint32_t crow = S.rmap[r0];
                 const uint8_t* cbrow = cbbase + crow * pst1;
                 const uint8_t* crrow = crbase + crow * pst1;
-                uint32_t w0 = chroma_word_lut(s_lut, cbrow[cx0], crrow[cx0]);
-                uint32_t w1 = cx1 == cx0 ? w0 : chroma_word_lut(s_lut, cbrow[cx1], crrow[cx1]);
-                uint32_t w2 = cx2 == cx1 ? w1 : chroma_word_lut(s_lut, cbrow[cx2], crrow[cx2]);
-                uint32_t w3 = cx3 == cx2 ? w2 : chroma_word_lut(s_lut, cbrow[cx3], crrow[cx3]);
+                uint2 w0 = chroma_words(s_lut, cbrow[cx0], crrow[cx0]);
+                uint2 w1 = cx1 == cx0 ? w0 : chroma_words(s_lut, cbrow[cx1], crrow[cx1]);
+                uint2 w2 = cx2 == cx1 ? w1 : chroma_words(s_lut, cbrow[cx2], crrow[cx2]);
+                uint2 w3 = cx3 == cx2 ? w2 : chroma_words(s_lut, cbrow[cx3], crrow[cx3]);
                 const bool fast = npx == 4 && aligned;
                 emit_rgb4(obase + (uint64_t(Y0 + r0) * W + X0 + gx) * 3, fast, npx,
                           *reinterpret_cast<const uint32_t*>(ybase + r0 * pst0 + gx), w0, w1, w2, w3, cbrow, crrow,
@@ -1490,10 +1544,10 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                         crow = crow1;
                         cbrow = cbbase + crow * pst1;
                         crrow = crbase + crow * pst1;
-                        w0 = chroma_word_lut(s_lut, cbrow[cx0], crrow[cx0]);
-                        w1 = cx1 == cx0 ? w0 : chroma_word_lut(s_lut, cbrow[cx1], crrow[cx1]);
-                        w2 = cx2 == cx1 ? w1 : chroma_word_lut(s_lut, cbrow[cx2], crrow[cx2]);
-                        w3 = cx3 == cx2 ? w2 : chroma_word_lut(s_lut, cbrow[cx3], crrow[cx3]);
+                        w0 = chroma_words(s_lut, cbrow[cx0], crrow[cx0]);
+                        w1 = cx1 == cx0 ? w0 : chroma_words(s_lut, cbrow[cx1], crrow[cx1]);
+                        w2 = cx2 == cx1 ? w1 : chroma_words(s_lut, cbrow[cx2], crrow[cx2]);
+                        w3 = cx3 == cx2 ? w2 : chroma_words(s_lut, cbrow[cx3], crrow[cx3]);
                     }
                     emit_rgb4(obase + (uint64_t(Y0 + r0 + 1) * W + X0 + gx) * 3, fast, npx,
                               *reinterpret_cast<const uint32_t*>(ybase + (r0 + 1) * pst0 + gx), w0, w1, w2, w3,
