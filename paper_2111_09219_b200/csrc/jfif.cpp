@@ -279,14 +279,7 @@ void build_fast(DevHuff* t, bool dc) {
                     ok = false;
                 }
             }
-            if (ok && clen + l <= uint32_t(kFastBits)) {
-                int32_t v = 0;
-                if (l) {
-                    const uint32_t bits = (w >> (kFastBits - clen - l)) & ((1u << l) - 1);
-                    v = bits >= (1u << (l - 1)) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1);
-                }
-                f = (clen + l) | (run << 5) | (kind << 11) | (uint32_t(uint16_t(int16_t(v))) << 16);
-            }
+            if (ok) f = clen | (l << 5) | (run << 9) | (kind << 15);
         }
         t->fast[w] = f;
     }

@@ -265,6 +265,36 @@ __device__ __forceinline__ void load_ctx(const Params& P, const ImgDesc& D, uint
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
 
+// Stages the unstuffed-scan bytes a CTA's subsequences touch into shared
+// memory (coalesced 16-byte loads) and returns a word pointer that decode_range
+// can index with absolute word positions (it then reads shared memory through
+// generic loads); returns the global pointer when the range does not fit.
+// [lo, hi) is this thread's byte range (empty when lo >= hi).
+constexpr int kStageBytes = 20480;
+__device__ __forceinline__ const uint32_t* stage_scan(const uint8_t* ubuf, uint64_t lo, uint64_t hi, int tid,
+                                                      int nthreads, int4* s_stage, unsigned long long* s_lo,
+                                                      unsigned long long* s_hi) {
+    if (tid == 0) {
+        *s_lo = ~0ull;
+        *s_hi = 0ull;
+    }
+    __syncthreads();
+    if (lo < hi) {
+        atomicMin(s_lo, (unsigned long long)lo);
+        atomicMax(s_hi, (unsigned long long)hi);
+    }
+    __syncthreads();
+    const uint64_t blo = *s_lo & ~15ull, bhi = *s_hi;
+    const uint32_t* global_words = reinterpret_cast<const uint32_t*>(ubuf);
+    if (!(bhi > blo) || bhi - blo > uint64_t(kStageBytes)) return global_words;
+    const uint32_t n16 = uint32_t((bhi - blo + 15) >> 4);
+    const int4* src = reinterpret_cast<const int4*>(ubuf + blo);
+    for (uint32_t q = tid; q < n16; q += nthreads) s_stage[q] = __ldcs(src + q);
+    __syncthreads();
+    return reinterpret_cast<const uint32_t*>(s_stage) - (blo >> 2);
+}
+
+
 // Device huff_lookup with read-only-path loads.
 __device__ __forceinline__ uint32_t dev_lookup(const DevHuff* t, uint32_t w16, uint32_t& maxlen) {
     maxlen = __ldg(&t->maxlen);
@@ -308,7 +338,7 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
     uint64_t abs = ic.bit_base + s.p;
     uint64_t widx = abs >> 5;
     uint32_t sh = uint32_t(abs & 31);
-    uint64_t acc = (uint64_t(bswap32(__ldg(ic.words + widx))) << 32) | bswap32(__ldg(ic.words + widx + 1));
+    uint64_t acc = (uint64_t(bswap32(ic.words[widx])) << 32) | bswap32(ic.words[widx + 1]);
     acc <<= sh;
     int cnt = 64 - int(sh);
     widx += 2;
@@ -319,7 +349,7 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
     while (p < end_bit) {
         if (Sink::kWrite && n >= cap) break;
         if (cnt <= 32) {
-            acc |= uint64_t(bswap32(__ldg(ic.words + widx))) << (32 - cnt);
+            acc |= uint64_t(bswap32(ic.words[widx])) << (32 - cnt);
             cnt += 32;
             ++widx;
         }
@@ -333,13 +363,19 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
         uint32_t len, l = 0, run = 0;
         bool eob = false, coefk = false;
         int32_t coef = 0;
-        if ((fe & 31u) != 0 && avail >= 16) {
-            len = fe & 31u;  // code + magnitude bits
-            const uint32_t kind = fe & (3u << 11);
+        if ((fe & 31u) != 0 && avail >= 32) {
+            // codeword resolved by one probe; magnitude bits read arithmetically
+            // (all code + magnitude bits are real: <= 11 + 11 < 32 <= avail)
+            const uint32_t clen = fe & 31u;
+            l = (fe >> 5) & 15u;
+            const uint32_t kind = fe & (3u << 15);
             eob = kind == kFastEOB;
             coefk = kind == 0;
-            run = eob ? 63 - z : ((fe >> 5) & 63u);
-            coef = int32_t(fe) >> 16;
+            run = eob ? 63 - z : ((fe >> 9) & 63u);
+            const uint32_t top = uint32_t((acc << clen) >> 32);
+            const uint32_t bits = l ? (top >> (32 - l)) : 0u;
+            coef = (l == 0 || (bits >> (l - 1))) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1);
+            len = clen + l;
         } else {
             uint32_t maxlen;
             const uint32_t e = dev_lookup(t, uint32_t(acc >> 48), maxlen);
@@ -471,6 +507,12 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     const bool real = inb && i < N;
     ImgCtx ic;
     load_ctx(P, D, L, ic);
+    {
+        __shared__ int4 s_stage[kStageBytes / 16];
+        __shared__ unsigned long long s_lo, s_hi;
+        const uint64_t lo = real ? D.raw_off + ((i * P.sb) >> 3) : 1, hi = real ? D.raw_off + ((min64((i + 1) * P.sb, L) + 7) >> 3) + 24 : 0;
+        ic.words = stage_scan(P.ubuf, lo, hi, tid, T, s_stage, &s_lo, &s_hi);
+    }
 
     // Round 0: every subsequence decodes from its origin (parallel_decode.hpp:187-195)
     Entry e;
@@ -845,15 +887,31 @@ struct BlockSink {
         const uint32_t comp = uint32_t(du_comp >> (4 * slot)) & 15u;
         qc = comp == 0 ? q0 : (comp == 1 ? q1 : q2);
     }
+    uint32_t dbg;
     __device__ __forceinline__ void flush(uint64_t b) {
+        if (dbg & 16) {  // ablation: no global stores
+            int4 zero = make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(buf)[q] = zero;
+            mflags = 0;
+            mS = 0.f;
+            slot = (slot + 1 == dpm) ? 0 : slot + 1;
+            set_unit_comp();
+            return;
+        }
         const uint64_t lo = max(own_lo, b * 64), hi = min(own_hi, b * 64 + 64);
         int16_t* dst = coef + (du_first + b) * 64;
         uint2* md = meta + du_first + b;
         if (lo == b * 64 && hi == b * 64 + 64) {
+            // full-sector 256-bit stores (STG.E.ENL2.256): no partial-sector merges in L2
             const int4* s4 = reinterpret_cast<const int4*>(buf);
-            int4* d4 = reinterpret_cast<int4*>(dst);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) d4[q] = s4[q];
+            for (int q = 0; q < 4; ++q) {
+                const int4 a = s4[2 * q], c = s4[2 * q + 1];
+                asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 16 * q), "r"(a.x),
+                             "r"(a.y), "r"(a.z), "r"(a.w), "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w)
+                             : "memory");
+            }
             *md = make_uint2(mflags, __float_as_uint(mS));
         } else {
             for (uint64_t sl = lo; sl < hi; ++sl) {
@@ -882,7 +940,7 @@ struct BlockSink {
         }
         const uint32_t r = zz2r[s & 63];
         buf[r] = int16_t(v);
-        if (int16_t(v) != 0) {
+        if (!(dbg & 32) && int16_t(v) != 0) {
             const int32_t F = int32_t(int16_t(v)) * int32_t(__ldg(qc + r));
             const uint32_t a = uint32_t(abs(F));
             mflags |= (1u << (r >> 3)) | (r ? kMetaNonDc : 0u) | (a >= (1u << 22) ? kMetaBig : 0u);
@@ -918,16 +976,24 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
         for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(buf)[q] = zero;
     }
     const uint64_t g = uint64_t(blockIdx.x) * kK3Threads + tid;
-    if (g >= P.total_subs) return;
-    const uint32_t cap = P.cap[g];
-    if (cap == 0) return;
-    const uint32_t k = find_seg(P.sub_first, P.n_img, g);
-    if (P.ist[k].status != 0) return;
+    const bool inb = g < P.total_subs;
+    const uint32_t cap = inb ? P.cap[g] : 0u;
+    const uint32_t k = find_seg(P.sub_first, P.n_img, inb ? g : P.total_subs - 1);
+    const bool active = inb && cap != 0 && P.ist[k].status == 0;
     const ImgDesc& D = P.img[k];
     const uint64_t i = g - P.sub_first[k];
     const uint64_t L = P.ist[k].bit_length;
     ImgCtx ic;
     load_ctx(P, D, L, ic);
+    {
+        __shared__ int4 s_stage[kStageBytes / 16];
+        __shared__ unsigned long long s_lo, s_hi;
+        // this subsequence's bits start at entries[g-1].p (inside [i*sb, ..)); stage from i*sb
+        const uint64_t lo = active ? D.raw_off + ((i * P.sb) >> 3) : 1;
+        const uint64_t hi = active ? D.raw_off + ((min64((i + 1) * P.sb, L) + 7) >> 3) + 24 : 0;
+        ic.words = stage_scan(P.ubuf, lo, hi, tid, kK3Threads, s_stage, &s_lo, &s_hi);
+    }
+    if (!active) return;
     DecState s;
     if (i == 0) {
         s.p = 0;
@@ -957,6 +1023,7 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
     sink.set_unit_comp();
     sink.mflags = 0;
     sink.mS = 0.f;
+    sink.dbg = P.debug;
     sink.buf = buf;
     sink.coef = P.coef;
     sink.du_first = D.du_first;

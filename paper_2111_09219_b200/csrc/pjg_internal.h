@@ -41,9 +41,11 @@ enum Status : int32_t {
 constexpr int kPrimaryBits = 9;
 
 constexpr int kFastBits = 11;
-// fast entry: bits 0-4 total length (code + magnitude, 0 = not fast), 5-10 run,
-// 11-12 kind (0 coefficient, 1 EOB, 2 ZRL), 16-31 coefficient (int16)
-constexpr uint32_t kFastEOB = 1u << 11, kFastZRL = 2u << 11;
+// fast entry for a kFastBits window whose codeword fits and decodes to a
+// symbol the reference accepts: bits 0-4 codeword length (0 = take the exact
+// path), 5-8 magnitude bits l, 9-14 run, 15-16 kind (0 coefficient, 1 EOB,
+// 2 ZRL).  The magnitude value itself is extracted arithmetically.
+constexpr uint32_t kFastEOB = 1u << 15, kFastZRL = 2u << 15;
 
 struct DevHuff {
     uint32_t fast[1 << kFastBits];    // code + magnitude in one probe when both fit in kFastBits
