@@ -282,8 +282,11 @@ class Batch:
             base = blob.ctypes.data if isinstance(blob, np.ndarray) else int(blob)
             self._keep = [blob]
             n = len(sizes)
-            ptrs = (u8p * n)(*[C.cast(base + int(o), u8p) for o in offsets])
-            szs = (C.c_size_t * n)(*[int(s) for s in sizes])
+            pa = (np.asarray(offsets, np.uint64) + np.uint64(base)).astype(np.uint64)
+            sa = np.asarray(sizes, np.uint64)
+            self._keep += [pa, sa]
+            ptrs = pa.ctypes.data_as(C.POINTER(u8p))
+            szs = sa.ctypes.data_as(C.POINTER(C.c_size_t))
         else:
             self._keep = [np.frombuffer(f, np.uint8) if not isinstance(f, np.ndarray) else f
                           for f in files]
@@ -297,12 +300,18 @@ class Batch:
         st = lib().pjg_batch_create(dec.handle, n, ptrs, szs, C.byref(cfg), C.byref(self._h))
         if st:
             raise Error(st, dec.last_error())
-        self.infos = []
-        self.header_status = []
-        for i in range(n):
-            inf = _Info()
-            self.header_status.append(lib().pjg_batch_info(self._h, i, C.byref(inf)))
-            self.infos.append(inf)
+        self._infos = None
+
+    @property
+    def infos(self):
+        """Per-image geometry (fetched lazily: the pipelined host path never needs it)."""
+        if self._infos is None:
+            self._infos, self.header_status = [], []
+            for i in range(self.n):
+                inf = _Info()
+                self.header_status.append(lib().pjg_batch_info(self._h, i, C.byref(inf)))
+                self._infos.append(inf)
+        return self._infos
 
     def _check(self, st):
         if st:

@@ -195,10 +195,8 @@ Header parse_header(const uint8_t* data, size_t size) {
                 // file only if the scan itself parsed, so the error is
                 // deferred until K0 has checked the scan (ImgDesc::deferred).
                 for (int i = 0; i < 4 && h.table_status == kOk; ++i) {
-                    DevHuff tmp;
-                    if (h.dc[i].present) h.table_status = build_dev_huff(h.dc[i], &tmp);
-                    if (h.table_status == kOk && h.ac[i].present)
-                        h.table_status = build_dev_huff(h.ac[i], &tmp);
+                    if (h.dc[i].present) h.table_status = validate_huff(h.dc[i]);
+                    if (h.table_status == kOk && h.ac[i].present) h.table_status = validate_huff(h.ac[i]);
                 }
                 return h;
             } else {
@@ -210,6 +208,25 @@ Header parse_header(const uint8_t* data, size_t size) {
         h.message = f.msg;
     }
     return h;
+}
+
+// build_table's error checks (huffman.hpp:60-93) without building the table.
+int32_t validate_huff(const HuffSpec& spec) {
+    uint32_t code = 0;
+    size_t si = 0;
+    uint32_t maxlen = 0;
+    for (uint32_t len = 1; len <= 16; ++len) {
+        const uint32_t n = spec.counts[len - 1];
+        if (code + n > (1u << len)) return kOversubscribedCode;
+        if (si + n > spec.symbols.size()) return kMalformedHeader;
+        si += n;
+        code += n;
+        if (n) maxlen = len;
+        code <<= 1;
+    }
+    if (si != spec.symbols.size()) return kMalformedHeader;
+    if (maxlen == 0) return kMalformedHeader;
+    return kOk;
 }
 
 int32_t build_dev_huff(const HuffSpec& spec, DevHuff* out) {

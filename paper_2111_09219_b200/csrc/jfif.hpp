@@ -49,6 +49,7 @@ Header parse_header(const uint8_t* data, size_t size);
 // build_table validation (huffman.hpp:60-93) + device two-level table.
 // Returns kOk or the reference's error (OversubscribedCode / MalformedHeader).
 int32_t build_dev_huff(const HuffSpec& spec, DevHuff* out);
+int32_t validate_huff(const HuffSpec& spec);
 // Fills DevHuff::fast for use as a DC (dc = true) or AC table.
 void build_fast(DevHuff* t, bool dc);
 

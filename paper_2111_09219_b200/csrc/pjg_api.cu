@@ -313,38 +313,38 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         }
     }
     // ---- tables: dedupe by content
-    std::map<std::vector<uint8_t>, uint32_t> huff_ids, quant_ids;
+    // tables dedupe by content: batches almost always share a handful, so a
+    // linear memcmp scan over the unique ones beats any map
     std::vector<DevHuff> huffs;
     std::vector<std::array<uint16_t, 64>> quants;
+    std::vector<std::pair<const HuffSpec*, bool>> huff_src;  // unique specs (first occurrence)
+    std::vector<std::array<uint16_t, 64>> quant_src;
+    auto same_spec = [](const HuffSpec& a, const HuffSpec& b) {
+        return a.counts == b.counts && a.symbols.size() == b.symbols.size() &&
+               std::memcmp(a.symbols.data(), b.symbols.data(), a.symbols.size()) == 0;
+    };
     auto huff_id = [&](const HuffSpec& s, bool dc) -> uint32_t {
-        std::vector<uint8_t> key(1, dc ? 0 : 1);
-        key.insert(key.end(), s.counts.begin(), s.counts.end());
-        key.insert(key.end(), s.symbols.begin(), s.symbols.end());
-        auto it = huff_ids.find(key);
-        if (it != huff_ids.end()) return it->second;
+        for (size_t u = 0; u < huff_src.size(); ++u)
+            if (huff_src[u].second == dc && same_spec(*huff_src[u].first, s)) return uint32_t(u);
         DevHuff d;
         build_dev_huff(s, &d);
         build_fast(&d, dc);
         huffs.push_back(d);
-        uint32_t id = uint32_t(huffs.size() - 1);
-        huff_ids.emplace(std::move(key), id);
-        return id;
+        huff_src.emplace_back(&s, dc);
+        return uint32_t(huffs.size() - 1);
     };
     static const uint8_t kZz2R[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
                                       12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
                                       35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
                                       58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
     auto quant_id = [&](const std::array<uint16_t, 64>& q) -> uint32_t {
-        std::vector<uint8_t> key(reinterpret_cast<const uint8_t*>(q.data()),
-                                 reinterpret_cast<const uint8_t*>(q.data()) + 128);
-        auto it = quant_ids.find(key);
-        if (it != quant_ids.end()) return it->second;
+        for (size_t u = 0; u < quant_src.size(); ++u)
+            if (std::memcmp(quant_src[u].data(), q.data(), 128) == 0) return uint32_t(u);
         std::array<uint16_t, 64> r{};
         for (int z = 0; z < 64; ++z) r[kZz2R[z]] = q[z];  // raster order
         quants.push_back(r);
-        uint32_t id = uint32_t(quants.size() - 1);
-        quant_ids.emplace(std::move(key), id);
-        return id;
+        quant_src.push_back(q);
+        return uint32_t(quants.size() - 1);
     };
 
     // ---- layout plan
