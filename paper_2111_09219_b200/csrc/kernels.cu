@@ -1570,7 +1570,45 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
         __syncwarp();
 
         // 3. output
-        if (I.rgb) {
+        // Fast path for whole-width 4:2:0 / 4:2:2 tiles whose exact chroma
+        // index maps (pipeline.hpp:182-187) are x>>1 and y>>1 (or y): one
+        // 16-bit Cb / Cr load gives the chroma of 4 pixels; 4:2:0 items cover
+        // a row pair sharing a chroma row.
+        bool fast420 = false;
+        if (I.rgb && I.h_max == 2 && cols == uint32_t(kTileW) && (I.width & 3) == 0 && (I.out_off & 3) == 0) {
+            const uint32_t x = lane;
+            bool okx = S.cmap[x] == (x >> 1);
+            bool oky = uint32_t(lane) >= rws || S.rmap[lane] == (I.v_max == 2 ? (uint32_t(lane) >> 1) : uint32_t(lane));
+            fast420 = __all_sync(0xFFFFFFFFu, okx && oky);
+        }
+        if (fast420) {
+            const bool pair = I.v_max == 2;
+            const uint32_t nrow = pair ? (rws + 1) >> 1 : rws;
+            uint8_t* obase = P.out + I.out_off + (uint64_t(Y0) * I.width + X0) * 3;
+            const uint64_t orow = uint64_t(I.width) * 3;
+            const uint8_t* ybase = S.pl + I.poff[0];
+            const uint8_t* cbbase = S.pl + I.poff[1];
+            const uint8_t* crbase = S.pl + I.poff[2];
+            const uint32_t pst0 = I.pst[0], pst1 = I.pst[1];
+            for (uint32_t itg = lane; itg < (nrow << 3); itg += 32) {
+                const uint32_t jr = itg >> 3, gx = (itg & 7) * 4;
+                const uint32_t r0 = pair ? 2 * jr : jr;
+                const uint32_t cofs = jr * pst1 + (gx >> 1);  // chroma row jr (= r0>>1 or r0), column gx/2
+                const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(cbbase + cofs);
+                const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(crbase + cofs);
+                const uint2 wa = chroma_words(s_lut, cb2 & 0xFFu, cr2 & 0xFFu);
+                const uint2 wb = chroma_words(s_lut, cb2 >> 8, cr2 >> 8);
+                const uint8_t* cbrow = cbbase + jr * pst1;
+                const uint8_t* crrow = crbase + jr * pst1;
+                const uint32_t c0 = gx >> 1, c1 = c0 + 1;
+                emit_rgb4(obase + r0 * orow + gx * 3, true, 4, *reinterpret_cast<const uint32_t*>(ybase + r0 * pst0 + gx),
+                          wa, wa, wb, wb, cbrow, crrow, c0, c0, c1, c1);
+                if (pair && r0 + 1 < rws)
+                    emit_rgb4(obase + (r0 + 1) * orow + gx * 3, true, 4,
+                              *reinterpret_cast<const uint32_t*>(ybase + (r0 + 1) * pst0 + gx), wa, wa, wb, wb,
+                              cbrow, crrow, c0, c0, c1, c1);
+            }
+        } else if (I.rgb) {
             // lane item = 4 pixels of one row, or of a row pair sharing a
             // chroma row (v_max == 2); 8 groups of 4 pixels per tile row
             const bool pair = I.v_max == 2;
