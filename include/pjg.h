@@ -141,8 +141,10 @@ int pjg_batch_info(const pjg_batch* b, size_t i, pjg_image_info* info);
 const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i);
 uint64_t pjg_batch_output_bytes(const pjg_batch* b);
 int pjg_batch_stage_times(const pjg_batch* b, double* ms /* PJG_NUM_STAGES */);
-/* Sync diagnostics: intra rounds (sum, max), inter-CTA hops, fix-up passes. */
-int pjg_batch_sync_stats(const pjg_batch* b, uint64_t* stats /* 4 */);
+/* Decode diagnostics: intra rounds (sum, max), inter-CTA hops, fix-up passes,
+ * K4 samples replayed in FP64 (near-tie or wide units), K4 units with AC terms. */
+#define PJG_NUM_SYNC_STATS 6
+int pjg_batch_sync_stats(const pjg_batch* b, uint64_t* stats /* PJG_NUM_SYNC_STATS */);
 void pjg_batch_destroy(pjg_batch* b);
 
 /* ---- parity taps -------------------------------------- */

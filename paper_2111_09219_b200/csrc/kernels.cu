@@ -37,11 +37,14 @@ namespace {
 
 constexpr uint32_t kInf32 = 0xFFFFFFFFu;
 
-__device__ __constant__ uint8_t c_zz2r[64] = {
-    0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
-    12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
-    35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
-    58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
+// zig-zag index -> COLUMN-MAJOR block index v*8 + u (F[u][v] at raster u*8+v):
+// the coefficient buffer holds each data unit transposed so K4's IDCT lanes
+// read one frequency column per 16-byte row (pjg_internal.h kCoefColMajor).
+__device__ __constant__ uint8_t c_zz2c[64] = {
+    0,  8,  1,  2,  9,  16, 24, 17, 10, 3,  4,  11, 18, 25, 32, 40,
+    33, 26, 19, 12, 5,  6,  13, 20, 27, 34, 41, 48, 56, 49, 42, 35,
+    28, 21, 14, 7,  15, 22, 29, 36, 43, 50, 57, 58, 51, 44, 37, 30,
+    23, 31, 38, 45, 52, 59, 60, 53, 46, 39, 47, 54, 61, 62, 55, 63};
 
 // ------------------------------------------------------------ utilities --
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
@@ -72,6 +75,22 @@ __device__ __forceinline__ uint32_t find_seg(const T* first, uint32_t n, uint64_
     return lo;
 }
 
+// image holding global subsequence g: sub_img[g >> 7] and sub_img[(g >> 7) + 1]
+// (host-built) bracket it, so the search is over a handful of images at most
+__device__ __forceinline__ uint32_t find_img(const Params& P, uint64_t g) {
+    const uint64_t c = g >> kSubImgShift;
+    uint32_t lo = __ldg(P.sub_img + c), hi = __ldg(P.sub_img + c + 1) + 1;
+    if (hi > P.n_img) hi = P.n_img;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(P.sub_first + mid) <= g)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
 __device__ __forceinline__ void set_status(ImgState* st, int32_t code) {
     atomicCAS(reinterpret_cast<int*>(&st->status), 0, code);
 }
@@ -87,6 +106,12 @@ __device__ __forceinline__ int lround_away(double s) {
 }
 __device__ __forceinline__ uint32_t clamp_u8(int v) { return v < 0 ? 0u : (v > 255 ? 255u : uint32_t(v)); }
 
+// nonzero iff some byte of w is 0xFF
+__device__ __forceinline__ uint32_t has_ff(uint32_t w) {
+    const uint32_t x = ~w;
+    return (x - 0x01010101u) & ~x & 0x80808080u;
+}
+
 // ========================================================= K0: unstuff ====
 // One CTA per 4 KB tile of raw scan bytes.  Per tile: number of stuffed zero
 // bytes (a 0x00 right after 0xFF) and the first marker position (0xFF not
@@ -95,9 +120,17 @@ __device__ __forceinline__ uint32_t clamp_u8(int v) { return v < 0 ? 0u : (v > 2
 // (removed, first-marker) prefix; kept bytes are then compacted into ubuf at
 // the same image offset.  The tile holding the first marker fixes the
 // unstuffed length U and the per-image error (EmptyScan / RST).
+// Tiles are 4 KB windows aligned to the 16-byte grid of the raw buffer (the
+// image's first window starts at raw_off & ~15), so every thread moves its
+// 16 bytes with one vector load, and the compacted bytes are staged in shared
+// memory on the destination's 16-byte grid and leave as full 16-byte stores
+// (only the two edge chunks a tile shares with its neighbours go byte-wise).
 __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     __shared__ uint32_t s_tile;
-    __shared__ uint8_t s_b[kK0Tile + 2];
+    // s_b[16 + i] = raw byte win0 + i; s_b[15] = byte before the window,
+    // s_b[16 + kK0Tile] = byte after it
+    __shared__ __align__(16) uint8_t s_b[kK0Tile + 32];
+    __shared__ __align__(16) uint8_t s_o[kK0Tile + 32];
     __shared__ uint32_t s_cnt[kK0Threads / 32];
     __shared__ uint32_t s_mk[kK0Threads / 32];
     __shared__ uint32_t s_excl_cnt, s_excl_mk, s_tile_cnt, s_tile_mk;
@@ -106,31 +139,47 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     if (tid == 0) s_tile = atomicAdd(&P.counters[kTicketK0], 1u);
     __syncthreads();
     const uint32_t t = s_tile;
-    const uint32_t k = find_seg(P.k0_first, P.n_img, t);
+    const uint32_t k = __ldg(P.k0_img + t);
     const uint32_t lt = t - P.k0_first[k];
     const ImgDesc& D = P.img[k];
     const uint64_t raw_len = D.raw_len;
-    const uint8_t* src = P.raw + D.raw_off;
-    const uint64_t j0 = uint64_t(lt) * kK0Tile;
-    const uint32_t nb = uint32_t(min64(kK0Tile, raw_len - j0));
+    const uint64_t a = D.raw_off, e = a + raw_len;  // the image's bytes [a, e) in the raw buffer
+    const uint64_t win0 = (a & ~15ull) + uint64_t(lt) * kK0Tile;
+    const uint64_t g_first = max(win0, a);            // first image byte in this window
+    const uint64_t j0 = g_first - a;                  // its image-relative index
 
-    // s_b[0] = byte j0-1 (not 0xFF at the scan start), s_b[1+i] = byte j0+i,
-    // s_b[1+nb] = byte after the tile (0 past the end: marker rule handles it).
-    for (uint32_t i = tid; i < nb; i += kK0Threads) s_b[1 + i] = src[j0 + i];
-    if (tid == 0) s_b[0] = j0 ? src[j0 - 1] : 0;
-    if (tid == 1) s_b[1 + nb] = (j0 + nb < raw_len) ? src[j0 + nb] : 0;
+    {
+        const uint64_t g = win0 + 16u * tid;
+        int4 v = make_int4(0, 0, 0, 0);
+        if (g < e) v = __ldcs(reinterpret_cast<const int4*>(P.raw + g));
+        reinterpret_cast<int4*>(s_b + 16)[tid] = v;
+        if (tid == 0) s_b[15] = win0 > a ? P.raw[win0 - 1] : 0;
+        if (tid == 1) s_b[16 + kK0Tile] = win0 + kK0Tile < e ? P.raw[win0 + kK0Tile] : 0;
+    }
     __syncthreads();
 
-    // this thread's 16 bytes
+    // this thread's 16 bytes: raw bytes win0 + b0 + q, image bytes only.
+    // Plain chunks (all 16 bytes inside the image, no 0xFF among them or just
+    // before them) have nothing to classify and copy straight through.
     const uint32_t b0 = tid * kK0BytesPerThread;
+    const bool inside = win0 + b0 > a && win0 + b0 + 16 <= e;
+    bool plain;
+    {
+        const uint4 w = reinterpret_cast<const uint4*>(s_b + 16)[tid];
+        const uint32_t f = has_ff(w.x) | has_ff(w.y) | has_ff(w.z) | has_ff(w.w);
+        plain = inside && f == 0 && s_b[15 + b0] != 0xFF;
+    }
     uint32_t cnt = 0, mk = kInf32;
+#pragma unroll
     for (int q = 0; q < kK0BytesPerThread; ++q) {
-        uint32_t i = b0 + q;
-        if (i >= nb) break;
-        uint8_t cur = s_b[1 + i], prev = s_b[i], next = s_b[2 + i];
-        uint64_t j = j0 + i;
+        if (plain) break;
+        const uint64_t g = win0 + b0 + q;
+        if (g < a || g >= e) continue;
+        const uint8_t cur = s_b[16 + b0 + q], next = s_b[17 + b0 + q];
+        const uint8_t prev = g > a ? s_b[15 + b0 + q] : 0;
+        const uint64_t j = g - a;
         if (cur == 0x00 && prev == 0xFF) ++cnt;
-        bool last = (j + 1 == raw_len);
+        const bool last = (j + 1 == raw_len);
         if (cur == 0xFF && (last || next != 0x00) && mk == kInf32) mk = uint32_t(j);
     }
     // block reduce (sum, min)
@@ -195,19 +244,31 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     for (int w = 0; w < warp; ++w) wbase += s_cnt[w];
     uint32_t removed = s_excl_cnt + wbase + inc - cnt;  // removed before this thread's bytes
 
-    uint8_t* dst = P.ubuf + D.raw_off;
+    // kept byte at image index j goes to image index j - removed; this tile's
+    // kept bytes form [dst_lo, dst_lo + kept) in raw-buffer coordinates
+    const uint64_t dst_lo = g_first - s_excl_cnt;
+    const uint64_t dst_al = dst_lo & ~15ull;
     const uint32_t first_mk = s_excl_mk == kInf32 ? s_tile_mk : kInf32;  // the image's scan end
+    if (plain) {
+        uint8_t* o = s_o + ((win0 + b0 - removed) - dst_al);
+#pragma unroll
+        for (int q = 0; q < kK0BytesPerThread; ++q) o[q] = s_b[16 + b0 + q];
+    }
+#pragma unroll
     for (int q = 0; q < kK0BytesPerThread; ++q) {
-        uint32_t i = b0 + q;
-        if (i >= nb) break;
-        uint8_t cur = s_b[1 + i], prev = s_b[i];
-        uint64_t j = j0 + i;
+        if (plain) break;
+        const uint64_t g = win0 + b0 + q;
+        if (g < a || g >= e) continue;
+        const uint8_t cur = s_b[16 + b0 + q];
+        const uint8_t prev = g > a ? s_b[15 + b0 + q] : 0;
+        const uint64_t j = g - a;
         if (first_mk != kInf32 && j == first_mk) {
             // scan ends here (extract_scan, parser.hpp:241-254)
             uint64_t U = j - removed;
             ImgState* st = P.ist + k;
             st->bit_length = U * 8;
-            bool rst = (j + 1 < raw_len) && s_b[2 + i] >= 0xD0 && s_b[2 + i] <= 0xD7;
+            const uint8_t nx = s_b[17 + b0 + q];
+            bool rst = (j + 1 < raw_len) && nx >= 0xD0 && nx <= 0xD7;
             if (rst)
                 set_status(st, kUnsupportedFeature);
             else if (U == 0)
@@ -218,11 +279,25 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
         if (cur == 0x00 && prev == 0xFF) {
             ++removed;
         } else {
-            dst[j - removed] = cur;
+            s_o[(a + j - removed) - dst_al] = cur;
+        }
+    }
+    __syncthreads();
+    {
+        const uint64_t dst_hi = dst_lo + (min64(e, win0 + kK0Tile) - g_first) - s_tile_cnt;
+        const uint32_t nchunks = uint32_t((dst_hi - dst_al + 15) >> 4);
+        for (uint32_t q = tid; q < nchunks; q += kK0Threads) {
+            const uint64_t G = dst_al + 16ull * q;
+            if (G >= dst_lo && G + 16 <= dst_hi) {
+                *reinterpret_cast<int4*>(P.ubuf + G) = reinterpret_cast<const int4*>(s_o)[q];
+            } else {
+                for (uint32_t x = 0; x < 16; ++x)
+                    if (G + x >= dst_lo && G + x < dst_hi) P.ubuf[G + x] = s_o[16 * q + x];
+            }
         }
     }
     // no marker anywhere: the scan runs to the end of the file
-    const uint32_t last_tile = uint32_t((raw_len + kK0Tile - 1) / kK0Tile) - 1;
+    const uint32_t last_tile = uint32_t(((a & 15ull) + raw_len + kK0Tile - 1) / kK0Tile) - 1;
     if (tid == 0 && lt == last_tile && s_excl_mk == kInf32 && s_tile_mk == kInf32) {
         uint64_t U = raw_len - (s_excl_cnt + s_tile_cnt);
         ImgState* st = P.ist + k;
@@ -498,7 +573,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     const uint32_t cta = s_cta;
     const uint64_t g = uint64_t(cta) * T + tid;
     const bool inb = g < P.total_subs;
-    const uint32_t k = find_seg(P.sub_first, P.n_img, inb ? g : P.total_subs - 1);
+    const uint32_t k = find_img(P, inb ? g : P.total_subs - 1);
     const ImgDesc& D = P.img[k];
     const uint64_t i = g - P.sub_first[k];
     const uint64_t L = P.ist[k].bit_length;
@@ -653,7 +728,7 @@ __global__ void __launch_bounds__(1024) k1c_fixup(Params P) {
             st.czd &= ~0x2000u;
             P.cta_start[cta] = st;
             uint64_t g0 = uint64_t(cta) * T;
-            uint32_t k = find_seg(P.sub_first, P.n_img, g0);
+            uint32_t k = find_img(P, g0);
             const ImgDesc& D = P.img[k];
             const uint64_t L = P.ist[k].bit_length;
             const uint64_t N = (L + P.sb - 1) / P.sb;
@@ -716,7 +791,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
     const uint32_t t = s_tile;
     const uint64_t g = uint64_t(t) * T + tid;
     const bool inb = g < P.total_subs;
-    uint32_t k = find_seg(P.sub_first, P.n_img, inb ? g : P.total_subs - 1);
+    uint32_t k = find_img(P, inb ? g : P.total_subs - 1);
     const uint64_t i = g - P.sub_first[k];
     ScanVal v;
     v.n = 0;
@@ -865,7 +940,7 @@ constexpr uint32_t kMetaNonDc = 1u << 8, kMetaBig = 1u << 9;
 
 struct BlockSink {
     static constexpr bool kWrite = true;
-    const uint8_t* zz2r; // zig-zag -> raster, in smem (lane-divergent index)
+    const uint8_t* zz2c; // zig-zag -> column-major, in smem (lane-divergent index)
     const float* wts;    // w_u * w_v per raster index, in smem
     int16_t* buf;        // this thread's smem block
     int16_t* coef;       // batch coefficient buffer
@@ -915,7 +990,7 @@ struct BlockSink {
             *md = make_uint2(mflags, __float_as_uint(mS));
         } else {
             for (uint64_t sl = lo; sl < hi; ++sl) {
-                int r = zz2r[sl & 63];
+                int r = zz2c[sl & 63];
                 dst[r] = buf[r];
             }
             if (mflags) atomicOr(&md->x, mflags);
@@ -938,7 +1013,7 @@ struct BlockSink {
             flush(cur);
             ++cur;
         }
-        const uint32_t r = zz2r[s & 63];
+        const uint32_t r = zz2c[s & 63];
         buf[r] = int16_t(v);
         if (!(dbg & 32) && int16_t(v) != 0) {
             const int32_t F = int32_t(int16_t(v)) * int32_t(__ldg(qc + r));
@@ -959,13 +1034,13 @@ struct BlockSink {
 
 __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
     __shared__ __align__(16) int16_t s_blk[kK3Threads * kBlkStride];
-    __shared__ uint8_t s_zz2r[64];
+    __shared__ uint8_t s_zz2c[64];
     __shared__ float s_wts[64];
     const int tid = threadIdx.x;
     if (tid < 64) {
         // max_x |basis[u][x]| rounded up, product over (row, column)
         const float w[8] = {0.35356f, 0.4904f, 0.46195f, 0.4904f, 0.35356f, 0.4904f, 0.46195f, 0.4904f};
-        s_zz2r[tid] = c_zz2r[tid];
+        s_zz2c[tid] = c_zz2c[tid];
         s_wts[tid] = w[tid >> 3] * w[tid & 7];
     }
     __syncthreads();
@@ -978,7 +1053,7 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
     const uint64_t g = uint64_t(blockIdx.x) * kK3Threads + tid;
     const bool inb = g < P.total_subs;
     const uint32_t cap = inb ? P.cap[g] : 0u;
-    const uint32_t k = find_seg(P.sub_first, P.n_img, inb ? g : P.total_subs - 1);
+    const uint32_t k = find_img(P, inb ? g : P.total_subs - 1);
     const bool active = inb && cap != 0 && P.ist[k].status == 0;
     const ImgDesc& D = P.img[k];
     const uint64_t i = g - P.sub_first[k];
@@ -1011,7 +1086,7 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
     s.dc2 = int16_t(pd.hi & 0xFFFFu);
     const uint64_t o = P.off[g];
     BlockSink sink;
-    sink.zz2r = s_zz2r;
+    sink.zz2c = s_zz2c;
     sink.wts = s_wts;
     sink.meta = P.meta;
     sink.du_comp = D.du_comp;
@@ -1044,27 +1119,36 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
 // Warp-independent persistent kernel: every warp owns a contiguous range of
 // tiles (one MCU-row segment 32 pixels wide: <= 12 data units) and runs the
 // whole pipeline for a tile with only __syncwarp — no CTA barriers, so the
-// ~24 resident warps per SM hide each other's latency.  The next tile's
-// coefficients are prefetched into registers (3 x 16 B per lane) while the
-// current tile computes.
+// resident warps hide each other's latency.  The next tile's coefficients and
+// K3's per-unit metadata are prefetched with cp.async while the current tile
+// computes.  Coefficients arrive column-major (F[u][v] at v*8+u).
 //
-//  1. dequantise (reference transform.hpp:146-161, int32 coef * Q) into a
-//     warp-private smem tile; per data unit: row mask and the weighted sum
-//     S = sum_uv w_u w_v |F_uv|
-//  2. IDCT, lane = (data unit, column y).  FP32 FMA separable sum with the
-//     rigorous bound |r32 - r64| <= 18u S (u = 2^-24); samples within that
-//     bound of a rounding boundary (x.5) are replayed exactly in FP64 in the
-//     reference's order (transform.hpp:114-142); DC-only units use the
-//     reference's two products fl(b0 * fl(b0 * F00)) directly.
-//  3. crop + chroma replication (pipeline.hpp:182-187, exact index maps) +
-//     YCbCr->RGB: Y integer => lround(Y + t) = Y + round(t) unless t is an
+//  1. classify the tile's units from K3's metadata: units with AC terms go to
+//     a compact list for the IDCT; DC-only units take the integer path
+//     (every sample = lround(b0 * (b0 * F00)) + 128; for F00 != 4 mod 8 that
+//     is floor((F00 + 4) / 8) exactly, ties replayed as the reference's two
+//     FP64 products, transform.hpp:114-142)
+//  2. dequantise the AC units' columns (int32 coef * Q, transform.hpp:146-161)
+//     into a float tile (stride 68 floats: 8 units' 16-byte loads hit 8
+//     disjoint bank groups)
+//  3. IDCT with packed FP32 (FFMA2): lane = (AC unit, row pair q, q+4), eight
+//     units per pass; out(x,y) = sum_v b[v][y] sum_u b[u][x] F[u][v] over the
+//     union of nonzero columns.  Rigorous bound |r32 - r64| <= 18 u S
+//     (u = 2^-24, S = sum w_u w_v |F_uv| from K3); samples within the bound of
+//     x.5 are replayed exactly in FP64 in the reference's summation order.
+//     Each lane then owns two whole 8-sample rows: 4 aligned 32-bit stores.
+//  4. YCbCr->RGB with the exact chroma maps (pipeline.hpp:182-187: x>>1 for
+//     h = 2, x for h = 1, likewise rows — an identity for every W, H) and
+//     integer colour: Y integer => lround(Y + t) = Y + round(t) unless t is an
 //     exact real half-integer; round(t) and the tie test are exact integer
-//     arithmetic on the decimal coefficients, ties are replayed in FP64
-//     (pipeline.hpp:190-197).  Packed 12-byte stores per 4 pixels.
+//     arithmetic on the decimal constants, ties replayed in FP64
+//     (pipeline.hpp:190-197).  Saturating byte packs, 3 x 32-bit stores per
+//     4 pixels.
 constexpr float kM128 = 12583040.0f;  // 1.5 * 2^23 + 128: round(acc) + 128 in the low mantissa bits
 constexpr int kMagicBits = 0x4B400000;
 constexpr int kK4Warps = kK4Threads / 32;
 constexpr int kTileW = 32;  // pixels per tile row
+constexpr int kFS = 68;     // floats per unit in the F tile
 
 __device__ __forceinline__ uint32_t pack4_sat(int a0, int a1, int a2, int a3) {
     uint32_t t, d;
@@ -1073,38 +1157,25 @@ __device__ __forceinline__ uint32_t pack4_sat(int a0, int a1, int a2, int a3) {
     return d;
 }
 
-// Exact FP64 replay of the samples of column y selected by `mask` (reference
-// order, zero terms skipped: transform.hpp:114-142).  The column pass
-// tmp[u][y] is shared by all selected rows.  Returns the 8 clamped samples
-// packed in two words (unselected bytes are unspecified).
-__device__ __noinline__ uint2 idct_column_fp64(const float* F, bool big, uint32_t rows, const double* b64, int y,
-                                               uint32_t mask) {
-    const int32_t* Fi = reinterpret_cast<const int32_t*>(F);
-    double tmp[8];
-#pragma unroll
+// Exact FP64 value of sample (x, y) of a unit in the reference's order
+// (transform.hpp:114-142): tmp[u] = sum_v b[v][y] F[u][v] (v ascending),
+// out = sum_u b[u][x] tmp[u] (u ascending), zero terms skipped (exact: the
+// running sums start at +0 and fl(s + +-0) = s).  Fc is column-major; `big`
+// units hold int32 bits.  Returns the clamped sample.
+__device__ __noinline__ uint32_t idct_sample_fp64(const float* Fc, bool big, uint32_t cols, const double* b64, int x,
+                                                  int y) {
+    const int32_t* Fi = reinterpret_cast<const int32_t*>(Fc);
+    double s = 0.0;
     for (int u = 0; u < 8; ++u) {
         double t = 0.0;
-        if (rows & (1u << u)) {
-            for (int v = 0; v < 8; ++v) {
-                const double f = big ? double(Fi[u * 8 + v]) : double(F[u * 8 + v]);
-                if (f != 0.0) t = __dadd_rn(t, __dmul_rn(b64[v * 8 + y], f));
-            }
+        for (uint32_t m = cols; m; m &= m - 1) {
+            const int v = __ffs(m) - 1;
+            const double f = big ? double(Fi[v * 8 + u]) : double(Fc[v * 8 + u]);
+            if (f != 0.0) t = __dadd_rn(t, __dmul_rn(b64[v * 8 + y], f));
         }
-        tmp[u] = t;
+        if (t != 0.0) s = __dadd_rn(s, __dmul_rn(b64[u * 8 + x], t));
     }
-    int o[8];
-#pragma unroll
-    for (int x = 0; x < 8; ++x) {
-        o[x] = 0;
-        if (mask & (1u << x)) {
-            double sacc = 0.0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (rows & (1u << u)) sacc = __dadd_rn(sacc, __dmul_rn(b64[u * 8 + x], tmp[u]));
-            o[x] = lround_away(sacc) + 128;
-        }
-    }
-    return make_uint2(pack4_sat(o[0], o[1], o[2], o[3]), pack4_sat(o[4], o[5], o[6], o[7]));
+    return clamp_u8(lround_away(s) + 128);
 }
 
 // exact FP64 colour of one pixel (pipeline.hpp:190-197): returns R | G << 8 | B << 16
@@ -1120,13 +1191,12 @@ __device__ __noinline__ uint32_t rgb_fp64(int Y, int Cb, int Cr) {
 // Per-warp image cache: layout of the tile's data units in the warp's sample
 // planes, quantisers, and the descriptor fields the tile loop needs.
 struct __align__(16) WarpImg {
-    uint16_t q[3][64];  // raster-order quantiser per component
+    uint16_t q[3][64];  // column-major quantiser per component
     uint32_t pst[3], poff[3];
     uint16_t boff[kK4MaxBlocks];  // plane byte offset of the unit's (0,0) sample
     uint16_t bps[kK4MaxBlocks];   // plane row stride
     uint8_t bcomp[kK4MaxBlocks];
     uint32_t width, height, ncomp, h_max, v_max, rgb, out_mode;
-    uint32_t pw1, ph1, ch1, cv1;
     uint32_t plane_w[3], plane_h[3], comp_h[3], comp_v[3];
     uint64_t out_off;
 };
@@ -1138,15 +1208,16 @@ struct TileWalk {
 };
 
 struct WarpSmem {
-    float F[kK4MaxBlocks * 64];  // dequantised (float, or int32 bits when big)
-    int4 raw[kK4MaxBlocks * 8];  // next tile's coefficients (cp.async staging)
-    uint2 meta[kK4MaxBlocks];    // next tile's per-unit metadata
-    uint8_t pl[1024];            // sample planes (row stride padded by 4)
+    float F[kK4MaxBlocks * kFS];  // dequantised AC units (float, or int32 bits when big), compact order
+    int4 raw[kK4MaxBlocks * 8];   // next tile's coefficients (cp.async staging)
+    uint2 meta[kK4MaxBlocks];     // next tile's per-unit metadata
+    uint8_t pl[1024];             // sample planes (row stride padded by 4)
     WarpImg img;
-    uint16_t cmap[kTileW];
-    uint8_t rmap[16];
-    uint16_t rows[kK4MaxBlocks];  // row mask | big << 8 | dc-only << 9
-    float lim[kK4MaxBlocks];
+    float lim[kK4MaxBlocks];      // per AC unit: 0.5 - error bound
+    uint16_t cm[kK4MaxBlocks];    // per AC unit: column mask | big << 8
+    uint8_t acl[kK4MaxBlocks];    // AC units (tile-local index), compact
+    uint8_t dcl[kK4MaxBlocks];    // DC-only units
+    uint16_t rep[32];             // FP64 replay work list: unit << 6 | x << 3 | y
     TileWalk w;
 };
 
@@ -1194,10 +1265,6 @@ __device__ __forceinline__ void fill_warp_img(const Params& P, uint32_t k, WarpI
         c.v_max = D.v_max;
         c.out_mode = D.out_mode;
         c.rgb = D.out_mode == 1 && ncomp == 3;
-        c.pw1 = D.plane_w[1];
-        c.ph1 = D.plane_h[1];
-        c.ch1 = D.comp_h[1];
-        c.cv1 = D.comp_v[1];
         c.out_off = D.out_off;
     }
     __syncwarp();
@@ -1220,98 +1287,134 @@ __device__ __forceinline__ void walk_enter_image(const Params& P, uint32_t t, Ti
     w.tx = lt % w.tiles_x;
 }
 
-// Colour LUTs per chroma value (exact integers).  A chroma sample maps to two
-// words: crg = (oR + 256) | (oG + 256) << 16 and cb = (oB + 256) | tie << 31,
-// where oX = round(kX * c) and tie marks an exact real half-integer (only
-// Cb = 3 / 253 for B and (Cb, Cr) = (78, 178) / (178, 78) for G).
+// Chroma offsets of one (Cb, Cr) sample, exact integers:
+//   r[Cr] = round(1.402 cr), b[Cb] = round(1.772 cb) (B ties: Cb = 3, 253),
+//   G: m = ga[Cb] + gb[Cr] = -344136 cb - 714136 cr + 500000 + 2e8 (+1 when Cb
+//   is a B tie; m is otherwise even), oG = floor(m / 1e6) - 200; a G tie is
+//   m == 0 mod 1e6, so (m mod 1e6) == 0 or odd flags any tie.
 struct ColourLut {
-    uint32_t r[256];   // oR + 256, indexed by Cr
-    uint32_t b[256];   // (oB + 256) | tieB << 31, indexed by Cb
-    int32_t ga[256];   // -344136 * cb + 500000 + 2e8
-    int32_t gb[256];   // -714136 * cr
+    int32_t r[256];
+    int32_t b[256];
+    int32_t ga[256];
+    int32_t gb[256];
 };
 
-__device__ __forceinline__ uint2 chroma_words(const ColourLut& L, uint32_t Cb, uint32_t Cr) {
-    const uint32_t mG = uint32_t(L.ga[Cb] + L.gb[Cr]);
-    const uint32_t qG = mG / 1000000u;  // oG = qG - 200
-    const uint32_t tieG = (mG - qG * 1000000u) == 0 ? (1u << 31) : 0u;
-    return make_uint2(L.r[Cr] | ((qG + 56u) << 16), L.b[Cb] | tieG);
+__device__ __forceinline__ void chroma_off(const ColourLut& L, uint32_t cb, uint32_t cr, int& oR, int& oG, int& oB,
+                                           uint32_t& tie) {
+    oR = L.r[cr];
+    oB = L.b[cb];
+    const uint32_t m = uint32_t(L.ga[cb] + L.gb[cr]);
+    const uint32_t q = m / 1000000u;
+    const uint32_t rem = m - q * 1000000u;
+    tie |= (rem & 1u) | uint32_t(rem == 0u);
+    oG = int(q) - 200;
 }
 
-__device__ __forceinline__ uint32_t vmax_s16x2(uint32_t a, uint32_t b) {
-    uint32_t d;
-    asm("max.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-    return d;
-}
-__device__ __forceinline__ uint32_t vmin_s16x2(uint32_t a, uint32_t b) {
-    uint32_t d;
-    asm("min.s16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-    return d;
-}
-// clamp both 16-bit lanes of (value + 256) to [256, 511]: the low byte of each
-// lane is then clamp_u8(value)
-__device__ __forceinline__ uint32_t clamp2(uint32_t v) {
-    return vmin_s16x2(vmax_s16x2(v, 0x01000100u), 0x01FF01FFu);
+__device__ __forceinline__ int ybyte(uint32_t y4, int i) { return int((y4 >> (8 * i)) & 0xFFu); }
+
+// 4 pixels of one row -> 12 RGB bytes (3 words); chroma offsets per pixel
+__device__ __forceinline__ uint3 rgb4(uint32_t y4, const int* oR, const int* oG, const int* oB) {
+    const int Y0 = ybyte(y4, 0), Y1 = ybyte(y4, 1), Y2 = ybyte(y4, 2), Y3 = ybyte(y4, 3);
+    uint3 w;
+    w.x = pack4_sat(Y0 + oR[0], Y0 + oG[0], Y0 + oB[0], Y1 + oR[1]);
+    w.y = pack4_sat(Y1 + oG[1], Y1 + oB[1], Y2 + oR[2], Y2 + oG[2]);
+    w.z = pack4_sat(Y2 + oB[2], Y3 + oR[3], Y3 + oG[3], Y3 + oB[3]);
+    return w;
 }
 
-// 4 pixels of one row: Y bytes in y4, chroma words per pixel.  16-bit SWAR:
-// (Y | Y << 16) + crg gives R and G in one add, clamps are VIMNMX.S16x2.
-__device__ __forceinline__ void emit_rgb4(uint8_t* dst, bool fast, uint32_t npx, uint32_t y4, uint2 c0, uint2 c1,
-                                          uint2 c2, uint2 c3, const uint8_t* cbrow, const uint8_t* crrow,
-                                          uint32_t cx0, uint32_t cx1, uint32_t cx2, uint32_t cx3) {
-    const uint32_t rg0 = clamp2(__byte_perm(y4, 0, 0x4040) + c0.x);
-    const uint32_t rg1 = clamp2(__byte_perm(y4, 0, 0x4141) + c1.x);
-    const uint32_t rg2 = clamp2(__byte_perm(y4, 0, 0x4242) + c2.x);
-    const uint32_t rg3 = clamp2(__byte_perm(y4, 0, 0x4343) + c3.x);
-    const uint32_t b01 = clamp2(__byte_perm(y4, 0, 0x4140) + __byte_perm(c0.y, c1.y, 0x5410));
-    const uint32_t b23 = clamp2(__byte_perm(y4, 0, 0x4342) + __byte_perm(c2.y, c3.y, 0x5410));
-    const uint32_t t = __byte_perm(rg0, rg1, 0x6420);  // R0 G0 R1 G1
-    const uint32_t u = __byte_perm(rg2, rg3, 0x6420);  // R2 G2 R3 G3
-    uint32_t o0 = __byte_perm(t, b01, 0x2410);                            // R0 G0 B0 R1
-    uint32_t o1 = __byte_perm(__byte_perm(t, b01, 0x0063), u, 0x5410);   // G1 B1 R2 G2
-    uint32_t o2 = __byte_perm(u, b23, 0x6324);                            // B2 R3 G3 B3
-    if ((c0.y | c1.y | c2.y | c3.y) >> 31) {
-        // exact real tie in some chroma sample: FP64 replay of those pixels
-        const uint2 cw[4] = {c0, c1, c2, c3};
-        const uint32_t cx[4] = {cx0, cx1, cx2, cx3};
-        uint8_t px[12];
+__device__ __forceinline__ void store_rgb4(uint8_t* dst, uint3 w, uint32_t npx, bool aligned) {
+    if (npx == 4 && aligned) {
+        uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+        d[0] = w.x;
+        d[1] = w.y;
+        d[2] = w.z;
+    } else {
+        const uint32_t ws[3] = {w.x, w.y, w.z};
+        for (uint32_t q = 0; q < npx * 3; ++q) dst[q] = uint8_t(ws[q >> 2] >> (8 * (q & 3)));
+    }
+}
+
+// exact replay of 4 pixels (some chroma sample is an exact real tie)
+__device__ __forceinline__ uint3 rgb4_exact(uint32_t y4, const uint8_t* cb, const uint8_t* cr, const uint32_t* cx) {
+    uint32_t px[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t w = q < 1 ? o0 : (q < 2 ? o0 : o1);
-            (void)w;
-        }
+    for (int i = 0; i < 4; ++i) px[i] = rgb_fp64(ybyte(y4, i), cb[cx[i]], cr[cx[i]]);
+    uint3 w;
+    w.x = (px[0] & 0xFFFFFFu) | (px[1] << 24);
+    w.y = ((px[1] >> 8) & 0xFFFFu) | (px[2] << 16);
+    w.z = ((px[2] >> 16) & 0xFFu) | (px[3] << 8);
+    return w;
+}
+
+// Colour stage of one tile.  HS = pixels per chroma sample horizontally (1
+// for 4:4:4, 2 for 4:2:2 / 4:2:0); PAIR: two rows share a chroma row (4:2:0).
+// Lane item = 4 pixels of one row (of a row pair when PAIR).
+template <int HS, bool PAIR>
+__device__ __forceinline__ void colour_tile(const WarpImg& I, const uint8_t* pl, const ColourLut& L, uint8_t* out,
+                                            uint32_t X0, uint32_t Y0, uint32_t cols, uint32_t rws, int lane) {
+    const uint32_t nrow = PAIR ? (rws + 1) >> 1 : rws;
+    const uint32_t W = I.width;
+    const bool aligned = ((W & 3) == 0) && ((I.out_off & 3) == 0);
+    const uint8_t* yb = pl + I.poff[0];
+    const uint8_t* cbb = pl + I.poff[1];
+    const uint8_t* crb = pl + I.poff[2];
+    const uint32_t pst0 = I.pst[0], pst1 = I.pst[1];
+    uint8_t* obase = out + I.out_off + (uint64_t(Y0) * W + X0) * 3;
+    const uint64_t orow = uint64_t(W) * 3;
+    for (uint32_t it = lane; it < (nrow << 3); it += 32) {
+        const uint32_t jr = it >> 3, gx = (it & 7) * 4;
+        if (gx >= cols) continue;
+        const uint32_t npx = min(4u, cols - gx);
+        const uint32_t r0 = PAIR ? 2 * jr : jr;
+        const uint8_t* cbrow = cbb + jr * pst1;
+        const uint8_t* crrow = crb + jr * pst1;
+        int oR[4], oG[4], oB[4];
+        uint32_t tie = 0;
+        uint32_t cx[4];
+        if (HS == 2) {
+            const uint32_t c0 = gx >> 1;
+            const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(cbrow + c0);
+            const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(crrow + c0);
+            chroma_off(L, cb2 & 0xFFu, cr2 & 0xFFu, oR[0], oG[0], oB[0], tie);
+            chroma_off(L, cb2 >> 8, cr2 >> 8, oR[2], oG[2], oB[2], tie);
+            oR[1] = oR[0], oG[1] = oG[0], oB[1] = oB[0];
+            oR[3] = oR[2], oG[3] = oG[2], oB[3] = oB[2];
+            cx[0] = cx[1] = c0;
+            cx[2] = cx[3] = c0 + 1;
+        } else {
+            const uint32_t cb4 = *reinterpret_cast<const uint32_t*>(cbrow + gx);
+            const uint32_t cr4 = *reinterpret_cast<const uint32_t*>(crrow + gx);
 #pragma unroll
-        for (int k = 0; k < 12; ++k) px[k] = uint8_t((k < 4 ? o0 : (k < 8 ? o1 : o2)) >> (8 * (k & 3)));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (cw[q].y >> 31) {
-                const uint32_t e = rgb_fp64(int((y4 >> (8 * q)) & 0xFFu), cbrow[cx[q]], crrow[cx[q]]);
-                px[3 * q] = uint8_t(e);
-                px[3 * q + 1] = uint8_t(e >> 8);
-                px[3 * q + 2] = uint8_t(e >> 16);
+            for (int i = 0; i < 4; ++i) {
+                chroma_off(L, (cb4 >> (8 * i)) & 0xFFu, (cr4 >> (8 * i)) & 0xFFu, oR[i], oG[i], oB[i], tie);
+                cx[i] = gx + i;
             }
         }
-        o0 = uint32_t(px[0]) | (uint32_t(px[1]) << 8) | (uint32_t(px[2]) << 16) | (uint32_t(px[3]) << 24);
-        o1 = uint32_t(px[4]) | (uint32_t(px[5]) << 8) | (uint32_t(px[6]) << 16) | (uint32_t(px[7]) << 24);
-        o2 = uint32_t(px[8]) | (uint32_t(px[9]) << 8) | (uint32_t(px[10]) << 16) | (uint32_t(px[11]) << 24);
-    }
-    if (fast) {
-        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-        d32[0] = o0;
-        d32[1] = o1;
-        d32[2] = o2;
-    } else {
-        for (uint32_t q = 0; q < npx * 3; ++q) {
-            const uint32_t wq = q < 4 ? o0 : (q < 8 ? o1 : o2);
-            dst[q] = uint8_t(wq >> (8 * (q & 3)));
+        {
+            const uint32_t y4 = *reinterpret_cast<const uint32_t*>(yb + r0 * pst0 + gx);
+            const uint3 w = tie ? rgb4_exact(y4, cbrow, crrow, cx) : rgb4(y4, oR, oG, oB);
+            store_rgb4(obase + r0 * orow + gx * 3, w, npx, aligned);
+        }
+        if (PAIR && r0 + 1 < rws) {
+            const uint32_t y4 = *reinterpret_cast<const uint32_t*>(yb + (r0 + 1) * pst0 + gx);
+            const uint3 w = tie ? rgb4_exact(y4, cbrow, crrow, cx) : rgb4(y4, oR, oG, oB);
+            store_rgb4(obase + (r0 + 1) * orow + gx * 3, w, npx, aligned);
         }
     }
+}
+
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<const unsigned long long*>(&a)), "l"(*reinterpret_cast<const unsigned long long*>(&b)));
+    return *reinterpret_cast<float2*>(&r);
 }
 
 __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
     __shared__ __align__(16) WarpSmem s_w[kK4Warps];
     __shared__ __align__(16) float s_b32[64];   // basis[u][x]
-    __shared__ __align__(16) float s_b32T[64];  // basis[v][y] at [y*8+v]
     __shared__ __align__(16) double s_b64[64];
     __shared__ __align__(16) ColourLut s_lut;
 
@@ -1320,16 +1423,14 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
         const double b = P.basis[tid];
         s_b64[tid] = b;
         s_b32[tid] = float(b);
-        s_b32T[(tid & 7) * 8 + (tid >> 3)] = float(b);
     }
     for (int c = tid; c < 256; c += kK4Threads) {
         const int v = c - 128;
-        const uint32_t mR = uint32_t(1402 * v + 500 + 200000), mB = uint32_t(1772 * v + 500 + 300000);
-        const uint32_t qR = mR / 1000u, qB = mB / 1000u;
-        // oR = qR - 200 (never an exact tie in [-128, 127]); oB = qB - 300
-        s_lut.r[c] = qR + 56u;
-        s_lut.b[c] = (qB - 44u) | ((mB - qB * 1000u) == 0 ? (1u << 31) : 0u);
-        s_lut.ga[c] = -344136 * v + 500000 + 200000000;
+        // round(k v) for decimal k, exactly: floor((1000 k v + 500) / 1000)
+        s_lut.r[c] = int((1402 * v + 500 + 200000) / 1000) - 200;
+        const int mB = 1772 * v + 500 + 300000;
+        s_lut.b[c] = mB / 1000 - 300;
+        s_lut.ga[c] = -344136 * v + 500000 + 200000000 + ((mB % 1000) == 0 ? 1 : 0);
         s_lut.gb[c] = -714136 * v;
     }
     __syncthreads();
@@ -1339,6 +1440,12 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
     const uint32_t t_begin = uint32_t(uint64_t(P.k4_tiles) * gw / nw);
     const uint32_t t_end = uint32_t(uint64_t(P.k4_tiles) * (gw + 1) / nw);
     if (t_begin >= t_end) return;
+
+    // IDCT lane constants: rows q and q+4 of the lane's unit
+    const uint32_t q = lane & 3;
+    float2 bq[8];  // (b[u][q], b[u][q+4])
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bq[u] = make_float2(s_b32[u * 8 + q], s_b32[u * 8 + q + 4]);
 
     TileWalk& w = S.w;
     if (lane == 0) {
@@ -1355,10 +1462,8 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
     }
     __syncwarp();
     uint32_t cached_k = 0xFFFFFFFFu;
-    // prefetch of the current tile: 3 x 16 B per lane (rows lane, lane+32, lane+64
-    // of the tile's units), issued one tile ahead
     // prefetch of a tile into the warp's smem staging (cp.async, no registers
-    // held): rows lane, lane+32, lane+64 of its units + per-unit metadata
+    // held): 16-byte columns lane, lane+32, lane+64 of its units + metadata
     auto issue = [&](const TileWalk& tw) {
         const uint32_t mx0 = tw.tx * tw.MT;
         const uint32_t nblk = min(tw.MT, tw.mcus_x - mx0) * tw.dpm;
@@ -1380,6 +1485,8 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     issue(w);
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t n_replay = 0, n_ac = 0;
     for (uint32_t t = t_begin; t < t_end; ++t) {
         const uint32_t cur_k = w.k, cur_my = w.my, cur_mx0 = w.tx * w.MT;
         const uint32_t cur_nm = min(w.MT, w.mcus_x - cur_mx0);
@@ -1392,55 +1499,78 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
         }
         const WarpImg& I = S.img;
 
-        // 1. dequantise the prefetched rows; row masks / bounds come from K3's
-        //    per-unit metadata (flags = rows | has-AC << 8 | big << 9, S)
+        // 1. classify units (K3 metadata: column mask | has-AC << 8 | big << 9, S)
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
-        const uint2 pm = uint32_t(lane) < nblk ? S.meta[lane] : make_uint2(0, 0);
+        uint32_t nac = 0, ndc = 0;
         if (cur_valid) {
-            if (uint32_t(lane) < nblk) {
+            const bool in = uint32_t(lane) < nblk;
+            const uint2 pm = in ? S.meta[lane] : make_uint2(0, 0);
+            const bool isac = in && (pm.x & kMetaNonDc);
+            const uint32_t acm = __ballot_sync(0xFFFFFFFFu, isac);
+            const uint32_t dcm = __ballot_sync(0xFFFFFFFFu, in && !isac);
+            nac = __popc(acm);
+            ndc = __popc(dcm);
+            if (isac) {
+                const uint32_t a = __popc(acm & lt_mask);
                 const float Sb = __uint_as_float(pm.y);
                 const bool big = (pm.x & kMetaBig) || Sb >= 2097152.f;
-                const bool dconly = (pm.x & 0xFFu) <= 1u && !(pm.x & kMetaNonDc);
-                S.rows[lane] = uint16_t((pm.x & 0xFFu) | (big ? 0x100u : 0u) | (dconly ? 0x200u : 0u));
+                S.acl[a] = uint8_t(lane);
+                S.cm[a] = uint16_t((pm.x & 0xFFu) | (big ? 0x100u : 0u));
                 // |r32 - r64| <= 18u S (+ FP64's own ~1e-15 S), u = 2^-24
-                S.lim[lane] = 0.5f - (1.1e-6f * Sb + 2.0e-6f);
+                S.lim[a] = 0.5f - (1.1e-6f * Sb + 2.0e-6f);
+            } else if (in) {
+                S.dcl[__popc(dcm & lt_mask)] = uint8_t(lane);
             }
+            __syncwarp();
+            // 2a. dequantise the AC units' columns: item = (AC unit, column v)
 #pragma unroll 1
-            for (int j = 0; j < 3; ++j) {
-                const uint32_t ch = lane + 32 * j, blk = ch >> 3, u = ch & 7;
-                const uint32_t flags = __shfl_sync(0xFFFFFFFFu, pm.x, blk & 31);
-                const float Sb = __uint_as_float(__shfl_sync(0xFFFFFFFFu, pm.y, blk & 31));
-                if (ch < nblk * 8) {
-                    float4* dst = reinterpret_cast<float4*>(S.F + ch * 8);
-                    if (!((flags >> u) & 1u)) {
-                        dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-                        dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    } else {
-                        const int4 rvi = S.raw[ch];
-                        const uint4 rv = make_uint4(uint32_t(rvi.x), uint32_t(rvi.y), uint32_t(rvi.z), uint32_t(rvi.w));
-                        const uint4 qv = *reinterpret_cast<const uint4*>(I.q[I.bcomp[blk]] + u * 8);
-                        const uint32_t rw[4] = {rv.x, rv.y, rv.z, rv.w}, qw[4] = {qv.x, qv.y, qv.z, qv.w};
-                        int32_t d[8];
+            for (uint32_t it = lane; it < nac * 8; it += 32) {
+                const uint32_t a = it >> 3, v = it & 7;
+                const uint32_t blk = S.acl[a], cm = S.cm[a];
+                float4* dst = reinterpret_cast<float4*>(S.F + a * kFS + v * 8);
+                if (!((cm >> v) & 1u)) {
+                    dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                } else {
+                    const int4 rvi = S.raw[blk * 8 + v];
+                    const uint4 qv = *reinterpret_cast<const uint4*>(I.q[I.bcomp[blk]] + v * 8);
+                    const uint32_t rw[4] = {uint32_t(rvi.x), uint32_t(rvi.y), uint32_t(rvi.z), uint32_t(rvi.w)};
+                    const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+                    int32_t d[8];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            d[2 * e] = int32_t(int16_t(rw[e] & 0xFFFFu)) * int32_t(qw[e] & 0xFFFFu);
-                            d[2 * e + 1] = (int32_t(rw[e]) >> 16) * int32_t(qw[e] >> 16);
-                        }
-                        if (!((flags & kMetaBig) || Sb >= 2097152.f)) {
-                            dst[0] = make_float4(float(d[0]), float(d[1]), float(d[2]), float(d[3]));
-                            dst[1] = make_float4(float(d[4]), float(d[5]), float(d[6]), float(d[7]));
-                        } else {  // exact-FP64 unit: keep the int32 bits
-                            dst[0] = make_float4(__int_as_float(d[0]), __int_as_float(d[1]), __int_as_float(d[2]),
-                                                 __int_as_float(d[3]));
-                            dst[1] = make_float4(__int_as_float(d[4]), __int_as_float(d[5]), __int_as_float(d[6]),
-                                                 __int_as_float(d[7]));
-                        }
+                    for (int e = 0; e < 4; ++e) {
+                        d[2 * e] = int32_t(int16_t(rw[e] & 0xFFFFu)) * int32_t(qw[e] & 0xFFFFu);
+                        d[2 * e + 1] = (int32_t(rw[e]) >> 16) * int32_t(qw[e] >> 16);
+                    }
+                    if (!(cm & 0x100u)) {
+                        dst[0] = make_float4(float(d[0]), float(d[1]), float(d[2]), float(d[3]));
+                        dst[1] = make_float4(float(d[4]), float(d[5]), float(d[6]), float(d[7]));
+                    } else {  // exact-FP64 unit: keep the int32 bits
+                        dst[0] = make_float4(__int_as_float(d[0]), __int_as_float(d[1]), __int_as_float(d[2]),
+                                             __int_as_float(d[3]));
+                        dst[1] = make_float4(__int_as_float(d[4]), __int_as_float(d[5]), __int_as_float(d[6]),
+                                             __int_as_float(d[7]));
                     }
                 }
             }
+            // 2b. DC-only units: item = (unit, row x), two 4-byte stores of the constant sample
+#pragma unroll 1
+            for (uint32_t it = lane; it < ndc * 8; it += 32) {
+                const uint32_t blk = S.dcl[it >> 3], x = it & 7;
+                const int32_t F00 = int32_t(int16_t(uint32_t(S.raw[blk * 8].x) & 0xFFFFu)) * int32_t(I.q[I.bcomp[blk]][0]);
+                int o;
+                if ((F00 & 7) != 4)
+                    o = (F00 + 4) >> 3;
+                else
+                    o = lround_away(__dmul_rn(s_b64[0], __dmul_rn(s_b64[0], double(F00))));
+                const uint32_t ov = clamp_u8(o + 128) * 0x01010101u;
+                uint32_t* row = reinterpret_cast<uint32_t*>(S.pl + I.boff[blk] + x * I.bps[blk]);
+                row[0] = ov;
+                row[1] = ov;
+            }
         }
-        // advance the walk and prefetch the next tile (in flight during 2 + 3)
+        // advance the walk and prefetch the next tile (in flight during 3 + 4)
         if (t + 1 < t_end) {
             __syncwarp();
             if (lane == 0) {
@@ -1457,212 +1587,150 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
             issue(w);
         }
         if (!cur_valid) continue;
-        // chroma index maps (pipeline.hpp:182-187), tile-local
+
+        // 3. IDCT of the AC units, eight per pass: lane = (unit a, rows q, q+4)
+        uint32_t pend = 0;  // per pass: bit y (row q) / 8 + y (row q+4) need the FP64 replay
+#pragma unroll 1
+        for (uint32_t g = 0; g * 8 < nac; ++g) {
+            const uint32_t a = g * 8 + (lane >> 2);
+            const bool act = a < nac;
+            const uint32_t cmw = act ? S.cm[a] : 0u;
+            const uint32_t ucols = __reduce_or_sync(0xFFFFFFFFu, cmw & 0xFFu);
+            const float* F = S.F + (act ? a : 0) * kFS;
+            float2 acc[8];
+#pragma unroll
+            for (int y = 0; y < 8; ++y) acc[y] = make_float2(0.f, 0.f);
+            for (uint32_t m = ucols; m; m &= m - 1) {
+                const uint32_t v = __ffs(m) - 1;
+                const float4 f0 = *reinterpret_cast<const float4*>(F + v * 8);
+                const float4 f1 = *reinterpret_cast<const float4*>(F + v * 8 + 4);
+                // s = sum_u (b[u][q], b[u][q+4]) F[u][v]
+                float2 sv = __fmul2_rn(bq[0], f2(f0.x));
+                sv = __ffma2_rn(bq[1], f2(f0.y), sv);
+                sv = __ffma2_rn(bq[2], f2(f0.z), sv);
+                sv = __ffma2_rn(bq[3], f2(f0.w), sv);
+                sv = __ffma2_rn(bq[4], f2(f1.x), sv);
+                sv = __ffma2_rn(bq[5], f2(f1.y), sv);
+                sv = __ffma2_rn(bq[6], f2(f1.z), sv);
+                sv = __ffma2_rn(bq[7], f2(f1.w), sv);
+                const float4 b0 = *reinterpret_cast<const float4*>(s_b32 + v * 8);
+                const float4 b1 = *reinterpret_cast<const float4*>(s_b32 + v * 8 + 4);
+                acc[0] = __ffma2_rn(f2(b0.x), sv, acc[0]);
+                acc[1] = __ffma2_rn(f2(b0.y), sv, acc[1]);
+                acc[2] = __ffma2_rn(f2(b0.z), sv, acc[2]);
+                acc[3] = __ffma2_rn(f2(b0.w), sv, acc[3]);
+                acc[4] = __ffma2_rn(f2(b1.x), sv, acc[4]);
+                acc[5] = __ffma2_rn(f2(b1.y), sv, acc[5]);
+                acc[6] = __ffma2_rn(f2(b1.z), sv, acc[6]);
+                acc[7] = __ffma2_rn(f2(b1.w), sv, acc[7]);
+            }
+            // round: v = acc + M holds round(acc) + 128 in its low bits
+            int o0[8], o1[8];
+            float mx = 0.f;
+            const float2 M2 = f2(kM128);
+#pragma unroll
+            for (int y = 0; y < 8; ++y) {
+                const float2 vv = __fadd2_rn(acc[y], M2);
+                const float2 dd = fsub2(acc[y], fsub2(vv, M2));
+                mx = fmaxf(mx, fmaxf(fabsf(dd.x), fabsf(dd.y)));
+                o0[y] = __float_as_int(vv.x) - kMagicBits;
+                o1[y] = __float_as_int(vv.y) - kMagicBits;
+            }
+            if (act) {
+                const uint32_t blk = S.acl[a];
+                uint8_t* pl = S.pl + I.boff[blk];
+                const uint32_t ps = I.bps[blk];
+                uint32_t* r0p = reinterpret_cast<uint32_t*>(pl + q * ps);
+                uint32_t* r1p = reinterpret_cast<uint32_t*>(pl + (q + 4) * ps);
+                r0p[0] = pack4_sat(o0[0], o0[1], o0[2], o0[3]);
+                r0p[1] = pack4_sat(o0[4], o0[5], o0[6], o0[7]);
+                r1p[0] = pack4_sat(o1[0], o1[1], o1[2], o1[3]);
+                r1p[1] = pack4_sat(o1[4], o1[5], o1[6], o1[7]);
+                if (cmw & 0x100u) {
+                    pend |= 0xFFFFu << (16 * g);
+                } else if (mx > S.lim[a]) {  // rare: the samples near x.5 get FP64 below
+                    const float lim = S.lim[a];
+                    uint32_t mask = 0;
+#pragma unroll
+                    for (int y = 0; y < 8; ++y) {
+                        const float2 vv = __fadd2_rn(acc[y], M2);
+                        const float2 dd = fsub2(acc[y], fsub2(vv, M2));
+                        if (fabsf(dd.x) > lim) mask |= 1u << y;
+                        if (fabsf(dd.y) > lim) mask |= 0x100u << y;
+                    }
+                    pend |= mask << (16 * g);
+                }
+            }
+        }
+        // exact FP64 replay of the flagged samples, off the hot loop and
+        // spread over the warp: lane i recomputes entry i of a work list
+        n_ac += nac;
+        if (__any_sync(0xFFFFFFFFu, pend)) {
+            const uint32_t cnt = __popc(pend);
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += x;
+            }
+            const uint32_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            const uint32_t base = incl - cnt;
+            n_replay += total;
+            for (uint32_t rb = 0; rb < total; rb += 32) {
+                if (cnt && base < rb + 32 && base + cnt > rb) {
+                    uint32_t k = base;
+                    for (uint32_t m = pend; m; m &= m - 1, ++k) {
+                        if (k < rb) continue;
+                        if (k >= rb + 32) break;
+                        const uint32_t bit = __ffs(m) - 1;  // 16 g + 8 h + y
+                        const uint32_t a = (bit >> 4) * 8 + (lane >> 2), x = q + 4 * ((bit >> 3) & 1u);
+                        S.rep[k - rb] = uint16_t((a << 6) | (x << 3) | (bit & 7u));
+                    }
+                }
+                __syncwarp();
+                if (rb + lane < total) {
+                    const uint32_t e = S.rep[lane];
+                    const uint32_t a = e >> 6, x = (e >> 3) & 7u, y = e & 7u;
+                    const uint32_t blk = S.acl[a], cmw = S.cm[a];
+                    const uint32_t o = idct_sample_fp64(S.F + a * kFS, cmw & 0x100u, cmw & 0xFFu, s_b64, int(x), int(y));
+                    S.pl[I.boff[blk] + x * I.bps[blk] + y] = uint8_t(o);
+                }
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+
+        // 4. output
         const uint32_t X0 = cur_mx0 * cur_mcuw, Y0 = cur_my * cur_mcuh;
         const uint32_t cols = min(cur_nm * cur_mcuw, I.width - X0), rws = min(cur_mcuh, I.height - Y0);
         if (I.rgb) {
-            const uint32_t cx0 = cur_mx0 * I.ch1 * 8, cy0 = cur_my * I.cv1 * 8;
-            if (uint32_t(lane) < cols) S.cmap[lane] = uint16_t(min((X0 + lane) * I.pw1 / I.width, I.pw1 - 1) - cx0);
-            if (uint32_t(lane) < rws) S.rmap[lane] = uint8_t(min((Y0 + lane) * I.ph1 / I.height, I.ph1 - 1) - cy0);
-        }
-        __syncwarp();
-
-        // 2. IDCT: lane = (unit (lane>>3) + 4j, column y)
-        const uint32_t y = lane & 7;
-        const float4 bc0 = *reinterpret_cast<const float4*>(s_b32T + y * 8);
-        const float4 bc1 = *reinterpret_cast<const float4*>(s_b32T + y * 8 + 4);
-        uint32_t pend = 0;  // per j: samples of column y that need the FP64 replay
-#pragma unroll 1
-        for (int j = 0; j < 3; ++j) {
-            const uint32_t blk = (lane >> 3) + 4 * j;
-            if (4 * uint32_t(j) >= nblk) break;  // warp-uniform
-            const bool act = blk < nblk;
-            const uint32_t rw = act ? S.rows[blk] : 0u;
-            const uint32_t rows = rw & 0xFFu;
-            const uint32_t urows = __reduce_or_sync(0xFFFFFFFFu, (rw & 0x200u) ? 0u : rows);
-            const float* F = S.F + (act ? blk : 0) * 64;
-            float acc[8];
-#pragma unroll
-            for (int x = 0; x < 8; ++x) acc[x] = 0.f;
-            // only the rows some unit of this warp uses (warp-uniform loop)
-            for (uint32_t m = urows; m; m &= m - 1) {
-                const uint32_t uu = __ffs(m) - 1;
-                {
-                    const float4 f0 = *reinterpret_cast<const float4*>(F + uu * 8);
-                    const float4 f1 = *reinterpret_cast<const float4*>(F + uu * 8 + 4);
-                    float tu = bc0.x * f0.x;
-                    tu = fmaf(bc0.y, f0.y, tu);
-                    tu = fmaf(bc0.z, f0.z, tu);
-                    tu = fmaf(bc0.w, f0.w, tu);
-                    tu = fmaf(bc1.x, f1.x, tu);
-                    tu = fmaf(bc1.y, f1.y, tu);
-                    tu = fmaf(bc1.z, f1.z, tu);
-                    tu = fmaf(bc1.w, f1.w, tu);
-                    const float4 b0 = *reinterpret_cast<const float4*>(s_b32 + uu * 8);
-                    const float4 b1 = *reinterpret_cast<const float4*>(s_b32 + uu * 8 + 4);
-                    acc[0] = fmaf(b0.x, tu, acc[0]);
-                    acc[1] = fmaf(b0.y, tu, acc[1]);
-                    acc[2] = fmaf(b0.z, tu, acc[2]);
-                    acc[3] = fmaf(b0.w, tu, acc[3]);
-                    acc[4] = fmaf(b1.x, tu, acc[4]);
-                    acc[5] = fmaf(b1.y, tu, acc[5]);
-                    acc[6] = fmaf(b1.z, tu, acc[6]);
-                    acc[7] = fmaf(b1.w, tu, acc[7]);
-                }
+            if (I.h_max == 2) {
+                if (I.v_max == 2)
+                    colour_tile<2, true>(I, S.pl, s_lut, P.out, X0, Y0, cols, rws, lane);
+                else
+                    colour_tile<2, false>(I, S.pl, s_lut, P.out, X0, Y0, cols, rws, lane);
+            } else {
+                colour_tile<1, false>(I, S.pl, s_lut, P.out, X0, Y0, cols, rws, lane);
             }
-            int out[8];
-            float mx = 0.f;
-#pragma unroll
-            for (int x = 0; x < 8; ++x) {
-                const float v = acc[x] + kM128;
-                mx = fmaxf(mx, fabsf(acc[x] - (v - kM128)));
-                out[x] = __float_as_int(v) - kMagicBits;
-            }
-            uint32_t lo = pack4_sat(out[0], out[1], out[2], out[3]);
-            uint32_t hi = pack4_sat(out[4], out[5], out[6], out[7]);
-            if (act) {
-                const bool big = rw & 0x100u;
-                if (rw & 0x200u) {
-                    // DC-only: fl(b0 * fl(b0 * F00)) for every sample, exactly the
-                    // reference's zero-skipped sums (ties at F00 = 8k+4 included)
-                    const double f00 = big ? double(reinterpret_cast<const int32_t*>(F)[0]) : double(F[0]);
-                    const int o = lround_away(__dmul_rn(s_b64[0], __dmul_rn(s_b64[0], f00))) + 128;
-                    lo = hi = pack4_sat(o, o, o, o);
-                } else if (big) {
-                    pend |= 0xFFu << (8 * j);
-                } else if (mx > S.lim[blk]) {  // rare: the samples near x.5 get FP64 below
-                    const float lim = S.lim[blk];
-                    uint32_t mask = 0;
-#pragma unroll
-                    for (int x = 0; x < 8; ++x) {
-                        const float v = acc[x] + kM128;
-                        if (fabsf(acc[x] - (v - kM128)) > lim) mask |= 1u << x;
-                    }
-                    pend |= mask << (8 * j);
-                }
-                const uint32_t ps = I.bps[blk];
-                uint8_t* pl = S.pl + I.boff[blk] + y;
-                pl[0] = uint8_t(lo);
-                pl[ps] = uint8_t(lo >> 8);
-                pl[2 * ps] = uint8_t(lo >> 16);
-                pl[3 * ps] = uint8_t(lo >> 24);
-                pl[4 * ps] = uint8_t(hi);
-                pl[5 * ps] = uint8_t(hi >> 8);
-                pl[6 * ps] = uint8_t(hi >> 16);
-                pl[7 * ps] = uint8_t(hi >> 24);
-            }
-        }
-        // exact FP64 replay of the flagged samples (reference order), off the
-        // hot loop so it costs no registers there
-        if (pend) {
-            for (int j = 0; j < 3; ++j) {
-                const uint32_t mask = (pend >> (8 * j)) & 0xFFu;
-                if (!mask) continue;
-                const uint32_t blk = (lane >> 3) + 4 * j;
-                const uint32_t rw = S.rows[blk];
-                const uint2 ex = idct_column_fp64(S.F + blk * 64, rw & 0x100u, rw & 0xFFu, s_b64, int(y), mask);
-                const uint32_t ps = I.bps[blk];
-                uint8_t* pl = S.pl + I.boff[blk] + y;
-                for (int x = 0; x < 8; ++x)
-                    if (mask & (1u << x)) pl[x * ps] = uint8_t((x < 4 ? ex.x : ex.y) >> (8 * (x & 3)));
-            }
-        }
-        __syncwarp();
-
-        // 3. output
-        // Fast path for whole-width 4:2:0 / 4:2:2 tiles whose exact chroma
-        // index maps (pipeline.hpp:182-187) are x>>1 and y>>1 (or y): one
-        // 16-bit Cb / Cr load gives the chroma of 4 pixels; 4:2:0 items cover
-        // a row pair sharing a chroma row.
-        bool fast420 = false;
-        if (I.rgb && I.h_max == 2 && cols == uint32_t(kTileW) && (I.width & 3) == 0 && (I.out_off & 3) == 0) {
-            const uint32_t x = lane;
-            bool okx = S.cmap[x] == (x >> 1);
-            bool oky = uint32_t(lane) >= rws || S.rmap[lane] == (I.v_max == 2 ? (uint32_t(lane) >> 1) : uint32_t(lane));
-            fast420 = __all_sync(0xFFFFFFFFu, okx && oky);
-        }
-        if (fast420) {
-            const bool pair = I.v_max == 2;
-            const uint32_t nrow = pair ? (rws + 1) >> 1 : rws;
-            uint8_t* obase = P.out + I.out_off + (uint64_t(Y0) * I.width + X0) * 3;
-            const uint64_t orow = uint64_t(I.width) * 3;
-            const uint8_t* ybase = S.pl + I.poff[0];
-            const uint8_t* cbbase = S.pl + I.poff[1];
-            const uint8_t* crbase = S.pl + I.poff[2];
-            const uint32_t pst0 = I.pst[0], pst1 = I.pst[1];
-            for (uint32_t itg = lane; itg < (nrow << 3); itg += 32) {
-                const uint32_t jr = itg >> 3, gx = (itg & 7) * 4;
-                const uint32_t r0 = pair ? 2 * jr : jr;
-                const uint32_t cofs = jr * pst1 + (gx >> 1);  // chroma row jr (= r0>>1 or r0), column gx/2
-                const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(cbbase + cofs);
-                const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(crbase + cofs);
-                const uint2 wa = chroma_words(s_lut, cb2 & 0xFFu, cr2 & 0xFFu);
-                const uint2 wb = chroma_words(s_lut, cb2 >> 8, cr2 >> 8);
-                const uint8_t* cbrow = cbbase + jr * pst1;
-                const uint8_t* crrow = crbase + jr * pst1;
-                const uint32_t c0 = gx >> 1, c1 = c0 + 1;
-                emit_rgb4(obase + r0 * orow + gx * 3, true, 4, *reinterpret_cast<const uint32_t*>(ybase + r0 * pst0 + gx),
-                          wa, wa, wb, wb, cbrow, crrow, c0, c0, c1, c1);
-                if (pair && r0 + 1 < rws)
-                    emit_rgb4(obase + (r0 + 1) * orow + gx * 3, true, 4,
-                              *reinterpret_cast<const uint32_t*>(ybase + (r0 + 1) * pst0 + gx), wa, wa, wb, wb,
-                              cbrow, crrow, c0, c0, c1, c1);
-            }
-        } else if (I.rgb) {
-            // lane item = 4 pixels of one row, or of a row pair sharing a
-            // chroma row (v_max == 2); 8 groups of 4 pixels per tile row
-            const bool pair = I.v_max == 2;
-            const uint32_t nrow = pair ? (rws + 1) >> 1 : rws;
-            const uint32_t groups = (cols + 3) >> 2;
-            uint8_t* obase = P.out + I.out_off;
+        } else if (I.out_mode == 1) {
+            // grayscale RGB output (1 channel, the Y plane): 4 pixels per item
             const uint32_t W = I.width;
             const bool aligned = ((W & 3) == 0) && ((I.out_off & 3) == 0);
-            const uint8_t* ybase = S.pl + I.poff[0];
-            const uint8_t* cbbase = S.pl + I.poff[1];
-            const uint8_t* crbase = S.pl + I.poff[2];
-            const uint32_t pst0 = I.pst[0], pst1 = I.pst[1];
-            for (uint32_t itg = lane; itg < (nrow << 3); itg += 32) {
-                const uint32_t jr = itg >> 3, gxi = itg & 7;
-                if (gxi >= groups) continue;
-                const uint32_t gx = gxi * 4;
-                const uint32_t npx = min(4u, cols - gx);
-                const uint2 cm = *reinterpret_cast<const uint2*>(S.cmap + gx);
-                uint32_t cx0 = cm.x & 0xFFFFu, cx1 = cm.x >> 16, cx2 = cm.y & 0xFFFFu, cx3 = cm.y >> 16;
-                if (npx < 2) cx1 = cx0;
-                if (npx < 3) cx2 = cx1;
-                if (npx < 4) cx3 = cx2;
-                const uint32_t r0 = pair ? 2 * jr : jr;
-                uint32_t crow = S.rmap[r0];
-                const uint8_t* cbrow = cbbase + crow * pst1;
-                const uint8_t* crrow = crbase + crow * pst1;
-                uint2 w0 = chroma_words(s_lut, cbrow[cx0], crrow[cx0]);
-                uint2 w1 = cx1 == cx0 ? w0 : chroma_words(s_lut, cbrow[cx1], crrow[cx1]);
-                uint2 w2 = cx2 == cx1 ? w1 : chroma_words(s_lut, cbrow[cx2], crrow[cx2]);
-                uint2 w3 = cx3 == cx2 ? w2 : chroma_words(s_lut, cbrow[cx3], crrow[cx3]);
-                const bool fast = npx == 4 && aligned;
-                emit_rgb4(obase + (uint64_t(Y0 + r0) * W + X0 + gx) * 3, fast, npx,
-                          *reinterpret_cast<const uint32_t*>(ybase + r0 * pst0 + gx), w0, w1, w2, w3, cbrow, crrow,
-                          cx0, cx1, cx2, cx3);
-                if (pair && r0 + 1 < rws) {
-                    const uint32_t crow1 = S.rmap[r0 + 1];
-                    if (crow1 != crow) {
-                        crow = crow1;
-                        cbrow = cbbase + crow * pst1;
-                        crrow = crbase + crow * pst1;
-                        w0 = chroma_words(s_lut, cbrow[cx0], crrow[cx0]);
-                        w1 = cx1 == cx0 ? w0 : chroma_words(s_lut, cbrow[cx1], crrow[cx1]);
-                        w2 = cx2 == cx1 ? w1 : chroma_words(s_lut, cbrow[cx2], crrow[cx2]);
-                        w3 = cx3 == cx2 ? w2 : chroma_words(s_lut, cbrow[cx3], crrow[cx3]);
-                    }
-                    emit_rgb4(obase + (uint64_t(Y0 + r0 + 1) * W + X0 + gx) * 3, fast, npx,
-                              *reinterpret_cast<const uint32_t*>(ybase + (r0 + 1) * pst0 + gx), w0, w1, w2, w3,
-                              cbrow, crrow, cx0, cx1, cx2, cx3);
+            uint8_t* obase = P.out + I.out_off + uint64_t(Y0) * W + X0;
+            for (uint32_t it = lane; it < (rws << 3); it += 32) {
+                const uint32_t r = it >> 3, gx = (it & 7) * 4;
+                if (gx >= cols) continue;
+                const uint32_t y4 = *reinterpret_cast<const uint32_t*>(S.pl + I.poff[0] + r * I.pst[0] + gx);
+                uint8_t* dst = obase + uint64_t(r) * W + gx;
+                if (gx + 4 <= cols && aligned) {
+                    *reinterpret_cast<uint32_t*>(dst) = y4;
+                } else {
+                    for (uint32_t i = 0; i < min(4u, cols - gx); ++i) dst[i] = uint8_t(y4 >> (8 * i));
                 }
             }
         } else {
-            // planes (extract_planes, transform.hpp:165-211) — or the Y plane
-            // only for grayscale output / single-component images
-            const uint32_t nplanes = (I.out_mode == 0) ? I.ncomp : 1;
+            // planes (extract_planes, transform.hpp:165-211)
+            const uint32_t nplanes = I.ncomp;
             uint64_t plane_base = I.out_off;
 #pragma unroll
             for (uint32_t c = 0; c < 3; ++c) {
@@ -1679,6 +1747,14 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
             }
         }
         __syncwarp();
+    }
+    if (P.stats) {
+        n_replay = __reduce_add_sync(0xFFFFFFFFu, lane == 0 ? n_replay : 0u);
+        n_ac = __reduce_add_sync(0xFFFFFFFFu, lane == 0 ? n_ac : 0u);
+        if (lane == 0) {
+            atomicAdd(P.stats + kStatReplays, (unsigned long long)n_replay);
+            atomicAdd(P.stats + kStatAcUnits, (unsigned long long)n_ac);
+        }
     }
 }
 

@@ -110,7 +110,7 @@ struct pjg_batch {
     bool packed = false;
     // meta blob layout (offsets into ctx->meta)
     size_t m_desc = 0, m_state = 0, m_huff = 0, m_quant = 0, m_basis = 0, m_k0 = 0, m_tile = 0,
-           m_sub = 0, m_total = 0;
+           m_sub = 0, m_k0img = 0, m_subimg = 0, m_total = 0;
     uint32_t n_huff = 0, n_quant = 0;
     uint32_t k0_tiles = 0, k4_tiles = 0, k1_ctas = 0, k2_tiles = 0;
     uint64_t total_subs = 0, total_dus = 0, out_bytes = 0;
@@ -341,7 +341,8 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         for (size_t u = 0; u < quant_src.size(); ++u)
             if (std::memcmp(quant_src[u].data(), q.data(), 128) == 0) return uint32_t(u);
         std::array<uint16_t, 64> r{};
-        for (int z = 0; z < 64; ++z) r[kZz2R[z]] = q[z];  // raster order
+        // column-major (index v*8 + u for raster u*8 + v), the coefficient buffer's order
+        for (int z = 0; z < 64; ++z) r[(kZz2R[z] & 7) * 8 + (kZz2R[z] >> 3)] = q[z];
         quants.push_back(r);
         quant_src.push_back(q);
         return uint32_t(quants.size() - 1);
@@ -425,7 +426,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
             d.q_tab[c] = uint16_t(quant_id(h.quant[h.comps[c].tq]));
         }
         // K0 tiles always run (scan checks precede table errors)
-        k0t += uint32_t((rl + kK0Tile - 1) / kK0Tile);
+        k0t += uint32_t(((d.raw_off & 15) + rl + kK0Tile - 1) / kK0Tile);  // 16-byte-grid windows
         if (h.table_status != kOk) continue;
         d.sub_count = (uint64_t(rl) * 8 + sb - 1) / sb;
         d.expected = h.total_dus() * 64;
@@ -480,6 +481,12 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     o = align_up(o + (n + 1) * 4, 16);
     b->m_sub = o;
     o = align_up(o + (n + 1) * 8, 16);
+    // image lookup tables: K0 tile -> image, subsequence (c << kSubImgShift) -> image
+    const uint64_t n_subimg = ((sub + (1u << kSubImgShift) - 1) >> kSubImgShift) + 2;
+    b->m_k0img = o;
+    o = align_up(o + (uint64_t(k0t) + 1) * 4, 16);
+    b->m_subimg = o;
+    o = align_up(o + n_subimg * 4, 16);
     b->m_total = o;
     CU(ctx->meta_host.ensure(o), "cudaMallocHost(meta)");
     uint8_t* mh = static_cast<uint8_t*>(ctx->meta_host.p);
@@ -495,6 +502,19 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     std::memcpy(mh + b->m_k0, k0_first.data(), (n + 1) * 4);
     std::memcpy(mh + b->m_tile, tile_first.data(), (n + 1) * 4);
     std::memcpy(mh + b->m_sub, sub_first.data(), (n + 1) * 8);
+    {
+        uint32_t* k0img = reinterpret_cast<uint32_t*>(mh + b->m_k0img);
+        for (size_t i = 0; i < n; ++i)
+            for (uint32_t t = k0_first[i]; t < k0_first[i + 1]; ++t) k0img[t] = uint32_t(i);
+        uint32_t* subimg = reinterpret_cast<uint32_t*>(mh + b->m_subimg);
+        size_t k = 0;
+        for (uint64_t c = 0; c < n_subimg; ++c) {
+            const uint64_t g = c << kSubImgShift;
+            // largest k < n with sub_first[k] <= g (find_seg semantics)
+            while (k + 1 < n && sub_first[k + 1] <= g) ++k;
+            subimg[c] = uint32_t(k);
+        }
+    }
 
     // ---- device reservation
     CU(ctx->meta.ensure(o), "cudaMalloc(meta)");
@@ -532,6 +552,8 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.raw = ctx->raw.as<uint8_t>();
     p.ubuf = ctx->ubuf.as<uint8_t>();
     p.k0_first = reinterpret_cast<const uint32_t*>(md + b->m_k0);
+    p.k0_img = reinterpret_cast<const uint32_t*>(md + b->m_k0img);
+    p.sub_img = reinterpret_cast<const uint32_t*>(md + b->m_subimg);
     p.k0_tiles = k0t;
     p.k1_ctas = b->k1_ctas;
     p.sb = sb;
@@ -729,6 +751,8 @@ int pjg_batch_sync_stats(const pjg_batch* b, uint64_t* stats) {
     stats[1] = b->stats[kStatRoundsMax];
     stats[2] = b->stats[kStatInterHops];
     stats[3] = b->stats[kStatFixPasses];
+    stats[4] = b->stats[kStatReplays];
+    stats[5] = b->stats[kStatAcUnits];
     return PJG_OK;
 }
 
@@ -750,10 +774,13 @@ int pjg_batch_dump_coefficients(const pjg_batch* b, size_t i, int pre_dc_zigzag,
     if (count < nco) return fail(ctx, PJG_CAPACITY, "coefficient buffer too small");
     if (b->host_status[i] != 0) return b->host_status[i];
     CU(cudaStreamSynchronize(ctx->stream), "sync");
-    std::vector<int16_t> raster(nco);
-    CU(cudaMemcpy(raster.data(), ctx->coef.as<int16_t>() + b->desc[i].du_first * 64, nco * 2,
+    std::vector<int16_t> colmaj(nco), raster(nco);
+    CU(cudaMemcpy(colmaj.data(), ctx->coef.as<int16_t>() + b->desc[i].du_first * 64, nco * 2,
                   cudaMemcpyDeviceToHost),
        "D2H coef");
+    // the device buffer holds each unit column-major (kernels.cu c_zz2c)
+    for (uint64_t d = 0; d < nco; d += 64)
+        for (int r = 0; r < 64; ++r) raster[d + r] = colmaj[d + (r & 7) * 8 + (r >> 3)];
     if (!pre_dc_zigzag) {
         std::memcpy(out, raster.data(), nco * 2);
         return PJG_OK;

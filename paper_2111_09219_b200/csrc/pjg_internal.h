@@ -140,6 +140,7 @@ struct DcSums {
 };
 
 // ------------------------------------------------------------- params --
+constexpr int kSubImgShift = 7;
 constexpr int kK0Threads = 256;
 constexpr int kK0BytesPerThread = 16;
 constexpr int kK0Tile = kK0Threads * kK0BytesPerThread;  // 4096 raw bytes per tile
@@ -163,6 +164,8 @@ struct Params {
     uint8_t* ubuf;
     // K0 tiles
     const uint32_t* k0_first;      // n_img + 1 prefix
+    const uint32_t* k0_img;        // image of each K0 tile
+    const uint32_t* sub_img;       // image of subsequence c << kSubImgShift, c = 0..ceil(total/128)
     uint32_t k0_tiles;
     uint32_t k1_ctas;
     // subsequences
@@ -202,7 +205,8 @@ enum StatIndex {
     kStatRoundsMax = 1,
     kStatInterHops = 2,    // subsequences decoded by inter-CTA overflows
     kStatFixPasses = 3,    // K1c passes that found work
-    kStatSymbols = 4,      // reserved
+    kStatReplays = 4,      // K4 samples recomputed in exact FP64
+    kStatAcUnits = 5,      // K4 data units with AC terms (FP32 IDCT path)
     kNumStats = 8
 };
 

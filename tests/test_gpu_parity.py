@@ -175,3 +175,30 @@ def test_restatement_agrees_on_gpu_box():
     """Sanity on the GPU box: the C restatement still matches the reference."""
     f = ref_jpeg(97, 33, 7, 90, "420")
     assert np.array_equal(Orc.decode(f).data, Ref.decode(f).data)
+
+
+def test_contiguous_region_unaligned_offsets(decoder):
+    """Files laid out back to back in one caller region at odd offsets (the
+    single-copy upload path): K0's 16-byte-grid windows start mid-chunk and
+    neighbouring images share edge chunks."""
+    corpus = acceptance_corpus()[::3] + [((1023, 769, 90, "420"), ref_jpeg(1023, 769, 5, 90, "420"))]
+    gaps = [1, 3, 7, 0, 13, 2, 5, 11, 0, 1, 9, 4, 6, 15, 3, 8, 1, 2, 0, 7, 5, 3]
+    parts, offs, sizes, pos = [], [], [], 0
+    for k, (_, f) in enumerate(corpus):
+        g = gaps[k % len(gaps)]
+        parts.append(b"\xa5" * g)
+        pos += g
+        offs.append(pos)
+        sizes.append(len(f))
+        parts.append(f)
+        pos += len(f)
+    blob = np.frombuffer(b"".join(parts) + b"\x00" * 64, np.uint8).copy()
+    with decoder.batch((blob, np.array(offs, np.uint64), np.array(sizes, np.uint64)), pj.DecodeConfig(),
+                       pj.OutputColorspace.RGBInterleaved) as b:
+        st = b.run()
+        assert (st == 0).all(), st
+        outs = b.download()
+        for i, (_, f) in enumerate(corpus):
+            ref = Ref.decode(f, rgb=True)
+            got = _rgb(outs[i], b.infos[i])
+            assert np.array_equal(got, ref.data), i
