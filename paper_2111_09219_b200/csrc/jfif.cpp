@@ -296,7 +296,8 @@ void build_fast(DevHuff* t, bool dc) {
                     ok = false;
                 }
             }
-            if (ok) f = clen | (l << 5) | (run << 9) | (kind << 15);
+            if (ok) f = clen | ((clen + l) << 5) | (l << 10) | (run << 14) | (kind == 1 ? kFastEOB : 0u) |
+                        (kind == 0 ? kFastCoef : 0u);
         }
         t->fast[w] = f;
     }

@@ -310,32 +310,32 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
 }
 
 // ============================================== entropy decode (shared) ====
+constexpr uint32_t kHuffWords = sizeof(DevHuff) / 4;  // fast[] sits at word 0 of each table
+
 struct ImgCtx {
-    const uint32_t* words;  // ubuf as 32-bit words
+    const uint32_t* words;  // ubuf as 32-bit words (or the CTA's shared-memory stage)
     uint64_t bit_base;      // 8 * raw_off
     uint64_t L;             // bit_length
-    uint64_t du_comp;
+    const uint32_t* fast;   // all tables as words: table t's fast[] at t * kHuffWords
+    uint32_t tdc[3], tac[3];  // fast-table word offsets per component
+    uint32_t duc;           // slot -> component, 2 bits per slot
     uint32_t dpm;
-    const DevHuff* dc0;
-    const DevHuff* dc1;
-    const DevHuff* dc2;
-    const DevHuff* ac0;
-    const DevHuff* ac1;
-    const DevHuff* ac2;
 };
 
 __device__ __forceinline__ void load_ctx(const Params& P, const ImgDesc& D, uint64_t L, ImgCtx& c) {
     c.words = reinterpret_cast<const uint32_t*>(P.ubuf);
     c.bit_base = D.raw_off * 8;
     c.L = L;
-    c.du_comp = D.du_comp;
+    c.fast = reinterpret_cast<const uint32_t*>(P.huff);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        c.tdc[k] = uint32_t(D.dc_tab[k]) * kHuffWords;
+        c.tac[k] = uint32_t(D.ac_tab[k]) * kHuffWords;
+    }
+    uint32_t duc = 0;
+    for (uint32_t s = 0; s < D.dpm; ++s) duc |= (uint32_t(D.du_comp >> (4 * s)) & 3u) << (2 * s);
+    c.duc = duc;
     c.dpm = D.dpm;
-    c.dc0 = P.huff + D.dc_tab[0];
-    c.dc1 = P.huff + D.dc_tab[1];
-    c.dc2 = P.huff + D.dc_tab[2];
-    c.ac0 = P.huff + D.ac_tab[0];
-    c.ac1 = P.huff + D.ac_tab[1];
-    c.ac2 = P.huff + D.ac_tab[2];
 }
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
@@ -395,6 +395,7 @@ struct DecState {
 struct NullSink {
     static constexpr bool kWrite = false;
     __device__ __forceinline__ void put(uint32_t, int32_t) {}
+    __device__ __forceinline__ void block_end(uint32_t) {}
 };
 
 // decode_subsequence (parallel_decode.hpp:122-164) with decode_next_symbol
@@ -402,124 +403,156 @@ struct NullSink {
 // [s.p, end_bit).  The caller seeds s (p, c, z, dc accumulators); n starts at
 // 0.  Sync mode: an InvalidCode/OutOfBits marks the state divergent at the
 // last good symbol.  Write mode: stops at `cap` slots; errors are reported.
+//
+// The hot loop keeps 32-bit bookkeeping (bits left in the range and, saturated,
+// to the scan end), refills its 64-bit window branch-free, and resolves code +
+// magnitude with one probe of an 11-bit table whose entry carries the code
+// length, total length, magnitude size, run and kind (jfif.cpp build_fast).
+// Windows the probe cannot settle (long codes, invalid prefixes, the last 32
+// bits of the scan) take the reference's exact path with its error order.
 template <class Sink>
-__device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint64_t end_bit,
-                                             uint32_t cap, Sink& sink) {
+__device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint64_t end_bit, uint32_t cap,
+                                             Sink& sink) {
     s.n = 0;
     s.div = false;
     s.err = 0;
     if (s.p >= end_bit) return;
     // 64-bit MSB-first window over the unstuffed bytes
-    uint64_t abs = ic.bit_base + s.p;
-    uint64_t widx = abs >> 5;
-    uint32_t sh = uint32_t(abs & 31);
-    uint64_t acc = (uint64_t(bswap32(ic.words[widx])) << 32) | bswap32(ic.words[widx + 1]);
-    acc <<= sh;
+    const uint64_t abs = ic.bit_base + s.p;
+    const uint32_t* wp = ic.words + (abs >> 5);
+    const uint32_t sh = uint32_t(abs & 31);
+    uint64_t acc = ((uint64_t(bswap32(wp[0])) << 32) | bswap32(wp[1])) << sh;
     int cnt = 64 - int(sh);
-    widx += 2;
+    wp += 2;
     uint64_t p = s.p;
     uint32_t c = s.c, z = s.z, n = 0;
     int32_t a0 = s.dc0, a1 = s.dc1, a2 = s.dc2;
-    const uint64_t L = ic.L;
-    while (p < end_bit) {
-        if (Sink::kWrite && n >= cap) break;
-        if (cnt <= 32) {
-            acc |= uint64_t(bswap32(ic.words[widx])) << (32 - cnt);
-            cnt += 32;
-            ++widx;
-        }
-        const uint32_t comp = uint32_t(ic.du_comp >> (4 * c)) & 15u;
-        const DevHuff* t = z == 0 ? (comp == 0 ? ic.dc0 : (comp == 1 ? ic.dc1 : ic.dc2))
-                                  : (comp == 0 ? ic.ac0 : (comp == 1 ? ic.ac1 : ic.ac2));
-        const uint64_t avail = L - p;  // >= 1 inside the loop
-        // fast path: code + magnitude resolved by one probe (valid symbols
-        // only, and only where all kFastBits window bits are real)
-        const uint32_t fe = __ldg(&t->fast[uint32_t(acc >> (64 - kFastBits))]);
-        uint32_t len, l = 0, run = 0;
-        bool eob = false, coefk = false;
-        int32_t coef = 0;
-        if ((fe & 31u) != 0 && avail >= 32) {
-            // codeword resolved by one probe; magnitude bits read arithmetically
-            // (all code + magnitude bits are real: <= 11 + 11 < 32 <= avail)
-            const uint32_t clen = fe & 31u;
-            l = (fe >> 5) & 15u;
-            const uint32_t kind = fe & (3u << 15);
-            eob = kind == kFastEOB;
-            coefk = kind == 0;
-            run = eob ? 63 - z : ((fe >> 9) & 63u);
-            const uint32_t top = uint32_t((acc << clen) >> 32);
-            const uint32_t bits = l ? (top >> (32 - l)) : 0u;
-            coef = (l == 0 || (bits >> (l - 1))) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1);
-            len = clen + l;
-        } else {
-            uint32_t maxlen;
-            const uint32_t e = dev_lookup(t, uint32_t(acc >> 48), maxlen);
-            const uint32_t clen = e >> 8, sym = e & 255u;
-            int32_t err = 0;
-            if (clen == 0) {
-                err = avail < maxlen ? kOutOfBits : kInvalidCode;
-            } else if (clen > avail) {
-                err = kOutOfBits;
-            } else if (z == 0) {
-                l = sym;
-                if (l > 11)
-                    err = kInvalidCode;
-                else if (avail - clen < l)
-                    err = kOutOfBits;
-                coefk = true;
-            } else {
-                const uint32_t r = sym >> 4;
-                l = sym & 15u;
-                if (l == 0) {
-                    if (r == 0) {
-                        eob = true;
-                        run = 63 - z;
-                    } else if (r == 15) {
-                        run = 15;
-                    } else {
-                        err = kInvalidCode;
-                    }
-                } else if (l > 10) {
-                    err = kInvalidCode;
-                } else if (avail - clen < l) {
-                    err = kOutOfBits;
-                } else {
-                    run = r;
-                    coefk = true;
-                }
-            }
-            if (err) {
-                s.div = true;
-                s.err = err;
+    uint32_t comp = (ic.duc >> (2 * c)) & 3u;
+    uint32_t tdc = comp == 0 ? ic.tdc[0] : (comp == 1 ? ic.tdc[1] : ic.tdc[2]);
+    uint32_t tac = comp == 0 ? ic.tac[0] : (comp == 1 ? ic.tac[1] : ic.tac[2]);
+    const uint64_t lr = ic.L - p;
+    int32_t lrem = lr > 0x40000000ull ? 0x40000000 : int32_t(lr);  // bits to the scan end, saturated
+    uint64_t left = end_bit - p;
+    bool stop = false;
+    while (!stop) {
+        // the range in chunks of < 2^30 bits (one chunk for any realistic subsequence)
+        int32_t rem = left > 0x40000000ull ? 0x40000000 : int32_t(left);
+        left -= uint64_t(rem);
+        const int32_t rem0 = rem;
+        while (rem > 0) {
+            if (Sink::kWrite && n >= cap) {
+                stop = true;
                 break;
             }
-            if (l) {
-                const uint32_t bits = uint32_t((acc << clen) >> (64 - l));
-                coef = bits >= (1u << (l - 1)) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1);
+            {  // refill to >= 32 valid bits, branch-free
+                const uint32_t w = bswap32(*wp);
+                const bool need = cnt <= 32;
+                acc |= need ? (uint64_t(w) << ((32 - cnt) & 63)) : 0ull;
+                wp += need ? 1 : 0;
+                cnt += need ? 32 : 0;
             }
-            len = clen + l;
+            const uint32_t hi = uint32_t(acc >> 32);
+            const uint32_t fe = __ldg(ic.fast + (z ? tac : tdc) + (hi >> (32 - kFastBits)));
+            uint32_t len, step, coefk;
+            int32_t coef;
+            if ((fe & 31u) != 0 && lrem >= 32) {
+                // code + magnitude (<= 11 + 11 bits) all real: lrem >= 32
+                const uint32_t clen = fe & 31u, l = (fe >> 10) & 15u;
+                len = (fe >> 5) & 31u;
+                const uint32_t bits = __funnelshift_l(hi << clen, 0u, l);  // top l bits after the code
+                const int32_t t = int32_t((1u << l) - 1u);
+                coef = int32_t(bits) - (((int32_t(bits) - ((t + 1) >> 1)) >> 31) & t);  // extend()
+                step = (fe & kFastEOB) ? 64u - z : ((fe >> 14) & 63u) + 1u;
+                coefk = fe & kFastCoef;
+            } else {
+                const DevHuff* t = reinterpret_cast<const DevHuff*>(ic.fast + (z ? tac : tdc));
+                uint32_t maxlen;
+                const uint32_t e = dev_lookup(t, hi >> 16, maxlen);
+                const uint32_t clen = e >> 8, sym = e & 255u;
+                const uint32_t avail = uint32_t(lrem);  // >= 1 inside the range
+                int32_t err = 0;
+                uint32_t l = 0, run = 0;
+                bool eob = false;
+                coefk = 0;
+                if (clen == 0) {
+                    err = avail < maxlen ? kOutOfBits : kInvalidCode;
+                } else if (clen > avail) {
+                    err = kOutOfBits;
+                } else if (z == 0) {
+                    l = sym;
+                    if (l > 11)
+                        err = kInvalidCode;
+                    else if (avail - clen < l)
+                        err = kOutOfBits;
+                    coefk = 1;
+                } else {
+                    const uint32_t r = sym >> 4;
+                    l = sym & 15u;
+                    if (l == 0) {
+                        if (r == 0) {
+                            eob = true;
+                        } else if (r == 15) {
+                            run = 15;
+                        } else {
+                            err = kInvalidCode;
+                        }
+                    } else if (l > 10) {
+                        err = kInvalidCode;
+                    } else if (avail - clen < l) {
+                        err = kOutOfBits;
+                    } else {
+                        run = r;
+                        coefk = 1;
+                    }
+                }
+                if (err) {
+                    s.div = true;
+                    s.err = err;
+                    stop = true;
+                    break;
+                }
+                coef = 0;
+                if (l) {
+                    const uint32_t bits = uint32_t((acc << clen) >> (64 - l));
+                    coef = bits >= (1u << (l - 1)) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1);
+                }
+                len = clen + l;
+                step = eob ? 64u - z : run + 1u;
+            }
+            if (Sink::kWrite && n + step > cap) {  // phantom tail past the true end
+                stop = true;
+                break;
+            }
+            if (z == 0) {
+                if (comp == 0)
+                    a0 += coef, coef = a0;
+                else if (comp == 1)
+                    a1 += coef, coef = a1;
+                else
+                    a2 += coef, coef = a2;
+            }
+            if (Sink::kWrite && coefk) sink.put(z + step - 1, coef);
+            acc <<= len;
+            cnt -= int(len);
+            rem -= int32_t(len);
+            lrem -= int32_t(len);
+            n += step;
+            z += step;
+            if (z >= 64) {
+                z = 0;
+                c = (c + 1 == ic.dpm) ? 0 : c + 1;
+                comp = (ic.duc >> (2 * c)) & 3u;
+                tdc = comp == 0 ? ic.tdc[0] : (comp == 1 ? ic.tdc[1] : ic.tdc[2]);
+                tac = comp == 0 ? ic.tac[0] : (comp == 1 ? ic.tac[1] : ic.tac[2]);
+                if (Sink::kWrite) sink.block_end(comp);
+            }
         }
-        const uint32_t total = len;
-        const uint32_t step = run + 1;
-        if (Sink::kWrite && n + step > cap) break;  // phantom tail past the true end
-        if (z == 0) {
-            if (comp == 0)
-                a0 += coef, coef = a0;
-            else if (comp == 1)
-                a1 += coef, coef = a1;
-            else
-                a2 += coef, coef = a2;
-        }
-        if (Sink::kWrite && coefk) sink.put(n + run, coef);
-        acc <<= total;
-        cnt -= int(total);
-        p += total;
-        n += step;
-        z += step;
-        if (z >= 64 || eob) {
-            z = 0;
-            c = (c + 1 == ic.dpm) ? 0 : c + 1;
-        }
+        p += uint64_t(int64_t(rem0) - int64_t(rem));
+        if (stop) break;
+        // rem <= 0: the last symbol ran -rem bits past the chunk end
+        const uint64_t over = uint64_t(-int64_t(rem));
+        if (left <= over) break;
+        left -= over;
     }
     s.p = p;
     s.n = n;
@@ -924,60 +957,53 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
 }
 
 // ======================================================= K3: write pass ====
-// Per-thread 64-coefficient staging block in shared memory (raster order,
-// stride 72 int16 → conflict-free 16-byte rows).  Blocks this thread fully
-// owns go out as 8 x 16-byte stores; the partial first/last blocks shared
-// with a neighbouring subsequence write only the owned slots.
-constexpr int kBlkStride = 72;
-
+// Each thread re-decodes its subsequence from the synchronised state and
+// stages the current data unit in a private shared-memory block (column-major,
+// stride 72 int16 → conflict-free 16-byte rows).  The decoder signals block
+// ends: a block this thread owns entirely leaves as 4 full-sector 32-byte
+// stores; the first / last blocks shared with a neighbouring subsequence write
+// only the owned slots.
+//
 // Per data unit K3 also emits K4's metadata (it sees the few nonzero
 // coefficients as it decodes them; K4 would have to scan all 64):
-//   flags = nonzero-row mask | has-AC << 8 | big << 9, and
-//   S = sum over nonzero F of w_u w_v |F| (bounds |r| and the FP32 IDCT error).
+//   flags = nonzero-column mask | has-AC << 8, and
+//   S = sum over nonzero F of w_u w_v |F| (bounds |r| and the FP32 IDCT error;
+//   w_u = max_x |basis[u][x]|, weights x quantiser precomputed per table).
 // Units split between two subsequences combine through atomics into the
 // buffer zeroed before K3.
-constexpr uint32_t kMetaNonDc = 1u << 8, kMetaBig = 1u << 9;
+constexpr int kBlkStride = 72;
+constexpr uint32_t kMetaNonDc = 1u << 8;
 
 struct BlockSink {
     static constexpr bool kWrite = true;
-    const uint8_t* zz2c; // zig-zag -> column-major, in smem (lane-divergent index)
-    const float* wts;    // w_u * w_v per raster index, in smem
+    const uint32_t* zt;  // smem, per zig-zag k: column-major index | (column bit | nonDC) << 8
+    const float* wq;     // per quant table, per zig-zag k: w_u w_v Q (global, read-only)
+    const uint16_t* qt;  // the image's quant table index per component
     int16_t* buf;        // this thread's smem block
     int16_t* coef;       // batch coefficient buffer
     uint2* meta;         // batch per-unit metadata
-    uint64_t du_first;   // image's first data unit
-    uint64_t own_lo;     // owned slots [own_lo, own_hi) within the image
-    uint64_t own_hi;
-    uint64_t cur;        // current block (image-relative)
-    uint64_t du_comp;    // slot -> component nibbles
-    const uint16_t* q0;  // raster quantisers of components 0..2
-    const uint16_t* q1;
-    const uint16_t* q2;
-    const uint16_t* qc;  // quantiser of the current unit
-    uint32_t slot, dpm;
+    uint64_t du;         // batch data unit of the current block
+    uint64_t slot0;      // image-relative slot of the current block's first coefficient
+    uint64_t own_hi;     // owned slots end (image-relative)
+    const float* wqc;    // wq row of the current block's component
+    uint32_t klo;        // first owned zig-zag position of the current block
     uint32_t mflags;     // metadata of the current unit (owned part)
     float mS;
 
-    __device__ __forceinline__ void set_unit_comp() {
-        const uint32_t comp = uint32_t(du_comp >> (4 * slot)) & 15u;
-        qc = comp == 0 ? q0 : (comp == 1 ? q1 : q2);
-    }
-    uint32_t dbg;
-    __device__ __forceinline__ void flush(uint64_t b) {
-        if (dbg & 16) {  // ablation: no global stores
-            int4 zero = make_int4(0, 0, 0, 0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(buf)[q] = zero;
-            mflags = 0;
-            mS = 0.f;
-            slot = (slot + 1 == dpm) ? 0 : slot + 1;
-            set_unit_comp();
-            return;
+    __device__ __forceinline__ void set_comp(uint32_t comp) { wqc = wq + 64u * qt[comp]; }
+    __device__ __forceinline__ void put(uint32_t k, int32_t v) {
+        const uint32_t t = zt[k];
+        buf[t & 0xFFu] = int16_t(v);
+        if (v != 0) {
+            mflags |= t >> 8;
+            mS = fmaf(__ldg(wqc + k), float(abs(v)), mS);
         }
-        const uint64_t lo = max(own_lo, b * 64), hi = min(own_hi, b * 64 + 64);
-        int16_t* dst = coef + (du_first + b) * 64;
-        uint2* md = meta + du_first + b;
-        if (lo == b * 64 && hi == b * 64 + 64) {
+    }
+    // flush the owned zig-zag range [klo, khi) of the current block and move on
+    __device__ __forceinline__ void flush(uint32_t khi) {
+        int16_t* dst = coef + du * 64;
+        uint2* md = meta + du;
+        if (klo == 0 && khi == 64) {
             // full-sector 256-bit stores (STG.E.ENL2.256): no partial-sector merges in L2
             const int4* s4 = reinterpret_cast<const int4*>(buf);
 #pragma unroll
@@ -989,64 +1015,44 @@ struct BlockSink {
             }
             *md = make_uint2(mflags, __float_as_uint(mS));
         } else {
-            for (uint64_t sl = lo; sl < hi; ++sl) {
-                int r = zz2c[sl & 63];
+            for (uint32_t k = klo; k < khi; ++k) {
+                const uint32_t r = zt[k] & 0xFFu;
                 dst[r] = buf[r];
             }
             if (mflags) atomicOr(&md->x, mflags);
             if (mS != 0.f) atomicAdd(reinterpret_cast<float*>(&md->y), mS);
         }
-        int4 zero = make_int4(0, 0, 0, 0);
+        const int4 zero = make_int4(0, 0, 0, 0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(buf)[q] = zero;
         mflags = 0;
         mS = 0.f;
-        slot = (slot + 1 == dpm) ? 0 : slot + 1;
-        set_unit_comp();
+        klo = 0;
+        ++du;
+        slot0 += 64;
     }
-    // slot relative to this subsequence's offset is passed as local index
-    uint64_t base;       // own_lo
-    __device__ __forceinline__ void put(uint32_t local, int32_t v) {
-        const uint64_t s = base + local;
-        const uint64_t b = s >> 6;
-        while (cur < b) {
-            flush(cur);
-            ++cur;
-        }
-        const uint32_t r = zz2c[s & 63];
-        buf[r] = int16_t(v);
-        if (!(dbg & 32) && int16_t(v) != 0) {
-            const int32_t F = int32_t(int16_t(v)) * int32_t(__ldg(qc + r));
-            const uint32_t a = uint32_t(abs(F));
-            mflags |= (1u << (r >> 3)) | (r ? kMetaNonDc : 0u) | (a >= (1u << 22) ? kMetaBig : 0u);
-            mS = fmaf(wts[r], float(a), mS);
-        }
+    // the decoder completed the current block (all of it from klo on is owned)
+    __device__ __forceinline__ void block_end(uint32_t next_comp) {
+        flush(64);
+        set_comp(next_comp);
     }
+    // the owned slots left after the last decoded symbol (zeros past it)
     __device__ __forceinline__ void finish() {
-        if (own_hi <= own_lo) return;
-        const uint64_t last = (own_hi - 1) >> 6;
-        while (cur <= last) {
-            flush(cur);
-            ++cur;
-        }
+        while (slot0 < own_hi) flush(uint32_t(min64(64, own_hi - slot0)));
     }
 };
 
 __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
     __shared__ __align__(16) int16_t s_blk[kK3Threads * kBlkStride];
-    __shared__ uint8_t s_zz2c[64];
-    __shared__ float s_wts[64];
+    __shared__ uint32_t s_zt[64];
     const int tid = threadIdx.x;
     if (tid < 64) {
-        // max_x |basis[u][x]| rounded up, product over (row, column)
-        const float w[8] = {0.35356f, 0.4904f, 0.46195f, 0.4904f, 0.35356f, 0.4904f, 0.46195f, 0.4904f};
-        s_zz2c[tid] = c_zz2c[tid];
-        s_wts[tid] = w[tid >> 3] * w[tid & 7];
+        const uint32_t c = c_zz2c[tid];
+        s_zt[tid] = c | (((1u << (c >> 3)) | (tid ? kMetaNonDc : 0u)) << 8);
     }
-    __syncthreads();
     int16_t* buf = s_blk + tid * kBlkStride;
     {
-        int4 zero = make_int4(0, 0, 0, 0);
+        const int4 zero = make_int4(0, 0, 0, 0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(buf)[q] = zero;
     }
@@ -1086,26 +1092,19 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
     s.dc2 = int16_t(pd.hi & 0xFFFFu);
     const uint64_t o = P.off[g];
     BlockSink sink;
-    sink.zz2c = s_zz2c;
-    sink.wts = s_wts;
-    sink.meta = P.meta;
-    sink.du_comp = D.du_comp;
-    sink.dpm = D.dpm;
-    sink.q0 = P.quant_raster + 64u * D.q_tab[0];
-    sink.q1 = P.quant_raster + 64u * D.q_tab[1];
-    sink.q2 = P.quant_raster + 64u * D.q_tab[2];
-    sink.slot = uint32_t((o >> 6) % D.dpm);
-    sink.set_unit_comp();
-    sink.mflags = 0;
-    sink.mS = 0.f;
-    sink.dbg = P.debug;
+    sink.zt = s_zt;
+    sink.wq = P.wq;
+    sink.qt = D.q_tab;
     sink.buf = buf;
     sink.coef = P.coef;
-    sink.du_first = D.du_first;
-    sink.own_lo = o;
+    sink.meta = P.meta;
+    sink.du = D.du_first + (o >> 6);
+    sink.slot0 = o & ~63ull;
     sink.own_hi = o + cap;
-    sink.base = o;
-    sink.cur = o >> 6;
+    sink.klo = uint32_t(o & 63);
+    sink.mflags = 0;
+    sink.mS = 0.f;
+    sink.set_comp(uint32_t(D.du_comp >> (4 * ((o >> 6) % D.dpm))) & 15u);
     const uint64_t end_bit = min((i + 1) * P.sb, L);
     decode_range(ic, s, end_bit, cap, sink);
     if (s.err) {
@@ -1514,7 +1513,9 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
             if (isac) {
                 const uint32_t a = __popc(acm & lt_mask);
                 const float Sb = __uint_as_float(pm.y);
-                const bool big = (pm.x & kMetaBig) || Sb >= 2097152.f;
+                // S >= 2^18 covers every unit with some |F| >= 2^21 (w_u w_v >= 1/8): those
+                // take exact FP64; below it F is exact in FP32 and |acc| <= S
+                const bool big = Sb >= 262144.f;
                 S.acl[a] = uint8_t(lane);
                 S.cm[a] = uint16_t((pm.x & 0xFFu) | (big ? 0x100u : 0u));
                 // |r32 - r64| <= 18u S (+ FP64's own ~1e-15 S), u = 2^-24

@@ -109,7 +109,7 @@ struct pjg_batch {
     size_t raw_bytes = 0;
     bool packed = false;
     // meta blob layout (offsets into ctx->meta)
-    size_t m_desc = 0, m_state = 0, m_huff = 0, m_quant = 0, m_basis = 0, m_k0 = 0, m_tile = 0,
+    size_t m_desc = 0, m_state = 0, m_huff = 0, m_quant = 0, m_wq = 0, m_basis = 0, m_k0 = 0, m_tile = 0,
            m_sub = 0, m_k0img = 0, m_subimg = 0, m_total = 0;
     uint32_t n_huff = 0, n_quant = 0;
     uint32_t k0_tiles = 0, k4_tiles = 0, k1_ctas = 0, k2_tiles = 0;
@@ -319,6 +319,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     std::vector<std::array<uint16_t, 64>> quants;
     std::vector<std::pair<const HuffSpec*, bool>> huff_src;  // unique specs (first occurrence)
     std::vector<std::array<uint16_t, 64>> quant_src;
+    std::vector<float> wqs;  // per quant table: 64 K3 metadata weights (zig-zag order)
     auto same_spec = [](const HuffSpec& a, const HuffSpec& b) {
         return a.counts == b.counts && a.symbols.size() == b.symbols.size() &&
                std::memcmp(a.symbols.data(), b.symbols.data(), a.symbols.size()) == 0;
@@ -345,6 +346,10 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         for (int z = 0; z < 64; ++z) r[(kZz2R[z] & 7) * 8 + (kZz2R[z] >> 3)] = q[z];
         quants.push_back(r);
         quant_src.push_back(q);
+        // K3 metadata weights: w_u w_v Q per zig-zag position, w_u >= max_x |basis[u][x]|
+        static const double kW[8] = {0.35356, 0.4904, 0.46195, 0.4904, 0.35356, 0.4904, 0.46195, 0.4904};
+        for (int z = 0; z < 64; ++z)
+            wqs.push_back(float(kW[kZz2R[z] >> 3] * kW[kZz2R[z] & 7] * double(q[z]) * (1.0 + 1e-6)));
         return uint32_t(quants.size() - 1);
     };
 
@@ -473,6 +478,8 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     o = align_up(o + huffs.size() * sizeof(DevHuff), 16);
     b->m_quant = o;
     o = align_up(o + quants.size() * 128, 16);
+    b->m_wq = o;
+    o = align_up(o + quants.size() * 64 * sizeof(float), 16);
     b->m_basis = o;
     o = align_up(o + 64 * sizeof(double), 16);
     b->m_k0 = o;
@@ -498,6 +505,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     }
     std::memcpy(mh + b->m_huff, huffs.data(), huffs.size() * sizeof(DevHuff));
     std::memcpy(mh + b->m_quant, quants.data(), quants.size() * 128);
+    if (!wqs.empty()) std::memcpy(mh + b->m_wq, wqs.data(), wqs.size() * sizeof(float));
     std::memcpy(mh + b->m_basis, ctx->basis, 64 * sizeof(double));
     std::memcpy(mh + b->m_k0, k0_first.data(), (n + 1) * 4);
     std::memcpy(mh + b->m_tile, tile_first.data(), (n + 1) * 4);
@@ -549,6 +557,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.huff = reinterpret_cast<const DevHuff*>(md + b->m_huff);
     p.quant_raster = reinterpret_cast<const uint16_t*>(md + b->m_quant);
     p.basis = reinterpret_cast<const double*>(md + b->m_basis);
+    p.wq = reinterpret_cast<const float*>(md + b->m_wq);
     p.raw = ctx->raw.as<uint8_t>();
     p.ubuf = ctx->ubuf.as<uint8_t>();
     p.k0_first = reinterpret_cast<const uint32_t*>(md + b->m_k0);

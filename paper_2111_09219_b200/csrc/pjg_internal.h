@@ -43,9 +43,10 @@ constexpr int kPrimaryBits = 9;
 constexpr int kFastBits = 11;
 // fast entry for a kFastBits window whose codeword fits and decodes to a
 // symbol the reference accepts: bits 0-4 codeword length (0 = take the exact
-// path), 5-8 magnitude bits l, 9-14 run, 15-16 kind (0 coefficient, 1 EOB,
-// 2 ZRL).  The magnitude value itself is extracted arithmetically.
-constexpr uint32_t kFastEOB = 1u << 15, kFastZRL = 2u << 15;
+// path), 5-9 code + magnitude length, 10-13 magnitude bits l, 14-19 run,
+// bit 20 EOB, bit 21 coefficient (as opposed to EOB / ZRL).  The magnitude
+// value itself is extracted arithmetically.
+constexpr uint32_t kFastEOB = 1u << 20, kFastCoef = 1u << 21;
 
 struct DevHuff {
     uint32_t fast[1 << kFastBits];    // code + magnitude in one probe when both fit in kFastBits
@@ -159,6 +160,7 @@ struct Params {
     const DevHuff* huff;
     const uint16_t* quant_raster;  // 64 uint16 per table, RASTER order
     const double* basis;           // 64 doubles, basis[u][x] (host std::cos)
+    const float* wq;               // per quant table, zig-zag order: w_u w_v Q (K3 metadata)
     // raw & unstuffed scan
     const uint8_t* raw;
     uint8_t* ubuf;
