@@ -345,7 +345,7 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 
 // can index with absolute word positions (it then reads shared memory through
 // generic loads); returns the global pointer when the range does not fit.
 // [lo, hi) is this thread's byte range (empty when lo >= hi).
-constexpr int kStageBytes = 20480;
+constexpr int kStageBytes = 20480;  // 128 subsequences x 1024 bits + an image boundary's header bytes
 __device__ __forceinline__ const uint32_t* stage_scan(const uint8_t* ubuf, uint64_t lo, uint64_t hi, int tid,
                                                       int nthreads, int4* s_stage, unsigned long long* s_lo,
                                                       unsigned long long* s_hi) {
@@ -972,13 +972,13 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
 // Units split between two subsequences combine through atomics into the
 // buffer zeroed before K3.
 constexpr int kBlkStride = 72;
+constexpr uint32_t kK3SmemQuant = 4;  // quant tables staged in shared memory
 constexpr uint32_t kMetaNonDc = 1u << 8;
 
 struct BlockSink {
     static constexpr bool kWrite = true;
     const uint32_t* zt;  // smem, per zig-zag k: column-major index | (column bit | nonDC) << 8
-    const float* wq;     // per quant table, per zig-zag k: w_u w_v Q (global, read-only)
-    const uint16_t* qt;  // the image's quant table index per component
+    const float* wq3[3]; // wq rows of the image's components
     int16_t* buf;        // this thread's smem block
     int16_t* coef;       // batch coefficient buffer
     uint2* meta;         // batch per-unit metadata
@@ -990,13 +990,13 @@ struct BlockSink {
     uint32_t mflags;     // metadata of the current unit (owned part)
     float mS;
 
-    __device__ __forceinline__ void set_comp(uint32_t comp) { wqc = wq + 64u * qt[comp]; }
+    __device__ __forceinline__ void set_comp(uint32_t comp) { wqc = comp == 0 ? wq3[0] : (comp == 1 ? wq3[1] : wq3[2]); }
     __device__ __forceinline__ void put(uint32_t k, int32_t v) {
         const uint32_t t = zt[k];
         buf[t & 0xFFu] = int16_t(v);
         if (v != 0) {
             mflags |= t >> 8;
-            mS = fmaf(__ldg(wqc + k), float(abs(v)), mS);
+            mS = fmaf(wqc[k], float(abs(v)), mS);
         }
     }
     // flush the owned zig-zag range [klo, khi) of the current block and move on
@@ -1042,14 +1042,18 @@ struct BlockSink {
     }
 };
 
-__global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
+__global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     __shared__ __align__(16) int16_t s_blk[kK3Threads * kBlkStride];
     __shared__ uint32_t s_zt[64];
+    __shared__ float s_wq[kK3SmemQuant * 64];  // the batch's metadata weights when they fit
     const int tid = threadIdx.x;
     if (tid < 64) {
         const uint32_t c = c_zz2c[tid];
         s_zt[tid] = c | (((1u << (c >> 3)) | (tid ? kMetaNonDc : 0u)) << 8);
     }
+    const bool wq_smem = P.n_quant <= kK3SmemQuant;
+    if (wq_smem)
+        for (uint32_t x = tid; x < P.n_quant * 64; x += kK3Threads) s_wq[x] = P.wq[x];
     int16_t* buf = s_blk + tid * kBlkStride;
     {
         const int4 zero = make_int4(0, 0, 0, 0);
@@ -1093,8 +1097,11 @@ __global__ void __launch_bounds__(kK3Threads) k3_write(Params P) {
     const uint64_t o = P.off[g];
     BlockSink sink;
     sink.zt = s_zt;
-    sink.wq = P.wq;
-    sink.qt = D.q_tab;
+    {
+        const float* wqb = wq_smem ? s_wq : P.wq;
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) sink.wq3[cc] = wqb + 64u * D.q_tab[cc];
+    }
     sink.buf = buf;
     sink.coef = P.coef;
     sink.meta = P.meta;

@@ -558,6 +558,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.quant_raster = reinterpret_cast<const uint16_t*>(md + b->m_quant);
     p.basis = reinterpret_cast<const double*>(md + b->m_basis);
     p.wq = reinterpret_cast<const float*>(md + b->m_wq);
+    p.n_quant = uint32_t(quants.size());
     p.raw = ctx->raw.as<uint8_t>();
     p.ubuf = ctx->ubuf.as<uint8_t>();
     p.k0_first = reinterpret_cast<const uint32_t*>(md + b->m_k0);

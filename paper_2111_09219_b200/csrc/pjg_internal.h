@@ -161,6 +161,7 @@ struct Params {
     const uint16_t* quant_raster;  // 64 uint16 per table, RASTER order
     const double* basis;           // 64 doubles, basis[u][x] (host std::cos)
     const float* wq;               // per quant table, zig-zag order: w_u w_v Q (K3 metadata)
+    uint32_t n_quant;              // quant tables in the batch
     // raw & unstuffed scan
     const uint8_t* raw;
     uint8_t* ubuf;
