@@ -343,30 +343,60 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 
 // Stages the unstuffed-scan bytes a CTA's subsequences touch into shared
 // memory (coalesced 16-byte loads) and returns a word pointer that decode_range
 // can index with absolute word positions (it then reads shared memory through
-// generic loads); returns the global pointer when the range does not fit.
-// [lo, hi) is this thread's byte range (empty when lo >= hi).
-constexpr int kStageBytes = 20480;  // 128 subsequences x 1024 bits + an image boundary's header bytes
-__device__ __forceinline__ const uint32_t* stage_scan(const uint8_t* ubuf, uint64_t lo, uint64_t hi, int tid,
-                                                      int nthreads, int4* s_stage, unsigned long long* s_lo,
-                                                      unsigned long long* s_hi) {
+// generic loads).  A CTA can straddle images, so the bytes are staged as up to
+// kStageSegs segments, one per image (the bytes between two images' scans —
+// the next file's headers — are skipped).  [lo, hi) is this thread's byte
+// range (empty when lo >= hi), k its image; segments that do not fit fall back
+// to the global pointer.
+constexpr int kStageBytes = 16512;  // 128 subsequences x 1024 bits + window slack + segment alignment
+constexpr int kStageSegs = 4;
+struct StageSmem {
+    unsigned long long lo[kStageSegs], hi[kStageSegs];
+    uint32_t off[kStageSegs];
+    uint32_t k0;
+};
+__device__ __forceinline__ const uint32_t* stage_scan(const uint8_t* ubuf, uint64_t lo, uint64_t hi, uint32_t k,
+                                                      int tid, int nthreads, int4* s_stage, StageSmem& sm) {
+    if (tid < kStageSegs) {
+        sm.lo[tid] = ~0ull;
+        sm.hi[tid] = 0ull;
+    }
+    if (tid == 0) sm.k0 = k;
+    __syncthreads();
+    const uint32_t seg = k - sm.k0;
+    if (lo < hi && seg < kStageSegs) {
+        atomicMin(&sm.lo[seg], (unsigned long long)lo);
+        atomicMax(&sm.hi[seg], (unsigned long long)hi);
+    }
+    __syncthreads();
     if (tid == 0) {
-        *s_lo = ~0ull;
-        *s_hi = 0ull;
+        uint32_t off = 0;
+        for (int q = 0; q < kStageSegs; ++q) {
+            sm.off[q] = 0xFFFFFFFFu;
+            if (sm.hi[q] > sm.lo[q]) {
+                const uint64_t blo = sm.lo[q] & ~15ull;
+                const uint64_t sz = (sm.hi[q] - blo + 15) & ~15ull;
+                if (off + sz <= uint64_t(kStageBytes)) {
+                    sm.off[q] = off;
+                    off += uint32_t(sz);
+                }
+            }
+        }
     }
     __syncthreads();
-    if (lo < hi) {
-        atomicMin(s_lo, (unsigned long long)lo);
-        atomicMax(s_hi, (unsigned long long)hi);
+#pragma unroll 1
+    for (int q = 0; q < kStageSegs; ++q) {
+        if (sm.off[q] == 0xFFFFFFFFu) continue;
+        const uint64_t blo = sm.lo[q] & ~15ull;
+        const uint32_t n16 = uint32_t((sm.hi[q] - blo + 15) >> 4);
+        const int4* src = reinterpret_cast<const int4*>(ubuf + blo);
+        int4* dst = s_stage + (sm.off[q] >> 4);
+        for (uint32_t x = tid; x < n16; x += nthreads) dst[x] = __ldcs(src + x);
     }
     __syncthreads();
-    const uint64_t blo = *s_lo & ~15ull, bhi = *s_hi;
-    const uint32_t* global_words = reinterpret_cast<const uint32_t*>(ubuf);
-    if (!(bhi > blo) || bhi - blo > uint64_t(kStageBytes)) return global_words;
-    const uint32_t n16 = uint32_t((bhi - blo + 15) >> 4);
-    const int4* src = reinterpret_cast<const int4*>(ubuf + blo);
-    for (uint32_t q = tid; q < n16; q += nthreads) s_stage[q] = __ldcs(src + q);
-    __syncthreads();
-    return reinterpret_cast<const uint32_t*>(s_stage) - (blo >> 2);
+    if (seg < kStageSegs && sm.off[seg] != 0xFFFFFFFFu)
+        return reinterpret_cast<const uint32_t*>(s_stage + (sm.off[seg] >> 4)) - ((sm.lo[seg] & ~15ull) >> 2);
+    return reinterpret_cast<const uint32_t*>(ubuf);
 }
 
 
@@ -617,9 +647,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     load_ctx(P, D, L, ic);
     {
         __shared__ int4 s_stage[kStageBytes / 16];
-        __shared__ unsigned long long s_lo, s_hi;
+        __shared__ StageSmem s_sm;
         const uint64_t lo = real ? D.raw_off + ((i * P.sb) >> 3) : 1, hi = real ? D.raw_off + ((min64((i + 1) * P.sb, L) + 7) >> 3) + 24 : 0;
-        ic.words = stage_scan(P.ubuf, lo, hi, tid, T, s_stage, &s_lo, &s_hi);
+        ic.words = stage_scan(P.ubuf, lo, hi, k, tid, T, s_stage, s_sm);
     }
 
     // Round 0: every subsequence decodes from its origin (parallel_decode.hpp:187-195)
@@ -1072,11 +1102,11 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     load_ctx(P, D, L, ic);
     {
         __shared__ int4 s_stage[kStageBytes / 16];
-        __shared__ unsigned long long s_lo, s_hi;
+        __shared__ StageSmem s_sm;
         // this subsequence's bits start at entries[g-1].p (inside [i*sb, ..)); stage from i*sb
         const uint64_t lo = active ? D.raw_off + ((i * P.sb) >> 3) : 1;
         const uint64_t hi = active ? D.raw_off + ((min64((i + 1) * P.sb, L) + 7) >> 3) + 24 : 0;
-        ic.words = stage_scan(P.ubuf, lo, hi, tid, kK3Threads, s_stage, &s_lo, &s_hi);
+        ic.words = stage_scan(P.ubuf, lo, hi, k, tid, kK3Threads, s_stage, s_sm);
     }
     if (!active) return;
     DecState s;
@@ -1409,6 +1439,66 @@ __device__ __forceinline__ void colour_tile(const WarpImg& I, const uint8_t* pl,
     }
 }
 
+// Whole 32-pixel-wide, full-height tile with 4-byte-aligned rows: two fixed
+// items per lane, no bounds checks.
+template <int HS, bool PAIR>
+__device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl, const ColourLut& L, uint8_t* out,
+                                            uint32_t X0, uint32_t Y0, int lane) {
+    const uint32_t W = I.width;
+    const uint32_t gx = (lane & 7) * 4, jr0 = lane >> 3;
+    const uint32_t cgx = HS == 2 ? gx >> 1 : gx;
+    const uint8_t* yb = pl + I.poff[0] + gx;
+    const uint8_t* cbb = pl + I.poff[1];
+    const uint8_t* crb = pl + I.poff[2];
+    const uint32_t pst0 = I.pst[0], pst1 = I.pst[1];
+    const uint64_t orow = uint64_t(W) * 3;
+    uint8_t* ob = out + I.out_off + (uint64_t(Y0) * W + X0 + gx) * 3;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t jr = jr0 + 4 * h;
+        const uint32_t r0 = PAIR ? 2 * jr : jr;
+        const uint8_t* cbrow = cbb + jr * pst1;
+        const uint8_t* crrow = crb + jr * pst1;
+        int oR[4], oG[4], oB[4];
+        uint32_t tie = 0;
+        uint32_t cx[4];
+        if (HS == 2) {
+            const uint32_t cb2 = *reinterpret_cast<const uint16_t*>(cbrow + cgx);
+            const uint32_t cr2 = *reinterpret_cast<const uint16_t*>(crrow + cgx);
+            chroma_off(L, cb2 & 0xFFu, cr2 & 0xFFu, oR[0], oG[0], oB[0], tie);
+            chroma_off(L, cb2 >> 8, cr2 >> 8, oR[2], oG[2], oB[2], tie);
+            oR[1] = oR[0], oG[1] = oG[0], oB[1] = oB[0];
+            oR[3] = oR[2], oG[3] = oG[2], oB[3] = oB[2];
+            cx[0] = cx[1] = cgx;
+            cx[2] = cx[3] = cgx + 1;
+        } else {
+            const uint32_t cb4 = *reinterpret_cast<const uint32_t*>(cbrow + cgx);
+            const uint32_t cr4 = *reinterpret_cast<const uint32_t*>(crrow + cgx);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                chroma_off(L, (cb4 >> (8 * i)) & 0xFFu, (cr4 >> (8 * i)) & 0xFFu, oR[i], oG[i], oB[i], tie);
+                cx[i] = cgx + i;
+            }
+        }
+        {
+            const uint32_t y4 = *reinterpret_cast<const uint32_t*>(yb + r0 * pst0);
+            const uint3 w = tie ? rgb4_exact(y4, cbrow, crrow, cx) : rgb4(y4, oR, oG, oB);
+            uint32_t* d = reinterpret_cast<uint32_t*>(ob + r0 * orow);
+            d[0] = w.x;
+            d[1] = w.y;
+            d[2] = w.z;
+        }
+        if (PAIR) {
+            const uint32_t y4 = *reinterpret_cast<const uint32_t*>(yb + (r0 + 1) * pst0);
+            const uint3 w = tie ? rgb4_exact(y4, cbrow, crrow, cx) : rgb4(y4, oR, oG, oB);
+            uint32_t* d = reinterpret_cast<uint32_t*>(ob + (r0 + 1) * orow);
+            d[0] = w.x;
+            d[1] = w.y;
+            d[2] = w.z;
+        }
+    }
+}
+
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
     unsigned long long r;
@@ -1537,10 +1627,7 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
                 const uint32_t a = it >> 3, v = it & 7;
                 const uint32_t blk = S.acl[a], cm = S.cm[a];
                 float4* dst = reinterpret_cast<float4*>(S.F + a * kFS + v * 8);
-                if (!((cm >> v) & 1u)) {
-                    dst[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    dst[1] = make_float4(0.f, 0.f, 0.f, 0.f);
-                } else {
+                {  // zero columns dequantise to zeros: no divergent skip
                     const int4 rvi = S.raw[blk * 8 + v];
                     const uint4 qv = *reinterpret_cast<const uint4*>(I.q[I.bcomp[blk]] + v * 8);
                     const uint32_t rw[4] = {uint32_t(rvi.x), uint32_t(rvi.y), uint32_t(rvi.z), uint32_t(rvi.w)};
@@ -1711,7 +1798,17 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
         // 4. output
         const uint32_t X0 = cur_mx0 * cur_mcuw, Y0 = cur_my * cur_mcuh;
         const uint32_t cols = min(cur_nm * cur_mcuw, I.width - X0), rws = min(cur_mcuh, I.height - Y0);
-        if (I.rgb) {
+        const bool full = cols == uint32_t(kTileW) && rws == cur_mcuh && (I.width & 3) == 0 && (I.out_off & 3) == 0;
+        if (I.rgb && full) {
+            if (I.h_max == 2) {
+                if (I.v_max == 2)
+                    colour_full<2, true>(I, S.pl, s_lut, P.out, X0, Y0, lane);
+                else
+                    colour_full<2, false>(I, S.pl, s_lut, P.out, X0, Y0, lane);
+            } else {
+                colour_full<1, false>(I, S.pl, s_lut, P.out, X0, Y0, lane);
+            }
+        } else if (I.rgb) {
             if (I.h_max == 2) {
                 if (I.v_max == 2)
                     colour_tile<2, true>(I, S.pl, s_lut, P.out, X0, Y0, cols, rws, lane);
