@@ -996,7 +996,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
 //
 // Per data unit K3 also emits K4's metadata (it sees the few nonzero
 // coefficients as it decodes them; K4 would have to scan all 64):
-//   flags = nonzero-column mask | has-AC << 8, and
+//   flags = nonzero-column mask | has-AC << 8 | nonzero-row mask << 16, and
 //   S = sum over nonzero F of w_u w_v |F| (bounds |r| and the FP32 IDCT error;
 //   w_u = max_x |basis[u][x]|, weights x quantiser precomputed per table).
 // Units split between two subsequences combine through atomics into the
@@ -1079,7 +1079,7 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     const int tid = threadIdx.x;
     if (tid < 64) {
         const uint32_t c = c_zz2c[tid];
-        s_zt[tid] = c | (((1u << (c >> 3)) | (tid ? kMetaNonDc : 0u)) << 8);
+        s_zt[tid] = c | (((1u << (c >> 3)) | (tid ? kMetaNonDc : 0u) | (1u << (16 + (c & 7)))) << 8);
     }
     const bool wq_smem = P.n_quant <= kK3SmemQuant;
     if (wq_smem)
@@ -1198,11 +1198,12 @@ __device__ __forceinline__ uint32_t pack4_sat(int a0, int a1, int a2, int a3) {
 // out = sum_u b[u][x] tmp[u] (u ascending), zero terms skipped (exact: the
 // running sums start at +0 and fl(s + +-0) = s).  Fc is column-major; `big`
 // units hold int32 bits.  Returns the clamped sample.
-__device__ __noinline__ uint32_t idct_sample_fp64(const float* Fc, bool big, uint32_t cols, const double* b64, int x,
-                                                  int y) {
+__device__ __noinline__ uint32_t idct_sample_fp64(const float* Fc, bool big, uint32_t cols, uint32_t rows,
+                                                  const double* b64, int x, int y) {
     const int32_t* Fi = reinterpret_cast<const int32_t*>(Fc);
     double s = 0.0;
-    for (int u = 0; u < 8; ++u) {
+    for (uint32_t um = rows; um; um &= um - 1) {  // all-zero rows give tmp = +0: skipped
+        const int u = __ffs(um) - 1;
         double t = 0.0;
         for (uint32_t m = cols; m; m &= m - 1) {
             const int v = __ffs(m) - 1;
@@ -1250,7 +1251,7 @@ struct WarpSmem {
     uint8_t pl[1024];             // sample planes (row stride padded by 4)
     WarpImg img;
     float lim[kK4MaxBlocks];      // per AC unit: 0.5 - error bound
-    uint16_t cm[kK4MaxBlocks];    // per AC unit: column mask | big << 8
+    uint32_t cm[kK4MaxBlocks];    // per AC unit: column mask | big << 8 | row mask << 16
     uint8_t acl[kK4MaxBlocks];    // AC units (tile-local index), compact
     uint8_t dcl[kK4MaxBlocks];    // DC-only units
     uint16_t rep[32];             // FP64 replay work list: unit << 6 | x << 3 | y
@@ -1614,9 +1615,16 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
                 // take exact FP64; below it F is exact in FP32 and |acc| <= S
                 const bool big = Sb >= 262144.f;
                 S.acl[a] = uint8_t(lane);
-                S.cm[a] = uint16_t((pm.x & 0xFFu) | (big ? 0x100u : 0u));
-                // |r32 - r64| <= 18u S (+ FP64's own ~1e-15 S), u = 2^-24
-                S.lim[a] = 0.5f - (1.1e-6f * Sb + 2.0e-6f);
+                const uint32_t cols = pm.x & 0xFFu, rows = (pm.x >> 16) & 0xFFu;
+                S.cm[a] = cols | (big ? 0x100u : 0u) | (rows << 16);
+                // Rounding analysis of step 3: the column sums see at most popc(rows)
+                // nonzero products (zero terms are exact in an FMA chain), the row sums
+                // popc(cols), and the two basis factors each carry one FP32 rounding, so
+                // |r32 - r_exact| <= (k + m + 2) u S to first order (k = popc(rows),
+                // m = popc(cols), u = 2^-24); one more u S covers second-order terms and
+                // the reference's own FP64 error (~1e-15 S).
+                const float km = float(__popc(rows) + __popc(cols) + 3);
+                S.lim[a] = 0.5f - (km * 5.9605e-8f * Sb * 1.001f + 1.0e-6f);
             } else if (in) {
                 S.dcl[__popc(dcm & lt_mask)] = uint8_t(lane);
             }
@@ -1787,7 +1795,8 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
                     const uint32_t e = S.rep[lane];
                     const uint32_t a = e >> 6, x = (e >> 3) & 7u, y = e & 7u;
                     const uint32_t blk = S.acl[a], cmw = S.cm[a];
-                    const uint32_t o = idct_sample_fp64(S.F + a * kFS, cmw & 0x100u, cmw & 0xFFu, s_b64, int(x), int(y));
+                    const uint32_t o = idct_sample_fp64(S.F + a * kFS, cmw & 0x100u, cmw & 0xFFu, (cmw >> 16) & 0xFFu,
+                                                        s_b64, int(x), int(y));
                     S.pl[I.boff[blk] + x * I.bps[blk] + y] = uint8_t(o);
                 }
                 __syncwarp();
