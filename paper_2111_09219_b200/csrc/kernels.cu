@@ -146,7 +146,6 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     const uint64_t a = D.raw_off, e = a + raw_len;  // the image's bytes [a, e) in the raw buffer
     const uint64_t win0 = (a & ~15ull) + uint64_t(lt) * kK0Tile;
     const uint64_t g_first = max(win0, a);            // first image byte in this window
-    const uint64_t j0 = g_first - a;                  // its image-relative index
 
     {
         const uint64_t g = win0 + 16u * tid;
@@ -628,7 +627,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     __shared__ uint32_t s_czd[T];
     __shared__ DcSums s_dc[T];
     __shared__ uint32_t s_cta;
-    __shared__ int s_rounds;
 
     const int tid = threadIdx.x;
     if (tid == 0) s_cta = atomicAdd(&P.counters[kTicketK1], 1u);
@@ -1183,7 +1181,8 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
 constexpr float kM128 = 12583040.0f;  // 1.5 * 2^23 + 128: round(acc) + 128 in the low mantissa bits
 constexpr int kMagicBits = 0x4B400000;
 constexpr int kK4Warps = kK4Threads / 32;
-constexpr int kTileW = 32;  // pixels per tile row
+constexpr int kTileW = 64;  // pixels per tile row
+constexpr int kGroups = kTileW / 4;  // 4-pixel items per tile row
 constexpr int kFS = 68;     // floats per unit in the F tile
 
 __device__ __forceinline__ uint32_t pack4_sat(int a0, int a1, int a2, int a3) {
@@ -1248,7 +1247,7 @@ struct WarpSmem {
     float F[kK4MaxBlocks * kFS];  // dequantised AC units (float, or int32 bits when big), compact order
     int4 raw[kK4MaxBlocks * 8];   // next tile's coefficients (cp.async staging)
     uint2 meta[kK4MaxBlocks];     // next tile's per-unit metadata
-    uint8_t pl[1024];             // sample planes (row stride padded by 4)
+    uint8_t pl[1792];             // sample planes (row stride padded by 4)
     WarpImg img;
     float lim[kK4MaxBlocks];      // per AC unit: 0.5 - error bound
     uint32_t cm[kK4MaxBlocks];    // per AC unit: column mask | big << 8 | row mask << 16
@@ -1398,8 +1397,8 @@ __device__ __forceinline__ void colour_tile(const WarpImg& I, const uint8_t* pl,
     const uint32_t pst0 = I.pst[0], pst1 = I.pst[1];
     uint8_t* obase = out + I.out_off + (uint64_t(Y0) * W + X0) * 3;
     const uint64_t orow = uint64_t(W) * 3;
-    for (uint32_t it = lane; it < (nrow << 3); it += 32) {
-        const uint32_t jr = it >> 3, gx = (it & 7) * 4;
+    for (uint32_t it = lane; it < nrow * kGroups; it += 32) {
+        const uint32_t jr = it / kGroups, gx = (it % kGroups) * 4;
         if (gx >= cols) continue;
         const uint32_t npx = min(4u, cols - gx);
         const uint32_t r0 = PAIR ? 2 * jr : jr;
@@ -1446,7 +1445,7 @@ template <int HS, bool PAIR>
 __device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl, const ColourLut& L, uint8_t* out,
                                             uint32_t X0, uint32_t Y0, int lane) {
     const uint32_t W = I.width;
-    const uint32_t gx = (lane & 7) * 4, jr0 = lane >> 3;
+    const uint32_t gx = (lane % kGroups) * 4, jr0 = lane / kGroups;
     const uint32_t cgx = HS == 2 ? gx >> 1 : gx;
     const uint8_t* yb = pl + I.poff[0] + gx;
     const uint8_t* cbb = pl + I.poff[1];
@@ -1455,8 +1454,8 @@ __device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl,
     const uint64_t orow = uint64_t(W) * 3;
     uint8_t* ob = out + I.out_off + (uint64_t(Y0) * W + X0 + gx) * 3;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const uint32_t jr = jr0 + 4 * h;
+    for (int h = 0; h < 8 * kGroups / 32; ++h) {
+        const uint32_t jr = jr0 + (32 / kGroups) * h;
         const uint32_t r0 = PAIR ? 2 * jr : jr;
         const uint8_t* cbrow = cbb + jr * pst1;
         const uint8_t* crrow = crb + jr * pst1;
@@ -1509,8 +1508,9 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
     return *reinterpret_cast<float2*>(&r);
 }
 
-__global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
-    __shared__ __align__(16) WarpSmem s_w[kK4Warps];
+__global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
+    extern __shared__ __align__(16) unsigned char k4_dyn[];  // kK4Warps x WarpSmem
+    WarpSmem* s_w = reinterpret_cast<WarpSmem*>(k4_dyn);
     __shared__ __align__(16) float s_b32[64];   // basis[u][x]
     __shared__ __align__(16) double s_b64[64];
     __shared__ __align__(16) ColourLut s_lut;
@@ -1568,7 +1568,7 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
         const int4* src = reinterpret_cast<const int4*>(P.coef + du0 * 64);
         if (tw.valid) {
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
+            for (int j = 0; j < kK4MaxBlocks / 4; ++j) {
                 const uint32_t ch = lane + 32 * j;
                 if (ch < nblk * 8)
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.raw[ch])), "l"(src + ch)
@@ -1692,7 +1692,7 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
         if (!cur_valid) continue;
 
         // 3. IDCT of the AC units, eight per pass: lane = (unit a, rows q, q+4)
-        uint32_t pend = 0;  // per pass: bit y (row q) / 8 + y (row q+4) need the FP64 replay
+        uint64_t pend = 0;  // per pass g: bit 16g + y (row q) / 16g + 8 + y (row q+4) need the FP64 replay
 #pragma unroll 1
         for (uint32_t g = 0; g * 8 < nac; ++g) {
             const uint32_t a = g * 8 + (lane >> 2);
@@ -1750,7 +1750,7 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
                 r1p[0] = pack4_sat(o1[0], o1[1], o1[2], o1[3]);
                 r1p[1] = pack4_sat(o1[4], o1[5], o1[6], o1[7]);
                 if (cmw & 0x100u) {
-                    pend |= 0xFFFFu << (16 * g);
+                    pend |= 0xFFFFull << (16 * g);
                 } else if (mx > S.lim[a]) {  // rare: the samples near x.5 get FP64 below
                     const float lim = S.lim[a];
                     uint32_t mask = 0;
@@ -1761,15 +1761,15 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
                         if (fabsf(dd.x) > lim) mask |= 1u << y;
                         if (fabsf(dd.y) > lim) mask |= 0x100u << y;
                     }
-                    pend |= mask << (16 * g);
+                    pend |= uint64_t(mask) << (16 * g);
                 }
             }
         }
         // exact FP64 replay of the flagged samples, off the hot loop and
         // spread over the warp: lane i recomputes entry i of a work list
         n_ac += nac;
-        if (__any_sync(0xFFFFFFFFu, pend)) {
-            const uint32_t cnt = __popc(pend);
+        if (__any_sync(0xFFFFFFFFu, pend != 0)) {
+            const uint32_t cnt = __popcll(pend);
             uint32_t incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -1782,10 +1782,10 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
             for (uint32_t rb = 0; rb < total; rb += 32) {
                 if (cnt && base < rb + 32 && base + cnt > rb) {
                     uint32_t k = base;
-                    for (uint32_t m = pend; m; m &= m - 1, ++k) {
+                    for (uint64_t m = pend; m; m &= m - 1, ++k) {
                         if (k < rb) continue;
                         if (k >= rb + 32) break;
-                        const uint32_t bit = __ffs(m) - 1;  // 16 g + 8 h + y
+                        const uint32_t bit = __ffsll(m) - 1;  // 16 g + 8 h + y
                         const uint32_t a = (bit >> 4) * 8 + (lane >> 2), x = q + 4 * ((bit >> 3) & 1u);
                         S.rep[k - rb] = uint16_t((a << 6) | (x << 3) | (bit & 7u));
                     }
@@ -1831,8 +1831,8 @@ __global__ void __launch_bounds__(kK4Threads, 6) k4_transform(Params P) {
             const uint32_t W = I.width;
             const bool aligned = ((W & 3) == 0) && ((I.out_off & 3) == 0);
             uint8_t* obase = P.out + I.out_off + uint64_t(Y0) * W + X0;
-            for (uint32_t it = lane; it < (rws << 3); it += 32) {
-                const uint32_t r = it >> 3, gx = (it & 7) * 4;
+            for (uint32_t it = lane; it < rws * kGroups; it += 32) {
+                const uint32_t r = it / kGroups, gx = (it % kGroups) * 4;
                 if (gx >= cols) continue;
                 const uint32_t y4 = *reinterpret_cast<const uint32_t*>(S.pl + I.poff[0] + r * I.pst[0] + gx);
                 uint8_t* dst = obase + uint64_t(r) * W + gx;
@@ -1925,16 +1925,18 @@ void launch_k3_write(const Params& p, void* stream) {
 void launch_k4_transform(const Params& p, void* stream) {
     if (!p.k4_tiles) return;
     static int grid_cap = 0;
+    constexpr size_t dyn = sizeof(WarpSmem) * kK4Warps;
     if (!grid_cap) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_transform, kK4Threads, 0);
+        cudaFuncSetAttribute(k4_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_transform, kK4Threads, dyn);
         grid_cap = std::max(1, sms * std::max(per_sm, 1));
     }
     const uint64_t want = (uint64_t(p.k4_tiles) + kK4Threads / 32 - 1) / (kK4Threads / 32);
     const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(grid_cap)));
-    k4_transform<<<grid, kK4Threads, 0, (cudaStream_t)stream>>>(p);
+    k4_transform<<<grid, kK4Threads, dyn, (cudaStream_t)stream>>>(p);
 }
 
 }  // namespace pjg

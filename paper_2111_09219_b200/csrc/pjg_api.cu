@@ -435,7 +435,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         if (h.table_status != kOk) continue;
         d.sub_count = (uint64_t(rl) * 8 + sb - 1) / sb;
         d.expected = h.total_dus() * 64;
-        d.mcus_per_tile = uint16_t(32 / (8 * h.h_max));  // 32-pixel-wide warp tiles (<= 12 data units)
+        d.mcus_per_tile = uint16_t(64 / (8 * h.h_max));  // 64-pixel-wide warp tiles (<= 24 data units)
         d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
         sub += d.sub_count;
         du += h.total_dus();

@@ -149,7 +149,7 @@ constexpr int kK1Threads = 128;                          // subsequences per K1 
 constexpr int kK2Threads = 256;
 constexpr int kK3Threads = 128;
 constexpr int kK4Threads = 128;
-constexpr int kK4MaxBlocks = 12;                         // data units per K4 (warp) tile
+constexpr int kK4MaxBlocks = 24;                         // data units per K4 (warp) tile
 
 struct Params {
     // batch
