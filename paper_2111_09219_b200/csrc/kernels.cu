@@ -1227,7 +1227,7 @@ __device__ __noinline__ uint32_t rgb_fp64(int Y, int Cb, int Cr) {
 // Per-warp image cache: layout of the tile's data units in the warp's sample
 // planes, quantisers, and the descriptor fields the tile loop needs.
 struct __align__(16) WarpImg {
-    uint16_t q[3][64];  // column-major quantiser per component
+    float qf[3][64];    // column-major quantiser per component, as float (exact: < 2^16)
     uint32_t pst[3], poff[3];
     uint16_t boff[kK4MaxBlocks];  // plane byte offset of the unit's (0,0) sample
     uint16_t bps[kK4MaxBlocks];   // plane row stride
@@ -1247,12 +1247,13 @@ struct WarpSmem {
     float F[kK4MaxBlocks * kFS];  // dequantised AC units (float, or int32 bits when big), compact order
     int4 raw[kK4MaxBlocks * 8];   // next tile's coefficients (cp.async staging)
     uint2 meta[kK4MaxBlocks];     // next tile's per-unit metadata
-    uint8_t pl[1792];             // sample planes (row stride padded by 4)
+    uint8_t pl[1664];             // sample planes (row stride padded by 4): 4:2:0 needs 68x16 + 2 x 36x8
     WarpImg img;
     float lim[kK4MaxBlocks];      // per AC unit: 0.5 - error bound
     uint32_t cm[kK4MaxBlocks];    // per AC unit: column mask | big << 8 | row mask << 16
     uint8_t acl[kK4MaxBlocks];    // AC units (tile-local index), compact
     uint8_t dcl[kK4MaxBlocks];    // DC-only units
+    uint8_t dq[kK4MaxBlocks * 8]; // nonzero columns of the AC units: a << 3 | v
     uint16_t rep[32];             // FP64 replay work list: unit << 6 | x << 3 | y
     TileWalk w;
 };
@@ -1271,9 +1272,12 @@ __device__ __forceinline__ void fill_warp_img(const Params& P, uint32_t k, WarpI
     }
     if (lane < 24) {  // 3 quantisers x 8 x 16 B
         const uint32_t cc = lane >> 3;
-        if (cc < ncomp)
-            reinterpret_cast<uint4*>(c.q[cc])[lane & 7] =
-                __ldg(reinterpret_cast<const uint4*>(P.quant_raster + 64u * D.q_tab[cc]) + (lane & 7));
+        if (cc < ncomp) {
+            const uint4 qv = __ldg(reinterpret_cast<const uint4*>(P.quant_raster + 64u * D.q_tab[cc]) + (lane & 7));
+            float4* qf = reinterpret_cast<float4*>(c.qf[cc] + 8 * (lane & 7));
+            qf[0] = make_float4(float(qv.x & 0xFFFFu), float(qv.x >> 16), float(qv.y & 0xFFFFu), float(qv.y >> 16));
+            qf[1] = make_float4(float(qv.z & 0xFFFFu), float(qv.z >> 16), float(qv.w & 0xFFFFu), float(qv.w >> 16));
+        }
     }
     if (lane < int(MT * dpm) && lane < kK4MaxBlocks) {
         const uint32_t blk = lane, slot = blk % dpm, m = blk / dpm;
@@ -1500,6 +1504,7 @@ __device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl,
 }
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+static_assert(sizeof(WarpSmem) * kK4Warps + 4864 + 1024 <= 228 * 1024 / 4, "K4 must fit 4 CTAs per SM");
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
     unsigned long long r;
     asm("sub.rn.f32x2 %0, %1, %2;"
@@ -1599,7 +1604,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
         // 1. classify units (K3 metadata: column mask | has-AC << 8 | big << 9, S)
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncwarp();
-        uint32_t nac = 0, ndc = 0;
+        uint32_t nac = 0, ndc = 0, ndq = 0;
         if (cur_valid) {
             const bool in = uint32_t(lane) < nblk;
             const uint2 pm = in ? S.meta[lane] : make_uint2(0, 0);
@@ -1608,8 +1613,30 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
             const uint32_t dcm = __ballot_sync(0xFFFFFFFFu, in && !isac);
             nac = __popc(acm);
             ndc = __popc(dcm);
+            // nonzero columns of the AC units -> dequantisation work list
+            const uint32_t ncol = isac ? __popc(pm.x & 0xFFu) : 0u;
+            uint32_t cincl = ncol;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, cincl, o);
+                if (lane >= o) cincl += x;
+            }
+            ndq = __shfl_sync(0xFFFFFFFFu, cincl, 31);
             if (isac) {
                 const uint32_t a = __popc(acm & lt_mask);
+                // columns: nonzero ones to the list, zero ones zero-filled (the IDCT
+                // reads every column any unit of its pass uses)
+                uint32_t j = cincl - ncol;
+                float4* Fa = reinterpret_cast<float4*>(S.F + a * kFS);
+#pragma unroll
+                for (uint32_t v = 0; v < 8; ++v) {
+                    if ((pm.x >> v) & 1u) {
+                        S.dq[j++] = uint8_t((a << 3) | v);
+                    } else {
+                        Fa[2 * v] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        Fa[2 * v + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
                 const float Sb = __uint_as_float(pm.y);
                 // S >= 2^18 covers every unit with some |F| >= 2^21 (w_u w_v >= 1/8): those
                 // take exact FP64; below it F is exact in FP32 and |acc| <= S
@@ -1629,39 +1656,51 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 S.dcl[__popc(dcm & lt_mask)] = uint8_t(lane);
             }
             __syncwarp();
-            // 2a. dequantise the AC units' columns: item = (AC unit, column v)
+            // 2a. dequantise the AC units' nonzero columns: coef * Q in FP32 is exact
+            //     (|coef * Q| < 2^21 below the exact-FP64 threshold); exact-FP64
+            //     units keep the int32 products
 #pragma unroll 1
-            for (uint32_t it = lane; it < nac * 8; it += 32) {
-                const uint32_t a = it >> 3, v = it & 7;
-                const uint32_t blk = S.acl[a], cm = S.cm[a];
+            for (uint32_t it = lane; it < ndq; it += 32) {
+                const uint32_t e = S.dq[it], a = e >> 3, v = e & 7u;
+                const uint32_t blk = S.acl[a];
                 float4* dst = reinterpret_cast<float4*>(S.F + a * kFS + v * 8);
-                {  // zero columns dequantise to zeros: no divergent skip
-                    const int4 rvi = S.raw[blk * 8 + v];
-                    const uint4 qv = *reinterpret_cast<const uint4*>(I.q[I.bcomp[blk]] + v * 8);
-                    const uint32_t rw[4] = {uint32_t(rvi.x), uint32_t(rvi.y), uint32_t(rvi.z), uint32_t(rvi.w)};
-                    const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+                const int4 rvi = S.raw[blk * 8 + v];
+                const uint32_t rw[4] = {uint32_t(rvi.x), uint32_t(rvi.y), uint32_t(rvi.z), uint32_t(rvi.w)};
+                const uint32_t comp = I.bcomp[blk];
+                if (!(S.cm[a] & 0x100u)) {
+                    const float4 q0 = *reinterpret_cast<const float4*>(I.qf[comp] + v * 8);
+                    const float4 q1 = *reinterpret_cast<const float4*>(I.qf[comp] + v * 8 + 4);
+                    float c[8];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        c[2 * k] = float(int32_t(rw[k] << 16) >> 16);
+                        c[2 * k + 1] = float(int32_t(rw[k]) >> 16);
+                    }
+                    const float2 p0 = __fmul2_rn(make_float2(c[0], c[1]), make_float2(q0.x, q0.y));
+                    const float2 p1 = __fmul2_rn(make_float2(c[2], c[3]), make_float2(q0.z, q0.w));
+                    const float2 p2 = __fmul2_rn(make_float2(c[4], c[5]), make_float2(q1.x, q1.y));
+                    const float2 p3 = __fmul2_rn(make_float2(c[6], c[7]), make_float2(q1.z, q1.w));
+                    dst[0] = make_float4(p0.x, p0.y, p1.x, p1.y);
+                    dst[1] = make_float4(p2.x, p2.y, p3.x, p3.y);
+                } else {  // exact-FP64 unit: keep the int32 bits
+                    const float* qf = I.qf[comp] + v * 8;
                     int32_t d[8];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        d[2 * e] = int32_t(int16_t(rw[e] & 0xFFFFu)) * int32_t(qw[e] & 0xFFFFu);
-                        d[2 * e + 1] = (int32_t(rw[e]) >> 16) * int32_t(qw[e] >> 16);
+                    for (int k = 0; k < 4; ++k) {
+                        d[2 * k] = int32_t(int16_t(rw[k] & 0xFFFFu)) * int32_t(qf[2 * k]);
+                        d[2 * k + 1] = (int32_t(rw[k]) >> 16) * int32_t(qf[2 * k + 1]);
                     }
-                    if (!(cm & 0x100u)) {
-                        dst[0] = make_float4(float(d[0]), float(d[1]), float(d[2]), float(d[3]));
-                        dst[1] = make_float4(float(d[4]), float(d[5]), float(d[6]), float(d[7]));
-                    } else {  // exact-FP64 unit: keep the int32 bits
-                        dst[0] = make_float4(__int_as_float(d[0]), __int_as_float(d[1]), __int_as_float(d[2]),
-                                             __int_as_float(d[3]));
-                        dst[1] = make_float4(__int_as_float(d[4]), __int_as_float(d[5]), __int_as_float(d[6]),
-                                             __int_as_float(d[7]));
-                    }
+                    dst[0] = make_float4(__int_as_float(d[0]), __int_as_float(d[1]), __int_as_float(d[2]),
+                                         __int_as_float(d[3]));
+                    dst[1] = make_float4(__int_as_float(d[4]), __int_as_float(d[5]), __int_as_float(d[6]),
+                                         __int_as_float(d[7]));
                 }
             }
             // 2b. DC-only units: item = (unit, row x), two 4-byte stores of the constant sample
 #pragma unroll 1
             for (uint32_t it = lane; it < ndc * 8; it += 32) {
                 const uint32_t blk = S.dcl[it >> 3], x = it & 7;
-                const int32_t F00 = int32_t(int16_t(uint32_t(S.raw[blk * 8].x) & 0xFFFFu)) * int32_t(I.q[I.bcomp[blk]][0]);
+                const int32_t F00 = int32_t(int16_t(uint32_t(S.raw[blk * 8].x) & 0xFFFFu)) * int32_t(I.qf[I.bcomp[blk]][0]);
                 int o;
                 if ((F00 & 7) != 4)
                     o = (F00 + 4) >> 3;

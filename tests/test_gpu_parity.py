@@ -202,3 +202,26 @@ def test_contiguous_region_unaligned_offsets(decoder):
             ref = Ref.decode(f, rgb=True)
             got = _rgb(outs[i], b.infos[i])
             assert np.array_equal(got, ref.data), i
+
+
+def test_random_shapes_batch_bit_exact(decoder):
+    """A mixed batch of seeded random shapes, samplings and qualities (full
+    and partial K4 tiles, 1-3 IDCT passes per tile, FP64 replays) against the
+    reference decoder, RGB bit-exact."""
+    rng = np.random.default_rng(2111)
+    cases = []
+    for k in range(14):
+        w = int(rng.integers(9, 700))
+        h = int(rng.integers(9, 300))
+        q = int(rng.choice([50, 75, 85, 90, 95, 100]))
+        s = ["444", "422", "420", "gray"][k % 4]
+        cases.append(((w, h, q, s), ref_jpeg(w, h, 5000 + k, q, s)))
+    files = [f for _, f in cases]
+    with decoder.batch(files, pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved) as b:
+        st = b.run()
+        assert (st == 0).all(), st
+        outs = b.download()
+        for i, (shape, f) in enumerate(cases):
+            ref = Ref.decode(f, rgb=True)
+            got = _rgb(outs[i], b.infos[i])
+            assert np.array_equal(got, ref.data), (shape, int((got != ref.data).sum()))
