@@ -54,6 +54,10 @@ typedef struct pjg_config {
     uint64_t subsequence_bits;  /* positive multiple of 32 (parallel_decode.hpp:51) */
     uint32_t sequence_length_b; /* >= 1; accepted for parity, grouping is per CTA */
     uint32_t output;            /* pjg_output_kind */
+    uint32_t restart_intervals; /* 0 (default): DRI != 0 is UnsupportedFeature, as the
+                                   reference (parser.hpp:299-302); 1: decode restart
+                                   intervals (DRI + RST0-7), an extension */
+    uint32_t reserved;
 } pjg_config;
 
 /* Geometry of one decoded image (ImagePlanes / RgbImage, transform.hpp:38-51,

@@ -67,6 +67,7 @@ struct DecodeConfig {
     uint32_t sequence_length_b = 256;
     unsigned worker_count = 1;  // accepted for signature parity
     OutputColorspace output_colorspace = OutputColorspace::YCbCrPlanes;
+    bool restart_intervals = false;  // extension: decode DRI/RSTn (reference: UnsupportedFeature)
 };
 
 struct StageTimings {  // device stage times, ms (CUDA events)
@@ -135,6 +136,8 @@ inline pjg_config to_c(const DecodeConfig& c, uint32_t out) {
     r.subsequence_bits = c.subsequence_bits;
     r.sequence_length_b = c.sequence_length_b;
     r.output = out;
+    r.restart_intervals = c.restart_intervals ? 1u : 0u;
+    r.reserved = 0;
     return r;
 }
 

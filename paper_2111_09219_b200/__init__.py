@@ -72,6 +72,9 @@ class DecodeConfig:
     sequence_length_b: int = 256
     worker_count: int = 1
     output_colorspace: OutputColorspace = OutputColorspace.YCbCrPlanes
+    # extension: decode restart intervals (DRI + RSTn); False = the reference's
+    # UnsupportedFeature for DRI != 0 (parser.hpp:299-302)
+    restart_intervals: bool = False
 
 
 @dataclass
@@ -135,7 +138,7 @@ class DecodeFailure:
 # ---------------------------------------------------------------- ctypes --
 class _Config(C.Structure):
     _fields_ = [("subsequence_bits", C.c_uint64), ("sequence_length_b", C.c_uint32),
-                ("output", C.c_uint32)]
+                ("output", C.c_uint32), ("restart_intervals", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class _Info(C.Structure):
@@ -229,7 +232,8 @@ def _status_name(st: int) -> str:
 def _cfg(config: DecodeConfig | None, output=None) -> _Config:
     config = config or DecodeConfig()
     out = int(config.output_colorspace if output is None else output)
-    return _Config(int(config.subsequence_bits), int(config.sequence_length_b), out)
+    return _Config(int(config.subsequence_bits), int(config.sequence_length_b), out,
+                   1 if config.restart_intervals else 0, 0)
 
 
 # ------------------------------------------------------------ staged API --

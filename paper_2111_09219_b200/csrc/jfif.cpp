@@ -127,7 +127,7 @@ void parse_sof0(Reader& r, uint16_t len, Header& h) {
 
 }  // namespace
 
-Header parse_header(const uint8_t* data, size_t size) {
+Header parse_header(const uint8_t* data, size_t size, bool allow_dri) {
     Header h;
     try {
         Reader r(data, size);
@@ -156,8 +156,10 @@ Header parse_header(const uint8_t* data, size_t size) {
                 have_frame = true;
             } else if (m == 0xDD) {
                 Reader s = r.take(len);
-                if (s.u16() != 0)
+                const uint16_t ri = s.u16();
+                if (ri != 0 && !allow_dri)
                     throw Fail{kUnsupportedFeature, "restart interval (DRI) not supported"};
+                h.restart_interval = ri;
             } else if (m == 0xDC) {
                 throw Fail{kUnsupportedFeature, "DNL segment not supported"};
             } else if (m == 0xDA) {

@@ -35,16 +35,23 @@ struct Header {
     std::array<bool, 4> quant_present{};
     std::array<HuffSpec, 4> dc, ac;
     size_t scan_start = 0;  // offset of the first entropy-coded byte
+    uint32_t restart_interval = 0;  // DRI Ri (MCUs per interval), 0 = none
     int32_t table_status = kOk;  // build_table error, reported after the scan checks
 
     uint64_t total_dus() const { return uint64_t(mcus_x) * mcus_y * dpm; }
+    uint64_t intervals() const {
+        const uint64_t m = uint64_t(mcus_x) * mcus_y;
+        return restart_interval ? (m + restart_interval - 1) / restart_interval : 1;
+    }
     uint32_t comp_width(size_t c) const { return (width * comps[c].h + h_max - 1) / h_max; }
     uint32_t comp_height(size_t c) const { return (height * comps[c].v + v_max - 1) / v_max; }
 };
 
 // Parses markers up to and including SOS.  Never throws; errors land in
 // Header::status with the reference's Errc (parser.hpp error sites).
-Header parse_header(const uint8_t* data, size_t size);
+// allow_dri: accept DRI != 0 (restart-interval extension) instead of the
+// reference's UnsupportedFeature.
+Header parse_header(const uint8_t* data, size_t size, bool allow_dri = false);
 
 // build_table validation (huffman.hpp:60-93) + device two-level table.
 // Returns kOk or the reference's error (OversubscribedCode / MalformedHeader).

@@ -91,6 +91,57 @@ __device__ __forceinline__ uint32_t find_img(const Params& P, uint64_t g) {
     return lo;
 }
 
+// Where image-local subsequence i lives.  Without restart intervals the image
+// is one segment partitioned like the reference (N = ceil(L / sb),
+// parallel_decode.hpp:31-62).  With them (extension), each interval m is its
+// own segment [x_m, x_{m+1}) of unstuffed bits, partitioned from its first
+// bit, starting in the known state c = 0, z = 0 with zero DC predictors;
+// Params::segs (built by K0b) holds the per-interval bit and subsequence
+// offsets.  Returns false for subsequences past the image's last one.
+struct SubInfo {
+    uint64_t lo, hi;          // this subsequence's bits [lo, hi)
+    uint64_t seg_lo, seg_hi;  // its segment's bits
+    uint64_t j;               // index within the segment (0: known start state)
+    uint64_t seg_sub0, seg_sub1;  // the segment's image-local subsequences
+    uint32_t m;               // segment (restart interval)
+};
+__device__ __forceinline__ bool sub_info(const Params& P, const ImgDesc& D, uint64_t L, uint64_t i, SubInfo& si) {
+    if (D.n_int <= 1) {
+        const uint64_t N = (L + P.sb - 1) / P.sb;
+        si.m = 0;
+        si.seg_lo = 0;
+        si.seg_hi = L;
+        si.seg_sub0 = 0;
+        si.seg_sub1 = N;
+        si.j = i;
+        if (i >= N) return false;
+    } else {
+        const uint2* sg = P.segs + D.seg_first;
+        if (i >= sg[D.n_int].y) return false;
+        uint32_t lo = 0, hi = D.n_int;  // largest m with sg[m].y <= i
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (sg[mid].y <= i)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        si.m = lo;
+        si.seg_lo = sg[lo].x;
+        si.seg_hi = sg[lo + 1].x;
+        si.seg_sub0 = sg[lo].y;
+        si.seg_sub1 = sg[lo + 1].y;
+        si.j = i - si.seg_sub0;
+    }
+    si.lo = si.seg_lo + si.j * P.sb;
+    si.hi = min64(si.lo + P.sb, si.seg_hi);
+    return true;
+}
+// end bit of subsequence i of the same segment
+__device__ __forceinline__ uint64_t seg_end_bit(const SubInfo& si, uint64_t sb, uint64_t i) {
+    return min64(si.seg_lo + (i - si.seg_sub0 + 1) * sb, si.seg_hi);
+}
+
 __device__ __forceinline__ void set_status(ImgState* st, int32_t code) {
     atomicCAS(reinterpret_cast<int*>(&st->status), 0, code);
 }
@@ -133,7 +184,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     __shared__ __align__(16) uint8_t s_o[kK0Tile + 32];
     __shared__ uint32_t s_cnt[kK0Threads / 32];
     __shared__ uint32_t s_mk[kK0Threads / 32];
-    __shared__ uint32_t s_excl_cnt, s_excl_mk, s_tile_cnt, s_tile_mk;
+    __shared__ uint32_t s_excl_cnt, s_excl_mk, s_tile_cnt, s_tile_mk, s_excl_rc;
 
     const int tid = threadIdx.x;
     if (tid == 0) s_tile = atomicAdd(&P.counters[kTicketK0], 1u);
@@ -146,6 +197,10 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     const uint64_t a = D.raw_off, e = a + raw_len;  // the image's bytes [a, e) in the raw buffer
     const uint64_t win0 = (a & ~15ull) + uint64_t(lt) * kK0Tile;
     const uint64_t g_first = max(win0, a);            // first image byte in this window
+    // restart intervals (extension): RSTn markers inside the scan are removed
+    // like stuffed zeros and their unstuffed positions recorded; without them a
+    // RST marker ends the scan and is UnsupportedFeature (parser.hpp:249-250)
+    const bool dri = D.n_int > 1;
 
     {
         const uint64_t g = win0 + 16u * tid;
@@ -168,7 +223,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
         const uint32_t f = has_ff(w.x) | has_ff(w.y) | has_ff(w.z) | has_ff(w.w);
         plain = inside && f == 0 && s_b[15 + b0] != 0xFF;
     }
-    uint32_t cnt = 0, mk = kInf32;
+    uint32_t cnt = 0, mk = kInf32, rc = 0;  // removed bytes, first marker, RST markers
 #pragma unroll
     for (int q = 0; q < kK0BytesPerThread; ++q) {
         if (plain) break;
@@ -177,12 +232,16 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
         const uint8_t cur = s_b[16 + b0 + q], next = s_b[17 + b0 + q];
         const uint8_t prev = g > a ? s_b[15 + b0 + q] : 0;
         const uint64_t j = g - a;
-        if (cur == 0x00 && prev == 0xFF) ++cnt;
         const bool last = (j + 1 == raw_len);
-        if (cur == 0xFF && (last || next != 0x00) && mk == kInf32) mk = uint32_t(j);
+        const bool rst_ff = dri && cur == 0xFF && !last && (next & 0xF8) == 0xD0;
+        const bool rst_x = dri && prev == 0xFF && (cur & 0xF8) == 0xD0;
+        if ((cur == 0x00 && prev == 0xFF) || rst_ff || rst_x) ++cnt;
+        rc += rst_ff;
+        if (cur == 0xFF && !rst_ff && (last || next != 0x00) && mk == kInf32) mk = uint32_t(j);
     }
-    // block reduce (sum, min)
-    uint32_t wc = cnt, wm = mk;
+    // block reduce (sum, min); removed | RST count << 16 (both < 2^16 per tile)
+    const uint32_t cr = cnt | (rc << 16);
+    uint32_t wc = cr, wm = mk;
     for (int o = 16; o; o >>= 1) {
         wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
         wm = min(wm, __shfl_xor_sync(0xFFFFFFFFu, wm, o));
@@ -194,21 +253,25 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     }
     __syncthreads();
     if (tid == 0) {
-        uint32_t tc = 0, tm = kInf32;
+        uint32_t tcr = 0, tm = kInf32;
         for (int w = 0; w < kK0Threads / 32; ++w) {
-            tc += s_cnt[w];
+            tcr += s_cnt[w];
             tm = min(tm, s_mk[w]);
         }
+        const uint32_t tc = tcr & 0xFFFFu, trc = tcr >> 16;
         s_tile_cnt = tc;
         s_tile_mk = tm;
-        // decoupled lookback, segmented at the image's first tile
+        // decoupled lookback, segmented at the image's first tile:
+        // [0] aggregate (mk << 32 | removed), [1] aggregate RST count, [2], [3] inclusive
         uint64_t* agg = P.k0_agg + 4ull * t;
-        uint32_t ec = 0, em = kInf32;
+        uint32_t ec = 0, em = kInf32, erc = 0;
         if (lt == 0) {
             agg[2] = (uint64_t(tm) << 32) | tc;
+            agg[3] = trc;
             st_release(P.k0_flag + t, (P.epoch << 2) | 2u);
         } else {
             agg[0] = (uint64_t(tm) << 32) | tc;
+            agg[1] = trc;
             st_release(P.k0_flag + t, (P.epoch << 2) | 1u);
             int64_t pr = int64_t(t) - 1;
             while (true) {
@@ -217,21 +280,25 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
                     spin_pause();
                     continue;
                 }
-                uint64_t v = __ldcg(P.k0_agg + 4ull * pr + ((f & 3u) == 2u ? 2 : 0));
+                const uint64_t* src = P.k0_agg + 4ull * pr + ((f & 3u) == 2u ? 2 : 0);
+                const uint64_t v = __ldcg(src);
                 ec += uint32_t(v);
                 em = min(em, uint32_t(v >> 32));
+                erc += uint32_t(__ldcg(src + 1));
                 if ((f & 3u) == 2u) break;
                 --pr;
             }
             agg[2] = (uint64_t(min(em, tm)) << 32) | (ec + tc);
+            agg[3] = erc + trc;
             st_release(P.k0_flag + t, (P.epoch << 2) | 2u);
         }
         s_excl_cnt = ec;
         s_excl_mk = em;
+        s_excl_rc = erc;
     }
     __syncthreads();
-    // exclusive scan of per-thread removed counts (warp shuffles + smem)
-    uint32_t inc = cnt;
+    // exclusive scan of per-thread (removed | RST << 16) counts (warp shuffles + smem)
+    uint32_t inc = cr;
     for (int o = 1; o < 32; o <<= 1) {
         uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
         if (lane >= o) inc += v;
@@ -241,7 +308,9 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     __syncthreads();
     uint32_t wbase = 0;
     for (int w = 0; w < warp; ++w) wbase += s_cnt[w];
-    uint32_t removed = s_excl_cnt + wbase + inc - cnt;  // removed before this thread's bytes
+    const uint32_t before_cr = wbase + inc - cr;
+    uint32_t removed = s_excl_cnt + (before_cr & 0xFFFFu);  // removed before this thread's bytes
+    uint32_t rst_before = s_excl_rc + (before_cr >> 16);    // RST markers before them
 
     // kept byte at image index j goes to image index j - removed; this tile's
     // kept bytes form [dst_lo, dst_lo + kept) in raw-buffer coordinates
@@ -258,7 +327,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
         if (plain) break;
         const uint64_t g = win0 + b0 + q;
         if (g < a || g >= e) continue;
-        const uint8_t cur = s_b[16 + b0 + q];
+        const uint8_t cur = s_b[16 + b0 + q], nx = s_b[17 + b0 + q];
         const uint8_t prev = g > a ? s_b[15 + b0 + q] : 0;
         const uint64_t j = g - a;
         if (first_mk != kInf32 && j == first_mk) {
@@ -266,7 +335,6 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
             uint64_t U = j - removed;
             ImgState* st = P.ist + k;
             st->bit_length = U * 8;
-            const uint8_t nx = s_b[17 + b0 + q];
             bool rst = (j + 1 < raw_len) && nx >= 0xD0 && nx <= 0xD7;
             if (rst)
                 set_status(st, kUnsupportedFeature);
@@ -275,7 +343,23 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
             else if (D.deferred)
                 set_status(st, D.deferred);
         }
-        if (cur == 0x00 && prev == 0xFF) {
+        const bool last = (j + 1 == raw_len);
+        const bool rst_ff = dri && cur == 0xFF && !last && (nx & 0xF8) == 0xD0;
+        const bool rst_x = dri && prev == 0xFF && (cur & 0xF8) == 0xD0;
+        if (rst_ff) {
+            // restart marker r = rst_before: interval r + 1 starts at unstuffed
+            // byte j - removed; markers past the scan end do not count
+            const uint32_t end_mk = s_excl_mk != kInf32 ? s_excl_mk : s_tile_mk;
+            if (j < end_mk) {
+                const uint32_t r = rst_before;
+                if (r + 1 >= D.n_int || (nx & 7u) != (r & 7u))
+                    set_status(P.ist + k, kConsistencyFailure);  // RST count / numbering vs DRI
+                else
+                    P.segs[D.seg_first + r + 1].x = uint32_t((j - removed) * 8);
+            }
+            ++rst_before;
+        }
+        if ((cur == 0x00 && prev == 0xFF) || rst_ff || rst_x) {
             ++removed;
         } else {
             s_o[(a + j - removed) - dst_al] = cur;
@@ -305,6 +389,59 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
             set_status(st, kEmptyScan);
         else if (D.deferred)
             set_status(st, D.deferred);
+    }
+}
+
+// ================================================ K0b: interval tables ====
+// One CTA per image with restart intervals: closes its segment table
+// (x_0 = 0, x_n = bit length), checks that every interval got its RST marker
+// and is non-empty, and partitions each interval into ceil(bits / sb)
+// subsequences (y = exclusive prefix; y_n = subsequences in use).
+__global__ void __launch_bounds__(256) k0b_segments(Params P) {
+    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_carry;
+    __shared__ int s_bad;
+    const uint32_t k = P.dri_img[blockIdx.x];
+    const ImgDesc& D = P.img[k];
+    ImgState* st = P.ist + k;
+    if (st->status != 0) return;
+    const uint32_t n = D.n_int;
+    uint2* sg = P.segs + D.seg_first;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        sg[0].x = 0;
+        sg[n].x = uint32_t(st->bit_length);
+        s_carry = 0;
+        s_bad = 0;
+    }
+    __syncthreads();
+    for (uint32_t base = 0; base < n; base += 256) {
+        const uint32_t m = base + tid;
+        uint32_t cntm = 0;
+        if (m < n) {
+            const uint32_t x0 = sg[m].x, x1 = sg[m + 1].x;
+            if (x0 == 0xFFFFFFFFu || x1 == 0xFFFFFFFFu || x1 <= x0)
+                s_bad = 1;  // a missing RST marker or an empty interval
+            else
+                cntm = uint32_t((uint64_t(x1 - x0) + P.sb - 1) / P.sb);
+        }
+        uint32_t inc = cntm;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane == 31) s_w[warp] = inc;
+        __syncthreads();
+        uint32_t wb = s_carry;
+        for (int w = 0; w < warp; ++w) wb += s_w[w];
+        if (m < n) sg[m].y = wb + inc - cntm;
+        __syncthreads();
+        if (tid == 255) s_carry = wb + inc;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        sg[n].y = s_carry;
+        if (s_bad) set_status(st, kConsistencyFailure);
     }
 }
 
@@ -599,16 +736,15 @@ __device__ __forceinline__ DcSums pack_dc(int32_t a0, int32_t a1, int32_t a2) {
     return d;
 }
 
-// Sync-mode decode of subsequence i from (p, c, z).
-__device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t sb, uint64_t i, uint64_t p,
-                                            uint32_t c, uint32_t z, Entry& e, DcSums& d) {
+// Sync-mode decode from (p, c, z) of the symbols starting before end_bit.
+__device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t end_bit, uint64_t p, uint32_t c, uint32_t z,
+                                            Entry& e, DcSums& d) {
     DecState s;
     s.p = p;
     s.c = c;
     s.z = z;
     s.dc0 = s.dc1 = s.dc2 = 0;
     NullSink sink;
-    uint64_t end_bit = min((i + 1) * sb, ic.L);
     decode_range(ic, s, end_bit, 0, sink);
     e.p = s.p;
     e.n = s.n;
@@ -639,24 +775,24 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     const uint64_t i = g - P.sub_first[k];
     const uint64_t L = P.ist[k].bit_length;
     const bool ok = P.ist[k].status == 0;
-    const uint64_t N = ok ? (L + P.sb - 1) / P.sb : 0;
-    const bool real = inb && i < N;
+    SubInfo si;
+    const bool real = inb && ok && sub_info(P, D, L, i, si);
     ImgCtx ic;
     load_ctx(P, D, L, ic);
     {
         __shared__ int4 s_stage[kStageBytes / 16];
         __shared__ StageSmem s_sm;
-        const uint64_t lo = real ? D.raw_off + ((i * P.sb) >> 3) : 1, hi = real ? D.raw_off + ((min64((i + 1) * P.sb, L) + 7) >> 3) + 24 : 0;
+        const uint64_t lo = real ? D.raw_off + (si.lo >> 3) : 1, hi = real ? D.raw_off + ((si.hi + 7) >> 3) + 24 : 0;
         ic.words = stage_scan(P.ubuf, lo, hi, k, tid, T, s_stage, s_sm);
     }
 
     // Round 0: every subsequence decodes from its origin (parallel_decode.hpp:187-195)
     Entry e;
     DcSums d = {0, 0};
-    e.p = i * P.sb;
+    e.p = real ? si.lo : 0;
     e.n = 0;
     e.czd = 0;
-    if (real) sync_decode(ic, P.sb, i, i * P.sb, 0, 0, e, d);
+    if (real) sync_decode(ic, si.hi, si.lo, 0, 0, e, d);
     s_p[tid] = e.p;
     s_n[tid] = e.n;
     s_czd[tid] = e.czd;
@@ -664,7 +800,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     Entry chain = e;
     uint64_t nxt = i + 1;
     int nt = tid + 1;
-    bool active = real && !czd_div(e.czd) && nxt < N && nt < T;
+    bool active = real && !czd_div(e.czd) && nxt < si.seg_sub1 && nt < T;
     // Rounds k >= 1: overflow into the next subsequence until (p,c,z) agrees
     // with the published entry (parallel_decode.hpp:197-220).  All active
     // threads target distinct subsequences, so one barrier per round suffices.
@@ -674,7 +810,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
         if (active) {
             Entry e2;
             DcSums d2;
-            sync_decode(ic, P.sb, nxt, chain.p, czd_c(chain.czd), czd_z(chain.czd), e2, d2);
+            sync_decode(ic, seg_end_bit(si, P.sb, nxt), chain.p, czd_c(chain.czd), czd_z(chain.czd), e2, d2);
             bool synced = sync_equal(e2.p, e2.czd, s_p[nt], s_czd[nt]);
             s_p[nt] = e2.p;
             s_n[nt] = e2.n;  // the overflow's n is authoritative (:211)
@@ -686,7 +822,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
                 chain = e2;
                 ++nxt;
                 ++nt;
-                active = nxt < N && nt < T;
+                active = nxt < si.seg_sub1 && nt < T;
             }
         }
     }
@@ -711,7 +847,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
         start.p = 0;
         start.n = 0;
         start.czd = 0;
-        const bool boundary = real && i > 0;  // CTA starts mid-image
+        const bool boundary = real && si.j > 0;  // CTA starts mid-segment
         if (boundary) {
             while (ld_acquire(P.k1_flag + cta - 1) != P.epoch) spin_pause();
             start.p = __ldcg(&P.cta_end[cta - 1].p);
@@ -722,10 +858,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
                 Entry ch = start;
                 uint64_t ii = i;
                 uint32_t hops = 0;
-                for (int tt = 0; tt < T && ii < N; ++tt, ++ii) {
+                for (int tt = 0; tt < T && ii < si.seg_sub1; ++tt, ++ii) {
                     Entry e2;
                     DcSums d2;
-                    sync_decode(ic, P.sb, ii, ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
+                    sync_decode(ic, seg_end_bit(si, P.sb, ii), ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
                     ++hops;
                     bool synced = sync_equal(e2.p, e2.czd, s_p[tt], s_czd[tt]);
                     s_p[tt] = e2.p;
@@ -792,19 +928,20 @@ __global__ void __launch_bounds__(1024) k1c_fixup(Params P) {
             uint32_t k = find_img(P, g0);
             const ImgDesc& D = P.img[k];
             const uint64_t L = P.ist[k].bit_length;
-            const uint64_t N = (L + P.sb - 1) / P.sb;
             uint64_t i = g0 - P.sub_first[k];
             if (czd_div(st.czd)) {
                 set_status(P.ist + k, kConsistencyFailure);
                 continue;
             }
+            SubInfo si;
+            if (!sub_info(P, D, L, i, si)) continue;
             ImgCtx ic;
             load_ctx(P, D, L, ic);
             Entry ch = st;
-            for (int tt = 0; tt < T && i < N; ++tt, ++i) {
+            for (int tt = 0; tt < T && i < si.seg_sub1; ++tt, ++i) {
                 Entry e2;
                 DcSums d2;
-                sync_decode(ic, P.sb, i, ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
+                sync_decode(ic, seg_end_bit(si, P.sb, i), ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
                 Entry old = P.ent[g0 + tt];
                 bool synced = sync_equal(e2.p, e2.czd, old.p, old.czd);
                 P.ent[g0 + tt] = e2;
@@ -854,6 +991,13 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
     const bool inb = g < P.total_subs;
     uint32_t k = find_img(P, inb ? g : P.total_subs - 1);
     const uint64_t i = g - P.sub_first[k];
+    const ImgDesc& D = P.img[k];
+    // segment heads: the image start, or (restart intervals) each interval's
+    // first subsequence; subsequences past the last one are inert heads
+    const bool dri = D.n_int > 1;
+    SubInfo si;
+    bool real = true;
+    if (dri) real = P.ist[k].status == 0 && sub_info(P, D, P.ist[k].bit_length, i, si);
     ScanVal v;
     v.n = 0;
     v.lo = v.hi = 0;
@@ -863,7 +1007,8 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
         v.n = e.n;
         v.lo = d.lo;
         v.hi = d.hi;
-        if (i == 0) v.n |= kHead;
+        if (!dri ? i == 0 : (!real || si.j == 0)) v.n |= kHead;
+        if (!real) v.n = kHead, v.lo = v.hi = 0;
     }
     // warp inclusive segmented scan
     ScanVal x = v;
@@ -967,18 +1112,34 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
         before.n = 0;
         before.lo = before.hi = 0;
     }
-    const ImgDesc& D = P.img[k];
-    const uint64_t E = D.expected;
+    // trimmed offsets (offsets(), parallel_decode.hpp:290-316), per segment:
+    // a restart interval expects 64 * dpm * (its MCUs) slots at slot base
+    // 64 * dpm * Ri * m
+    uint64_t E = D.expected, base = 0;
+    bool last = i + 1 == D.sub_count;
+    if (dri) {
+        if (!real) {
+            P.off[g] = 0;
+            P.cap[g] = 0;
+            P.pred[g] = DcSums{0, 0};
+            return;
+        }
+        const uint64_t mcus = uint64_t(D.mcus_x) * D.mcus_y;
+        const uint64_t m0 = uint64_t(si.m) * D.ri;
+        E = 64ull * D.dpm * min64(D.ri, mcus - m0);
+        base = 64ull * D.dpm * m0;
+        last = i + 1 == si.seg_sub1;
+    }
     const uint64_t pre = before.n & ~kHead;
     const uint64_t n = v.n & ~kHead;
     const uint64_t o = min(pre, E);
-    P.off[g] = o;
+    P.off[g] = base + o;
     P.cap[g] = uint32_t(min(pre + n, E) - o);
     DcSums pd;
     pd.lo = before.lo;
     pd.hi = before.hi;
     P.pred[g] = pd;
-    if (i + 1 == D.sub_count && P.ist[k].status == 0) {
+    if (last && P.ist[k].status == 0) {
         const uint64_t total = pre + n;
         if (total < E || total - E > 512) set_status(P.ist + k, kConsistencyFailure);
     }
@@ -1092,24 +1253,25 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     const bool inb = g < P.total_subs;
     const uint32_t cap = inb ? P.cap[g] : 0u;
     const uint32_t k = find_img(P, inb ? g : P.total_subs - 1);
-    const bool active = inb && cap != 0 && P.ist[k].status == 0;
     const ImgDesc& D = P.img[k];
     const uint64_t i = g - P.sub_first[k];
     const uint64_t L = P.ist[k].bit_length;
+    SubInfo si;
+    const bool active = inb && cap != 0 && P.ist[k].status == 0 && sub_info(P, D, L, i, si);
     ImgCtx ic;
     load_ctx(P, D, L, ic);
     {
         __shared__ int4 s_stage[kStageBytes / 16];
         __shared__ StageSmem s_sm;
-        // this subsequence's bits start at entries[g-1].p (inside [i*sb, ..)); stage from i*sb
-        const uint64_t lo = active ? D.raw_off + ((i * P.sb) >> 3) : 1;
-        const uint64_t hi = active ? D.raw_off + ((min64((i + 1) * P.sb, L) + 7) >> 3) + 24 : 0;
+        // this subsequence's bits start at entries[g-1].p (inside [lo, hi)); stage from lo
+        const uint64_t lo = active ? D.raw_off + (si.lo >> 3) : 1;
+        const uint64_t hi = active ? D.raw_off + ((si.hi + 7) >> 3) + 24 : 0;
         ic.words = stage_scan(P.ubuf, lo, hi, k, tid, kK3Threads, s_stage, s_sm);
     }
     if (!active) return;
     DecState s;
-    if (i == 0) {
-        s.p = 0;
+    if (si.j == 0) {  // segment start: the known state (restart: c = z = 0, DC reset)
+        s.p = si.lo;
         s.c = 0;
         s.z = 0;
     } else {
@@ -1140,8 +1302,7 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     sink.mflags = 0;
     sink.mS = 0.f;
     sink.set_comp(uint32_t(D.du_comp >> (4 * ((o >> 6) % D.dpm))) & 15u);
-    const uint64_t end_bit = min((i + 1) * P.sb, L);
-    decode_range(ic, s, end_bit, cap, sink);
+    decode_range(ic, s, si.hi, cap, sink);
     if (s.err) {
         set_status(P.ist + k, s.err);  // write mode rethrows (parallel_decode.hpp:142)
         return;
@@ -1946,6 +2107,9 @@ void launch_k5_color(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, uin
 // ------------------------------------------------------------ launchers --
 void launch_k0_unstuff(const Params& p, void* stream) {
     if (p.k0_tiles) k0_unstuff<<<p.k0_tiles, kK0Threads, 0, (cudaStream_t)stream>>>(p);
+}
+void launch_k0b_segments(const Params& p, void* stream) {
+    if (p.n_dri) k0b_segments<<<p.n_dri, 256, 0, (cudaStream_t)stream>>>(p);
 }
 void launch_k1_sync(const Params& p, void* stream) {
     if (p.k1_ctas) k1_sync<<<p.k1_ctas, kK1Threads, 0, (cudaStream_t)stream>>>(p);

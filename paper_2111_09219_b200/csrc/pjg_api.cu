@@ -89,7 +89,7 @@ struct pjg_ctx {
     bool busy = false;
     double basis[64];
     cudaEvent_t ev[kNumEvents] = {};
-    DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out,
+    DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out, segs,
         counters, k0_flag, k0_agg, k2_flag, k2_agg, stats;
     HostBuf stage, meta_host, status_host;
 };
@@ -109,11 +109,11 @@ struct pjg_batch {
     size_t raw_bytes = 0;
     bool packed = false;
     // meta blob layout (offsets into ctx->meta)
-    size_t m_desc = 0, m_state = 0, m_huff = 0, m_quant = 0, m_wq = 0, m_basis = 0, m_k0 = 0, m_tile = 0,
+    size_t m_dri = 0, m_desc = 0, m_state = 0, m_huff = 0, m_quant = 0, m_wq = 0, m_basis = 0, m_k0 = 0, m_tile = 0,
            m_sub = 0, m_k0img = 0, m_subimg = 0, m_total = 0;
     uint32_t n_huff = 0, n_quant = 0;
     uint32_t k0_tiles = 0, k4_tiles = 0, k1_ctas = 0, k2_tiles = 0;
-    uint64_t total_subs = 0, total_dus = 0, out_bytes = 0;
+    uint64_t total_subs = 0, total_dus = 0, out_bytes = 0, seg_total = 0;
     Params prm{};
     bool uploaded = false, decoded = false, synced = false;
     std::vector<ImgState> dev_state;  // fetched at synchronize
@@ -231,6 +231,8 @@ void pjg_default_config(pjg_config* cfg) {
     cfg->subsequence_bits = 1024;
     cfg->sequence_length_b = 256;
     cfg->output = PJG_OUT_PLANES;
+    cfg->restart_intervals = 0;
+    cfg->reserved = 0;
 }
 
 int pjg_ctx_create(int device, pjg_ctx** out) {
@@ -258,7 +260,7 @@ void pjg_ctx_destroy(pjg_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->raw, &c->ubuf, &c->meta, &c->blkmeta, &c->ent, &c->dcs, &c->off, &c->cap, &c->pred,
                       &c->cta_end, &c->cta_start, &c->k1_flag, &c->coef, &c->out, &c->counters,
-                      &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats})
+                      &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats, &c->segs})
         b->release();
     c->stage.release();
     c->meta_host.release();
@@ -302,7 +304,8 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     {
         unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         auto body = [&](size_t lo, size_t step) {
-            for (size_t i = lo; i < n; i += step) b->hdr[i] = parse_header(files[i], sizes[i]);
+            for (size_t i = lo; i < n; i += step)
+                b->hdr[i] = parse_header(files[i], sizes[i], cfg->restart_intervals != 0);
         };
         if (n >= 256 && hw > 1) {
             std::vector<std::thread> th;
@@ -355,7 +358,8 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
 
     // ---- layout plan
     const uint64_t sb = cfg->subsequence_bits;
-    uint64_t sub = 0, du = 0, outb = 0;
+    uint64_t sub = 0, du = 0, outb = 0, seg_total = 0;
+    std::vector<uint32_t> dri;  // images with restart intervals
     uint32_t k0t = 0, k4t = 0;
     std::vector<uint32_t> k0_first(n + 1), tile_first(n + 1);
     std::vector<uint64_t> sub_first(n + 1);
@@ -432,8 +436,24 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         }
         // K0 tiles always run (scan checks precede table errors)
         k0t += uint32_t(((d.raw_off & 15) + rl + kK0Tile - 1) / kK0Tile);  // 16-byte-grid windows
+        d.n_int = 1;
         if (h.table_status != kOk) continue;
         d.sub_count = (uint64_t(rl) * 8 + sb - 1) / sb;
+        if (h.restart_interval && h.intervals() > 1) {
+            // restart intervals: one subsequence partition per interval (K0b), at
+            // most ceil(bits / sb) + intervals subsequences; segment bit offsets are
+            // 32-bit
+            if (uint64_t(rl) * 8 >= (1ull << 32)) {
+                b->host_status[i] = h.status = kUnsupportedFeature;
+                continue;
+            }
+            d.n_int = uint32_t(h.intervals());
+            d.ri = h.restart_interval;
+            d.seg_first = seg_total;
+            seg_total += d.n_int + 1;
+            d.sub_count += d.n_int;
+            dri.push_back(uint32_t(i));
+        }
         d.expected = h.total_dus() * 64;
         d.mcus_per_tile = uint16_t(64 / (8 * h.h_max));  // 64-pixel-wide warp tiles (<= 24 data units)
         d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
@@ -453,6 +473,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     b->k4_tiles = k4t;
     b->total_subs = sub;
     b->total_dus = du;
+    b->seg_total = seg_total;
     b->out_bytes = outb;
     b->k1_ctas = uint32_t((sub + kK1Threads - 1) / kK1Threads);
     b->k2_tiles = uint32_t((sub + kK2Threads - 1) / kK2Threads);
@@ -494,6 +515,8 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     o = align_up(o + (uint64_t(k0t) + 1) * 4, 16);
     b->m_subimg = o;
     o = align_up(o + n_subimg * 4, 16);
+    b->m_dri = o;
+    o = align_up(o + (dri.size() + 1) * 4, 16);
     b->m_total = o;
     CU(ctx->meta_host.ensure(o), "cudaMallocHost(meta)");
     uint8_t* mh = static_cast<uint8_t*>(ctx->meta_host.p);
@@ -510,6 +533,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     std::memcpy(mh + b->m_k0, k0_first.data(), (n + 1) * 4);
     std::memcpy(mh + b->m_tile, tile_first.data(), (n + 1) * 4);
     std::memcpy(mh + b->m_sub, sub_first.data(), (n + 1) * 8);
+    if (!dri.empty()) std::memcpy(mh + b->m_dri, dri.data(), dri.size() * 4);
     {
         uint32_t* k0img = reinterpret_cast<uint32_t*>(mh + b->m_k0img);
         for (size_t i = 0; i < n; ++i)
@@ -538,6 +562,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     CU(ctx->cta_start.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_start)");
     CU(ctx->k1_flag.ensure((b->k1_ctas + 1) * 4), "cudaMalloc(k1_flag)");
     CU(ctx->coef.ensure(std::max<uint64_t>(du, 1) * 128), "cudaMalloc(coef)");
+    CU(ctx->segs.ensure(std::max<uint64_t>(seg_total, 1) * sizeof(uint2)), "cudaMalloc(segs)");
     CU(ctx->blkmeta.ensure(std::max<uint64_t>(du, 1) * 8), "cudaMalloc(blkmeta)");
     CU(ctx->out.ensure(std::max<uint64_t>(outb, 1)), "cudaMalloc(out)");
     CU(ctx->counters.ensure(kNumCounters * 4), "cudaMalloc(counters)");
@@ -564,6 +589,9 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.k0_first = reinterpret_cast<const uint32_t*>(md + b->m_k0);
     p.k0_img = reinterpret_cast<const uint32_t*>(md + b->m_k0img);
     p.sub_img = reinterpret_cast<const uint32_t*>(md + b->m_subimg);
+    p.segs = ctx->segs.as<uint2>();
+    p.dri_img = reinterpret_cast<const uint32_t*>(md + b->m_dri);
+    p.n_dri = uint32_t(dri.size());
     p.k0_tiles = k0t;
     p.k1_ctas = b->k1_ctas;
     p.sb = sb;
@@ -628,7 +656,10 @@ int pjg_batch_decode(pjg_batch* b) {
     CU(cudaMemsetAsync(ctx->stats.p, 0, kNumStats * 8, s), "memset stats");
     b->prm.epoch = ++ctx->epoch;
     CU(cudaEventRecord(ctx->ev[2], s), "ev");
+    if (b->prm.n_dri)  // interval starts not written by K0 stay ~0 (K0b flags them)
+        CU(cudaMemsetAsync(ctx->segs.p, 0xFF, b->seg_total * sizeof(uint2), s), "memset segs");
     launch_k0_unstuff(b->prm, s);
+    launch_k0b_segments(b->prm, s);
     CU(cudaEventRecord(ctx->ev[3], s), "ev");
     launch_k1_sync(b->prm, s);
     launch_k1c_fixup(b->prm, s);
@@ -823,7 +854,14 @@ int pjg_batch_dump_sync_states(const pjg_batch* b, size_t i, pjg_sync_entry* out
     if (st) return st;
     if (b->host_status[i] != 0) return b->host_status[i];
     const uint64_t L = b->dev_state[i].bit_length;
-    const uint64_t N = (L + b->cfg.subsequence_bits - 1) / b->cfg.subsequence_bits;
+    uint64_t N = (L + b->cfg.subsequence_bits - 1) / b->cfg.subsequence_bits;
+    if (b->desc[i].n_int > 1) {  // restart intervals: the subsequences in use (K0b)
+        uint2 last;
+        CU(cudaMemcpy(&last, ctx->segs.as<uint2>() + b->desc[i].seg_first + b->desc[i].n_int, sizeof(uint2),
+                      cudaMemcpyDeviceToHost),
+           "D2H segs");
+        N = last.y;
+    }
     *n_out = N;
     if (!out) return PJG_OK;
     if (cap < N) return fail(ctx, PJG_CAPACITY, "sync state buffer too small");

@@ -98,7 +98,11 @@ struct ImgDesc {
     uint32_t out_mode;     // pjg_output_kind
     int32_t deferred;      // build_table error, applied after K0's scan checks
     uint32_t tiles_x;      // K4 tiles per MCU row
+    // restart intervals (extension; 1 interval = the reference's single scan)
+    uint32_t n_int;        // intervals; > 1 only with DRI and RST markers
+    uint32_t ri;           // MCUs per interval (DRI Ri), 0 = none
     uint32_t pad1;
+    uint64_t seg_first;    // this image's segment table in Params::segs (n_int + 1 entries)
 };
 
 // Per-image results written by the device.
@@ -169,6 +173,12 @@ struct Params {
     const uint32_t* k0_first;      // n_img + 1 prefix
     const uint32_t* k0_img;        // image of each K0 tile
     const uint32_t* sub_img;       // image of subsequence c << kSubImgShift, c = 0..ceil(total/128)
+    // restart-interval segments (DRI images only): per image n_int + 1 entries,
+    // x = first unstuffed bit of interval m (x[n_int] = bit length), y = first
+    // image-local subsequence of interval m (y[n_int] = subsequences in use)
+    uint2* segs;
+    const uint32_t* dri_img;       // the batch's DRI images
+    uint32_t n_dri;
     uint32_t k0_tiles;
     uint32_t k1_ctas;
     // subsequences
@@ -215,6 +225,7 @@ enum StatIndex {
 
 // Kernel launchers (kernels.cu).  All are stream-ordered, no host syncs.
 void launch_k0_unstuff(const Params& p, void* stream);
+void launch_k0b_segments(const Params& p, void* stream);
 void launch_k1_sync(const Params& p, void* stream);
 void launch_k1c_fixup(const Params& p, void* stream);
 void launch_k2_scan(const Params& p, void* stream);
