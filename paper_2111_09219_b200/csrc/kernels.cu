@@ -105,8 +105,9 @@ struct SubInfo {
     uint64_t seg_sub0, seg_sub1;  // the segment's image-local subsequences
     uint32_t m;               // segment (restart interval)
 };
+template <bool DRI = true>
 __device__ __forceinline__ bool sub_info(const Params& P, const ImgDesc& D, uint64_t L, uint64_t i, SubInfo& si) {
-    if (D.n_int <= 1) {
+    if (!DRI || D.n_int <= 1) {
         const uint64_t N = (L + P.sb - 1) / P.sb;
         si.m = 0;
         si.seg_lo = 0;
@@ -176,6 +177,7 @@ __device__ __forceinline__ uint32_t has_ff(uint32_t w) {
 // 16 bytes with one vector load, and the compacted bytes are staged in shared
 // memory on the destination's 16-byte grid and leave as full 16-byte stores
 // (only the two edge chunks a tile shares with its neighbours go byte-wise).
+template <bool DRI>
 __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     __shared__ uint32_t s_tile;
     // s_b[16 + i] = raw byte win0 + i; s_b[15] = byte before the window,
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     // restart intervals (extension): RSTn markers inside the scan are removed
     // like stuffed zeros and their unstuffed positions recorded; without them a
     // RST marker ends the scan and is UnsupportedFeature (parser.hpp:249-250)
-    const bool dri = D.n_int > 1;
+    const bool dri = DRI && D.n_int > 1;
 
     {
         const uint64_t g = win0 + 16u * tid;
@@ -756,6 +758,7 @@ __device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t end_bit, 
 // Thread t of logical CTA j owns global subsequence g = j*T + t.  Images are
 // flattened into one subsequence space; a CTA may hold the tail of one image
 // and the head of the next, and overflow chains stop at image ends.
+template <bool DRI>
 __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     constexpr int T = kK1Threads;
     __shared__ uint64_t s_p[T];
@@ -776,7 +779,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     const uint64_t L = P.ist[k].bit_length;
     const bool ok = P.ist[k].status == 0;
     SubInfo si;
-    const bool real = inb && ok && sub_info(P, D, L, i, si);
+    const bool real = inb && ok && sub_info<DRI>(P, D, L, i, si);
     ImgCtx ic;
     load_ctx(P, D, L, ic);
     {
@@ -2106,13 +2109,21 @@ void launch_k5_color(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, uin
 
 // ------------------------------------------------------------ launchers --
 void launch_k0_unstuff(const Params& p, void* stream) {
-    if (p.k0_tiles) k0_unstuff<<<p.k0_tiles, kK0Threads, 0, (cudaStream_t)stream>>>(p);
+    if (!p.k0_tiles) return;
+    if (p.n_dri)
+        k0_unstuff<true><<<p.k0_tiles, kK0Threads, 0, (cudaStream_t)stream>>>(p);
+    else
+        k0_unstuff<false><<<p.k0_tiles, kK0Threads, 0, (cudaStream_t)stream>>>(p);
 }
 void launch_k0b_segments(const Params& p, void* stream) {
     if (p.n_dri) k0b_segments<<<p.n_dri, 256, 0, (cudaStream_t)stream>>>(p);
 }
 void launch_k1_sync(const Params& p, void* stream) {
-    if (p.k1_ctas) k1_sync<<<p.k1_ctas, kK1Threads, 0, (cudaStream_t)stream>>>(p);
+    if (!p.k1_ctas) return;
+    if (p.n_dri)
+        k1_sync<true><<<p.k1_ctas, kK1Threads, 0, (cudaStream_t)stream>>>(p);
+    else
+        k1_sync<false><<<p.k1_ctas, kK1Threads, 0, (cudaStream_t)stream>>>(p);
 }
 void launch_k1c_fixup(const Params& p, void* stream) {
     if (p.k1_ctas > 1) k1c_fixup<<<1, 1024, 0, (cudaStream_t)stream>>>(p);
