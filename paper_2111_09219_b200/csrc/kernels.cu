@@ -158,11 +158,12 @@ __device__ __forceinline__ int lround_away(double s) {
 }
 __device__ __forceinline__ uint32_t clamp_u8(int v) { return v < 0 ? 0u : (v > 255 ? 255u : uint32_t(v)); }
 
-// nonzero iff some byte of w is 0xFF
-__device__ __forceinline__ uint32_t has_ff(uint32_t w) {
-    const uint32_t x = ~w;
-    return (x - 0x01010101u) & ~x & 0x80808080u;
+// 0x80 in every zero byte of x (exact, no borrow between bytes)
+__device__ __forceinline__ uint32_t eq0_bytes(uint32_t x) {
+    return ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;
 }
+// the four 0x80 byte flags of x as a 4-bit mask (bit i = byte i)
+__device__ __forceinline__ uint32_t movemask4(uint32_t x) { return (x * 0x00204081u) >> 28; }
 
 // ========================================================= K0: unstuff ====
 // One CTA per 4 KB tile of raw scan bytes.  Per tile: number of stuffed zero
@@ -214,33 +215,37 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     }
     __syncthreads();
 
-    // this thread's 16 bytes: raw bytes win0 + b0 + q, image bytes only.
-    // Plain chunks (all 16 bytes inside the image, no 0xFF among them or just
-    // before them) have nothing to classify and copy straight through.
+    // this thread's 16 bytes (raw bytes win0 + b0 + i), classified branch-free
+    // with SWAR byte compares into 16-bit masks (bit i = byte i): a divergent
+    // per-byte loop would cost every warp that holds a single 0xFF byte
     const uint32_t b0 = tid * kK0BytesPerThread;
-    const bool inside = win0 + b0 > a && win0 + b0 + 16 <= e;
-    bool plain;
+    const uint64_t gb = win0 + b0;
+    uint32_t inr = 0xFFFFu;  // bytes inside the image [a, e)
+    if (gb < a) inr &= a - gb >= 16 ? 0u : (0xFFFFu << uint32_t(a - gb)) & 0xFFFFu;
+    if (gb + 16 > e) inr &= e <= gb ? 0u : 0xFFFFu >> uint32_t(16 - (e - gb));
+    uint32_t mFF, m00, mR;
     {
         const uint4 w = reinterpret_cast<const uint4*>(s_b + 16)[tid];
-        const uint32_t f = has_ff(w.x) | has_ff(w.y) | has_ff(w.z) | has_ff(w.w);
-        plain = inside && f == 0 && s_b[15 + b0] != 0xFF;
-    }
-    uint32_t cnt = 0, mk = kInf32, rc = 0;  // removed bytes, first marker, RST markers
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        mFF = m00 = mR = 0;
 #pragma unroll
-    for (int q = 0; q < kK0BytesPerThread; ++q) {
-        if (plain) break;
-        const uint64_t g = win0 + b0 + q;
-        if (g < a || g >= e) continue;
-        const uint8_t cur = s_b[16 + b0 + q], next = s_b[17 + b0 + q];
-        const uint8_t prev = g > a ? s_b[15 + b0 + q] : 0;
-        const uint64_t j = g - a;
-        const bool last = (j + 1 == raw_len);
-        const bool rst_ff = dri && cur == 0xFF && !last && (next & 0xF8) == 0xD0;
-        const bool rst_x = dri && prev == 0xFF && (cur & 0xF8) == 0xD0;
-        if ((cur == 0x00 && prev == 0xFF) || rst_ff || rst_x) ++cnt;
-        rc += rst_ff;
-        if (cur == 0xFF && !rst_ff && (last || next != 0x00) && mk == kInf32) mk = uint32_t(j);
+        for (int q = 0; q < 4; ++q) {
+            mFF |= movemask4(eq0_bytes(~ws[q])) << (4 * q);
+            m00 |= movemask4(eq0_bytes(ws[q])) << (4 * q);
+            if (DRI) mR |= movemask4(eq0_bytes((ws[q] ^ 0xD0D0D0D0u) & 0xF8F8F8F8u)) << (4 * q);
+        }
     }
+    const uint8_t pb = s_b[15 + b0], nb = s_b[32 + b0];  // bytes before / after the chunk
+    const uint32_t prevFF = (((mFF & inr) << 1) | ((gb > a && pb == 0xFF) ? 1u : 0u)) & 0xFFFFu;  // prev in the image
+    const uint32_t next00 = (m00 >> 1) | (nb == 0x00 ? 0x8000u : 0u);
+    const uint32_t nextR = (mR >> 1) | (((nb & 0xF8) == 0xD0) ? 0x8000u : 0u);
+    const uint32_t lastb = (e - 1 >= gb && e - 1 < gb + 16) ? (1u << uint32_t(e - 1 - gb)) : 0u;
+    const uint32_t rstFF = dri ? (mFF & nextR & ~lastb & inr) : 0u;
+    const uint32_t rstX = dri ? (mR & prevFF & inr) : 0u;
+    const uint32_t remv = ((m00 & prevFF) | rstFF | rstX) & inr;  // removed bytes
+    const uint32_t mark = mFF & inr & ~rstFF & (~next00 | lastb);   // markers ending the scan
+    const uint32_t cnt = __popc(remv), rc = __popc(rstFF);
+    const uint32_t mk = mark ? uint32_t(gb - a) + (__ffs(mark) - 1) : kInf32;
     // block reduce (sum, min); removed | RST count << 16 (both < 2^16 per tile)
     const uint32_t cr = cnt | (rc << 16);
     uint32_t wc = cr, wm = mk;
@@ -254,49 +259,71 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
         s_mk[warp] = wm;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {
+        // tile totals, then a warp-parallel decoupled lookback (32 predecessors
+        // per step), segmented at the image's first tile:
+        // agg [0] aggregate (mk << 32 | removed), [1] aggregate RST count, [2], [3] inclusive
         uint32_t tcr = 0, tm = kInf32;
         for (int w = 0; w < kK0Threads / 32; ++w) {
             tcr += s_cnt[w];
             tm = min(tm, s_mk[w]);
         }
         const uint32_t tc = tcr & 0xFFFFu, trc = tcr >> 16;
-        s_tile_cnt = tc;
-        s_tile_mk = tm;
-        // decoupled lookback, segmented at the image's first tile:
-        // [0] aggregate (mk << 32 | removed), [1] aggregate RST count, [2], [3] inclusive
         uint64_t* agg = P.k0_agg + 4ull * t;
         uint32_t ec = 0, em = kInf32, erc = 0;
         if (lt == 0) {
-            agg[2] = (uint64_t(tm) << 32) | tc;
-            agg[3] = trc;
-            st_release(P.k0_flag + t, (P.epoch << 2) | 2u);
-        } else {
-            agg[0] = (uint64_t(tm) << 32) | tc;
-            agg[1] = trc;
-            st_release(P.k0_flag + t, (P.epoch << 2) | 1u);
-            int64_t pr = int64_t(t) - 1;
-            while (true) {
-                uint32_t f = ld_acquire(P.k0_flag + pr);
-                if ((f >> 2) != P.epoch) {
-                    spin_pause();
-                    continue;
-                }
-                const uint64_t* src = P.k0_agg + 4ull * pr + ((f & 3u) == 2u ? 2 : 0);
-                const uint64_t v = __ldcg(src);
-                ec += uint32_t(v);
-                em = min(em, uint32_t(v >> 32));
-                erc += uint32_t(__ldcg(src + 1));
-                if ((f & 3u) == 2u) break;
-                --pr;
+            if (lane == 0) {
+                agg[2] = (uint64_t(tm) << 32) | tc;
+                agg[3] = trc;
+                st_release(P.k0_flag + t, (P.epoch << 2) | 2u);
             }
-            agg[2] = (uint64_t(min(em, tm)) << 32) | (ec + tc);
-            agg[3] = erc + trc;
-            st_release(P.k0_flag + t, (P.epoch << 2) | 2u);
+        } else {
+            if (lane == 0) {
+                agg[0] = (uint64_t(tm) << 32) | tc;
+                agg[1] = trc;
+                st_release(P.k0_flag + t, (P.epoch << 2) | 1u);
+            }
+            const int64_t first_t = int64_t(P.k0_first[k]);
+            int64_t base = int64_t(t) - 1;
+            while (true) {
+                const int64_t pr = base - lane;  // lane 0: nearest predecessor
+                uint32_t f = 2u;                 // before the image: an empty inclusive prefix
+                if (pr >= first_t) {
+                    f = ld_acquire(P.k0_flag + pr);
+                    while ((f >> 2) != P.epoch) {
+                        spin_pause();
+                        f = ld_acquire(P.k0_flag + pr);
+                    }
+                }
+                const uint32_t incl = __ballot_sync(0xFFFFFFFFu, (f & 3u) == 2u);
+                const int lim = incl ? __ffs(incl) - 1 : 31;
+                uint32_t c = 0, m = kInf32, r = 0;
+                if (lane <= lim && pr >= first_t) {
+                    const uint64_t* src = P.k0_agg + 4ull * pr + ((f & 3u) == 2u ? 2 : 0);
+                    const uint64_t v = __ldcg(src);
+                    c = uint32_t(v);
+                    m = uint32_t(v >> 32);
+                    r = uint32_t(__ldcg(src + 1));
+                }
+                ec += __reduce_add_sync(0xFFFFFFFFu, c);
+                em = min(em, __reduce_min_sync(0xFFFFFFFFu, m));
+                erc += __reduce_add_sync(0xFFFFFFFFu, r);
+                if (incl) break;
+                base -= 32;
+            }
+            if (lane == 0) {
+                agg[2] = (uint64_t(min(em, tm)) << 32) | (ec + tc);
+                agg[3] = erc + trc;
+                st_release(P.k0_flag + t, (P.epoch << 2) | 2u);
+            }
         }
-        s_excl_cnt = ec;
-        s_excl_mk = em;
-        s_excl_rc = erc;
+        if (lane == 0) {
+            s_tile_cnt = tc;
+            s_tile_mk = tm;
+            s_excl_cnt = ec;
+            s_excl_mk = em;
+            s_excl_rc = erc;
+        }
     }
     __syncthreads();
     // exclusive scan of per-thread (removed | RST << 16) counts (warp shuffles + smem)
@@ -319,52 +346,48 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     const uint64_t dst_lo = g_first - s_excl_cnt;
     const uint64_t dst_al = dst_lo & ~15ull;
     const uint32_t first_mk = s_excl_mk == kInf32 ? s_tile_mk : kInf32;  // the image's scan end
-    if (plain) {
-        uint8_t* o = s_o + ((win0 + b0 - removed) - dst_al);
+    {
+        // kept bytes to their compacted positions: byte i moves left by the
+        // removed bytes before it in this chunk
+        const uint32_t keep = inr & ~remv;
+        uint8_t* o = s_o + ((gb - removed) - dst_al);
+        const uint4 w = reinterpret_cast<const uint4*>(s_b + 16)[tid];
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int q = 0; q < kK0BytesPerThread; ++q) o[q] = s_b[16 + b0 + q];
+        for (int i = 0; i < kK0BytesPerThread; ++i)
+            if ((keep >> i) & 1u) o[i - __popc(remv & ((1u << i) - 1u))] = uint8_t(ws[i >> 2] >> (8 * (i & 3)));
     }
-#pragma unroll
-    for (int q = 0; q < kK0BytesPerThread; ++q) {
-        if (plain) break;
-        const uint64_t g = win0 + b0 + q;
-        if (g < a || g >= e) continue;
-        const uint8_t cur = s_b[16 + b0 + q], nx = s_b[17 + b0 + q];
-        const uint8_t prev = g > a ? s_b[15 + b0 + q] : 0;
-        const uint64_t j = g - a;
-        if (first_mk != kInf32 && j == first_mk) {
-            // scan ends here (extract_scan, parser.hpp:241-254)
-            uint64_t U = j - removed;
-            ImgState* st = P.ist + k;
-            st->bit_length = U * 8;
-            bool rst = (j + 1 < raw_len) && nx >= 0xD0 && nx <= 0xD7;
-            if (rst)
-                set_status(st, kUnsupportedFeature);
-            else if (U == 0)
-                set_status(st, kEmptyScan);
-            else if (D.deferred)
-                set_status(st, D.deferred);
-        }
-        const bool last = (j + 1 == raw_len);
-        const bool rst_ff = dri && cur == 0xFF && !last && (nx & 0xF8) == 0xD0;
-        const bool rst_x = dri && prev == 0xFF && (cur & 0xF8) == 0xD0;
-        if (rst_ff) {
-            // restart marker r = rst_before: interval r + 1 starts at unstuffed
-            // byte j - removed; markers past the scan end do not count
-            const uint32_t end_mk = s_excl_mk != kInf32 ? s_excl_mk : s_tile_mk;
-            if (j < end_mk) {
-                const uint32_t r = rst_before;
-                if (r + 1 >= D.n_int || (nx & 7u) != (r & 7u))
-                    set_status(P.ist + k, kConsistencyFailure);  // RST count / numbering vs DRI
-                else
-                    P.segs[D.seg_first + r + 1].x = uint32_t((j - removed) * 8);
-            }
-            ++rst_before;
-        }
-        if ((cur == 0x00 && prev == 0xFF) || rst_ff || rst_x) {
-            ++removed;
-        } else {
-            s_o[(a + j - removed) - dst_al] = cur;
+    // rare events, off the branch-free path: the scan end and restart markers
+    if (first_mk != kInf32 && first_mk - uint32_t(gb - a) < 16u && (mark >> (first_mk - uint32_t(gb - a))) & 1u) {
+        // scan ends here (extract_scan, parser.hpp:241-254)
+        const uint32_t i = first_mk - uint32_t(gb - a);
+        const uint64_t j = first_mk;
+        const uint64_t U = j - (removed + __popc(remv & ((1u << i) - 1u)));
+        ImgState* st = P.ist + k;
+        st->bit_length = U * 8;
+        const uint8_t nx = s_b[17 + b0 + i];
+        const bool rst = (j + 1 < raw_len) && nx >= 0xD0 && nx <= 0xD7;
+        if (rst)
+            set_status(st, kUnsupportedFeature);
+        else if (U == 0)
+            set_status(st, kEmptyScan);
+        else if (D.deferred)
+            set_status(st, D.deferred);
+    }
+    if (DRI && rstFF) {
+        // restart marker r: interval r + 1 starts at unstuffed byte j - removed;
+        // markers past the scan end do not count
+        const uint32_t end_mk = s_excl_mk != kInf32 ? s_excl_mk : s_tile_mk;
+        for (uint32_t m = rstFF; m; m &= m - 1) {
+            const uint32_t i = __ffs(m) - 1;
+            const uint64_t j = gb - a + i;
+            const uint32_t r = rst_before + __popc(rstFF & ((1u << i) - 1u));
+            if (j >= end_mk) continue;
+            const uint8_t nx = s_b[17 + b0 + i];
+            if (r + 1 >= D.n_int || (nx & 7u) != (r & 7u))
+                set_status(P.ist + k, kConsistencyFailure);  // RST count / numbering vs DRI
+            else
+                P.segs[D.seg_first + r + 1].x = uint32_t((j - (removed + __popc(remv & ((1u << i) - 1u)))) * 8);
         }
     }
     __syncthreads();

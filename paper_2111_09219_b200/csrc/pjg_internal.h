@@ -146,7 +146,7 @@ struct DcSums {
 
 // ------------------------------------------------------------- params --
 constexpr int kSubImgShift = 7;
-constexpr int kK0Threads = 256;
+constexpr int kK0Threads = 512;
 constexpr int kK0BytesPerThread = 16;
 constexpr int kK0Tile = kK0Threads * kK0BytesPerThread;  // 4096 raw bytes per tile
 constexpr int kK1Threads = 128;                          // subsequences per K1 CTA
