@@ -108,6 +108,23 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def profiled_traffic(cfg_key):
+    """dram__bytes_read.sum + dram__bytes_write.sum of K4 from the committed
+    ncu --set full capture of the same workload (config 3), bytes per launch."""
+    if cfg_key != "3":
+        return None
+    try:
+        vals = {}
+        with open(os.path.join(ROOT, "profiles", "round1", "ncu_k4_transform.txt")) as f:
+            for line in f:
+                parts = line.split()
+                if len(parts) == 2 and parts[0].startswith("dram__bytes_"):
+                    vals[parts[0]] = float(parts[1]) * 1e9  # Gbyte
+        return int(vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
+    except Exception:
+        return None
+
+
 def dist_env():
     from paper_2111_09219_b200.dist import rank_env
     return rank_env()
@@ -312,6 +329,18 @@ def main():
     k4_ms = st_mean["idct"]
     achieved = k4_bytes / (k4_ms / 1e3) / 1e9
     dominant = max(st_mean, key=st_mean.get)
+    # the other bandwidth-bound stages against the same peak:
+    # K0 reads + writes the scan (2 C), K3 reads it and writes the coefficients
+    stage_roof = {
+        "k0_unstuff": {"algorithmic_bytes": 2 * comp_bytes, "ms": st_mean["unstuff"]},
+        "k3_write": {"algorithmic_bytes": comp_bytes + dus * 128, "ms": st_mean["write"]},
+        "k4_transform": {"algorithmic_bytes": k4_bytes, "ms": k4_ms},
+    }
+    for v in stage_roof.values():
+        v["achieved_gbs"] = round(v["algorithmic_bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 else None
+        v["frac"] = round(v["achieved_gbs"] / peak, 4) if v["achieved_gbs"] else None
+        v["ms"] = round(v["ms"], 4)
+    traffic = profiled_traffic(args.config)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -343,8 +372,11 @@ def main():
                     "path": "decode_to_host_pipelined: per chunk pjg_batch_create+upload+decode+download_all_async "
                             "over 2 contexts (pinned host in/out)", "chunk_images": args.chunk},
             "roofline": {"bound": "hbm", "kernel": "k4_transform", "achieved": round(achieved, 1),
-                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "peak_kind": peak_kind, "algorithmic_bytes": k4_bytes},
+                         "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "peak_kind": peak_kind, "algorithmic_bytes": k4_bytes,
+                         "traffic_source": "profiles/round1/ncu_k4_transform.txt (dram read + write, one launch)"
+                         if traffic else None},
+            "stage_rooflines": stage_roof,
             "stages_ms": {k: round(v, 4) for k, v in st_mean.items()},
             "dominant_stage": dominant,
             "sync": sync_stats,

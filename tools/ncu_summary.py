@@ -24,15 +24,18 @@ def run(args):
     return subprocess.run(["ncu", "-i"] + args, capture_output=True, text=True).stdout
 
 
+KERNEL = []
+
+
 def main(path, segments=True):
-    raw = list(csv.reader(io.StringIO(run([path, "--page", "raw", "--csv"]))))
+    raw = list(csv.reader(io.StringIO(run([path] + KERNEL + ["--page", "raw", "--csv"]))))
     h, v = raw[0], raw[2]
     for name in HEAD:
         if name in h:
             print(f"{name:70s} {v[h.index(name)]}")
     if not segments:
         return
-    src = list(csv.reader(io.StringIO(run([path, "--page", "source", "--csv", "--print-source=sass"]))))
+    src = list(csv.reader(io.StringIO(run([path] + KERNEL + ["--page", "source", "--csv", "--print-source=sass"]))))
     hdr, data = src[1], src[2:]
     iA, iS, iE = hdr.index("Address"), hdr.index("Source"), hdr.index("Instructions Executed")
     cols = {x: i for i, x in enumerate(hdr)}
@@ -58,4 +61,6 @@ def main(path, segments=True):
 
 
 if __name__ == "__main__":
+    if "-k" in sys.argv:
+        KERNEL[:] = ["-k", "regex:" + sys.argv[sys.argv.index("-k") + 1]]
     main(sys.argv[1], "--no-seg" not in sys.argv)
