@@ -225,3 +225,16 @@ def test_random_shapes_batch_bit_exact(decoder):
             ref = Ref.decode(f, rgb=True)
             got = _rgb(outs[i], b.infos[i])
             assert np.array_equal(got, ref.data), (shape, int((got != ref.data).sum()))
+
+
+def test_cpp_dropin_binary_matches_reference(tmp_path):
+    """The C++ shim (include/pjpeg_gpu.hpp) and the reference in one binary:
+    identical planes checksum and RGB."""
+    import subprocess
+    from tests.test_host import _build_dropin
+    exe = _build_dropin(tmp_path)
+    f = tmp_path / "img.jpg"
+    f.write_bytes(ref_jpeg(333, 257, 6, 95, "422"))
+    r = subprocess.run([exe, str(f)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert ("IDENTICAL" in r.stdout) or ("ref:" not in r.stdout)

@@ -137,3 +137,26 @@ def test_synthetic_bench_corpus_is_valid_baseline_jpeg():
             f = blob[o: o + n].tobytes()
             d = Ref.decode(f)
             assert d.status == 0 and (d.width, d.height) == (w, h)
+
+
+def _build_dropin(tmp_path):
+    """tools/cpp_dropin_check.cpp: the reference (when its headers are here)
+    and the pjpeg::gpu shim in ONE binary (SURVEY.md §8b), linked to libpjg.so."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.join(root, "paper_2111_09219_b200")
+    exe = str(tmp_path / "dropin")
+    cmd = ["g++", "-O1", "-std=c++20", "-I" + os.path.join(root, "include"),
+           os.path.join(root, "tools", "cpp_dropin_check.cpp"), "-o", exe, "-L" + lib_dir, "-lpjg",
+           "-Wl,-rpath," + lib_dir, "-pthread"]
+    ref_inc = "/root/reference/proj/include"
+    if os.path.isdir(ref_inc):
+        cmd[4:4] = ["-I" + ref_inc]
+    else:
+        cmd.insert(4, "-DPJPEG_NO_REF")
+    subprocess.run(cmd, check=True, capture_output=True)
+    return exe
+
+
+def test_cpp_dropin_header_builds_and_links(tmp_path):
+    assert os.path.exists(_build_dropin(tmp_path))
