@@ -173,18 +173,296 @@ __device__ __forceinline__ uint32_t movemask4(uint32_t x) { return (x * 0x002040
 // (removed, first-marker) prefix; kept bytes are then compacted into ubuf at
 // the same image offset.  The tile holding the first marker fixes the
 // unstuffed length U and the per-image error (EmptyScan / RST).
-// Tiles are 4 KB windows aligned to the 16-byte grid of the raw buffer (the
+// Tiles are windows of 512 x BPT bytes aligned to the 16-byte grid of the raw
+// buffer (the image's first window starts at raw_off & ~15); thread t owns
+// bytes [BPT t, BPT t + BPT) of its window (BPT / 16 vector loads).  Batches of
+// large scans use 32 KB tiles (BPT 64: more bytes in flight per CTA, the
+// per-tile ticket / lookback / scan amortised), batches of small files 8 KB
+// tiles (BPT 16: a file of ~16 KB should not occupy a half-empty 32 KB tile).  The compacted bytes are staged in shared memory on the
+// destination's 16-byte grid and leave as full 16-byte stores (only the two
+// edge chunks a tile shares with its neighbours go byte-wise).
+template <bool DRI, int BPT>
+__global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
+    constexpr int kTile = kK0Threads * BPT;
+    extern __shared__ __align__(16) uint8_t k0_dyn[];
+    uint8_t* s_b = k0_dyn;                 // s_b[16 + i] = raw byte win0 + i; [15] before, [16 + tile] after
+    uint8_t* s_o = k0_dyn + kTile + 32;  // compacted bytes on the destination's 16-byte grid
+    __shared__ unsigned long long s_cnt[kK0Threads / 32];  // per warp: removed | RST << 32
+    __shared__ uint32_t s_mk[kK0Threads / 32];
+    __shared__ uint32_t s_tile, s_excl_cnt, s_excl_mk, s_tile_cnt, s_tile_mk, s_excl_rc;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) s_tile = atomicAdd(&P.counters[kTicketK0], 1u);
+    __syncthreads();
+    const uint32_t t = s_tile;
+    const uint32_t k = __ldg(P.k0_img + t);
+    const uint32_t lt = t - P.k0_first[k];
+    const ImgDesc& D = P.img[k];
+    const uint64_t raw_len = D.raw_len;
+    const uint64_t a = D.raw_off, e = a + raw_len;  // the image's bytes [a, e) in the raw buffer
+    const uint64_t win0 = (a & ~15ull) + uint64_t(lt) * kTile;
+    const uint64_t g_first = max(win0, a);            // first image byte in this window
+    // restart intervals (extension): RSTn markers inside the scan are removed
+    // like stuffed zeros and their unstuffed positions recorded; without them a
+    // RST marker ends the scan and is UnsupportedFeature (parser.hpp:249-250)
+    const bool dri = DRI && D.n_int > 1;
+
+    const uint32_t b0 = tid * BPT;
+    const uint64_t gb = win0 + b0;
+#pragma unroll
+    for (int c = 0; c < BPT / 16; ++c) {
+        const uint64_t g = gb + 16 * c;
+        int4 v = make_int4(0, 0, 0, 0);
+        if (g < e) v = __ldcs(reinterpret_cast<const int4*>(P.raw + g));
+        reinterpret_cast<int4*>(s_b + 16 + b0)[c] = v;
+    }
+    if (tid == 0) s_b[15] = win0 > a ? P.raw[win0 - 1] : 0;
+    if (tid == 1) s_b[16 + kTile] = win0 + kTile < e ? P.raw[win0 + kTile] : 0;
+    __syncthreads();
+
+    // this thread's 64 bytes, classified branch-free with SWAR byte compares
+    // into 64-bit masks (bit i = byte i): a divergent per-byte loop would cost
+    // every warp that holds a single 0xFF byte
+    uint64_t inr = BPT == 64 ? ~0ull : ((1ull << BPT) - 1ull);  // bytes inside the image [a, e)
+    if (gb < a) inr &= a - gb >= BPT ? 0ull : (~0ull << uint32_t(a - gb));
+    if (gb + BPT > e) inr &= e <= gb ? 0ull : (~0ull >> uint32_t(64 - (e - gb)));
+    uint32_t ws[BPT / 4];
+#pragma unroll
+    for (int c = 0; c < BPT / 16; ++c) {
+        const uint4 w = reinterpret_cast<const uint4*>(s_b + 16 + b0)[c];
+        ws[4 * c] = w.x, ws[4 * c + 1] = w.y, ws[4 * c + 2] = w.z, ws[4 * c + 3] = w.w;
+    }
+    uint64_t mFF = 0, m00 = 0, mR = 0;
+#pragma unroll
+    for (int q = 0; q < BPT / 4; ++q) {
+        mFF |= uint64_t(movemask4(eq0_bytes(~ws[q]))) << (4 * q);
+        m00 |= uint64_t(movemask4(eq0_bytes(ws[q]))) << (4 * q);
+        if (DRI) mR |= uint64_t(movemask4(eq0_bytes((ws[q] ^ 0xD0D0D0D0u) & 0xF8F8F8F8u))) << (4 * q);
+    }
+    const uint8_t pb = s_b[15 + b0], nb = s_b[16 + b0 + BPT];  // bytes before / after the thread's bytes
+    const uint64_t prevFF = ((mFF & inr) << 1) | ((gb > a && pb == 0xFF) ? 1ull : 0ull);  // prev in the image
+    const uint64_t next00 = (m00 >> 1) | (nb == 0x00 ? (1ull << (BPT - 1)) : 0ull);
+    const uint64_t nextR = (mR >> 1) | (((nb & 0xF8) == 0xD0) ? (1ull << (BPT - 1)) : 0ull);
+    const uint64_t lastb = (e - 1 >= gb && e - 1 < gb + BPT) ? (1ull << uint32_t(e - 1 - gb)) : 0ull;
+    const uint64_t rstFF = dri ? (mFF & nextR & ~lastb & inr) : 0ull;
+    const uint64_t rstX = dri ? (mR & prevFF & inr) : 0ull;
+    const uint64_t remv = ((m00 & prevFF) | rstFF | rstX) & inr;  // removed bytes
+    const uint64_t mark = mFF & inr & ~rstFF & (~next00 | lastb);   // markers ending the scan
+    const uint64_t cr = uint64_t(__popcll(remv)) | (uint64_t(__popcll(rstFF)) << 32);
+    const uint32_t mk = mark ? uint32_t(gb - a) + (__ffsll(mark) - 1) : kInf32;
+
+    // block reduce (sum, min)
+    unsigned long long wc = cr;
+    uint32_t wm = mk;
+    for (int o = 16; o; o >>= 1) {
+        wc += __shfl_xor_sync(0xFFFFFFFFu, wc, o);
+        wm = min(wm, __shfl_xor_sync(0xFFFFFFFFu, wm, o));
+    }
+    if (lane == 0) {
+        s_cnt[warp] = wc;
+        s_mk[warp] = wm;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // tile totals, then a warp-parallel decoupled lookback (32 predecessors
+        // per step), segmented at the image's first tile:
+        // agg [0] aggregate (mk << 32 | removed), [1] aggregate RST count, [2], [3] inclusive
+        unsigned long long tcr = 0;
+        uint32_t tm = kInf32;
+        for (int w = 0; w < kK0Threads / 32; ++w) {
+            tcr += s_cnt[w];
+            tm = min(tm, s_mk[w]);
+        }
+        const uint32_t tc = uint32_t(tcr), trc = uint32_t(tcr >> 32);
+        uint64_t* agg = P.k0_agg + 4ull * t;
+        uint32_t ec = 0, em = kInf32, erc = 0;
+        if (lt == 0) {
+            if (lane == 0) {
+                agg[2] = (uint64_t(tm) << 32) | tc;
+                agg[3] = trc;
+                st_release(P.k0_flag + t, (P.epoch << 2) | 2u);
+            }
+        } else {
+            if (lane == 0) {
+                agg[0] = (uint64_t(tm) << 32) | tc;
+                agg[1] = trc;
+                st_release(P.k0_flag + t, (P.epoch << 2) | 1u);
+            }
+            const int64_t first_t = int64_t(P.k0_first[k]);
+            int64_t base = int64_t(t) - 1;
+            while (true) {
+                const int64_t pr = base - lane;  // lane 0: nearest predecessor
+                uint32_t f = 2u;                 // before the image: an empty inclusive prefix
+                if (pr >= first_t) {
+                    f = ld_acquire(P.k0_flag + pr);
+                    while ((f >> 2) != P.epoch) {
+                        spin_pause();
+                        f = ld_acquire(P.k0_flag + pr);
+                    }
+                }
+                const uint32_t incl = __ballot_sync(0xFFFFFFFFu, (f & 3u) == 2u);
+                const int lim = incl ? __ffs(incl) - 1 : 31;
+                uint32_t c = 0, m = kInf32, r = 0;
+                if (lane <= lim && pr >= first_t) {
+                    const uint64_t* src = P.k0_agg + 4ull * pr + ((f & 3u) == 2u ? 2 : 0);
+                    const uint64_t v = __ldcg(src);
+                    c = uint32_t(v);
+                    m = uint32_t(v >> 32);
+                    r = uint32_t(__ldcg(src + 1));
+                }
+                ec += __reduce_add_sync(0xFFFFFFFFu, c);
+                em = min(em, __reduce_min_sync(0xFFFFFFFFu, m));
+                erc += __reduce_add_sync(0xFFFFFFFFu, r);
+                if (incl) break;
+                base -= 32;
+            }
+            if (lane == 0) {
+                agg[2] = (uint64_t(min(em, tm)) << 32) | (ec + tc);
+                agg[3] = erc + trc;
+                st_release(P.k0_flag + t, (P.epoch << 2) | 2u);
+            }
+        }
+        if (lane == 0) {
+            s_tile_cnt = tc;
+            s_tile_mk = tm;
+            s_excl_cnt = ec;
+            s_excl_mk = em;
+            s_excl_rc = erc;
+        }
+    }
+    __syncthreads();
+    // exclusive scan of per-thread (removed | RST << 32) counts
+    unsigned long long inc = cr;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    __syncthreads();
+    if (lane == 31) s_cnt[warp] = inc;
+    __syncthreads();
+    unsigned long long wtot = lane < kK0Threads / 32 ? s_cnt[lane] : 0ull;
+    unsigned long long wsc = wtot;
+    for (int o = 1; o < kK0Threads / 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, wsc, o);
+        if (lane >= o) wsc += v;
+    }
+    const unsigned long long before_cr = __shfl_sync(0xFFFFFFFFu, wsc - wtot, warp) + inc - cr;
+    const uint32_t removed = s_excl_cnt + uint32_t(before_cr);        // removed before this thread's bytes
+    const uint32_t rst_before = s_excl_rc + uint32_t(before_cr >> 32);  // RST markers before them
+
+    // kept byte at image index j goes to image index j - removed; this tile's
+    // kept bytes form [dst_lo, dst_lo + kept) in raw-buffer coordinates
+    const uint64_t dst_lo = g_first - s_excl_cnt;
+    const uint64_t dst_al = dst_lo & ~15ull;
+    const uint32_t first_mk = s_excl_mk == kInf32 ? s_tile_mk : kInf32;  // the image's scan end
+    const uint64_t keep = inr & ~remv;
+#pragma unroll
+    for (int c = 0; c < BPT / 16; ++c) {
+        // kept bytes of 16-byte chunk c move left by the removed bytes before them
+        const uint32_t keep16 = uint32_t(keep >> (16 * c)) & 0xFFFFu;
+        const uint32_t remv16 = uint32_t(remv >> (16 * c)) & 0xFFFFu;
+        const uint32_t rbefore = removed + uint32_t(__popcll(remv & ((1ull << (16 * c)) - 1ull)));
+        const uint32_t off = uint32_t((gb + 16 * c - rbefore) - dst_al);
+        uint8_t* o = s_o + off;
+        const uint32_t* w = ws + 4 * c;
+        if (keep16 == 0xFFFFu) {
+            // 16 contiguous bytes: aligned words by funnel shifts, the two edge
+            // words byte-wise (a neighbour owns their other bytes)
+            const uint32_t r = off & 3u;
+            uint32_t* o32 = reinterpret_cast<uint32_t*>(s_o + (off & ~3u));
+            if (r == 0) {
+                o32[0] = w[0], o32[1] = w[1], o32[2] = w[2], o32[3] = w[3];
+            } else {
+                const uint32_t sh = 8 * r;
+                o32[1] = __funnelshift_l(w[0], w[1], sh);
+                o32[2] = __funnelshift_l(w[1], w[2], sh);
+                o32[3] = __funnelshift_l(w[2], w[3], sh);
+                for (uint32_t i = 0; i < 4 - r; ++i) o[i] = uint8_t(w[0] >> (8 * i));
+                for (uint32_t i = 0; i < r; ++i) o[16 - r + i] = uint8_t(w[3] >> (8 * (4 - r + i)));
+            }
+        } else if (keep16) {
+            for (uint32_t m = keep16; m; m &= m - 1) {
+                const uint32_t i = __ffs(m) - 1;
+                o[i - __popc(remv16 & ((1u << i) - 1u))] = s_b[16 + b0 + 16 * c + i];
+            }
+        }
+    }
+    // rare events, off the branch-free path: the scan end and restart markers
+    if (first_mk != kInf32 && first_mk - uint32_t(gb - a) < uint32_t(BPT) && (mark >> (first_mk - uint32_t(gb - a))) & 1ull) {
+        // scan ends here (extract_scan, parser.hpp:241-254)
+        const uint32_t i = first_mk - uint32_t(gb - a);
+        const uint64_t j = first_mk;
+        const uint64_t U = j - (removed + __popcll(remv & ((1ull << i) - 1ull)));
+        ImgState* st = P.ist + k;
+        st->bit_length = U * 8;
+        const uint8_t nx = s_b[17 + b0 + i];
+        const bool rst = (j + 1 < raw_len) && nx >= 0xD0 && nx <= 0xD7;
+        if (rst)
+            set_status(st, kUnsupportedFeature);
+        else if (U == 0)
+            set_status(st, kEmptyScan);
+        else if (D.deferred)
+            set_status(st, D.deferred);
+    }
+    if (DRI && rstFF) {
+        // restart marker r: interval r + 1 starts at unstuffed byte j - removed;
+        // markers past the scan end do not count
+        const uint32_t end_mk = s_excl_mk != kInf32 ? s_excl_mk : s_tile_mk;
+        for (uint64_t m = rstFF; m; m &= m - 1) {
+            const uint32_t i = __ffsll(m) - 1;
+            const uint64_t j = gb - a + i;
+            const uint32_t r = rst_before + uint32_t(__popcll(rstFF & ((1ull << i) - 1ull)));
+            if (j >= end_mk) continue;
+            const uint8_t nx = s_b[17 + b0 + i];
+            if (r + 1 >= D.n_int || (nx & 7u) != (r & 7u))
+                set_status(P.ist + k, kConsistencyFailure);  // RST count / numbering vs DRI
+            else
+                P.segs[D.seg_first + r + 1].x =
+                    uint32_t((j - (removed + __popcll(remv & ((1ull << i) - 1ull)))) * 8);
+        }
+    }
+    __syncthreads();
+    {
+        const uint64_t dst_hi = dst_lo + (min64(e, win0 + kTile) - g_first) - s_tile_cnt;
+        const uint32_t nchunks = uint32_t((dst_hi - dst_al + 15) >> 4);
+        for (uint32_t q = tid; q < nchunks; q += kK0Threads) {
+            const uint64_t G = dst_al + 16ull * q;
+            if (G >= dst_lo && G + 16 <= dst_hi) {
+                *reinterpret_cast<int4*>(P.ubuf + G) = reinterpret_cast<const int4*>(s_o)[q];
+            } else {
+                for (uint32_t x = 0; x < 16; ++x)
+                    if (G + x >= dst_lo && G + x < dst_hi) P.ubuf[G + x] = s_o[16 * q + x];
+            }
+        }
+    }
+    // no marker anywhere: the scan runs to the end of the file
+    const uint32_t last_tile = uint32_t(((a & 15ull) + raw_len + kTile - 1) / kTile) - 1;
+    if (tid == 0 && lt == last_tile && s_excl_mk == kInf32 && s_tile_mk == kInf32) {
+        uint64_t U = raw_len - (s_excl_cnt + s_tile_cnt);
+        ImgState* st = P.ist + k;
+        st->bit_length = U * 8;
+        if (U == 0)
+            set_status(st, kEmptyScan);
+        else if (D.deferred)
+            set_status(st, D.deferred);
+    }
+}
+
+// Small-file variant (8 KB tiles, 16 bytes per thread, 32-bit scan words):
+// windows aligned to the 16-byte grid of the raw buffer (the
 // image's first window starts at raw_off & ~15), so every thread moves its
 // 16 bytes with one vector load, and the compacted bytes are staged in shared
 // memory on the destination's 16-byte grid and leave as full 16-byte stores
 // (only the two edge chunks a tile shares with its neighbours go byte-wise).
 template <bool DRI>
-__global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
+__global__ void __launch_bounds__(kK0Threads) k0_unstuff_small(Params P) {
+    constexpr int kSmallTile = kK0Threads * 16;
     __shared__ uint32_t s_tile;
     // s_b[16 + i] = raw byte win0 + i; s_b[15] = byte before the window,
-    // s_b[16 + kK0Tile] = byte after it
-    __shared__ __align__(16) uint8_t s_b[kK0Tile + 32];
-    __shared__ __align__(16) uint8_t s_o[kK0Tile + 32];
+    // s_b[16 + kSmallTile] = byte after it
+    __shared__ __align__(16) uint8_t s_b[kSmallTile + 32];
+    __shared__ __align__(16) uint8_t s_o[kSmallTile + 32];
     __shared__ uint32_t s_cnt[kK0Threads / 32];
     __shared__ uint32_t s_mk[kK0Threads / 32];
     __shared__ uint32_t s_excl_cnt, s_excl_mk, s_tile_cnt, s_tile_mk, s_excl_rc;
@@ -198,7 +476,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     const ImgDesc& D = P.img[k];
     const uint64_t raw_len = D.raw_len;
     const uint64_t a = D.raw_off, e = a + raw_len;  // the image's bytes [a, e) in the raw buffer
-    const uint64_t win0 = (a & ~15ull) + uint64_t(lt) * kK0Tile;
+    const uint64_t win0 = (a & ~15ull) + uint64_t(lt) * kSmallTile;
     const uint64_t g_first = max(win0, a);            // first image byte in this window
     // restart intervals (extension): RSTn markers inside the scan are removed
     // like stuffed zeros and their unstuffed positions recorded; without them a
@@ -211,14 +489,14 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
         if (g < e) v = __ldcs(reinterpret_cast<const int4*>(P.raw + g));
         reinterpret_cast<int4*>(s_b + 16)[tid] = v;
         if (tid == 0) s_b[15] = win0 > a ? P.raw[win0 - 1] : 0;
-        if (tid == 1) s_b[16 + kK0Tile] = win0 + kK0Tile < e ? P.raw[win0 + kK0Tile] : 0;
+        if (tid == 1) s_b[16 + kSmallTile] = win0 + kSmallTile < e ? P.raw[win0 + kSmallTile] : 0;
     }
     __syncthreads();
 
     // this thread's 16 bytes (raw bytes win0 + b0 + i), classified branch-free
     // with SWAR byte compares into 16-bit masks (bit i = byte i): a divergent
     // per-byte loop would cost every warp that holds a single 0xFF byte
-    const uint32_t b0 = tid * kK0BytesPerThread;
+    const uint32_t b0 = tid * 16;
     const uint64_t gb = win0 + b0;
     uint32_t inr = 0xFFFFu;  // bytes inside the image [a, e)
     if (gb < a) inr &= a - gb >= 16 ? 0u : (0xFFFFu << uint32_t(a - gb)) & 0xFFFFu;
@@ -354,7 +632,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
         const uint4 w = reinterpret_cast<const uint4*>(s_b + 16)[tid];
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int i = 0; i < kK0BytesPerThread; ++i)
+        for (int i = 0; i < 16; ++i)
             if ((keep >> i) & 1u) o[i - __popc(remv & ((1u << i) - 1u))] = uint8_t(ws[i >> 2] >> (8 * (i & 3)));
     }
     // rare events, off the branch-free path: the scan end and restart markers
@@ -392,7 +670,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
     }
     __syncthreads();
     {
-        const uint64_t dst_hi = dst_lo + (min64(e, win0 + kK0Tile) - g_first) - s_tile_cnt;
+        const uint64_t dst_hi = dst_lo + (min64(e, win0 + kSmallTile) - g_first) - s_tile_cnt;
         const uint32_t nchunks = uint32_t((dst_hi - dst_al + 15) >> 4);
         for (uint32_t q = tid; q < nchunks; q += kK0Threads) {
             const uint64_t G = dst_al + 16ull * q;
@@ -405,7 +683,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
         }
     }
     // no marker anywhere: the scan runs to the end of the file
-    const uint32_t last_tile = uint32_t(((a & 15ull) + raw_len + kK0Tile - 1) / kK0Tile) - 1;
+    const uint32_t last_tile = uint32_t(((a & 15ull) + raw_len + kSmallTile - 1) / kSmallTile) - 1;
     if (tid == 0 && lt == last_tile && s_excl_mk == kInf32 && s_tile_mk == kInf32) {
         uint64_t U = raw_len - (s_excl_cnt + s_tile_cnt);
         ImgState* st = P.ist + k;
@@ -2133,10 +2411,25 @@ void launch_k5_color(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, uin
 // ------------------------------------------------------------ launchers --
 void launch_k0_unstuff(const Params& p, void* stream) {
     if (!p.k0_tiles) return;
-    if (p.n_dri)
-        k0_unstuff<true><<<p.k0_tiles, kK0Threads, 0, (cudaStream_t)stream>>>(p);
-    else
-        k0_unstuff<false><<<p.k0_tiles, kK0Threads, 0, (cudaStream_t)stream>>>(p);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k0_unstuff<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (kK0Threads * 64 + 32));
+        cudaFuncSetAttribute(k0_unstuff<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (kK0Threads * 64 + 32));
+        attr = true;
+    }
+    const int dyn = 2 * (kK0Threads * int(p.k0_bpt) + 32);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p.k0_bpt == 64) {
+        if (p.n_dri)
+            k0_unstuff<true, 64><<<p.k0_tiles, kK0Threads, dyn, s>>>(p);
+        else
+            k0_unstuff<false, 64><<<p.k0_tiles, kK0Threads, dyn, s>>>(p);
+    } else {
+        if (p.n_dri)
+            k0_unstuff_small<true><<<p.k0_tiles, kK0Threads, 0, s>>>(p);
+        else
+            k0_unstuff_small<false><<<p.k0_tiles, kK0Threads, 0, s>>>(p);
+    }
 }
 void launch_k0b_segments(const Params& p, void* stream) {
     if (p.n_dri) k0b_segments<<<p.n_dri, 256, 0, (cudaStream_t)stream>>>(p);

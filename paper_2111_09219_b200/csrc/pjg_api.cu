@@ -366,7 +366,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     // raw extent: contiguous user region or pack
     const uint8_t* lo = nullptr;
     const uint8_t* hi = nullptr;
-    uint64_t raw_sum = 0;
+    uint64_t raw_sum = 0, n_ok = 0;
     for (size_t i = 0; i < n; ++i) {
         Header& h = b->hdr[i];
         fill_info(h, cfg->output, sizes[i], &b->info[i]);
@@ -380,7 +380,11 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         if (!lo || s < lo) lo = s;
         if (!hi || s + rl > hi) hi = s + rl;
         raw_sum += rl;
+        ++n_ok;
     }
+    // K0 tile size: 32 KB windows when the scans are large on average, else 8 KB
+    const uint32_t k0_bpt = (n_ok && raw_sum / n_ok >= 48 * 1024) ? kK0BigBpt : kK0SmallBpt;
+    const uint64_t k0_tile = uint64_t(kK0Threads) * k0_bpt;
     b->packed = !(lo && uint64_t(hi - lo) <= raw_sum + raw_sum / 2 + (1u << 20));
     uint64_t pack_off = 0;
     std::vector<std::pair<const uint8_t*, size_t>> pk_src;
@@ -435,7 +439,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
             d.q_tab[c] = uint16_t(quant_id(h.quant[h.comps[c].tq]));
         }
         // K0 tiles always run (scan checks precede table errors)
-        k0t += uint32_t(((d.raw_off & 15) + rl + kK0Tile - 1) / kK0Tile);  // 16-byte-grid windows
+        k0t += uint32_t(((d.raw_off & 15) + rl + k0_tile - 1) / k0_tile);  // 16-byte-grid windows
         d.n_int = 1;
         if (h.table_status != kOk) continue;
         d.sub_count = (uint64_t(rl) * 8 + sb - 1) / sb;
@@ -593,6 +597,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.dri_img = reinterpret_cast<const uint32_t*>(md + b->m_dri);
     p.n_dri = uint32_t(dri.size());
     p.k0_tiles = k0t;
+    p.k0_bpt = k0_bpt;
     p.k1_ctas = b->k1_ctas;
     p.sb = sb;
     p.sub_first = reinterpret_cast<const uint64_t*>(md + b->m_sub);

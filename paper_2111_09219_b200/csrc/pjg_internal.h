@@ -147,8 +147,7 @@ struct DcSums {
 // ------------------------------------------------------------- params --
 constexpr int kSubImgShift = 7;
 constexpr int kK0Threads = 512;
-constexpr int kK0BytesPerThread = 16;
-constexpr int kK0Tile = kK0Threads * kK0BytesPerThread;  // 4096 raw bytes per tile
+constexpr uint32_t kK0BigBpt = 64, kK0SmallBpt = 16;  // bytes per K0 thread: 32 KB or 8 KB tiles
 constexpr int kK1Threads = 128;                          // subsequences per K1 CTA
 constexpr int kK2Threads = 256;
 constexpr int kK3Threads = 128;
@@ -181,6 +180,7 @@ struct Params {
     uint32_t n_dri;
     uint32_t k0_tiles;
     uint32_t k1_ctas;
+    uint32_t k0_bpt;               // K0 bytes per thread (tile = 512 x this)
     // subsequences
     uint64_t sb;                   // subsequence_bits
     const uint64_t* sub_first;     // n_img + 1 prefix

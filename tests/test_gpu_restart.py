@@ -96,3 +96,12 @@ def test_restart_corrupt_markers(decoder):
         st = b.run()
     assert st[0] != 0 and st[1] != 0 and st[2] != 0, st
     assert st[3] == 0
+
+
+def test_restart_large_single_image(decoder):
+    """A single large DRI scan (K0's 32 KB-tile path, many intervals)."""
+    plain, dri = _twins(1536, 1024, 95, "444", 13, 21)
+    with decoder.batch([dri], DRI, pj.OutputColorspace.RGBInterleaved) as b:
+        assert b.run()[0] == 0
+        got = _rgb(b.download()[0], b.infos[0])
+    assert np.array_equal(got, Ref.decode(plain, rgb=True).data)
