@@ -748,6 +748,17 @@ __global__ void __launch_bounds__(256) k0b_segments(Params P) {
     }
 }
 
+// Copies the batch's fast tables into shared memory (P.smem_tables tables,
+// dynamic shared memory) and returns them, or nullptr when not enabled.
+__device__ __forceinline__ const uint32_t* stage_tables(const Params& P, uint32_t* s_fast, int tid, int nthreads) {
+    if (!P.smem_tables) return nullptr;
+    for (uint32_t x = tid; x < P.smem_tables * (kFastWords / 4); x += nthreads) {
+        const uint32_t t = x / (kFastWords / 4), q = x % (kFastWords / 4);
+        reinterpret_cast<uint4*>(s_fast)[x] = __ldg(reinterpret_cast<const uint4*>(P.huff[t].fast) + q);
+    }
+    return s_fast;  // the caller's __syncthreads (stage_scan) publishes it
+}
+
 // ============================================== entropy decode (shared) ====
 constexpr uint32_t kHuffWords = sizeof(DevHuff) / 4;  // fast[] sits at word 0 of each table
 
@@ -755,21 +766,32 @@ struct ImgCtx {
     const uint32_t* words;  // ubuf as 32-bit words (or the CTA's shared-memory stage)
     uint64_t bit_base;      // 8 * raw_off
     uint64_t L;             // bit_length
-    const uint32_t* fast;   // all tables as words: table t's fast[] at t * kHuffWords
+    const uint32_t* fast;   // fast[] of table t at t * stride (the global DevHuff array, or smem copies)
+    const DevHuff* huff;    // the tables (exact path)
     uint32_t tdc[3], tac[3];  // fast-table word offsets per component
     uint32_t duc;           // slot -> component, 2 bits per slot
     uint32_t dpm;
 };
+template <bool ST>
+struct TabStride {
+    static constexpr uint32_t value = ST ? kFastWords : kHuffWords;
+};
 
-__device__ __forceinline__ void load_ctx(const Params& P, const ImgDesc& D, uint64_t L, ImgCtx& c) {
+// sfast: the batch's fast tables staged in shared memory (nullptr: global).
+// Small batches have few resident CTAs per SM, so each symbol's table probe
+// would otherwise often miss L1 on the decoder's serial dependency chain.
+template <bool ST = false>
+__device__ __forceinline__ void load_ctx(const Params& P, const ImgDesc& D, uint64_t L, ImgCtx& c,
+                                         const uint32_t* sfast = nullptr) {
     c.words = reinterpret_cast<const uint32_t*>(P.ubuf);
     c.bit_base = D.raw_off * 8;
     c.L = L;
-    c.fast = reinterpret_cast<const uint32_t*>(P.huff);
+    c.huff = P.huff;
+    c.fast = ST ? sfast : reinterpret_cast<const uint32_t*>(P.huff);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        c.tdc[k] = uint32_t(D.dc_tab[k]) * kHuffWords;
-        c.tac[k] = uint32_t(D.ac_tab[k]) * kHuffWords;
+        c.tdc[k] = uint32_t(D.dc_tab[k]) * TabStride<ST>::value;
+        c.tac[k] = uint32_t(D.ac_tab[k]) * TabStride<ST>::value;
     }
     uint32_t duc = 0;
     for (uint32_t s = 0; s < D.dpm; ++s) duc |= (uint32_t(D.du_comp >> (4 * s)) & 3u) << (2 * s);
@@ -879,7 +901,7 @@ struct NullSink {
 // length, total length, magnitude size, run and kind (jfif.cpp build_fast).
 // Windows the probe cannot settle (long codes, invalid prefixes, the last 32
 // bits of the scan) take the reference's exact path with its error order.
-template <class Sink>
+template <class Sink, bool ST = false>
 __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint64_t end_bit, uint32_t cap,
                                              Sink& sink) {
     s.n = 0;
@@ -921,7 +943,8 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
                 cnt += need ? 32 : 0;
             }
             const uint32_t hi = uint32_t(acc >> 32);
-            const uint32_t fe = __ldg(ic.fast + (z ? tac : tdc) + (hi >> (32 - kFastBits)));
+            const uint32_t fi = (z ? tac : tdc) + (hi >> (32 - kFastBits));
+            const uint32_t fe = ST ? ic.fast[fi] : __ldg(ic.fast + fi);
             uint32_t len, step, coefk;
             int32_t coef;
             if ((fe & 31u) != 0 && lrem >= 32) {
@@ -934,7 +957,8 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
                 step = (fe & kFastEOB) ? 64u - z : ((fe >> 14) & 63u) + 1u;
                 coefk = fe & kFastCoef;
             } else {
-                const DevHuff* t = reinterpret_cast<const DevHuff*>(ic.fast + (z ? tac : tdc));
+                const DevHuff* t = ST ? ic.huff + (z ? tac : tdc) / TabStride<ST>::value
+                                      : reinterpret_cast<const DevHuff*>(ic.fast + (z ? tac : tdc));
                 uint32_t maxlen;
                 const uint32_t e = dev_lookup(t, hi >> 16, maxlen);
                 const uint32_t clen = e >> 8, sym = e & 255u;
@@ -1040,6 +1064,7 @@ __device__ __forceinline__ DcSums pack_dc(int32_t a0, int32_t a1, int32_t a2) {
 }
 
 // Sync-mode decode from (p, c, z) of the symbols starting before end_bit.
+template <bool ST = false>
 __device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t end_bit, uint64_t p, uint32_t c, uint32_t z,
                                             Entry& e, DcSums& d) {
     DecState s;
@@ -1048,7 +1073,7 @@ __device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t end_bit, 
     s.z = z;
     s.dc0 = s.dc1 = s.dc2 = 0;
     NullSink sink;
-    decode_range(ic, s, end_bit, 0, sink);
+    decode_range<NullSink, ST>(ic, s, end_bit, 0, sink);
     e.p = s.p;
     e.n = s.n;
     e.czd = pack_czd(s.c, s.z, s.div);
@@ -1059,7 +1084,7 @@ __device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t end_bit, 
 // Thread t of logical CTA j owns global subsequence g = j*T + t.  Images are
 // flattened into one subsequence space; a CTA may hold the tail of one image
 // and the head of the next, and overflow chains stop at image ends.
-template <bool DRI>
+template <bool DRI, bool ST>
 __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     constexpr int T = kK1Threads;
     __shared__ uint64_t s_p[T];
@@ -1081,8 +1106,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     const bool ok = P.ist[k].status == 0;
     SubInfo si;
     const bool real = inb && ok && sub_info<DRI>(P, D, L, i, si);
+    extern __shared__ uint32_t s_fast_k1[];
     ImgCtx ic;
-    load_ctx(P, D, L, ic);
+    load_ctx<ST>(P, D, L, ic, ST ? stage_tables(P, s_fast_k1, tid, T) : nullptr);
     {
         __shared__ int4 s_stage[kStageBytes / 16];
         __shared__ StageSmem s_sm;
@@ -1096,7 +1122,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     e.p = real ? si.lo : 0;
     e.n = 0;
     e.czd = 0;
-    if (real) sync_decode(ic, si.hi, si.lo, 0, 0, e, d);
+    if (real) sync_decode<ST>(ic, si.hi, si.lo, 0, 0, e, d);
     s_p[tid] = e.p;
     s_n[tid] = e.n;
     s_czd[tid] = e.czd;
@@ -1114,7 +1140,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
         if (active) {
             Entry e2;
             DcSums d2;
-            sync_decode(ic, seg_end_bit(si, P.sb, nxt), chain.p, czd_c(chain.czd), czd_z(chain.czd), e2, d2);
+            sync_decode<ST>(ic, seg_end_bit(si, P.sb, nxt), chain.p, czd_c(chain.czd), czd_z(chain.czd), e2, d2);
             bool synced = sync_equal(e2.p, e2.czd, s_p[nt], s_czd[nt]);
             s_p[nt] = e2.p;
             s_n[nt] = e2.n;  // the overflow's n is authoritative (:211)
@@ -1165,7 +1191,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
                 for (int tt = 0; tt < T && ii < si.seg_sub1; ++tt, ++ii) {
                     Entry e2;
                     DcSums d2;
-                    sync_decode(ic, seg_end_bit(si, P.sb, ii), ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
+                    sync_decode<ST>(ic, seg_end_bit(si, P.sb, ii), ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
                     ++hops;
                     bool synced = sync_equal(e2.p, e2.czd, s_p[tt], s_czd[tt]);
                     s_p[tt] = e2.p;
@@ -1535,6 +1561,7 @@ struct BlockSink {
     }
 };
 
+template <bool ST>
 __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     __shared__ __align__(16) int16_t s_blk[kK3Threads * kBlkStride];
     __shared__ uint32_t s_zt[64];
@@ -1562,8 +1589,9 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     const uint64_t L = P.ist[k].bit_length;
     SubInfo si;
     const bool active = inb && cap != 0 && P.ist[k].status == 0 && sub_info(P, D, L, i, si);
+    extern __shared__ uint32_t s_fast_k3[];
     ImgCtx ic;
-    load_ctx(P, D, L, ic);
+    load_ctx<ST>(P, D, L, ic, ST ? stage_tables(P, s_fast_k3, tid, kK3Threads) : nullptr);
     {
         __shared__ int4 s_stage[kStageBytes / 16];
         __shared__ StageSmem s_sm;
@@ -1606,7 +1634,7 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     sink.mflags = 0;
     sink.mS = 0.f;
     sink.set_comp(uint32_t(D.du_comp >> (4 * ((o >> 6) % D.dpm))) & 15u);
-    decode_range(ic, s, si.hi, cap, sink);
+    decode_range<BlockSink, ST>(ic, s, si.hi, cap, sink);
     if (s.err) {
         set_status(P.ist + k, s.err);  // write mode rethrows (parallel_decode.hpp:142)
         return;
@@ -2436,10 +2464,25 @@ void launch_k0b_segments(const Params& p, void* stream) {
 }
 void launch_k1_sync(const Params& p, void* stream) {
     if (!p.k1_ctas) return;
-    if (p.n_dri)
-        k1_sync<true><<<p.k1_ctas, kK1Threads, 0, (cudaStream_t)stream>>>(p);
-    else
-        k1_sync<false><<<p.k1_ctas, kK1Threads, 0, (cudaStream_t)stream>>>(p);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k1_sync<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemTables * kFastWords * 4);
+        cudaFuncSetAttribute(k1_sync<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemTables * kFastWords * 4);
+        attr = true;
+    }
+    const size_t dyn = size_t(p.smem_tables) * kFastWords * 4;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p.smem_tables) {
+        if (p.n_dri)
+            k1_sync<true, true><<<p.k1_ctas, kK1Threads, dyn, s>>>(p);
+        else
+            k1_sync<false, true><<<p.k1_ctas, kK1Threads, dyn, s>>>(p);
+    } else {
+        if (p.n_dri)
+            k1_sync<true, false><<<p.k1_ctas, kK1Threads, 0, s>>>(p);
+        else
+            k1_sync<false, false><<<p.k1_ctas, kK1Threads, 0, s>>>(p);
+    }
 }
 void launch_k1c_fixup(const Params& p, void* stream) {
     if (p.k1_ctas > 1) k1c_fixup<<<1, 1024, 0, (cudaStream_t)stream>>>(p);
@@ -2448,9 +2491,17 @@ void launch_k2_scan(const Params& p, void* stream) {
     if (p.k2_tiles) k2_scan<<<p.k2_tiles, kK2Threads, 0, (cudaStream_t)stream>>>(p);
 }
 void launch_k3_write(const Params& p, void* stream) {
-    if (p.total_subs)
-        k3_write<<<unsigned((p.total_subs + kK3Threads - 1) / kK3Threads), kK3Threads, 0,
-                   (cudaStream_t)stream>>>(p);
+    if (!p.total_subs) return;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k3_write<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemTables * kFastWords * 4);
+        attr = true;
+    }
+    const unsigned grid = unsigned((p.total_subs + kK3Threads - 1) / kK3Threads);
+    if (p.smem_tables)
+        k3_write<true><<<grid, kK3Threads, size_t(p.smem_tables) * kFastWords * 4, (cudaStream_t)stream>>>(p);
+    else
+        k3_write<false><<<grid, kK3Threads, 0, (cudaStream_t)stream>>>(p);
 }
 void launch_k4_transform(const Params& p, void* stream) {
     if (!p.k4_tiles) return;

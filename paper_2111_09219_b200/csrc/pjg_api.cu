@@ -598,6 +598,10 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.n_dri = uint32_t(dri.size());
     p.k0_tiles = k0t;
     p.k0_bpt = k0_bpt;
+    // small batches (under ~4 K1 CTAs per SM): the decoders' table probes sit on a
+    // serial dependency chain with few warps to hide an L1 miss — stage the
+    // tables in shared memory
+    p.smem_tables = (b->n_huff <= kMaxSmemTables && sub < uint64_t(kK1Threads) * 148 * 4) ? b->n_huff : 0;
     p.k1_ctas = b->k1_ctas;
     p.sb = sb;
     p.sub_first = reinterpret_cast<const uint64_t*>(md + b->m_sub);

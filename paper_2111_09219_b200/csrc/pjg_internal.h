@@ -41,6 +41,7 @@ enum Status : int32_t {
 constexpr int kPrimaryBits = 9;
 
 constexpr int kFastBits = 11;
+constexpr uint32_t kFastWords = 1u << kFastBits;
 // fast entry for a kFastBits window whose codeword fits and decodes to a
 // symbol the reference accepts: bits 0-4 codeword length (0 = take the exact
 // path), 5-9 code + magnitude length, 10-13 magnitude bits l, 14-19 run,
@@ -146,6 +147,7 @@ struct DcSums {
 
 // ------------------------------------------------------------- params --
 constexpr int kSubImgShift = 7;
+constexpr uint32_t kMaxSmemTables = 4;  // fast tables K1/K3 stage in shared memory (8 KB each)
 constexpr int kK0Threads = 512;
 constexpr uint32_t kK0BigBpt = 64, kK0SmallBpt = 16;  // bytes per K0 thread: 32 KB or 8 KB tiles
 constexpr int kK1Threads = 128;                          // subsequences per K1 CTA
@@ -181,6 +183,7 @@ struct Params {
     uint32_t k0_tiles;
     uint32_t k1_ctas;
     uint32_t k0_bpt;               // K0 bytes per thread (tile = 512 x this)
+    uint32_t smem_tables;          // K1/K3 stage this many fast tables in shared memory (0: read global)
     // subsequences
     uint64_t sb;                   // subsequence_bits
     const uint64_t* sub_first;     // n_img + 1 prefix
