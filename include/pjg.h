@@ -143,6 +143,10 @@ int pjg_batch_download_all_async(pjg_batch* b, void* host, size_t cap);
 uint64_t pjg_batch_output_offset(const pjg_batch* b, size_t i);
 int pjg_batch_info(const pjg_batch* b, size_t i, pjg_image_info* info);
 const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i);
+/* Device-to-device copy of every decoded image i with dst[i] != NULL into
+ * caller device buffers (e.g. torch CUDA tensors), ordered on the context's
+ * stream after the decode; no host round trip. */
+int pjg_batch_copy_outputs(pjg_batch* b, void* const* dst, const size_t* caps);
 uint64_t pjg_batch_output_bytes(const pjg_batch* b);
 int pjg_batch_stage_times(const pjg_batch* b, double* ms /* PJG_NUM_STAGES */);
 /* Decode diagnostics: intra rounds (sum, max), inter-CTA hops, fix-up passes,

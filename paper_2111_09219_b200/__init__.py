@@ -25,6 +25,7 @@ __all__ = [
     "Errc", "Error", "DecodeConfig", "OutputColorspace", "ImagePlanes", "Plane", "RgbImage",
     "StageTimings", "DecodeSuccess", "DecodeFailure", "decode_single", "decode_batch",
     "upsample_and_convert", "planes_checksum", "Decoder", "Batch", "lib", "LIB_PATH",
+    "decode_to_tensors",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -191,6 +192,7 @@ def lib():
             L.pjg_batch_output_offset.restype = C.c_uint64
             L.pjg_batch_info.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(_Info)]
             L.pjg_batch_device_output.argtypes = [C.c_void_p, C.c_size_t]
+            L.pjg_batch_copy_outputs.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]
             L.pjg_batch_output_bytes.argtypes = [C.c_void_p]
             L.pjg_batch_stage_times.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
             L.pjg_batch_sync_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
@@ -215,7 +217,7 @@ EXPORTED_SYMBOLS = [
     "pjg_ctx_create", "pjg_ctx_destroy", "pjg_last_error", "pjg_status_name", "pjg_default_config",
     "pjg_ctx_stream", "pjg_inspect", "pjg_decode", "pjg_decode_batch", "pjg_batch_create",
     "pjg_batch_upload", "pjg_batch_decode", "pjg_batch_synchronize", "pjg_batch_download",
-    "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_download_all", "pjg_batch_download_all_async", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
+    "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_copy_outputs", "pjg_batch_download_all", "pjg_batch_download_all_async", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
     "pjg_batch_sync_stats", "pjg_batch_destroy", "pjg_batch_dump_coefficients",
     "pjg_batch_dump_sync_states", "pjg_batch_dump_segment", "pjg_upsample_and_convert",
     "pjg_debug_huff_decode",
@@ -332,6 +334,7 @@ class Batch:
     def synchronize(self) -> np.ndarray:
         out = np.zeros(self.n, np.int32)
         self._check(lib().pjg_batch_synchronize(self._h, out.ctypes.data_as(C.c_void_p)))
+        self.status = out
         return out
 
     def run(self) -> np.ndarray:
@@ -342,6 +345,37 @@ class Batch:
 
     def device_output(self, i) -> int:
         return int(lib().pjg_batch_device_output(self._h, i) or 0)
+
+    def tensors(self):
+        """The decoded images as CUDA uint8 torch tensors on the decoder's device
+        ((H, W, 3) RGB, (H, W) gray, flat planes otherwise), filled by
+        device-to-device copies ordered after the decode; torch's current
+        stream waits for them.  Failed images get None."""
+        import torch
+        dev = torch.device("cuda", self.dec.device)
+        outs, ptrs, caps = [], [], []
+        for i, inf in enumerate(self.infos):
+            nb = int(inf.output_bytes)
+            if (getattr(self, "status", None) is not None and self.status[i] != 0) or nb == 0:
+                outs.append(None)
+                ptrs.append(None)
+                caps.append(0)
+                continue
+            if self.output == int(OutputColorspace.RGBInterleaved) and inf.channels == 3:
+                t = torch.empty((inf.height, inf.width, 3), dtype=torch.uint8, device=dev)
+            elif inf.channels == 1 and self.output != int(OutputColorspace.YCbCrPlanes):
+                t = torch.empty((inf.height, inf.width), dtype=torch.uint8, device=dev)
+            else:
+                t = torch.empty((nb,), dtype=torch.uint8, device=dev)
+            outs.append(t)
+            ptrs.append(t.data_ptr())
+            caps.append(t.numel())
+        arr = (C.c_void_p * self.n)(*ptrs)
+        carr = (C.c_size_t * self.n)(*caps)
+        self._check(lib().pjg_batch_copy_outputs(self._h, arr, carr))
+        ext = torch.cuda.ExternalStream(self.dec.stream(), device=dev)
+        torch.cuda.current_stream(dev).wait_stream(ext)
+        return outs
 
     def download(self, outs=None):
         """D2H into numpy buffers (allocated if not given); returns the list."""
@@ -482,6 +516,24 @@ def decode_batch(files, config: DecodeConfig | None = None):
             else:
                 res.append(_success(b, i, outs[i], OutputColorspace.YCbCrPlanes))
         return res
+
+
+def decode_to_tensors(files, device: int = 0, config: DecodeConfig | None = None,
+                      output=OutputColorspace.RGBInterleaved, decoder: "Decoder | None" = None):
+    """Decodes a batch straight into CUDA uint8 torch tensors on `device`
+    (RGB: (H, W, 3)); per-file statuses (0 = ok, else Errc + 1) alongside.
+    No host copy of any pixel."""
+    own = decoder is None
+    dec = decoder or Decoder(device)
+    try:
+        with dec.batch(files, config or DecodeConfig(), output) as b:
+            st = b.run()
+            return b.tensors(), st
+    finally:
+        if own:
+            import torch
+            torch.cuda.synchronize(dec.device)
+            dec.close()
 
 
 def decode_rgb(file_bytes, config: DecodeConfig | None = None) -> RgbImage:

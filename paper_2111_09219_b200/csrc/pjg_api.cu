@@ -789,6 +789,23 @@ const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i) {
 
 uint64_t pjg_batch_output_bytes(const pjg_batch* b) { return b ? b->out_bytes : 0; }
 
+int pjg_batch_copy_outputs(pjg_batch* b, void* const* dst, const size_t* caps) {
+    if (!b || !dst || !caps) return PJG_INVALID_ARGUMENT;
+    pjg_ctx* ctx = b->ctx;
+    if (!b->decoded) return fail(ctx, PJG_NOT_DECODED, "batch not decoded");
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    for (size_t i = 0; i < b->n; ++i) {
+        if (!dst[i]) continue;
+        const uint64_t nb = b->info[i].output_bytes;
+        if (caps[i] < nb) return fail(ctx, PJG_CAPACITY, "device output buffer too small");
+        if (b->host_status[i] != 0 || nb == 0) continue;
+        CU(cudaMemcpyAsync(dst[i], ctx->out.as<uint8_t>() + b->desc[i].out_off, nb, cudaMemcpyDeviceToDevice,
+                           ctx->stream),
+           "D2D output");
+    }
+    return PJG_OK;
+}
+
 int pjg_batch_stage_times(const pjg_batch* b, double* ms) {
     if (!b || !ms) return PJG_INVALID_ARGUMENT;
     for (int k = 0; k < PJG_NUM_STAGES; ++k) ms[k] = b->stage_ms[k];

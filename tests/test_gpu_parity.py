@@ -238,3 +238,18 @@ def test_cpp_dropin_binary_matches_reference(tmp_path):
     r = subprocess.run([exe, str(f)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert ("IDENTICAL" in r.stdout) or ("ref:" not in r.stdout)
+
+
+def test_decode_to_cuda_tensors():
+    """CUDA uint8 torch tensors straight from the device output (D2D copies on
+    the decoder's stream), equal to the reference; failed files give None."""
+    import torch
+    files = [ref_jpeg(96, 64, 31, 80, "420"), ref_jpeg(40, 24, 32, 90, "gray"), b"\xde\xad\xbe\xef",
+             ref_jpeg(33, 17, 33, 70, "444")]
+    ts, st = pj.decode_to_tensors(files, device=0)
+    assert list(st[[0, 1, 3]]) == [0, 0, 0] and st[2] != 0 and ts[2] is None
+    for t, f in ((ts[0], files[0]), (ts[1], files[1]), (ts[3], files[3])):
+        assert t.is_cuda and t.dtype == torch.uint8
+        ref = Ref.decode(f, rgb=True).data
+        assert tuple(t.shape) == ref.shape
+        assert np.array_equal(t.cpu().numpy(), ref)
