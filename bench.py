@@ -227,10 +227,15 @@ def main():
     import torch
     import paper_2111_09219_b200 as pj
 
+    # PJG_BENCH_ONE_DEVICE=1: every rank on cuda:0 with gloo plumbing — exercises
+    # the N > 1 path (barrier, max-over-ranks, rank-0 line) on a one-GPU box
+    one_dev = os.environ.get("PJG_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     from paper_2111_09219_b200 import dist as pdist
-    dist = pdist.init("nccl", local) if world > 1 else None
-    dev = torch.device("cuda", local)
+    dist = pdist.init("gloo" if one_dev else "nccl", local) if world > 1 else None
+    dev = torch.device("cpu") if one_dev else torch.device("cuda", local)  # reduction tensors
 
     n, w, h, q, s, _ = CONFIGS[args.config]
     pinned_t, blob, offs, sizes = make_corpus(args.config, rank)
@@ -270,28 +275,75 @@ def main():
         b.synchronize()
         return e0.elapsed_time(e1), b.stage_times()
 
+    # (a) one stream: per-stage CUDA-event times for the rooflines
     for _ in range(args.warmup):
         one_step()
+    torch.cuda.synchronize()
+    single_ms, stages = [], []
+    for _ in range(args.steps):
+        ms, stt = one_step()
+        single_ms.append(ms)
+        stages.append(stt)
+    torch.cuda.synchronize()
+    sync_stats = b.sync_stats()
+    st_mean = {k: float(np.mean([getattr(x, k) for x in stages])) for k in
+               ("unstuff", "sync", "scan", "write", "idct")}
+    if n >= 2:
+        b.close()
+
+    # (b) the step as deployed: the batch as two concurrent half-batches on two
+    # contexts (streams), so one half's latency-bound Huffman kernels overlap the
+    # other half's bandwidth-bound transform; timed from one event to the join
+    dec2 = pj.Decoder(local)
+    halves = []
+    if n >= 2:
+        h = n // 2
+        for lo, hi, d in ((0, h, dec), (h, n, dec2)):
+            bb = d.batch((blob, offs[lo:hi], sizes[lo:hi]), cfg, out_kind)
+            bb.upload()
+            assert (bb.decode().synchronize() == 0).all()
+            halves.append(bb)
+    stream2 = torch.cuda.ExternalStream(dec2.stream(), device=torch.device("cuda", local))
+
+    def two_stream_step():
+        with torch.cuda.stream(stream):
+            flush_buf.zero_()  # untimed L2 flush
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            j = torch.cuda.Event()
+            e0.record(stream)
+        stream2.wait_event(e0)
+        halves[0].decode()
+        halves[1].decode()
+        j.record(stream2)
+        stream.wait_event(j)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        halves[0].synchronize()
+        halves[1].synchronize()
+        return e0.elapsed_time(e1)
+
+    step_fn = two_stream_step if halves else (lambda: one_step()[0])
+    for _ in range(args.warmup):
+        step_fn()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     clk.start()
-    step_ms, stages = [], []
-    for _ in range(args.steps):
-        ms, stt = one_step()
-        step_ms.append(ms)
-        stages.append(stt)
+    step_ms = [step_fn() for _ in range(args.steps)]
     torch.cuda.synchronize()
     clocks = clk.stop()
-    sync_stats = b.sync_stats()
+    for bb in halves:
+        bb.close()
+    if not halves:
+        b.close()
     tot_ms = pdist.max_over_ranks(float(np.sum(step_ms)), dev)
     ms_per_step = tot_ms / args.steps
     value = world * rgb_bytes / (ms_per_step / 1e3) / 1e9
     img_s = world * n / (ms_per_step / 1e3)
-    st_mean = {k: float(np.mean([getattr(x, k) for x in stages])) for k in
-               ("unstuff", "sync", "scan", "write", "idct")}
-    b.close()
+    single_tot = pdist.max_over_ranks(float(np.sum(single_ms)), dev)
+    single_value = world * rgb_bytes / (single_tot / args.steps / 1e3) / 1e9
 
     # ---------------- end-to-end through the C-ABI with host buffers ------
     host_out = torch.empty(rgb_bytes + n * 256 + 4096, dtype=torch.uint8).pin_memory()
@@ -299,7 +351,7 @@ def main():
     e2e_ms = []
     h2d = d2h = 0
 
-    decs = [dec, pj.Decoder(local)]
+    decs = [dec, dec2]
 
     def e2e_step():
         # the public API a host caller uses: pinned JPEG bytes in, pinned RGB
@@ -366,7 +418,9 @@ def main():
             "config": {"workload": CONFIG_NAMES[args.config], "images_per_gpu": n, "width": w, "height": h,
                        "quality": q, "sampling": s, "subsequence_bits": args.sb,
                        "compressed_bytes_per_gpu": comp_bytes, "rgb_bytes_per_gpu": rgb_bytes,
-                       "l2": "flushed between steps (256 MB write, untimed)"},
+                       "l2": "flushed between steps (256 MB write, untimed)",
+                       "streams": 2 if halves else 1},
+            "single_stream_value": round(single_value, 3),
             "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_tot / args.steps, 3),
                     "path": "decode_to_host_pipelined: per chunk pjg_batch_create+upload+decode+download_all_async "
