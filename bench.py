@@ -286,6 +286,7 @@ def main():
         stages.append(stt)
     torch.cuda.synchronize()
     sync_stats = b.sync_stats()
+    scan_bits = b.scan_bits()
     st_mean = {k: float(np.mean([getattr(x, k) for x in stages])) for k in
                ("unstuff", "sync", "scan", "write", "idct")}
     if n >= 2:
@@ -434,6 +435,12 @@ def main():
             "stages_ms": {k: round(v, 4) for k, v in st_mean.items()},
             "dominant_stage": dominant,
             "sync": sync_stats,
+            # Huffman stages (not roofline stages): bits of entropy-coded data
+            # decoded per second (K1 decodes each bit >= twice: round 0 + overflow)
+            "huffman": {"scan_bits_per_gpu": scan_bits,
+                        "k1_sync_gbit_s": round(scan_bits / (st_mean["sync"] / 1e3) / 1e9, 1),
+                        "k3_write_gbit_s": round(scan_bits / (st_mean["write"] / 1e3) / 1e9, 1),
+                        "intra_rounds_per_cta": round(sync_stats["intra_rounds_sum"] / max(1, -(-scan_bits // (args.sb * 128))), 2)},
             "compressed_mb_per_s": round(world * comp_bytes / (ms_per_step / 1e3) / 1e6, 1),
             "gpu_launches": 6 * args.steps,
             "clocks": clocks,

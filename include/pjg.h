@@ -143,6 +143,9 @@ int pjg_batch_download_all_async(pjg_batch* b, void* host, size_t cap);
 uint64_t pjg_batch_output_offset(const pjg_batch* b, size_t i);
 int pjg_batch_info(const pjg_batch* b, size_t i, pjg_image_info* info);
 const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i);
+/* Unstuffed entropy-coded bits of the decoded images (after synchronize):
+ * the Huffman stages' work, for bits-decoded/s figures. */
+uint64_t pjg_batch_scan_bits(const pjg_batch* b);
 /* Device-to-device copy of every decoded image i with dst[i] != NULL into
  * caller device buffers (e.g. torch CUDA tensors), ordered on the context's
  * stream after the decode; no host round trip. */

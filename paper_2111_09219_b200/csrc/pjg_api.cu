@@ -789,6 +789,15 @@ const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i) {
 
 uint64_t pjg_batch_output_bytes(const pjg_batch* b) { return b ? b->out_bytes : 0; }
 
+uint64_t pjg_batch_scan_bits(const pjg_batch* b) {
+    if (!b || !b->synced) return 0;
+    uint64_t bits = 0;
+    for (size_t i = 0; i < b->n; ++i)
+        if (b->host_status[i] == 0 && i < b->dev_state.size() && b->dev_state[i].status == 0)
+            bits += b->dev_state[i].bit_length;
+    return bits;
+}
+
 int pjg_batch_copy_outputs(pjg_batch* b, void* const* dst, const size_t* caps) {
     if (!b || !dst || !caps) return PJG_INVALID_ARGUMENT;
     pjg_ctx* ctx = b->ctx;
