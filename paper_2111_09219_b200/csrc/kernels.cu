@@ -1522,12 +1522,17 @@ struct BlockSink {
     __device__ __forceinline__ void flush(uint32_t khi) {
         int16_t* dst = coef + du * 64;
         uint2* md = meta + du;
+        // only the columns holding a nonzero coefficient (mflags bits 0-7) are
+        // read back and re-zeroed: the rest of the staging block is zero
+        const uint32_t cm = mflags & 0xFFu;
         if (klo == 0 && khi == 64) {
             // full-sector 256-bit stores (STG.E.ENL2.256): no partial-sector merges in L2
             const int4* s4 = reinterpret_cast<const int4*>(buf);
+            const int4 z4 = make_int4(0, 0, 0, 0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const int4 a = s4[2 * q], c = s4[2 * q + 1];
+                const int4 a = (cm >> (2 * q)) & 1u ? s4[2 * q] : z4;
+                const int4 c = (cm >> (2 * q + 1)) & 1u ? s4[2 * q + 1] : z4;
                 asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 16 * q), "r"(a.x),
                              "r"(a.y), "r"(a.z), "r"(a.w), "r"(c.x), "r"(c.y), "r"(c.z), "r"(c.w)
                              : "memory");
@@ -1543,7 +1548,8 @@ struct BlockSink {
         }
         const int4 zero = make_int4(0, 0, 0, 0);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(buf)[q] = zero;
+        for (int q = 0; q < 8; ++q)
+            if ((cm >> q) & 1u) reinterpret_cast<int4*>(buf)[q] = zero;
         mflags = 0;
         mS = 0.f;
         klo = 0;
