@@ -1683,6 +1683,9 @@ constexpr int kK4Warps = kK4Threads / 32;
 constexpr int kTileW = 64;  // pixels per tile row
 constexpr int kGroups = kTileW / 4;  // 4-pixel items per tile row
 constexpr int kFS = 68;     // floats per unit in the F tile
+// raw staging row of (unit, column v): rows XOR-swizzled so that reading the
+// same column of different units hits different bank groups
+__device__ __forceinline__ uint32_t raw_row(uint32_t blk, uint32_t v) { return blk * 8 + (v ^ (blk & 7u)); }
 
 __device__ __forceinline__ uint32_t pack4_sat(int a0, int a1, int a2, int a3) {
     uint32_t t, d;
@@ -2075,7 +2078,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
             for (int j = 0; j < kK4MaxBlocks / 4; ++j) {
                 const uint32_t ch = lane + 32 * j;
                 if (ch < nblk * 8)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.raw[ch])), "l"(src + ch)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.raw[raw_row(ch >> 3, ch & 7)])), "l"(src + ch)
                                  : "memory");
             }
             if (uint32_t(lane) < nblk)
@@ -2163,7 +2166,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 const uint32_t e = S.dq[it], a = e >> 3, v = e & 7u;
                 const uint32_t blk = S.acl[a];
                 float4* dst = reinterpret_cast<float4*>(S.F + a * kFS + v * 8);
-                const int4 rvi = S.raw[blk * 8 + v];
+                const int4 rvi = S.raw[raw_row(blk, v)];
                 const uint32_t rw[4] = {uint32_t(rvi.x), uint32_t(rvi.y), uint32_t(rvi.z), uint32_t(rvi.w)};
                 const uint32_t comp = I.bcomp[blk];
                 if (!(S.cm[a] & 0x100u)) {
@@ -2199,7 +2202,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
 #pragma unroll 1
             for (uint32_t it = lane; it < ndc * 8; it += 32) {
                 const uint32_t blk = S.dcl[it >> 3], x = it & 7;
-                const int32_t F00 = int32_t(int16_t(uint32_t(S.raw[blk * 8].x) & 0xFFFFu)) * int32_t(I.qf[I.bcomp[blk]][0]);
+                const int32_t F00 = int32_t(int16_t(uint32_t(S.raw[raw_row(blk, 0)].x) & 0xFFFFu)) * int32_t(I.qf[I.bcomp[blk]][0]);
                 int o;
                 if ((F00 & 7) != 4)
                     o = (F00 + 4) >> 3;
