@@ -29,7 +29,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpjg.so")
+LIB_PATH = os.environ.get("PJG_LIB") or os.path.join(HERE, "libpjg.so")  # PJG_LIB: A/B experiments
 
 
 class Errc(enum.IntEnum):
