@@ -32,6 +32,7 @@ public:
         return r;
     }
     bool eof() const { return pos_ >= n_; }
+    const uint8_t* ptr() const { return b_ + pos_; }
     size_t pos() const { return pos_; }
 
 private:
@@ -74,10 +75,10 @@ void parse_dht(Reader& r, uint16_t len, Header& h) {
         }
         if (total > 256) throw Fail{kMalformedHeader, "more than 256 huffman symbols"};
         Reader syms = s.take(total);
-        sp.symbols.resize(total);
-        for (size_t i = 0; i < total; ++i) sp.symbols[i] = syms.u8();
+        sp.symbols.p = syms.ptr();
+        sp.symbols.n = uint32_t(total);
         sp.present = true;
-        (cls ? h.ac : h.dc)[id] = std::move(sp);
+        (cls ? h.ac : h.dc)[id] = sp;
     }
 }
 

@@ -14,9 +14,36 @@
 
 namespace pjg {
 
+// Fixed-capacity vector: headers are parsed for every file of a batch (tens of
+// thousands for thumbnail batches), so they must not touch the allocator.
+template <class T, size_t N>
+struct SmallVec {
+    T v[N];
+    uint32_t n = 0;
+    size_t size() const { return n; }
+    bool empty() const { return n == 0; }
+    void push_back(const T& x) { v[n++] = x; }
+    T& operator[](size_t i) { return v[i]; }
+    const T& operator[](size_t i) const { return v[i]; }
+    T* begin() { return v; }
+    T* end() { return v + n; }
+    const T* begin() const { return v; }
+    const T* end() const { return v + n; }
+};
+
+// Symbols of a DHT table: a view into the file bytes (valid while the batch
+// is being planned).
+struct SymSpan {
+    const uint8_t* p = nullptr;
+    uint32_t n = 0;
+    size_t size() const { return n; }
+    const uint8_t& operator[](size_t i) const { return p[i]; }
+    const uint8_t* data() const { return p; }
+};
+
 struct HuffSpec {
     std::array<uint8_t, 16> counts{};
-    std::vector<uint8_t> symbols;
+    SymSpan symbols;
     bool present = false;
 };
 
@@ -28,9 +55,9 @@ struct Header {
     int32_t status = kOk;
     std::string message;
     uint32_t width = 0, height = 0;
-    std::vector<Component> comps;
+    SmallVec<Component, 3> comps;
     uint32_t h_max = 1, v_max = 1, mcus_x = 0, mcus_y = 0, dpm = 0;
-    std::vector<uint8_t> du_seq;
+    SmallVec<uint8_t, 16> du_seq;
     std::array<std::array<uint16_t, 64>, 4> quant{};
     std::array<bool, 4> quant_present{};
     std::array<HuffSpec, 4> dc, ac;

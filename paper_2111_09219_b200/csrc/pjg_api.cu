@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -91,17 +92,22 @@ struct pjg_ctx {
     cudaEvent_t ev[kNumEvents] = {};
     DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out, segs,
         counters, k0_flag, k0_agg, k2_flag, k2_agg, stats;
-    HostBuf stage, meta_host, status_host;
+    HostBuf stage, meta_host, status_host, desc_host;
+    // Per-image host arrays, lent to the live batch and taken back at destroy:
+    // thumbnail batches hold tens of thousands of images, and fresh vectors
+    // would be mmap'd and page-faulted again on every batch.
+    struct Scratch {
+        std::vector<int32_t> host_status;
+        std::vector<pjg_image_info> info;
+        std::vector<ImgState> dev_state;
+    } pool;
 };
 
 struct pjg_batch {
     pjg_ctx* ctx = nullptr;
     pjg_config cfg{};
     size_t n = 0;
-    std::vector<const uint8_t*> files;
-    std::vector<size_t> sizes;
-    std::vector<Header> hdr;
-    std::vector<ImgDesc> desc;
+    const ImgDesc* desc = nullptr;  // n descriptors in ctx->desc_host
     std::vector<int32_t> host_status;
     std::vector<pjg_image_info> info;
     // raw layout
@@ -117,6 +123,11 @@ struct pjg_batch {
     Params prm{};
     bool uploaded = false, decoded = false, synced = false;
     std::vector<ImgState> dev_state;  // fetched at synchronize
+    void swap_pool(pjg_ctx::Scratch& p) {
+        host_status.swap(p.host_status);
+        info.swap(p.info);
+        dev_state.swap(p.dev_state);
+    }
     double stage_ms[PJG_NUM_STAGES] = {};
     unsigned long long stats[kNumStats] = {};
 };
@@ -264,6 +275,7 @@ void pjg_ctx_destroy(pjg_ctx* c) {
         b->release();
     c->stage.release();
     c->meta_host.release();
+    c->desc_host.release();
     c->status_host.release();
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
@@ -293,178 +305,248 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     b->ctx = ctx;
     b->cfg = *cfg;
     b->n = n;
-    b->files.assign(files, files + n);
-    b->sizes.assign(sizes, sizes + n);
-    b->hdr.resize(n);
-    b->desc.resize(n);
-    b->host_status.assign(n, 0);
+    // PJG_HOST_TIMING=1: per-phase planning times on stderr (diagnostics)
+    static const bool timing = getenv("PJG_HOST_TIMING") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!timing) return;
+        auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "pjg_batch_create %-10s %8.3f ms\n", what,
+                std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
+    b->swap_pool(ctx->pool);
+    b->dev_state.clear();
+    b->host_status.resize(n);
     b->info.resize(n);
+    // descriptors are written straight into their pinned upload buffer
+    CU(ctx->desc_host.ensure(n * sizeof(ImgDesc) + 16), "cudaMallocHost(desc)");
+    ImgDesc* const desc = static_cast<ImgDesc*>(ctx->desc_host.p);
+    b->desc = desc;
+    mark("arrays");
 
-    // ---- host header parse (parallel for large batches)
-    {
-        unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        auto body = [&](size_t lo, size_t step) {
-            for (size_t i = lo; i < n; i += step)
-                b->hdr[i] = parse_header(files[i], sizes[i], cfg->restart_intervals != 0);
+    // ---- phase A (parallel, contiguous image chunks): header parse, geometry,
+    // per-image descriptor fields, table dedup against a per-worker unique list
+    struct Worker {
+        std::vector<HuffSpec> huff;  // unique specs, first-occurrence order
+        std::vector<uint8_t> huff_dc;
+        std::vector<std::array<uint16_t, 64>> quant;
+        const uint8_t* lo = nullptr;
+        const uint8_t* hi = nullptr;
+        uint64_t raw_sum = 0, n_ok = 0;
+    };
+    auto same_spec = [](const HuffSpec& a, const HuffSpec& c) {
+        return a.counts == c.counts && a.symbols.size() == c.symbols.size() &&
+               std::memcmp(a.symbols.data(), c.symbols.data(), a.symbols.size()) == 0;
+    };
+    const bool allow_dri = cfg->restart_intervals != 0;
+    const uint64_t sb = cfg->subsequence_bits;
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const unsigned nw = (n >= 1024 && hw > 1) ? hw : 1;
+    const size_t chunk = (n + nw - 1) / nw;
+    std::vector<Worker> wk(nw);
+    auto phase_a = [&](unsigned w) {
+        Worker& W = wk[w];
+        auto local_huff = [&](const HuffSpec& s, bool dc) -> uint16_t {
+            for (size_t u = 0; u < W.huff.size(); ++u)
+                if (W.huff_dc[u] == dc && same_spec(W.huff[u], s)) return uint16_t(u);
+            W.huff.push_back(s);
+            W.huff_dc.push_back(dc);
+            return uint16_t(W.huff.size() - 1);
         };
-        if (n >= 256 && hw > 1) {
-            std::vector<std::thread> th;
-            for (unsigned w = 0; w < hw; ++w) th.emplace_back(body, w, hw);
-            for (auto& t : th) t.join();
-        } else {
-            body(0, 1);
+        auto local_quant = [&](const std::array<uint16_t, 64>& q) -> uint16_t {
+            for (size_t u = 0; u < W.quant.size(); ++u)
+                if (std::memcmp(W.quant[u].data(), q.data(), 128) == 0) return uint16_t(u);
+            W.quant.push_back(q);
+            return uint16_t(W.quant.size() - 1);
+        };
+        const size_t i1 = std::min(n, (w + 1) * chunk);
+        for (size_t i = w * chunk; i < i1; ++i) {
+            Header h = parse_header(files[i], sizes[i], allow_dri);
+            fill_info(h, cfg->output, sizes[i], &b->info[i]);
+            ImgDesc& d = desc[i];
+            std::memset(&d, 0, sizeof(d));
+            d.out_mode = cfg->output;
+            d.n_int = 1;
+            // extract_scan of nothing → unstuff throws EmptyScan
+            if (h.status == kOk && sizes[i] == h.scan_start) h.status = kEmptyScan;
+            b->host_status[i] = h.status;
+            if (h.status != kOk) continue;
+            const size_t rl = sizes[i] - h.scan_start;
+            const uint8_t* s = files[i] + h.scan_start;
+            if (!W.lo || s < W.lo) W.lo = s;
+            if (!W.hi || s + rl > W.hi) W.hi = s + rl;
+            W.raw_sum += rl;
+            ++W.n_ok;
+            d.raw_off = uint64_t(reinterpret_cast<uintptr_t>(s));  // absolute until phase B
+            d.raw_len = rl;
+            d.deferred = h.table_status;
+            d.width = h.width;
+            d.height = h.height;
+            d.mcus_x = h.mcus_x;
+            d.mcus_y = h.mcus_y;
+            d.ncomp = uint32_t(h.comps.size());
+            d.dpm = h.dpm;
+            d.h_max = h.h_max;
+            d.v_max = h.v_max;
+            uint32_t seen[4] = {0, 0, 0, 0};
+            for (uint32_t k = 0; k < h.dpm; ++k) {
+                uint32_t c = h.du_seq[k];
+                d.du_comp |= uint64_t(c) << (4 * k);
+                d.du_kslot |= uint64_t(seen[c]++) << (4 * k);
+            }
+            for (size_t c = 0; c < h.comps.size(); ++c) {
+                d.comp_h[c] = h.comps[c].h;
+                d.comp_v[c] = h.comps[c].v;
+                d.plane_w[c] = h.comp_width(c);
+                d.plane_h[c] = h.comp_height(c);
+                if (h.table_status == kOk) {
+                    d.dc_tab[c] = local_huff(h.dc[h.comps[c].td], true);
+                    d.ac_tab[c] = local_huff(h.ac[h.comps[c].ta], false);
+                }
+                d.q_tab[c] = local_quant(h.quant[h.comps[c].tq]);
+            }
+            if (h.table_status != kOk) continue;
+            d.sub_count = (uint64_t(rl) * 8 + sb - 1) / sb;
+            if (h.restart_interval && h.intervals() > 1) {
+                d.n_int = uint32_t(h.intervals());  // checked and finished in phase B
+                d.ri = h.restart_interval;
+            }
+            d.expected = h.total_dus() * 64;
+            d.mcus_per_tile = uint16_t(64 / (8 * h.h_max));  // 64-pixel-wide warp tiles (<= 24 data units)
+            d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
         }
+    };
+    if (nw > 1) {
+        std::vector<std::thread> th;
+        for (unsigned w = 0; w < nw; ++w) th.emplace_back(phase_a, w);
+        for (auto& t : th) t.join();
+    } else {
+        phase_a(0);
     }
-    // ---- tables: dedupe by content
-    // tables dedupe by content: batches almost always share a handful, so a
-    // linear memcmp scan over the unique ones beats any map
+    mark("parse");
+
+    // ---- tables: merge the workers' unique lists (batches almost always share
+    // a handful, so a linear memcmp scan over the unique ones beats any map)
     std::vector<DevHuff> huffs;
     std::vector<std::array<uint16_t, 64>> quants;
     std::vector<std::pair<const HuffSpec*, bool>> huff_src;  // unique specs (first occurrence)
-    std::vector<std::array<uint16_t, 64>> quant_src;
+    std::vector<const std::array<uint16_t, 64>*> quant_src;
     std::vector<float> wqs;  // per quant table: 64 K3 metadata weights (zig-zag order)
-    auto same_spec = [](const HuffSpec& a, const HuffSpec& b) {
-        return a.counts == b.counts && a.symbols.size() == b.symbols.size() &&
-               std::memcmp(a.symbols.data(), b.symbols.data(), a.symbols.size()) == 0;
-    };
-    auto huff_id = [&](const HuffSpec& s, bool dc) -> uint32_t {
-        for (size_t u = 0; u < huff_src.size(); ++u)
-            if (huff_src[u].second == dc && same_spec(*huff_src[u].first, s)) return uint32_t(u);
-        DevHuff d;
-        build_dev_huff(s, &d);
-        build_fast(&d, dc);
-        huffs.push_back(d);
-        huff_src.emplace_back(&s, dc);
-        return uint32_t(huffs.size() - 1);
-    };
     static const uint8_t kZz2R[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24, 32, 25, 18, 11, 4,  5,
                                       12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
                                       35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
                                       58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
-    auto quant_id = [&](const std::array<uint16_t, 64>& q) -> uint32_t {
-        for (size_t u = 0; u < quant_src.size(); ++u)
-            if (std::memcmp(quant_src[u].data(), q.data(), 128) == 0) return uint32_t(u);
-        std::array<uint16_t, 64> r{};
-        // column-major (index v*8 + u for raster u*8 + v), the coefficient buffer's order
-        for (int z = 0; z < 64; ++z) r[(kZz2R[z] & 7) * 8 + (kZz2R[z] >> 3)] = q[z];
-        quants.push_back(r);
-        quant_src.push_back(q);
-        // K3 metadata weights: w_u w_v Q per zig-zag position, w_u >= max_x |basis[u][x]|
-        static const double kW[8] = {0.35356, 0.4904, 0.46195, 0.4904, 0.35356, 0.4904, 0.46195, 0.4904};
-        for (int z = 0; z < 64; ++z)
-            wqs.push_back(float(kW[kZz2R[z] >> 3] * kW[kZz2R[z] & 7] * double(q[z]) * (1.0 + 1e-6)));
-        return uint32_t(quants.size() - 1);
-    };
+    std::vector<std::vector<uint16_t>> huff_map(nw), quant_map(nw);
+    for (unsigned w = 0; w < nw; ++w) {
+        const Worker& W = wk[w];
+        for (size_t u = 0; u < W.huff.size(); ++u) {
+            const HuffSpec& s = W.huff[u];
+            const bool dc = W.huff_dc[u] != 0;
+            size_t g = 0;
+            while (g < huff_src.size() && !(huff_src[g].second == dc && same_spec(*huff_src[g].first, s))) ++g;
+            if (g == huff_src.size()) {
+                DevHuff d;
+                build_dev_huff(s, &d);
+                build_fast(&d, dc);
+                huffs.push_back(d);
+                huff_src.emplace_back(&s, dc);
+            }
+            huff_map[w].push_back(uint16_t(g));
+        }
+        for (const auto& q : W.quant) {
+            size_t g = 0;
+            while (g < quant_src.size() && std::memcmp(quant_src[g]->data(), q.data(), 128) != 0) ++g;
+            if (g == quant_src.size()) {
+                std::array<uint16_t, 64> r{};
+                // column-major (index v*8 + u for raster u*8 + v), the coefficient buffer's order
+                for (int z = 0; z < 64; ++z) r[(kZz2R[z] & 7) * 8 + (kZz2R[z] >> 3)] = q[z];
+                quants.push_back(r);
+                quant_src.push_back(&q);
+                // K3 metadata weights: w_u w_v Q per zig-zag position, w_u >= max_x |basis[u][x]|
+                static const double kW[8] = {0.35356, 0.4904, 0.46195, 0.4904, 0.35356, 0.4904, 0.46195, 0.4904};
+                for (int z = 0; z < 64; ++z)
+                    wqs.push_back(float(kW[kZz2R[z] >> 3] * kW[kZz2R[z] & 7] * double(q[z]) * (1.0 + 1e-6)));
+            }
+            quant_map[w].push_back(uint16_t(g));
+        }
+    }
 
-    // ---- layout plan
-    const uint64_t sb = cfg->subsequence_bits;
+    // ---- phase B (serial prefix sums): raw placement, global table ids, layout
+    const uint8_t* lo = nullptr;
+    const uint8_t* hi = nullptr;
+    uint64_t raw_sum = 0, n_ok = 0;
+    for (const Worker& W : wk) {
+        if (W.lo && (!lo || W.lo < lo)) lo = W.lo;
+        if (W.hi && (!hi || W.hi > hi)) hi = W.hi;
+        raw_sum += W.raw_sum;
+        n_ok += W.n_ok;
+    }
+    // K0 tile size: 32 KB windows when the scans are large on average, else 8 KB
+    const uint32_t k0_bpt = (n_ok && raw_sum / n_ok >= 48 * 1024) ? kK0BigBpt : kK0SmallBpt;
+    const uint64_t k0_tile = uint64_t(kK0Threads) * k0_bpt;
+    // raw extent: contiguous user region or pack
+    b->packed = !(lo && uint64_t(hi - lo) <= raw_sum + raw_sum / 2 + (1u << 20));
     uint64_t sub = 0, du = 0, outb = 0, seg_total = 0;
     std::vector<uint32_t> dri;  // images with restart intervals
     uint32_t k0t = 0, k4t = 0;
     std::vector<uint32_t> k0_first(n + 1), tile_first(n + 1);
     std::vector<uint64_t> sub_first(n + 1);
-    // raw extent: contiguous user region or pack
-    const uint8_t* lo = nullptr;
-    const uint8_t* hi = nullptr;
-    uint64_t raw_sum = 0, n_ok = 0;
-    for (size_t i = 0; i < n; ++i) {
-        Header& h = b->hdr[i];
-        fill_info(h, cfg->output, sizes[i], &b->info[i]);
-        if (h.status != kOk) continue;
-        size_t rl = sizes[i] - h.scan_start;
-        if (rl == 0) {  // extract_scan of nothing → unstuff throws EmptyScan
-            h.status = kEmptyScan;
-            continue;
-        }
-        const uint8_t* s = files[i] + h.scan_start;
-        if (!lo || s < lo) lo = s;
-        if (!hi || s + rl > hi) hi = s + rl;
-        raw_sum += rl;
-        ++n_ok;
-    }
-    // K0 tile size: 32 KB windows when the scans are large on average, else 8 KB
-    const uint32_t k0_bpt = (n_ok && raw_sum / n_ok >= 48 * 1024) ? kK0BigBpt : kK0SmallBpt;
-    const uint64_t k0_tile = uint64_t(kK0Threads) * k0_bpt;
-    b->packed = !(lo && uint64_t(hi - lo) <= raw_sum + raw_sum / 2 + (1u << 20));
     uint64_t pack_off = 0;
     std::vector<std::pair<const uint8_t*, size_t>> pk_src;
     std::vector<size_t> pk_dst;
     for (size_t i = 0; i < n; ++i) {
-        Header& h = b->hdr[i];
-        ImgDesc& d = b->desc[i];
-        std::memset(&d, 0, sizeof(d));
+        ImgDesc& d = desc[i];
         k0_first[i] = k0t;
         tile_first[i] = k4t;
         sub_first[i] = sub;
         d.sub_first = sub;
         d.du_first = du;
-        d.out_mode = cfg->output;
         d.out_off = outb;
-        b->host_status[i] = h.status;
-        if (h.status != kOk) continue;
-        const size_t rl = sizes[i] - h.scan_start;
+        if (b->host_status[i] != kOk) continue;
+        const size_t rl = d.raw_len;
+        const uint8_t* s = reinterpret_cast<const uint8_t*>(uintptr_t(d.raw_off));
         if (b->packed) {
             d.raw_off = pack_off;
-            pk_src.emplace_back(files[i] + h.scan_start, rl);
+            pk_src.emplace_back(s, rl);
             pk_dst.push_back(pack_off);
             pack_off = align_up(pack_off + rl, 16);
         } else {
-            d.raw_off = uint64_t(files[i] + h.scan_start - lo);
+            d.raw_off = uint64_t(s - lo);
         }
-        d.raw_len = rl;
-        d.deferred = h.table_status;
-        d.width = h.width;
-        d.height = h.height;
-        d.mcus_x = h.mcus_x;
-        d.mcus_y = h.mcus_y;
-        d.ncomp = uint32_t(h.comps.size());
-        d.dpm = h.dpm;
-        d.h_max = h.h_max;
-        d.v_max = h.v_max;
-        uint32_t seen[4] = {0, 0, 0, 0};
-        for (uint32_t s = 0; s < h.dpm; ++s) {
-            uint32_t c = h.du_seq[s];
-            d.du_comp |= uint64_t(c) << (4 * s);
-            d.du_kslot |= uint64_t(seen[c]++) << (4 * s);
-        }
-        for (size_t c = 0; c < h.comps.size(); ++c) {
-            d.comp_h[c] = h.comps[c].h;
-            d.comp_v[c] = h.comps[c].v;
-            d.plane_w[c] = h.comp_width(c);
-            d.plane_h[c] = h.comp_height(c);
-            if (h.table_status == kOk) {
-                d.dc_tab[c] = uint16_t(huff_id(h.dc[h.comps[c].td], true));
-                d.ac_tab[c] = uint16_t(huff_id(h.ac[h.comps[c].ta], false));
+        const unsigned w = unsigned(i / chunk);
+        for (uint32_t c = 0; c < d.ncomp; ++c) {
+            if (d.deferred == kOk) {
+                d.dc_tab[c] = huff_map[w][d.dc_tab[c]];
+                d.ac_tab[c] = huff_map[w][d.ac_tab[c]];
             }
-            d.q_tab[c] = uint16_t(quant_id(h.quant[h.comps[c].tq]));
+            d.q_tab[c] = quant_map[w][d.q_tab[c]];
         }
         // K0 tiles always run (scan checks precede table errors)
         k0t += uint32_t(((d.raw_off & 15) + rl + k0_tile - 1) / k0_tile);  // 16-byte-grid windows
-        d.n_int = 1;
-        if (h.table_status != kOk) continue;
-        d.sub_count = (uint64_t(rl) * 8 + sb - 1) / sb;
-        if (h.restart_interval && h.intervals() > 1) {
+        if (d.deferred != kOk) continue;
+        if (d.n_int > 1) {
             // restart intervals: one subsequence partition per interval (K0b), at
             // most ceil(bits / sb) + intervals subsequences; segment bit offsets are
             // 32-bit
             if (uint64_t(rl) * 8 >= (1ull << 32)) {
-                b->host_status[i] = h.status = kUnsupportedFeature;
+                b->host_status[i] = kUnsupportedFeature;
+                d.n_int = 1;
+                d.ri = 0;
+                d.expected = 0;
+                d.mcus_per_tile = 0;
+                d.tiles_x = 0;
                 continue;
             }
-            d.n_int = uint32_t(h.intervals());
-            d.ri = h.restart_interval;
             d.seg_first = seg_total;
             seg_total += d.n_int + 1;
             d.sub_count += d.n_int;
             dri.push_back(uint32_t(i));
         }
-        d.expected = h.total_dus() * 64;
-        d.mcus_per_tile = uint16_t(64 / (8 * h.h_max));  // 64-pixel-wide warp tiles (<= 24 data units)
-        d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
         sub += d.sub_count;
-        du += h.total_dus();
-        k4t += d.tiles_x * h.mcus_y;
-        outb = align_up(outb + out_bytes_for(h, cfg->output), 256);
+        du += d.expected / 64;
+        k4t += d.tiles_x * d.mcus_y;
+        outb = align_up(outb + b->info[i].output_bytes, 256);
     }
     k0_first[n] = k0t;
     tile_first[n] = k4t;
@@ -481,6 +563,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     b->out_bytes = outb;
     b->k1_ctas = uint32_t((sub + kK1Threads - 1) / kK1Threads);
     b->k2_tiles = uint32_t((sub + kK2Threads - 1) / kK2Threads);
+    mark("layout");
 
     // ---- raw bytes: user region or pinned staging
     if (b->packed) {
@@ -493,6 +576,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         b->raw_bytes = lo ? uint64_t(hi - lo) : 0;
     }
 
+    mark("raw");
     // ---- meta blob
     size_t o = 0;
     b->m_desc = o;
@@ -524,10 +608,10 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     b->m_total = o;
     CU(ctx->meta_host.ensure(o), "cudaMallocHost(meta)");
     uint8_t* mh = static_cast<uint8_t*>(ctx->meta_host.p);
-    std::memcpy(mh + b->m_desc, b->desc.data(), n * sizeof(ImgDesc));
+    // [m_desc, m_state) of the device blob comes from ctx->desc_host (see upload)
     for (size_t i = 0; i < n; ++i) {
         ImgState s{};
-        s.status = b->hdr[i].status;
+        s.status = b->host_status[i];
         std::memcpy(mh + b->m_state + i * sizeof(ImgState), &s, sizeof(s));
     }
     std::memcpy(mh + b->m_huff, huffs.data(), huffs.size() * sizeof(DevHuff));
@@ -552,6 +636,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         }
     }
 
+    mark("meta");
     // ---- device reservation
     CU(ctx->meta.ensure(o), "cudaMalloc(meta)");
     CU(ctx->raw.ensure(b->raw_bytes + 64), "cudaMalloc(raw)");
@@ -626,6 +711,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.k2_flag = ctx->k2_flag.as<uint32_t>();
     p.k2_agg = ctx->k2_agg.as<uint64_t>();
     p.stats = ctx->stats.as<unsigned long long>();
+    mark("reserve");
     p.debug = getenv("PJG_K4_DEBUG") ? uint32_t(atoi(getenv("PJG_K4_DEBUG"))) : 0u;
 
     ctx->busy = true;
@@ -641,7 +727,12 @@ int pjg_batch_upload(pjg_batch* b) {
     if (b->raw_bytes)
         CU(cudaMemcpyAsync(ctx->raw.p, b->raw_src, b->raw_bytes, cudaMemcpyHostToDevice, ctx->stream),
            "H2D raw");
-    CU(cudaMemcpyAsync(ctx->meta.p, ctx->meta_host.p, b->m_total, cudaMemcpyHostToDevice, ctx->stream),
+    if (b->m_state > b->m_desc)
+        CU(cudaMemcpyAsync(ctx->meta.as<uint8_t>() + b->m_desc, ctx->desc_host.p, b->n * sizeof(ImgDesc),
+                           cudaMemcpyHostToDevice, ctx->stream),
+           "H2D desc");
+    CU(cudaMemcpyAsync(ctx->meta.as<uint8_t>() + b->m_state, static_cast<uint8_t*>(ctx->meta_host.p) + b->m_state,
+                       b->m_total - b->m_state, cudaMemcpyHostToDevice, ctx->stream),
        "H2D meta");
     CU(cudaEventRecord(ctx->ev[1], ctx->stream), "cudaEventRecord");
     b->uploaded = true;
@@ -838,6 +929,7 @@ void pjg_batch_destroy(pjg_batch* b) {
         cudaSetDevice(b->ctx->device);
         cudaStreamSynchronize(b->ctx->stream);
         b->ctx->busy = false;
+        b->swap_pool(b->ctx->pool);
     }
     delete b;
 }
@@ -845,18 +937,19 @@ void pjg_batch_destroy(pjg_batch* b) {
 int pjg_batch_dump_coefficients(const pjg_batch* b, size_t i, int pre_dc_zigzag, int16_t* out, size_t count) {
     if (!b || i >= b->n || !out) return PJG_INVALID_ARGUMENT;
     pjg_ctx* ctx = b->ctx;
-    const Header& h = b->hdr[i];
-    uint64_t nco = h.total_dus() * 64;
+    const ImgDesc& d = b->desc[i];
+    const uint64_t dus = uint64_t(d.mcus_x) * d.mcus_y * d.dpm;
+    uint64_t nco = dus * 64;
     if (count < nco) return fail(ctx, PJG_CAPACITY, "coefficient buffer too small");
     if (b->host_status[i] != 0) return b->host_status[i];
     CU(cudaStreamSynchronize(ctx->stream), "sync");
     std::vector<int16_t> colmaj(nco), raster(nco);
-    CU(cudaMemcpy(colmaj.data(), ctx->coef.as<int16_t>() + b->desc[i].du_first * 64, nco * 2,
+    CU(cudaMemcpy(colmaj.data(), ctx->coef.as<int16_t>() + d.du_first * 64, nco * 2,
                   cudaMemcpyDeviceToHost),
        "D2H coef");
     // the device buffer holds each unit column-major (kernels.cu c_zz2c)
-    for (uint64_t d = 0; d < nco; d += 64)
-        for (int r = 0; r < 64; ++r) raster[d + r] = colmaj[d + (r & 7) * 8 + (r >> 3)];
+    for (uint64_t u = 0; u < nco; u += 64)
+        for (int r = 0; r < 64; ++r) raster[u + r] = colmaj[u + (r & 7) * 8 + (r >> 3)];
     if (!pre_dc_zigzag) {
         std::memcpy(out, raster.data(), nco * 2);
         return PJG_OK;
@@ -865,14 +958,13 @@ int pjg_batch_dump_coefficients(const pjg_batch* b, size_t i, int pre_dc_zigzag,
                                       12, 19, 26, 33, 40, 48, 41, 34, 27, 20, 13, 6,  7,  14, 21, 28,
                                       35, 42, 49, 56, 57, 50, 43, 36, 29, 22, 15, 23, 30, 37, 44, 51,
                                       58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
-    const uint64_t dus = h.total_dus();
     int32_t last[3] = {0, 0, 0};
     bool seen[3] = {false, false, false};
-    for (uint64_t d = 0; d < dus; ++d) {
-        const int16_t* r = raster.data() + d * 64;
-        int16_t* z = out + d * 64;
+    for (uint64_t u = 0; u < dus; ++u) {
+        const int16_t* r = raster.data() + u * 64;
+        int16_t* z = out + u * 64;
         for (int k = 0; k < 64; ++k) z[k] = r[kZz2R[k]];
-        unsigned comp = h.du_seq[d % h.dpm];
+        unsigned comp = unsigned(d.du_comp >> (4 * (u % d.dpm))) & 15;
         int32_t abs_dc = z[0];
         // inverse of dc_prefix_sum (transform.hpp:56-74), exact mod 2^16
         if (seen[comp]) z[0] = int16_t(uint16_t(abs_dc - last[comp]));
@@ -1006,7 +1098,8 @@ int pjg_debug_huff_decode(const uint8_t* counts16, const uint8_t* symbols, size_
                           size_t nwin, uint32_t* out) {
     HuffSpec s;
     std::memcpy(s.counts.data(), counts16, 16);
-    s.symbols.assign(symbols, symbols + nsym);
+    s.symbols.p = symbols;
+    s.symbols.n = uint32_t(nsym);
     s.present = true;
     DevHuff d;
     int32_t st = build_dev_huff(s, &d);
