@@ -325,6 +325,8 @@ def main():
         return e0.elapsed_time(e1)
 
     step_fn = two_stream_step if halves else (lambda: one_step()[0])
+    # our kernels per timed step (the library's own count of its launches)
+    launches_per_step = sum(x.kernel_launches() for x in halves) if halves else b.kernel_launches()
     for _ in range(args.warmup):
         step_fn()
     if dist:
@@ -440,9 +442,9 @@ def main():
             "huffman": {"scan_bits_per_gpu": scan_bits,
                         "k1_sync_gbit_s": round(scan_bits / (st_mean["sync"] / 1e3) / 1e9, 1),
                         "k3_write_gbit_s": round(scan_bits / (st_mean["write"] / 1e3) / 1e9, 1),
-                        "intra_rounds_per_cta": round(sync_stats["intra_rounds_sum"] / max(1, -(-scan_bits // (args.sb * 128))), 2)},
+                        "intra_rounds_per_cta": round(sync_stats["intra_rounds_sum"] / max(1, -(-scan_bits // (args.sb * 127))), 2)},
             "compressed_mb_per_s": round(world * comp_bytes / (ms_per_step / 1e3) / 1e6, 1),
-            "gpu_launches": 6 * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
             "cpu_baseline": cpu,
         }

@@ -146,6 +146,9 @@ const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i);
 /* Unstuffed entropy-coded bits of the decoded images (after synchronize):
  * the Huffman stages' work, for bits-decoded/s figures. */
 uint64_t pjg_batch_scan_bits(const pjg_batch* b);
+/* Kernel launches one pjg_batch_decode of this batch issues (the same launch
+ * conditions the decode applies), for launch-count accounting. */
+uint32_t pjg_batch_kernel_launches(const pjg_batch* b);
 /* Device-to-device copy of every decoded image i with dst[i] != NULL into
  * caller device buffers (e.g. torch CUDA tensors), ordered on the context's
  * stream after the decode; no host round trip. */

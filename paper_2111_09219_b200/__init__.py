@@ -195,6 +195,8 @@ def lib():
             L.pjg_batch_copy_outputs.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t)]
             L.pjg_batch_scan_bits.argtypes = [C.c_void_p]
             L.pjg_batch_scan_bits.restype = C.c_uint64
+            L.pjg_batch_kernel_launches.argtypes = [C.c_void_p]
+            L.pjg_batch_kernel_launches.restype = C.c_uint32
             L.pjg_batch_output_bytes.argtypes = [C.c_void_p]
             L.pjg_batch_stage_times.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
             L.pjg_batch_sync_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
@@ -219,7 +221,7 @@ EXPORTED_SYMBOLS = [
     "pjg_ctx_create", "pjg_ctx_destroy", "pjg_last_error", "pjg_status_name", "pjg_default_config",
     "pjg_ctx_stream", "pjg_inspect", "pjg_decode", "pjg_decode_batch", "pjg_batch_create",
     "pjg_batch_upload", "pjg_batch_decode", "pjg_batch_synchronize", "pjg_batch_download",
-    "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_copy_outputs", "pjg_batch_scan_bits", "pjg_batch_download_all", "pjg_batch_download_all_async", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
+    "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_copy_outputs", "pjg_batch_scan_bits", "pjg_batch_kernel_launches", "pjg_batch_download_all", "pjg_batch_download_all_async", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
     "pjg_batch_sync_stats", "pjg_batch_destroy", "pjg_batch_dump_coefficients",
     "pjg_batch_dump_sync_states", "pjg_batch_dump_segment", "pjg_upsample_and_convert",
     "pjg_debug_huff_decode",
@@ -345,6 +347,10 @@ class Batch:
     def scan_bits(self) -> int:
         """Unstuffed entropy-coded bits of the decoded images (after synchronize)."""
         return int(lib().pjg_batch_scan_bits(self._h))
+
+    def kernel_launches(self) -> int:
+        """Kernels one decode() of this batch launches."""
+        return int(lib().pjg_batch_kernel_launches(self._h))
 
     def output_bytes(self) -> int:
         return int(lib().pjg_batch_output_bytes(self._h))

@@ -859,6 +859,14 @@ __device__ __forceinline__ const uint32_t* stage_scan(const uint8_t* ubuf, uint6
         return reinterpret_cast<const uint32_t*>(s_stage + (sm.off[seg] >> 4)) - ((sm.lo[seg] & ~15ull) >> 2);
     return reinterpret_cast<const uint32_t*>(ubuf);
 }
+// The word pointer stage_scan returned for image k (after stage_scan).
+__device__ __forceinline__ const uint32_t* stage_words(const uint8_t* ubuf, const int4* s_stage, const StageSmem& sm,
+                                                       uint32_t k) {
+    const uint32_t seg = k - sm.k0;
+    if (seg < kStageSegs && sm.off[seg] != 0xFFFFFFFFu)
+        return reinterpret_cast<const uint32_t*>(s_stage + (sm.off[seg] >> 4)) - ((sm.lo[seg] & ~15ull) >> 2);
+    return reinterpret_cast<const uint32_t*>(ubuf);
+}
 
 
 // Device huff_lookup with read-only-path loads.
@@ -1081,25 +1089,56 @@ __device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t end_bit, 
 }
 
 // ======================================================== K1: sync pass ====
-// Thread t of logical CTA j owns global subsequence g = j*T + t.  Images are
-// flattened into one subsequence space; a CTA may hold the tail of one image
-// and the head of the next, and overflow chains stop at image ends.
-template <bool DRI, bool ST>
+// CTA j owns the kK1Own global subsequences [j*kK1Own, (j+1)*kK1Own); thread
+// t >= 1 owns subsequence j*kK1Own + t - 1.  Thread 0 re-decodes the
+// predecessor CTA's last subsequence from its origin (round 0 only) and its
+// overflow chain carries that speculative state into this CTA — the
+// inter-sequence overflow of sync_inter_sequence (parallel_decode.hpp:247-270)
+// started without waiting for the predecessor.  After the intra rounds the
+// speculative start is checked against the predecessor's published
+// post-intra last entry and re-chained only where they differ (a few % of
+// CTAs); K1c then re-runs every boundary whose start differs from the
+// predecessor's final entry (the reference's end_changed passes).  Images are flattened into one
+// subsequence space; a CTA may hold the tail of one image and the head of the
+// next, and overflow chains stop at image (and restart-interval) ends.
+//
+// Overflow rounds are lane-compacted: the live chains of a round are listed in
+// shared memory and taken by threads 0..n-1, so a round with few live chains
+// occupies one warp instead of every warp that holds one.  A chain into
+// subsequence t runs in t's image context (the same image: chains stop at
+// segment ends).
+struct K1Chain {
+    uint64_t p;
+    uint32_t czd;
+    uint32_t nt;
+};
+template <bool DRI, bool ST, bool HOP>
 __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     constexpr int T = kK1Threads;
+    constexpr int TO = kK1Own;
     __shared__ uint64_t s_p[T];
     __shared__ uint32_t s_n[T];
     __shared__ uint32_t s_czd[T];
     __shared__ DcSums s_dc[T];
+    __shared__ uint64_t s_hi[T];  // end bit of thread t's subsequence
+    __shared__ uint32_t s_km[T];  // image of thread t | 1 << 31 when a chain may continue past t
+    __shared__ K1Chain s_list[2][T];
+    __shared__ uint32_t s_cnt[2];
+    __shared__ int4 s_stage[kStageBytes / 16];
+    __shared__ StageSmem s_sm;
     __shared__ uint32_t s_cta;
 
     const int tid = threadIdx.x;
-    if (tid == 0) s_cta = atomicAdd(&P.counters[kTicketK1], 1u);
-    __syncthreads();
-    const uint32_t cta = s_cta;
-    const uint64_t g = uint64_t(cta) * T + tid;
-    const bool inb = g < P.total_subs;
-    const uint32_t k = find_img(P, inb ? g : P.total_subs - 1);
+    if (HOP) {
+        if (tid == 0) s_cta = atomicAdd(&P.counters[kTicketK1], 1u);
+        __syncthreads();
+    }
+    // ticket order (HOP): a predecessor is never waiting on this CTA
+    const uint32_t cta = HOP ? s_cta : blockIdx.x;
+    const int64_t gs = int64_t(cta) * TO + tid - 1;
+    const bool inb = gs >= 0 && uint64_t(gs) < P.total_subs;
+    const uint64_t g = inb ? uint64_t(gs) : (gs < 0 ? 0 : P.total_subs - 1);
+    const uint32_t k = find_img(P, g);
     const ImgDesc& D = P.img[k];
     const uint64_t i = g - P.sub_first[k];
     const uint64_t L = P.ist[k].bit_length;
@@ -1107,11 +1146,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     SubInfo si;
     const bool real = inb && ok && sub_info<DRI>(P, D, L, i, si);
     extern __shared__ uint32_t s_fast_k1[];
+    const uint32_t* sfast = ST ? stage_tables(P, s_fast_k1, tid, T) : nullptr;
     ImgCtx ic;
-    load_ctx<ST>(P, D, L, ic, ST ? stage_tables(P, s_fast_k1, tid, T) : nullptr);
+    load_ctx<ST>(P, D, L, ic, sfast);
+    if (tid < 2) s_cnt[tid] = 0;
     {
-        __shared__ int4 s_stage[kStageBytes / 16];
-        __shared__ StageSmem s_sm;
         const uint64_t lo = real ? D.raw_off + (si.lo >> 3) : 1, hi = real ? D.raw_off + ((si.hi + 7) >> 3) + 24 : 0;
         ic.words = stage_scan(P.ubuf, lo, hi, k, tid, T, s_stage, s_sm);
     }
@@ -1127,41 +1166,58 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     s_n[tid] = e.n;
     s_czd[tid] = e.czd;
     s_dc[tid] = d;
-    Entry chain = e;
-    uint64_t nxt = i + 1;
-    int nt = tid + 1;
-    bool active = real && !czd_div(e.czd) && nxt < si.seg_sub1 && nt < T;
+    s_hi[tid] = real ? si.hi : 0;
+    const bool more = real && i + 1 < si.seg_sub1 && tid + 1 < T;
+    s_km[tid] = k | (more ? 0x80000000u : 0u);
+    if (more && !czd_div(e.czd)) {
+        const uint32_t slot = atomicAdd(&s_cnt[0], 1u);
+        s_list[0][slot] = K1Chain{e.p, e.czd, uint32_t(tid + 1)};
+    }
+    __syncthreads();
     // Rounds k >= 1: overflow into the next subsequence until (p,c,z) agrees
-    // with the published entry (parallel_decode.hpp:197-220).  All active
-    // threads target distinct subsequences, so one barrier per round suffices.
-    int rounds = 0;
-    while (__syncthreads_or(active)) {
+    // with the published entry (parallel_decode.hpp:197-220).  Live chains
+    // target distinct subsequences, so one barrier per round orders them.
+    int rounds = 0, cur = 0;
+    uint32_t ick = k;
+    for (;;) {
+        const uint32_t nact = s_cnt[cur];
+        __syncthreads();  // everyone has read the count
+        if (tid == 0) s_cnt[cur] = 0;  // refilled two rounds later
+        if (nact == 0) break;
         ++rounds;
-        if (active) {
+        if (uint32_t(tid) < nact) {
+            const K1Chain ch = s_list[cur][tid];
+            const uint32_t nt = ch.nt;
+            const uint32_t km = s_km[nt];
+            const uint32_t kk = km & 0x7FFFFFFFu;
+            if (kk != ick) {  // chain of another image of this CTA
+                const ImgDesc& D2 = P.img[kk];
+                load_ctx<ST>(P, D2, P.ist[kk].bit_length, ic, sfast);
+                ic.words = stage_words(P.ubuf, s_stage, s_sm, kk);
+                ick = kk;
+            }
             Entry e2;
             DcSums d2;
-            sync_decode<ST>(ic, seg_end_bit(si, P.sb, nxt), chain.p, czd_c(chain.czd), czd_z(chain.czd), e2, d2);
-            bool synced = sync_equal(e2.p, e2.czd, s_p[nt], s_czd[nt]);
+            sync_decode<ST>(ic, s_hi[nt], ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
+            const bool synced = sync_equal(e2.p, e2.czd, s_p[nt], s_czd[nt]);
             s_p[nt] = e2.p;
             s_n[nt] = e2.n;  // the overflow's n is authoritative (:211)
             s_czd[nt] = e2.czd;
             s_dc[nt] = d2;
-            if (synced || czd_div(e2.czd)) {
-                active = false;
-            } else {
-                chain = e2;
-                ++nxt;
-                ++nt;
-                active = nxt < si.seg_sub1 && nt < T;
+            if (!synced && !czd_div(e2.czd) && (km >> 31)) {
+                const uint32_t slot = atomicAdd(&s_cnt[cur ^ 1], 1u);
+                s_list[cur ^ 1][slot] = K1Chain{e2.p, e2.czd, nt + 1};
             }
         }
+        __syncthreads();
+        cur ^= 1;
     }
     if (tid == 0) {
         atomicAdd(P.stats + kStatRoundsSum, (unsigned long long)rounds);
         atomicMax(P.stats + kStatRoundsMax, (unsigned long long)rounds);
     }
     // Publish this CTA's last entry (post-intra) for the successor CTA.
-    if (tid == T - 1) {
+    if (HOP && tid == T - 1) {
         Entry last;
         last.p = s_p[T - 1];
         last.n = s_n[T - 1];
@@ -1170,30 +1226,40 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
         __threadfence();
         st_release(P.k1_flag + cta, P.epoch);
     }
-    // Inter-CTA overflow (sync_inter_sequence, parallel_decode.hpp:247-270):
-    // thread 0 chains from the predecessor CTA's last entry into this CTA.
-    if (tid == 0) {
+    // Inter-CTA check: the speculative start (thread 0's round-0 entry) against
+    // the predecessor's published post-intra last entry; where they differ,
+    // the first owned thread re-chains from the published entry (in its own
+    // image context) until it meets an entry it agrees with.  K1c compares the
+    // start used with the predecessor's FINAL last entry.
+    if (tid == 1) {
         Entry start;
         start.p = 0;
         start.n = 0;
         start.czd = 0;
-        const bool boundary = real && si.j > 0;  // CTA starts mid-segment
-        if (boundary) {
+        if (!HOP && real && si.j > 0) {  // K1c's first pass checks the speculative start
+            start.p = s_p[0];
+            start.n = s_n[0];
+            start.czd = s_czd[0] | kBoundaryBit;
+        } else if (real && si.j > 0) {  // CTA starts mid-segment
             while (ld_acquire(P.k1_flag + cta - 1) != P.epoch) spin_pause();
             start.p = __ldcg(&P.cta_end[cta - 1].p);
-            uint64_t nc = __ldcg(reinterpret_cast<const unsigned long long*>(&P.cta_end[cta - 1]) + 1);
+            const uint64_t nc = __ldcg(reinterpret_cast<const unsigned long long*>(&P.cta_end[cta - 1]) + 1);
             start.n = uint32_t(nc);
             start.czd = uint32_t(nc >> 32);
-            if (!czd_div(start.czd)) {
+            if (!sync_equal(start.p, start.czd, s_p[0], s_czd[0]) && !czd_div(start.czd)) {
                 Entry ch = start;
                 uint64_t ii = i;
                 uint32_t hops = 0;
-                for (int tt = 0; tt < T && ii < si.seg_sub1; ++tt, ++ii) {
+                if (ick != k) {
+                    load_ctx<ST>(P, D, L, ic, sfast);
+                    ic.words = stage_words(P.ubuf, s_stage, s_sm, k);
+                }
+                for (int tt = 1; tt < T && ii < si.seg_sub1; ++tt, ++ii) {
                     Entry e2;
                     DcSums d2;
-                    sync_decode<ST>(ic, seg_end_bit(si, P.sb, ii), ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
+                    sync_decode<ST>(ic, s_hi[tt], ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
                     ++hops;
-                    bool synced = sync_equal(e2.p, e2.czd, s_p[tt], s_czd[tt]);
+                    const bool synced = sync_equal(e2.p, e2.czd, s_p[tt], s_czd[tt]);
                     s_p[tt] = e2.p;
                     s_n[tt] = e2.n;
                     s_czd[tt] = e2.czd;
@@ -1208,7 +1274,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
         P.cta_start[cta] = start;
     }
     __syncthreads();
-    if (inb) {
+    if (inb && tid >= 1) {
         Entry o;
         o.p = s_p[tid];
         o.n = s_n[tid];
@@ -1219,16 +1285,73 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
 }
 
 // ================================================ K1c: inter fix-up pass ====
-// Each CTA j>0 that starts mid-image overflowed from CTA j-1's post-intra end
-// state.  If CTA j-1's own inter overflow later changed that end state
-// (the chain ran through the whole CTA), CTA j must redo its overflow from
-// the final state — the reference's `end_changed` invalidation
-// (parallel_decode.hpp:272-276).  Passes repeat until no boundary is stale.
+// Each CTA j>0 that starts mid-segment chained from a speculative state (the
+// predecessor's last subsequence decoded from its origin).  Where that
+// differs from the predecessor's final entry, CTA j's overflow is redone from
+// the final state until it meets an entry it agrees with; a redo that runs
+// through the whole CTA changes CTA j's last entry and stales CTA j+1 — the
+// reference's `end_changed` invalidation (parallel_decode.hpp:272-276).
+
+// Redoes CTA cta's overflow from start state st (its predecessor's final
+// last entry) until it meets an entry it agrees with.
+__device__ __forceinline__ void k1c_redo(const Params& P, uint32_t cta, Entry st, unsigned long long& redone) {
+    constexpr int TO = kK1Own;
+    const uint64_t g0 = uint64_t(cta) * TO;
+    const uint32_t k = find_img(P, g0);
+    const ImgDesc& D = P.img[k];
+    const uint64_t L = P.ist[k].bit_length;
+    uint64_t i = g0 - P.sub_first[k];
+    if (czd_div(st.czd)) {
+        set_status(P.ist + k, kConsistencyFailure);
+        return;
+    }
+    SubInfo si;
+    if (!sub_info(P, D, L, i, si)) return;
+    ImgCtx ic;
+    load_ctx(P, D, L, ic);
+    Entry ch = st;
+    for (int tt = 0; tt < TO && i < si.seg_sub1 && g0 + tt < P.total_subs; ++tt, ++i) {
+        Entry e2;
+        DcSums d2;
+        sync_decode(ic, seg_end_bit(si, P.sb, i), ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
+        ++redone;
+        Entry old = P.ent[g0 + tt];
+        bool synced = sync_equal(e2.p, e2.czd, old.p, old.czd);
+        P.ent[g0 + tt] = e2;
+        P.dcs[g0 + tt] = d2;
+        if (synced || czd_div(e2.czd)) break;
+        ch = e2;
+    }
+}
+
+// First pass, one thread per CTA boundary (all stale boundaries in parallel):
+// CTA starts are speculative when K1 ran without the in-kernel check.  A
+// redo that runs through a whole CTA races with its successor's check; the
+// fix-point pass below catches that (it compares against the final entries).
+__global__ void __launch_bounds__(128) k1c_first(Params P) {
+    const uint32_t cta = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long redone = 0;
+    if (cta < P.k1_ctas) {
+        const Entry st = P.cta_start[cta];
+        if (st.czd & kBoundaryBit) {
+            Entry pe = P.ent[uint64_t(cta) * kK1Own - 1];
+            if (!sync_equal(st.p, st.czd, pe.p, pe.czd)) {
+                pe.czd |= kBoundaryBit;
+                P.cta_start[cta] = pe;
+                k1c_redo(P, cta, pe, redone);
+            }
+        }
+    }
+    if (redone) atomicAdd(P.stats + kStatInterHops, redone);
+}
+
+// Fix-point passes (one CTA): repeat until no boundary is stale.
 __global__ void __launch_bounds__(1024) k1c_fixup(Params P) {
-    constexpr int T = kK1Threads;
+    constexpr int TO = kK1Own;
     __shared__ int s_any;
     __shared__ int s_passes;
     if (threadIdx.x == 0) s_passes = 0;
+    unsigned long long redone = 0;
     for (uint32_t pass = 0; pass <= P.k1_ctas; ++pass) {
         if (threadIdx.x == 0) s_any = 0;
         __syncthreads();
@@ -1236,10 +1359,8 @@ __global__ void __launch_bounds__(1024) k1c_fixup(Params P) {
         for (uint32_t cta = 1 + threadIdx.x; cta < P.k1_ctas; cta += blockDim.x) {
             Entry st = P.cta_start[cta];
             if (!(st.czd & kBoundaryBit)) continue;
-            uint64_t g0 = uint64_t(cta) * T;
-            Entry pe = P.ent[g0 - 1];
-            bool stale = !sync_equal(st.p, st.czd, pe.p, pe.czd);
-            if (stale) {
+            Entry pe = P.ent[uint64_t(cta) * TO - 1];
+            if (!sync_equal(st.p, st.czd, pe.p, pe.czd)) {
                 // stash the new start; mark for this pass
                 pe.czd |= kBoundaryBit | 0x2000u;
                 P.cta_start[cta] = pe;
@@ -1254,35 +1375,12 @@ __global__ void __launch_bounds__(1024) k1c_fixup(Params P) {
             if (!(st.czd & 0x2000u)) continue;
             st.czd &= ~0x2000u;
             P.cta_start[cta] = st;
-            uint64_t g0 = uint64_t(cta) * T;
-            uint32_t k = find_img(P, g0);
-            const ImgDesc& D = P.img[k];
-            const uint64_t L = P.ist[k].bit_length;
-            uint64_t i = g0 - P.sub_first[k];
-            if (czd_div(st.czd)) {
-                set_status(P.ist + k, kConsistencyFailure);
-                continue;
-            }
-            SubInfo si;
-            if (!sub_info(P, D, L, i, si)) continue;
-            ImgCtx ic;
-            load_ctx(P, D, L, ic);
-            Entry ch = st;
-            for (int tt = 0; tt < T && i < si.seg_sub1; ++tt, ++i) {
-                Entry e2;
-                DcSums d2;
-                sync_decode(ic, seg_end_bit(si, P.sb, i), ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
-                Entry old = P.ent[g0 + tt];
-                bool synced = sync_equal(e2.p, e2.czd, old.p, old.czd);
-                P.ent[g0 + tt] = e2;
-                P.dcs[g0 + tt] = d2;
-                if (synced || czd_div(e2.czd)) break;
-                ch = e2;
-            }
+            k1c_redo(P, cta, st, redone);
         }
         __threadfence_block();
         __syncthreads();
     }
+    if (redone) atomicAdd(P.stats + kStatInterHops, redone);
     if (threadIdx.x == 0 && s_passes) atomicAdd(P.stats + kStatFixPasses, (unsigned long long)s_passes);
 }
 
@@ -2446,6 +2544,11 @@ void launch_k5_color(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, uin
 }
 
 // ------------------------------------------------------------ launchers --
+uint32_t kernel_launches(const Params& p) {
+    // mirrors the launch conditions of the launchers below
+    return (p.k0_tiles ? 1u : 0u) + (p.n_dri ? 1u : 0u) + (p.k1_ctas ? 1u : 0u) + (p.k1_ctas > 1 ? (p.k1_hop ? 1u : 2u) : 0u) +
+           (p.k2_tiles ? 1u : 0u) + (p.total_subs ? 1u : 0u) + (p.k4_tiles ? 1u : 0u);
+}
 void launch_k0_unstuff(const Params& p, void* stream) {
     if (!p.k0_tiles) return;
     static bool attr = false;
@@ -2471,30 +2574,43 @@ void launch_k0_unstuff(const Params& p, void* stream) {
 void launch_k0b_segments(const Params& p, void* stream) {
     if (p.n_dri) k0b_segments<<<p.n_dri, 256, 0, (cudaStream_t)stream>>>(p);
 }
-void launch_k1_sync(const Params& p, void* stream) {
-    if (!p.k1_ctas) return;
+template <bool DRI, bool ST, bool HOP>
+static void launch_k1_variant(const Params& p, size_t dyn, cudaStream_t s) {
     static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k1_sync<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemTables * kFastWords * 4);
-        cudaFuncSetAttribute(k1_sync<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemTables * kFastWords * 4);
+    if (ST && !attr) {
+        cudaFuncSetAttribute(k1_sync<DRI, ST, HOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kMaxSmemTables * kFastWords * 4);
         attr = true;
     }
+    k1_sync<DRI, ST, HOP><<<p.k1_ctas, kK1Threads, dyn, s>>>(p);
+}
+template <bool DRI, bool ST>
+static void launch_k1_hop(const Params& p, size_t dyn, cudaStream_t s) {
+    if (p.k1_hop)
+        launch_k1_variant<DRI, ST, true>(p, dyn, s);
+    else
+        launch_k1_variant<DRI, ST, false>(p, dyn, s);
+}
+void launch_k1_sync(const Params& p, void* stream) {
+    if (!p.k1_ctas) return;
     const size_t dyn = size_t(p.smem_tables) * kFastWords * 4;
     cudaStream_t s = (cudaStream_t)stream;
     if (p.smem_tables) {
         if (p.n_dri)
-            k1_sync<true, true><<<p.k1_ctas, kK1Threads, dyn, s>>>(p);
+            launch_k1_hop<true, true>(p, dyn, s);
         else
-            k1_sync<false, true><<<p.k1_ctas, kK1Threads, dyn, s>>>(p);
+            launch_k1_hop<false, true>(p, dyn, s);
     } else {
         if (p.n_dri)
-            k1_sync<true, false><<<p.k1_ctas, kK1Threads, 0, s>>>(p);
+            launch_k1_hop<true, false>(p, 0, s);
         else
-            k1_sync<false, false><<<p.k1_ctas, kK1Threads, 0, s>>>(p);
+            launch_k1_hop<false, false>(p, 0, s);
     }
 }
 void launch_k1c_fixup(const Params& p, void* stream) {
-    if (p.k1_ctas > 1) k1c_fixup<<<1, 1024, 0, (cudaStream_t)stream>>>(p);
+    if (p.k1_ctas <= 1) return;
+    if (!p.k1_hop) k1c_first<<<(p.k1_ctas - 1 + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p);
+    k1c_fixup<<<1, 1024, 0, (cudaStream_t)stream>>>(p);
 }
 void launch_k2_scan(const Params& p, void* stream) {
     if (p.k2_tiles) k2_scan<<<p.k2_tiles, kK2Threads, 0, (cudaStream_t)stream>>>(p);

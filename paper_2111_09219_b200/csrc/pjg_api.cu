@@ -561,7 +561,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     b->total_dus = du;
     b->seg_total = seg_total;
     b->out_bytes = outb;
-    b->k1_ctas = uint32_t((sub + kK1Threads - 1) / kK1Threads);
+    b->k1_ctas = uint32_t((sub + kK1Own - 1) / kK1Own);
     b->k2_tiles = uint32_t((sub + kK2Threads - 1) / kK2Threads);
     mark("layout");
 
@@ -688,6 +688,11 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     // tables in shared memory
     p.smem_tables = (b->n_huff <= kMaxSmemTables && sub < uint64_t(kK1Threads) * 148 * 4) ? b->n_huff : 0;
     p.k1_ctas = b->k1_ctas;
+    // grids that do not fill the GPU are latency-bound: a stale CTA start is
+    // re-chained inside K1 from shared memory; full grids skip the wait and
+    // leave the (few) stale starts to K1c's parallel first pass
+    p.k1_hop = b->k1_ctas < 2 * 148 ? 1u : 0u;
+    if (const char* e = getenv("PJG_K1_HOP")) p.k1_hop = atoi(e) ? 1u : 0u;  // override (tests, A/B)
     p.sb = sb;
     p.sub_first = reinterpret_cast<const uint64_t*>(md + b->m_sub);
     p.total_subs = sub;
@@ -887,6 +892,11 @@ uint64_t pjg_batch_scan_bits(const pjg_batch* b) {
         if (b->host_status[i] == 0 && i < b->dev_state.size() && b->dev_state[i].status == 0)
             bits += b->dev_state[i].bit_length;
     return bits;
+}
+
+uint32_t pjg_batch_kernel_launches(const pjg_batch* b) {
+    if (!b) return 0;
+    return kernel_launches(b->prm);
 }
 
 int pjg_batch_copy_outputs(pjg_batch* b, void* const* dst, const size_t* caps) {

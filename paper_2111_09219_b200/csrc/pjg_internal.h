@@ -150,7 +150,8 @@ constexpr int kSubImgShift = 7;
 constexpr uint32_t kMaxSmemTables = 4;  // fast tables K1/K3 stage in shared memory (8 KB each)
 constexpr int kK0Threads = 512;
 constexpr uint32_t kK0BigBpt = 64, kK0SmallBpt = 16;  // bytes per K0 thread: 32 KB or 8 KB tiles
-constexpr int kK1Threads = 128;                          // subsequences per K1 CTA
+constexpr int kK1Threads = 128;                          // threads per K1 CTA
+constexpr int kK1Own = kK1Threads - 1;                   // subsequences owned per K1 CTA (thread 0: predecessor's last)
 constexpr int kK2Threads = 256;
 constexpr int kK3Threads = 128;
 constexpr int kK4Threads = 128;
@@ -184,6 +185,7 @@ struct Params {
     uint32_t k1_ctas;
     uint32_t k0_bpt;               // K0 bytes per thread (tile = 512 x this)
     uint32_t smem_tables;          // K1/K3 stage this many fast tables in shared memory (0: read global)
+    uint32_t k1_hop;               // K1 re-chains stale CTA starts in-kernel (small grids); else K1c first pass
     // subsequences
     uint64_t sb;                   // subsequence_bits
     const uint64_t* sub_first;     // n_img + 1 prefix
@@ -227,6 +229,7 @@ enum StatIndex {
 };
 
 // Kernel launchers (kernels.cu).  All are stream-ordered, no host syncs.
+uint32_t kernel_launches(const Params& p);  // kernels one decode launches
 void launch_k0_unstuff(const Params& p, void* stream);
 void launch_k0b_segments(const Params& p, void* stream);
 void launch_k1_sync(const Params& p, void* stream);
