@@ -299,7 +299,8 @@ void build_fast(DevHuff* t, bool dc) {
                     ok = false;
                 }
             }
-            if (ok) f = clen | ((clen + l) << 5) | (l << 10) | (run << 14) | (kind == 1 ? kFastEOB : 0u) |
+            // bits 14-19: slots the symbol advances (run + 1), 0 for EOB (64 - z, known on the device)
+            if (ok) f = clen | ((clen + l) << 5) | (l << 10) | ((kind == 1 ? 0u : run + 1u) << 14) | (kind == 1 ? kFastEOB : 0u) |
                         (kind == 0 ? kFastCoef : 0u);
         }
         t->fast[w] = f;

@@ -763,7 +763,9 @@ __device__ __forceinline__ const uint32_t* stage_tables(const Params& P, uint32_
 constexpr uint32_t kHuffWords = sizeof(DevHuff) / 4;  // fast[] sits at word 0 of each table
 
 struct ImgCtx {
-    const uint32_t* words;  // ubuf as 32-bit words (or the CTA's shared-memory stage)
+    const uint32_t* words;  // ubuf as 32-bit words (when not staged)
+    uint32_t sbase;         // staged: shared address of absolute word 0 (mod 2^32; words byte-swapped)
+    bool staged;
     uint64_t bit_base;      // 8 * raw_off
     uint64_t L;             // bit_length
     const uint32_t* fast;   // fast[] of table t at t * stride (the global DevHuff array, or smem copies)
@@ -784,6 +786,8 @@ template <bool ST = false>
 __device__ __forceinline__ void load_ctx(const Params& P, const ImgDesc& D, uint64_t L, ImgCtx& c,
                                          const uint32_t* sfast = nullptr) {
     c.words = reinterpret_cast<const uint32_t*>(P.ubuf);
+    c.sbase = 0;
+    c.staged = false;
     c.bit_base = D.raw_off * 8;
     c.L = L;
     c.huff = P.huff;
@@ -816,8 +820,8 @@ struct StageSmem {
     uint32_t off[kStageSegs];
     uint32_t k0;
 };
-__device__ __forceinline__ const uint32_t* stage_scan(const uint8_t* ubuf, uint64_t lo, uint64_t hi, uint32_t k,
-                                                      int tid, int nthreads, int4* s_stage, StageSmem& sm) {
+__device__ __forceinline__ void stage_scan(const uint8_t* ubuf, uint64_t lo, uint64_t hi, uint32_t k, int tid,
+                                           int nthreads, int4* s_stage, StageSmem& sm) {
     if (tid < kStageSegs) {
         sm.lo[tid] = ~0ull;
         sm.hi[tid] = 0ull;
@@ -852,20 +856,24 @@ __device__ __forceinline__ const uint32_t* stage_scan(const uint8_t* ubuf, uint6
         const uint32_t n16 = uint32_t((sm.hi[q] - blo + 15) >> 4);
         const int4* src = reinterpret_cast<const int4*>(ubuf + blo);
         int4* dst = s_stage + (sm.off[q] >> 4);
-        for (uint32_t x = tid; x < n16; x += nthreads) dst[x] = __ldcs(src + x);
+        for (uint32_t x = tid; x < n16; x += nthreads) {
+            int4 v = __ldcs(src + x);  // stored byte-swapped: the decoder's MSB-first words
+            v.x = int(bswap32(uint32_t(v.x)));
+            v.y = int(bswap32(uint32_t(v.y)));
+            v.z = int(bswap32(uint32_t(v.z)));
+            v.w = int(bswap32(uint32_t(v.w)));
+            dst[x] = v;
+        }
     }
     __syncthreads();
-    if (seg < kStageSegs && sm.off[seg] != 0xFFFFFFFFu)
-        return reinterpret_cast<const uint32_t*>(s_stage + (sm.off[seg] >> 4)) - ((sm.lo[seg] & ~15ull) >> 2);
-    return reinterpret_cast<const uint32_t*>(ubuf);
 }
-// The word pointer stage_scan returned for image k (after stage_scan).
-__device__ __forceinline__ const uint32_t* stage_words(const uint8_t* ubuf, const int4* s_stage, const StageSmem& sm,
-                                                       uint32_t k) {
+// Points the decoder of image k at its staged bytes (after stage_scan), or
+// leaves it on global memory when k's segment did not fit.
+__device__ __forceinline__ void set_stage(ImgCtx& ic, const int4* s_stage, const StageSmem& sm, uint32_t k) {
     const uint32_t seg = k - sm.k0;
-    if (seg < kStageSegs && sm.off[seg] != 0xFFFFFFFFu)
-        return reinterpret_cast<const uint32_t*>(s_stage + (sm.off[seg] >> 4)) - ((sm.lo[seg] & ~15ull) >> 2);
-    return reinterpret_cast<const uint32_t*>(ubuf);
+    ic.staged = seg < kStageSegs && sm.off[seg] != 0xFFFFFFFFu;
+    if (ic.staged)
+        ic.sbase = uint32_t(__cvta_generic_to_shared(s_stage + (sm.off[seg] >> 4))) - uint32_t(sm.lo[seg] & ~15ull);
 }
 
 
@@ -903,32 +911,63 @@ struct NullSink {
 // 0.  Sync mode: an InvalidCode/OutOfBits marks the state divergent at the
 // last good symbol.  Write mode: stops at `cap` slots; errors are reported.
 //
-// The hot loop keeps 32-bit bookkeeping (bits left in the range and, saturated,
-// to the scan end), refills its 64-bit window branch-free, and resolves code +
-// magnitude with one probe of an 11-bit table whose entry carries the code
-// length, total length, magnitude size, run and kind (jfif.cpp build_fast).
-// Windows the probe cannot settle (long codes, invalid prefixes, the last 32
-// bits of the scan) take the reference's exact path with its error order.
-template <class Sink, bool ST = false>
-__device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint64_t end_bit, uint32_t cap,
-                                             Sink& sink) {
-    s.n = 0;
-    s.div = false;
-    s.err = 0;
-    if (s.p >= end_bit) return;
-    // 64-bit MSB-first window over the unstuffed bytes
+// The hot loop keeps a 32-bit window taken by a funnel shift from two
+// consecutive words (w0:w1) at bit offset bp < 32 — any symbol (<= 16 code +
+// 11 magnitude bits) fits in it — and advances by at most one word per symbol,
+// branch-free, with the following word already loaded.  Staged scan bytes are
+// read from shared memory with 32-bit addresses (stored byte-swapped by the
+// stage copy); otherwise from global memory.  One probe of an 11-bit table
+// resolves code + magnitude; its entry carries the code length, total length,
+// magnitude size, run+1 and kind (jfif.cpp build_fast).  Windows the probe
+// cannot settle (long codes, invalid prefixes, the last 32 bits of the scan)
+// take the reference's exact path with its error order.  The DC accumulator
+// of the current block's component is kept in one register (swapped at block
+// ends).
+template <bool SW>
+struct WordReader {
+    const uint32_t* g;  // global words (SW = false)
+    uint32_t sbase;     // shared address of word 0 (SW = true; mod 2^32)
+    __device__ __forceinline__ uint32_t operator()(uint32_t wi) const {
+        if (SW) {
+            uint32_t v;
+            asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sbase + 4u * wi));
+            return v;  // staged byte-swapped
+        }
+        return bswap32(__ldg(g + wi));
+    }
+};
+
+template <bool ST>
+__device__ __forceinline__ uint32_t fast_entry(const ImgCtx& ic, uint32_t tsh, uint32_t fi) {
+    if (ST) {
+        uint32_t v;
+        asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(tsh + 4u * fi));
+        return v;
+    }
+    return __ldg(ic.fast + fi);
+}
+
+template <class Sink, bool ST, bool SW>
+__device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint64_t end_bit, uint32_t cap,
+                                            Sink& sink) {
+    WordReader<SW> W;
+    W.g = ic.words;
+    W.sbase = ic.sbase;
+    const uint32_t tsh = ST ? uint32_t(__cvta_generic_to_shared(ic.fast)) : 0u;
+    // MSB-first window over the unstuffed bytes
     const uint64_t abs = ic.bit_base + s.p;
-    const uint32_t* wp = ic.words + (abs >> 5);
-    const uint32_t sh = uint32_t(abs & 31);
-    uint64_t acc = ((uint64_t(bswap32(wp[0])) << 32) | bswap32(wp[1])) << sh;
-    int cnt = 64 - int(sh);
-    wp += 2;
+    uint32_t wi = uint32_t(abs >> 5);
+    uint32_t bp = uint32_t(abs & 31);
+    uint32_t w0 = W(wi), w1 = W(wi + 1);
+    wi += 2;
+    uint32_t nw = W(wi);  // the word after w1
     uint64_t p = s.p;
     uint32_t c = s.c, z = s.z, n = 0;
     int32_t a0 = s.dc0, a1 = s.dc1, a2 = s.dc2;
     uint32_t comp = (ic.duc >> (2 * c)) & 3u;
     uint32_t tdc = comp == 0 ? ic.tdc[0] : (comp == 1 ? ic.tdc[1] : ic.tdc[2]);
     uint32_t tac = comp == 0 ? ic.tac[0] : (comp == 1 ? ic.tac[1] : ic.tac[2]);
+    int32_t acur = comp == 0 ? a0 : (comp == 1 ? a1 : a2);
     const uint64_t lr = ic.L - p;
     int32_t lrem = lr > 0x40000000ull ? 0x40000000 : int32_t(lr);  // bits to the scan end, saturated
     uint64_t left = end_bit - p;
@@ -943,32 +982,27 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
                 stop = true;
                 break;
             }
-            {  // refill to >= 32 valid bits, branch-free
-                const uint32_t w = bswap32(*wp);
-                const bool need = cnt <= 32;
-                acc |= need ? (uint64_t(w) << ((32 - cnt) & 63)) : 0ull;
-                wp += need ? 1 : 0;
-                cnt += need ? 32 : 0;
-            }
-            const uint32_t hi = uint32_t(acc >> 32);
-            const uint32_t fi = (z ? tac : tdc) + (hi >> (32 - kFastBits));
-            const uint32_t fe = ST ? ic.fast[fi] : __ldg(ic.fast + fi);
+            const uint32_t win = __funnelshift_l(w1, w0, bp);
+            const bool dcs = z == 0;
+            const uint32_t fe = fast_entry<ST>(ic, tsh, (dcs ? tdc : tac) + (win >> (32 - kFastBits)));
             uint32_t len, step, coefk;
             int32_t coef;
             if ((fe & 31u) != 0 && lrem >= 32) {
                 // code + magnitude (<= 11 + 11 bits) all real: lrem >= 32
                 const uint32_t clen = fe & 31u, l = (fe >> 10) & 15u;
                 len = (fe >> 5) & 31u;
-                const uint32_t bits = __funnelshift_l(hi << clen, 0u, l);  // top l bits after the code
-                const int32_t t = int32_t((1u << l) - 1u);
-                coef = int32_t(bits) - (((int32_t(bits) - ((t + 1) >> 1)) >> 31) & t);  // extend()
-                step = (fe & kFastEOB) ? 64u - z : ((fe >> 14) & 63u) + 1u;
+                const uint32_t w2 = win << clen;
+                const uint32_t v = __funnelshift_l(w2, 0u, l);  // top l bits after the code
+                // extend(): a leading 1 is positive, else v - (2^l - 1)
+                coef = int32_t(v) + (int32_t(1u - (1u << l)) & ~(int32_t(w2) >> 31));
+                const uint32_t r1 = (fe >> 14) & 63u;  // run + 1 (0: EOB)
+                step = r1 ? r1 : 64u - z;
                 coefk = fe & kFastCoef;
             } else {
-                const DevHuff* t = ST ? ic.huff + (z ? tac : tdc) / TabStride<ST>::value
-                                      : reinterpret_cast<const DevHuff*>(ic.fast + (z ? tac : tdc));
+                const DevHuff* t = ST ? ic.huff + (dcs ? tdc : tac) / TabStride<ST>::value
+                                      : reinterpret_cast<const DevHuff*>(ic.fast + (dcs ? tdc : tac));
                 uint32_t maxlen;
-                const uint32_t e = dev_lookup(t, hi >> 16, maxlen);
+                const uint32_t e = dev_lookup(t, win >> 16, maxlen);
                 const uint32_t clen = e >> 8, sym = e & 255u;
                 const uint32_t avail = uint32_t(lrem);  // >= 1 inside the range
                 int32_t err = 0;
@@ -979,7 +1013,7 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
                     err = avail < maxlen ? kOutOfBits : kInvalidCode;
                 } else if (clen > avail) {
                     err = kOutOfBits;
-                } else if (z == 0) {
+                } else if (dcs) {
                     l = sym;
                     if (l > 11)
                         err = kInvalidCode;
@@ -1014,7 +1048,7 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
                 }
                 coef = 0;
                 if (l) {
-                    const uint32_t bits = uint32_t((acc << clen) >> (64 - l));
+                    const uint32_t bits = (win << clen) >> (32 - l);
                     coef = bits >= (1u << (l - 1)) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1);
                 }
                 len = clen + l;
@@ -1024,27 +1058,36 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
                 stop = true;
                 break;
             }
-            if (z == 0) {
-                if (comp == 0)
-                    a0 += coef, coef = a0;
-                else if (comp == 1)
-                    a1 += coef, coef = a1;
-                else
-                    a2 += coef, coef = a2;
+            if (dcs) {
+                acur += coef;
+                coef = acur;
             }
             if (Sink::kWrite && coefk) sink.put(z + step - 1, coef);
-            acc <<= len;
-            cnt -= int(len);
+            // advance: bp + len <= 31 + 27, so at most one word
+            bp += len;
+            const bool adv = bp >= 32u;
+            bp &= 31u;
+            w0 = adv ? w1 : w0;
+            w1 = adv ? nw : w1;
+            wi += adv ? 1u : 0u;
+            nw = W(wi);
             rem -= int32_t(len);
             lrem -= int32_t(len);
             n += step;
             z += step;
             if (z >= 64) {
+                if (comp == 0)
+                    a0 = acur;
+                else if (comp == 1)
+                    a1 = acur;
+                else
+                    a2 = acur;
                 z = 0;
                 c = (c + 1 == ic.dpm) ? 0 : c + 1;
                 comp = (ic.duc >> (2 * c)) & 3u;
                 tdc = comp == 0 ? ic.tdc[0] : (comp == 1 ? ic.tdc[1] : ic.tdc[2]);
                 tac = comp == 0 ? ic.tac[0] : (comp == 1 ? ic.tac[1] : ic.tac[2]);
+                acur = comp == 0 ? a0 : (comp == 1 ? a1 : a2);
                 if (Sink::kWrite) sink.block_end(comp);
             }
         }
@@ -1055,6 +1098,12 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
         if (left <= over) break;
         left -= over;
     }
+    if (comp == 0)
+        a0 = acur;
+    else if (comp == 1)
+        a1 = acur;
+    else
+        a2 = acur;
     s.p = p;
     s.n = n;
     s.c = c;
@@ -1062,6 +1111,19 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
     s.dc0 = a0;
     s.dc1 = a1;
     s.dc2 = a2;
+}
+
+template <class Sink, bool ST = false>
+__device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint64_t end_bit, uint32_t cap,
+                                             Sink& sink) {
+    s.n = 0;
+    s.div = false;
+    s.err = 0;
+    if (s.p >= end_bit) return;
+    if (ic.staged)
+        decode_core<Sink, ST, true>(ic, s, end_bit, cap, sink);
+    else
+        decode_core<Sink, ST, false>(ic, s, end_bit, cap, sink);
 }
 
 __device__ __forceinline__ DcSums pack_dc(int32_t a0, int32_t a1, int32_t a2) {
@@ -1152,7 +1214,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     if (tid < 2) s_cnt[tid] = 0;
     {
         const uint64_t lo = real ? D.raw_off + (si.lo >> 3) : 1, hi = real ? D.raw_off + ((si.hi + 7) >> 3) + 24 : 0;
-        ic.words = stage_scan(P.ubuf, lo, hi, k, tid, T, s_stage, s_sm);
+        stage_scan(P.ubuf, lo, hi, k, tid, T, s_stage, s_sm);
+        set_stage(ic, s_stage, s_sm, k);
     }
 
     // Round 0: every subsequence decodes from its origin (parallel_decode.hpp:187-195)
@@ -1193,7 +1256,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
             if (kk != ick) {  // chain of another image of this CTA
                 const ImgDesc& D2 = P.img[kk];
                 load_ctx<ST>(P, D2, P.ist[kk].bit_length, ic, sfast);
-                ic.words = stage_words(P.ubuf, s_stage, s_sm, kk);
+                set_stage(ic, s_stage, s_sm, kk);
                 ick = kk;
             }
             Entry e2;
@@ -1252,7 +1315,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
                 uint32_t hops = 0;
                 if (ick != k) {
                     load_ctx<ST>(P, D, L, ic, sfast);
-                    ic.words = stage_words(P.ubuf, s_stage, s_sm, k);
+                    set_stage(ic, s_stage, s_sm, k);
                 }
                 for (int tt = 1; tt < T && ii < si.seg_sub1; ++tt, ++ii) {
                     Entry e2;
@@ -1702,7 +1765,8 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
         // this subsequence's bits start at entries[g-1].p (inside [lo, hi)); stage from lo
         const uint64_t lo = active ? D.raw_off + (si.lo >> 3) : 1;
         const uint64_t hi = active ? D.raw_off + ((si.hi + 7) >> 3) + 24 : 0;
-        ic.words = stage_scan(P.ubuf, lo, hi, k, tid, kK3Threads, s_stage, s_sm);
+        stage_scan(P.ubuf, lo, hi, k, tid, kK3Threads, s_stage, s_sm);
+        set_stage(ic, s_stage, s_sm, k);
     }
     if (!active) return;
     DecState s;

@@ -44,8 +44,8 @@ constexpr int kFastBits = 11;
 constexpr uint32_t kFastWords = 1u << kFastBits;
 // fast entry for a kFastBits window whose codeword fits and decodes to a
 // symbol the reference accepts: bits 0-4 codeword length (0 = take the exact
-// path), 5-9 code + magnitude length, 10-13 magnitude bits l, 14-19 run,
-// bit 20 EOB, bit 21 coefficient (as opposed to EOB / ZRL).  The magnitude
+// path), 5-9 code + magnitude length, 10-13 magnitude bits l, 14-19 run + 1
+// (0 for EOB), bit 20 EOB, bit 21 coefficient (as opposed to EOB / ZRL).  The magnitude
 // value itself is extracted arithmetically.
 constexpr uint32_t kFastEOB = 1u << 20, kFastCoef = 1u << 21;
 
