@@ -766,6 +766,7 @@ struct ImgCtx {
     const uint32_t* words;  // ubuf as 32-bit words (when not staged)
     uint32_t sbase;         // staged: shared address of absolute word 0 (mod 2^32; words byte-swapped)
     bool staged;
+    uint32_t sacc, sacc_stride;  // shared address of this thread's DC accumulator for component 0; stride
     uint64_t bit_base;      // 8 * raw_off
     uint64_t L;             // bit_length
     const uint32_t* fast;   // fast[] of table t at t * stride (the global DevHuff array, or smem copies)
@@ -867,6 +868,12 @@ __device__ __forceinline__ void stage_scan(const uint8_t* ubuf, uint64_t lo, uin
     }
     __syncthreads();
 }
+// The thread's three DC accumulators in shared memory (s_acc[3 * nthreads]).
+__device__ __forceinline__ void set_sacc(ImgCtx& ic, int32_t* s_acc, int tid, int nthreads) {
+    ic.sacc = uint32_t(__cvta_generic_to_shared(s_acc + tid));
+    ic.sacc_stride = uint32_t(nthreads) * 4u;
+}
+
 // Points the decoder of image k at its staged bytes (after stage_scan), or
 // leaves it on global memory when k's segment did not fit.
 __device__ __forceinline__ void set_stage(ImgCtx& ic, const int4* s_stage, const StageSmem& sm, uint32_t k) {
@@ -937,6 +944,15 @@ struct WordReader {
     }
 };
 
+__device__ __forceinline__ int32_t lds_i32(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_i32(uint32_t a, int32_t v) {
+    asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
 template <bool ST>
 __device__ __forceinline__ uint32_t fast_entry(const ImgCtx& ic, uint32_t tsh, uint32_t fi) {
     if (ST) {
@@ -967,7 +983,13 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
     uint32_t comp = (ic.duc >> (2 * c)) & 3u;
     uint32_t tdc = comp == 0 ? ic.tdc[0] : (comp == 1 ? ic.tdc[1] : ic.tdc[2]);
     uint32_t tac = comp == 0 ? ic.tac[0] : (comp == 1 ? ic.tac[1] : ic.tac[2]);
-    int32_t acur = comp == 0 ? a0 : (comp == 1 ? a1 : a2);
+    // DC accumulators live in shared memory: a DC symbol (once per block)
+    // updates the current component's, and a block end only moves the address
+    const uint32_t sa0 = ic.sacc, sst = ic.sacc_stride;
+    sts_i32(sa0, a0);
+    sts_i32(sa0 + sst, a1);
+    sts_i32(sa0 + 2 * sst, a2);
+    uint32_t sa = sa0 + comp * sst;
     const uint64_t lr = ic.L - p;
     int32_t lrem = lr > 0x40000000ull ? 0x40000000 : int32_t(lr);  // bits to the scan end, saturated
     uint64_t left = end_bit - p;
@@ -1059,8 +1081,8 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
                 break;
             }
             if (dcs) {
-                acur += coef;
-                coef = acur;
+                coef += lds_i32(sa);
+                sts_i32(sa, coef);
             }
             if (Sink::kWrite && coefk) sink.put(z + step - 1, coef);
             // advance: bp + len <= 31 + 27, so at most one word
@@ -1076,18 +1098,12 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
             n += step;
             z += step;
             if (z >= 64) {
-                if (comp == 0)
-                    a0 = acur;
-                else if (comp == 1)
-                    a1 = acur;
-                else
-                    a2 = acur;
                 z = 0;
                 c = (c + 1 == ic.dpm) ? 0 : c + 1;
                 comp = (ic.duc >> (2 * c)) & 3u;
                 tdc = comp == 0 ? ic.tdc[0] : (comp == 1 ? ic.tdc[1] : ic.tdc[2]);
                 tac = comp == 0 ? ic.tac[0] : (comp == 1 ? ic.tac[1] : ic.tac[2]);
-                acur = comp == 0 ? a0 : (comp == 1 ? a1 : a2);
+                sa = sa0 + comp * sst;
                 if (Sink::kWrite) sink.block_end(comp);
             }
         }
@@ -1098,12 +1114,9 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
         if (left <= over) break;
         left -= over;
     }
-    if (comp == 0)
-        a0 = acur;
-    else if (comp == 1)
-        a1 = acur;
-    else
-        a2 = acur;
+    a0 = lds_i32(sa0);
+    a1 = lds_i32(sa0 + sst);
+    a2 = lds_i32(sa0 + 2 * sst);
     s.p = p;
     s.n = n;
     s.c = c;
@@ -1211,6 +1224,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     const uint32_t* sfast = ST ? stage_tables(P, s_fast_k1, tid, T) : nullptr;
     ImgCtx ic;
     load_ctx<ST>(P, D, L, ic, sfast);
+    __shared__ int32_t s_acc[3 * T];
+    set_sacc(ic, s_acc, tid, T);
     if (tid < 2) s_cnt[tid] = 0;
     {
         const uint64_t lo = real ? D.raw_off + (si.lo >> 3) : 1, hi = real ? D.raw_off + ((si.hi + 7) >> 3) + 24 : 0;
@@ -1357,7 +1372,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
 
 // Redoes CTA cta's overflow from start state st (its predecessor's final
 // last entry) until it meets an entry it agrees with.
-__device__ __forceinline__ void k1c_redo(const Params& P, uint32_t cta, Entry st, unsigned long long& redone) {
+__device__ __forceinline__ void k1c_redo(const Params& P, uint32_t cta, Entry st, unsigned long long& redone,
+                                         int32_t* s_acc) {
     constexpr int TO = kK1Own;
     const uint64_t g0 = uint64_t(cta) * TO;
     const uint32_t k = find_img(P, g0);
@@ -1372,6 +1388,7 @@ __device__ __forceinline__ void k1c_redo(const Params& P, uint32_t cta, Entry st
     if (!sub_info(P, D, L, i, si)) return;
     ImgCtx ic;
     load_ctx(P, D, L, ic);
+    set_sacc(ic, s_acc, threadIdx.x, blockDim.x);
     Entry ch = st;
     for (int tt = 0; tt < TO && i < si.seg_sub1 && g0 + tt < P.total_subs; ++tt, ++i) {
         Entry e2;
@@ -1393,6 +1410,7 @@ __device__ __forceinline__ void k1c_redo(const Params& P, uint32_t cta, Entry st
 // fix-point pass below catches that (it compares against the final entries).
 __global__ void __launch_bounds__(128) k1c_first(Params P) {
     const uint32_t cta = 1 + blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ int32_t s_acc[3 * 128];
     unsigned long long redone = 0;
     if (cta < P.k1_ctas) {
         const Entry st = P.cta_start[cta];
@@ -1401,7 +1419,7 @@ __global__ void __launch_bounds__(128) k1c_first(Params P) {
             if (!sync_equal(st.p, st.czd, pe.p, pe.czd)) {
                 pe.czd |= kBoundaryBit;
                 P.cta_start[cta] = pe;
-                k1c_redo(P, cta, pe, redone);
+                k1c_redo(P, cta, pe, redone, s_acc);
             }
         }
     }
@@ -1412,6 +1430,7 @@ __global__ void __launch_bounds__(128) k1c_first(Params P) {
 __global__ void __launch_bounds__(1024) k1c_fixup(Params P) {
     constexpr int TO = kK1Own;
     __shared__ int s_any;
+    __shared__ int32_t s_acc[3 * 1024];
     __shared__ int s_passes;
     if (threadIdx.x == 0) s_passes = 0;
     unsigned long long redone = 0;
@@ -1438,7 +1457,7 @@ __global__ void __launch_bounds__(1024) k1c_fixup(Params P) {
             if (!(st.czd & 0x2000u)) continue;
             st.czd &= ~0x2000u;
             P.cta_start[cta] = st;
-            k1c_redo(P, cta, st, redone);
+            k1c_redo(P, cta, st, redone, s_acc);
         }
         __threadfence_block();
         __syncthreads();
@@ -1759,6 +1778,8 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     extern __shared__ uint32_t s_fast_k3[];
     ImgCtx ic;
     load_ctx<ST>(P, D, L, ic, ST ? stage_tables(P, s_fast_k3, tid, kK3Threads) : nullptr);
+    __shared__ int32_t s_acc3[3 * kK3Threads];
+    set_sacc(ic, s_acc3, tid, kK3Threads);
     {
         __shared__ int4 s_stage[kStageBytes / 16];
         __shared__ StageSmem s_sm;
