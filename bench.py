@@ -73,27 +73,32 @@ class ClockSampler:
         self.stop_evt = threading.Event()
         self.max_mhz = None
 
-    def _run(self):
+    def _sample(self):
         import pynvml as N
-        h = N.nvmlDeviceGetHandleByIndex(self.index)
-        self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
         bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                 "sw_power_cap": 0x4}
+        try:
+            self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for k, m in bits.items():
+                if r & m:
+                    self.reasons.add(k)
+        except Exception:
+            pass
+
+    def _run(self):
         while not self.stop_evt.is_set():
-            try:
-                self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
-                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-                for k, m in bits.items():
-                    if r & m:
-                        self.reasons.add(k)
-            except Exception:
-                pass
-            time.sleep(0.01)
+            self._sample()
+            time.sleep(0.005)
 
     def start(self):
+        # the NVML handle is taken here, so the sampling thread samples from
+        # the first millisecond of the timed region
         try:
             import pynvml as N
             N.nvmlInit()
+            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
@@ -104,6 +109,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
         self.stop_evt.set()
         self.t.join(timeout=2)
+        if not self.samples:  # a timed region shorter than one sampling period
+            self._sample()
         return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 

@@ -766,7 +766,8 @@ struct ImgCtx {
     const uint32_t* words;  // ubuf as 32-bit words (when not staged)
     uint32_t sbase;         // staged: shared address of absolute word 0 (mod 2^32; words byte-swapped)
     bool staged;
-    uint32_t sacc, sacc_stride;  // shared address of this thread's DC accumulator for component 0; stride
+    int32_t* sacc;          // this thread's DC accumulator of component 0 (shared memory)
+    uint32_t sacc_stride;   // ... components apart (elements)
     uint64_t bit_base;      // 8 * raw_off
     uint64_t L;             // bit_length
     const uint32_t* fast;   // fast[] of table t at t * stride (the global DevHuff array, or smem copies)
@@ -870,8 +871,8 @@ __device__ __forceinline__ void stage_scan(const uint8_t* ubuf, uint64_t lo, uin
 }
 // The thread's three DC accumulators in shared memory (s_acc[3 * nthreads]).
 __device__ __forceinline__ void set_sacc(ImgCtx& ic, int32_t* s_acc, int tid, int nthreads) {
-    ic.sacc = uint32_t(__cvta_generic_to_shared(s_acc + tid));
-    ic.sacc_stride = uint32_t(nthreads) * 4u;
+    ic.sacc = s_acc + tid;
+    ic.sacc_stride = uint32_t(nthreads);
 }
 
 // Points the decoder of image k at its staged bytes (after stage_scan), or
@@ -944,15 +945,6 @@ struct WordReader {
     }
 };
 
-__device__ __forceinline__ int32_t lds_i32(uint32_t a) {
-    int32_t v;
-    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts_i32(uint32_t a, int32_t v) {
-    asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-
 template <bool ST>
 __device__ __forceinline__ uint32_t fast_entry(const ImgCtx& ic, uint32_t tsh, uint32_t fi) {
     if (ST) {
@@ -983,13 +975,20 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
     uint32_t comp = (ic.duc >> (2 * c)) & 3u;
     uint32_t tdc = comp == 0 ? ic.tdc[0] : (comp == 1 ? ic.tdc[1] : ic.tdc[2]);
     uint32_t tac = comp == 0 ? ic.tac[0] : (comp == 1 ? ic.tac[1] : ic.tac[2]);
-    // DC accumulators live in shared memory: a DC symbol (once per block)
-    // updates the current component's, and a block end only moves the address
-    const uint32_t sa0 = ic.sacc, sst = ic.sacc_stride;
-    sts_i32(sa0, a0);
-    sts_i32(sa0 + sst, a1);
-    sts_i32(sa0 + 2 * sst, a2);
-    uint32_t sa = sa0 + comp * sst;
+    // Sync mode: the DC accumulators live in shared memory — a DC symbol (once
+    // per block) updates the current component's, and a block end only moves
+    // the address.  Write mode needs each absolute DC at once (the sink): the
+    // current component's accumulator is a register, swapped at block ends.
+    constexpr bool kRegAcc = Sink::kWrite;
+    int32_t* const sa0 = ic.sacc;
+    const uint32_t sst = ic.sacc_stride;
+    if (!kRegAcc) {
+        sa0[0] = a0;
+        sa0[sst] = a1;
+        sa0[2 * sst] = a2;
+    }
+    int32_t* sa = sa0 + comp * sst;
+    int32_t acur = comp == 0 ? a0 : (comp == 1 ? a1 : a2);
     const uint64_t lr = ic.L - p;
     int32_t lrem = lr > 0x40000000ull ? 0x40000000 : int32_t(lr);  // bits to the scan end, saturated
     uint64_t left = end_bit - p;
@@ -1081,8 +1080,13 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
                 break;
             }
             if (dcs) {
-                coef += lds_i32(sa);
-                sts_i32(sa, coef);
+                if (kRegAcc) {
+                    acur += coef;
+                    coef = acur;
+                } else {
+                    coef += *sa;
+                    *sa = coef;
+                }
             }
             if (Sink::kWrite && coefk) sink.put(z + step - 1, coef);
             // advance: bp + len <= 31 + 27, so at most one word
@@ -1098,12 +1102,23 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
             n += step;
             z += step;
             if (z >= 64) {
+                if (kRegAcc) {
+                    if (comp == 0)
+                        a0 = acur;
+                    else if (comp == 1)
+                        a1 = acur;
+                    else
+                        a2 = acur;
+                }
                 z = 0;
                 c = (c + 1 == ic.dpm) ? 0 : c + 1;
                 comp = (ic.duc >> (2 * c)) & 3u;
                 tdc = comp == 0 ? ic.tdc[0] : (comp == 1 ? ic.tdc[1] : ic.tdc[2]);
                 tac = comp == 0 ? ic.tac[0] : (comp == 1 ? ic.tac[1] : ic.tac[2]);
-                sa = sa0 + comp * sst;
+                if (kRegAcc)
+                    acur = comp == 0 ? a0 : (comp == 1 ? a1 : a2);
+                else
+                    sa = sa0 + comp * sst;
                 if (Sink::kWrite) sink.block_end(comp);
             }
         }
@@ -1114,9 +1129,18 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
         if (left <= over) break;
         left -= over;
     }
-    a0 = lds_i32(sa0);
-    a1 = lds_i32(sa0 + sst);
-    a2 = lds_i32(sa0 + 2 * sst);
+    if (kRegAcc) {
+        if (comp == 0)
+            a0 = acur;
+        else if (comp == 1)
+            a1 = acur;
+        else
+            a2 = acur;
+    } else {
+        a0 = sa0[0];
+        a1 = sa0[sst];
+        a2 = sa0[2 * sst];
+    }
     s.p = p;
     s.n = n;
     s.c = c;
