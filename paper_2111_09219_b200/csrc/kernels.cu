@@ -750,9 +750,11 @@ __global__ void __launch_bounds__(256) k0b_segments(Params P) {
 
 // Copies the batch's fast tables into shared memory (P.smem_tables tables,
 // dynamic shared memory) and returns them, or nullptr when not enabled.
-__device__ __forceinline__ const uint32_t* stage_tables(const Params& P, uint32_t* s_fast, int tid, int nthreads) {
-    if (!P.smem_tables) return nullptr;
-    for (uint32_t x = tid; x < P.smem_tables * (kFastWords / 4); x += nthreads) {
+__device__ __forceinline__ const uint32_t* stage_tables(const Params& P, uint32_t* s_fast, int tid, int nthreads,
+                                                       uint32_t ntab = 0xFFFFFFFFu) {
+    if (ntab == 0xFFFFFFFFu) ntab = P.smem_tables;
+    if (!ntab) return nullptr;
+    for (uint32_t x = tid; x < ntab * (kFastWords / 4); x += nthreads) {
         const uint32_t t = x / (kFastWords / 4), q = x % (kFastWords / 4);
         reinterpret_cast<uint4*>(s_fast)[x] = __ldg(reinterpret_cast<const uint4*>(P.huff[t].fast) + q);
     }
@@ -1228,12 +1230,10 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     __shared__ uint32_t s_cta;
 
     const int tid = threadIdx.x;
-    if (HOP) {
-        if (tid == 0) s_cta = atomicAdd(&P.counters[kTicketK1], 1u);
-        __syncthreads();
-    }
-    // ticket order (HOP): a predecessor is never waiting on this CTA
-    const uint32_t cta = HOP ? s_cta : blockIdx.x;
+    if (tid == 0) s_cta = atomicAdd(&P.counters[kTicketK1], 1u);
+    __syncthreads();
+    // ticket order: a predecessor started earlier and is never waiting on this CTA
+    const uint32_t cta = s_cta;
     const int64_t gs = int64_t(cta) * TO + tid - 1;
     const bool inb = gs >= 0 && uint64_t(gs) < P.total_subs;
     const uint64_t g = inb ? uint64_t(gs) : (gs < 0 ? 0 : P.total_subs - 1);
@@ -1319,7 +1319,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
         atomicMax(P.stats + kStatRoundsMax, (unsigned long long)rounds);
     }
     // Publish this CTA's last entry (post-intra) for the successor CTA.
-    if (HOP && tid == T - 1) {
+    if (tid == T - 1) {
         Entry last;
         last.p = s_p[T - 1];
         last.n = s_n[T - 1];
@@ -1331,19 +1331,28 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     // Inter-CTA check: the speculative start (thread 0's round-0 entry) against
     // the predecessor's published post-intra last entry; where they differ,
     // the first owned thread re-chains from the published entry (in its own
-    // image context) until it meets an entry it agrees with.  K1c compares the
-    // start used with the predecessor's FINAL last entry.
+    // image context) until it meets an entry it agrees with.  HOP waits for
+    // the predecessor; otherwise the check is taken only if the predecessor
+    // has already published (usually: it started earlier) and the start stays
+    // speculative if not.  K1c compares the start used with the predecessor's
+    // FINAL last entry.
     if (tid == 1) {
         Entry start;
         start.p = 0;
         start.n = 0;
         start.czd = 0;
-        if (!HOP && real && si.j > 0) {  // K1c's first pass checks the speculative start
-            start.p = s_p[0];
-            start.n = s_n[0];
-            start.czd = s_czd[0] | kBoundaryBit;
-        } else if (real && si.j > 0) {  // CTA starts mid-segment
-            while (ld_acquire(P.k1_flag + cta - 1) != P.epoch) spin_pause();
+        bool ready = false;
+        if (real && si.j > 0) {  // CTA starts mid-segment
+            if (HOP)
+                while (ld_acquire(P.k1_flag + cta - 1) != P.epoch) spin_pause();
+            ready = HOP || ld_acquire(P.k1_flag + cta - 1) == P.epoch;
+            if (!ready) {  // K1c's first pass checks the speculative start
+                start.p = s_p[0];
+                start.n = s_n[0];
+                start.czd = s_czd[0] | kBoundaryBit;
+            }
+        }
+        if (ready) {
             start.p = __ldcg(&P.cta_end[cta - 1].p);
             const uint64_t nc = __ldcg(reinterpret_cast<const unsigned long long*>(&P.cta_end[cta - 1]) + 1);
             start.n = uint32_t(nc);
@@ -1396,8 +1405,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
 
 // Redoes CTA cta's overflow from start state st (its predecessor's final
 // last entry) until it meets an entry it agrees with.
+template <bool ST = false>
 __device__ __forceinline__ void k1c_redo(const Params& P, uint32_t cta, Entry st, unsigned long long& redone,
-                                         int32_t* s_acc) {
+                                         int32_t* s_acc, const uint32_t* sfast = nullptr) {
     constexpr int TO = kK1Own;
     const uint64_t g0 = uint64_t(cta) * TO;
     const uint32_t k = find_img(P, g0);
@@ -1411,13 +1421,13 @@ __device__ __forceinline__ void k1c_redo(const Params& P, uint32_t cta, Entry st
     SubInfo si;
     if (!sub_info(P, D, L, i, si)) return;
     ImgCtx ic;
-    load_ctx(P, D, L, ic);
+    load_ctx<ST>(P, D, L, ic, sfast);
     set_sacc(ic, s_acc, threadIdx.x, blockDim.x);
     Entry ch = st;
     for (int tt = 0; tt < TO && i < si.seg_sub1 && g0 + tt < P.total_subs; ++tt, ++i) {
         Entry e2;
         DcSums d2;
-        sync_decode(ic, seg_end_bit(si, P.sb, i), ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
+        sync_decode<ST>(ic, seg_end_bit(si, P.sb, i), ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
         ++redone;
         Entry old = P.ent[g0 + tt];
         bool synced = sync_equal(e2.p, e2.czd, old.p, old.czd);
@@ -1432,9 +1442,15 @@ __device__ __forceinline__ void k1c_redo(const Params& P, uint32_t cta, Entry st
 // CTA starts are speculative when K1 ran without the in-kernel check.  A
 // redo that runs through a whole CTA races with its successor's check; the
 // fix-point pass below catches that (it compares against the final entries).
+// ST: the batch's fast tables are staged in shared memory (a redo chain is a
+// serial dependency chain, and this kernel's L1 starts cold).
+template <bool ST>
 __global__ void __launch_bounds__(128) k1c_first(Params P) {
     const uint32_t cta = 1 + blockIdx.x * blockDim.x + threadIdx.x;
     __shared__ int32_t s_acc[3 * 128];
+    extern __shared__ uint32_t s_fast_k1c[];
+    const uint32_t* sfast = ST ? stage_tables(P, s_fast_k1c, threadIdx.x, 128, P.n_huff) : nullptr;
+    if (ST) __syncthreads();
     unsigned long long redone = 0;
     if (cta < P.k1_ctas) {
         const Entry st = P.cta_start[cta];
@@ -1443,7 +1459,7 @@ __global__ void __launch_bounds__(128) k1c_first(Params P) {
             if (!sync_equal(st.p, st.czd, pe.p, pe.czd)) {
                 pe.czd |= kBoundaryBit;
                 P.cta_start[cta] = pe;
-                k1c_redo(P, cta, pe, redone, s_acc);
+                k1c_redo<ST>(P, cta, pe, redone, s_acc, sfast);
             }
         }
     }
@@ -2718,7 +2734,20 @@ void launch_k1_sync(const Params& p, void* stream) {
 }
 void launch_k1c_fixup(const Params& p, void* stream) {
     if (p.k1_ctas <= 1) return;
-    if (!p.k1_hop) k1c_first<<<(p.k1_ctas - 1 + 127) / 128, 128, 0, (cudaStream_t)stream>>>(p);
+    if (!p.k1_hop) {
+        const unsigned grid = (p.k1_ctas - 1 + 127) / 128;
+        if (p.n_huff <= kMaxSmemTables) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k1c_first<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kMaxSmemTables * kFastWords * 4);
+                attr = true;
+            }
+            k1c_first<true><<<grid, 128, size_t(p.n_huff) * kFastWords * 4, (cudaStream_t)stream>>>(p);
+        } else {
+            k1c_first<false><<<grid, 128, 0, (cudaStream_t)stream>>>(p);
+        }
+    }
     k1c_fixup<<<1, 1024, 0, (cudaStream_t)stream>>>(p);
 }
 void launch_k2_scan(const Params& p, void* stream) {

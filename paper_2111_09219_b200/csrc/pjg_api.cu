@@ -688,6 +688,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     // tables in shared memory
     p.smem_tables = (b->n_huff <= kMaxSmemTables && sub < uint64_t(kK1Threads) * 148 * 4) ? b->n_huff : 0;
     p.k1_ctas = b->k1_ctas;
+    p.n_huff = b->n_huff;
     // grids that do not fill the GPU are latency-bound: a stale CTA start is
     // re-chained inside K1 from shared memory; full grids skip the wait and
     // leave the (few) stale starts to K1c's parallel first pass

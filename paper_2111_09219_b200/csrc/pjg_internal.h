@@ -185,6 +185,7 @@ struct Params {
     uint32_t k1_ctas;
     uint32_t k0_bpt;               // K0 bytes per thread (tile = 512 x this)
     uint32_t smem_tables;          // K1/K3 stage this many fast tables in shared memory (0: read global)
+    uint32_t n_huff;               // unique Huffman tables of the batch
     uint32_t k1_hop;               // K1 re-chains stale CTA starts in-kernel (small grids); else K1c first pass
     // subsequences
     uint64_t sb;                   // subsequence_bits
