@@ -1818,8 +1818,8 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     extern __shared__ uint32_t s_fast_k3[];
     ImgCtx ic;
     load_ctx<ST>(P, D, L, ic, ST ? stage_tables(P, s_fast_k3, tid, kK3Threads) : nullptr);
-    __shared__ int32_t s_acc3[3 * kK3Threads];
-    set_sacc(ic, s_acc3, tid, kK3Threads);
+    ic.sacc = nullptr;  // write mode keeps its DC accumulators in registers
+    ic.sacc_stride = 0;
     {
         __shared__ int4 s_stage[kStageBytes / 16];
         __shared__ StageSmem s_sm;
