@@ -125,8 +125,10 @@ def profiled_traffic(cfg_key):
         with open(os.path.join(ROOT, "profiles", "round1", "ncu_k4_transform.txt")) as f:
             for line in f:
                 parts = line.split()
-                if len(parts) == 2 and parts[0].startswith("dram__bytes_"):
-                    vals[parts[0]] = float(parts[1]) * 1e9  # Gbyte
+                if len(parts) >= 2 and parts[0].startswith("dram__bytes_"):
+                    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(
+                        parts[2] if len(parts) > 2 else "Gbyte", 1e9)
+                    vals[parts[0]] = float(parts[1]) * scale
         return int(vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
     except Exception:
         return None

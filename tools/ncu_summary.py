@@ -29,10 +29,10 @@ KERNEL = []
 
 def main(path, segments=True):
     raw = list(csv.reader(io.StringIO(run([path] + KERNEL + ["--page", "raw", "--csv"]))))
-    h, v = raw[0], raw[2]
+    h, u, v = raw[0], raw[1], raw[2]
     for name in HEAD:
         if name in h:
-            print(f"{name:70s} {v[h.index(name)]}")
+            print(f"{name:70s} {v[h.index(name)]:>20s} {u[h.index(name)]}")
     if not segments:
         return
     src = list(csv.reader(io.StringIO(run([path] + KERNEL + ["--page", "source", "--csv", "--print-source=sass"]))))
