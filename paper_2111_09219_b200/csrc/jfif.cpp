@@ -299,9 +299,11 @@ void build_fast(DevHuff* t, bool dc) {
                     ok = false;
                 }
             }
-            // bits 14-19: slots the symbol advances (run + 1), 0 for EOB (64 - z, known on the device)
-            if (ok) f = clen | ((clen + l) << 5) | (l << 10) | ((kind == 1 ? 0u : run + 1u) << 14) | (kind == 1 ? kFastEOB : 0u) |
-                        (kind == 0 ? kFastCoef : 0u);
+            // layout: pjg_internal.h (kFast*); slots advanced = run + 1, 0 for EOB
+            // (64 - z, known on the device)
+            if (ok)
+                f = clen | (l << kFastLShift) | (((1u << l) - 1u) << kFastTShift) |
+                    ((kind == 1 ? 0u : run + 1u) << kFastR1Shift) | ((clen + l) << kFastLenShift);
         }
         t->fast[w] = f;
     }

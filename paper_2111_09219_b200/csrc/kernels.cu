@@ -1000,6 +1000,8 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
         int32_t rem = left > 0x40000000ull ? 0x40000000 : int32_t(left);
         left -= uint64_t(rem);
         const int32_t rem0 = rem;
+        // lrem - rem is constant in the chunk: lrem >= 32 <=> rem >= rthr
+        const int32_t rthr = 32 - (lrem - rem);
         while (rem > 0) {
             if (Sink::kWrite && n >= cap) {
                 stop = true;
@@ -1010,24 +1012,26 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
             const uint32_t fe = fast_entry<ST>(ic, tsh, (dcs ? tdc : tac) + (win >> (32 - kFastBits)));
             uint32_t len, step, coefk;
             int32_t coef;
-            if ((fe & 31u) != 0 && lrem >= 32) {
-                // code + magnitude (<= 11 + 11 bits) all real: lrem >= 32
-                const uint32_t clen = fe & 31u, l = (fe >> 10) & 15u;
-                len = (fe >> 5) & 31u;
+            if ((fe & 31u) != 0 && rem >= rthr) {
+                // code + magnitude (<= 11 + 11 bits) all real: >= 32 bits to the scan end
+                const uint32_t clen = fe & 31u;
+                len = fe >> kFastLenShift;
                 const uint32_t w2 = win << clen;
-                const uint32_t v = __funnelshift_l(w2, 0u, l);  // top l bits after the code
+                // top l bits after the code (the shift count wraps mod 32; bit 9 is 0)
+                const uint32_t v = __funnelshift_l(w2, 0u, fe >> kFastLShift);
                 // extend(): a leading 1 is positive, else v - (2^l - 1)
-                coef = int32_t(v) + (int32_t(1u - (1u << l)) & ~(int32_t(w2) >> 31));
-                const uint32_t r1 = (fe >> 14) & 63u;  // run + 1 (0: EOB)
+                const uint32_t t = (fe >> kFastTShift) & 0x7FFu;
+                coef = int32_t(v - (t & ~uint32_t(int32_t(w2) >> 31)));
+                const uint32_t r1 = (fe >> kFastR1Shift) & 63u;  // run + 1 (0: EOB)
                 step = r1 ? r1 : 64u - z;
-                coefk = fe & kFastCoef;
+                coefk = (dcs || t != 0) ? 1u : 0u;
             } else {
                 const DevHuff* t = ST ? ic.huff + (dcs ? tdc : tac) / TabStride<ST>::value
                                       : reinterpret_cast<const DevHuff*>(ic.fast + (dcs ? tdc : tac));
                 uint32_t maxlen;
                 const uint32_t e = dev_lookup(t, win >> 16, maxlen);
                 const uint32_t clen = e >> 8, sym = e & 255u;
-                const uint32_t avail = uint32_t(lrem);  // >= 1 inside the range
+                const uint32_t avail = uint32_t(lrem - (rem0 - rem));  // bits to the scan end, >= 1 inside the range
                 int32_t err = 0;
                 uint32_t l = 0, run = 0;
                 bool eob = false;
@@ -1100,7 +1104,6 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
             wi += adv ? 1u : 0u;
             nw = W(wi);
             rem -= int32_t(len);
-            lrem -= int32_t(len);
             n += step;
             z += step;
             if (z >= 64) {
@@ -1125,6 +1128,7 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
             }
         }
         p += uint64_t(int64_t(rem0) - int64_t(rem));
+        lrem -= rem0 - rem;
         if (stop) break;
         // rem <= 0: the last symbol ran -rem bits past the chunk end
         const uint64_t over = uint64_t(-int64_t(rem));

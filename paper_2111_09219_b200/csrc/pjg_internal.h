@@ -43,11 +43,12 @@ constexpr int kPrimaryBits = 9;
 constexpr int kFastBits = 11;
 constexpr uint32_t kFastWords = 1u << kFastBits;
 // fast entry for a kFastBits window whose codeword fits and decodes to a
-// symbol the reference accepts: bits 0-4 codeword length (0 = take the exact
-// path), 5-9 code + magnitude length, 10-13 magnitude bits l, 14-19 run + 1
-// (0 for EOB), bit 20 EOB, bit 21 coefficient (as opposed to EOB / ZRL).  The magnitude
-// value itself is extracted arithmetically.
-constexpr uint32_t kFastEOB = 1u << 20, kFastCoef = 1u << 21;
+// symbol the reference accepts (0 = take the exact path):
+//   bits 0-4 codeword length, 5-8 magnitude bits l, bit 9 zero (so that
+//   entry >> 5 is a valid 5-bit shift count l), 10-20 2^l - 1 (extend()'s
+//   offset), 21-26 slots advanced (run + 1; 0 = EOB), 27-31 code + magnitude
+//   length.  A coefficient is written for DC symbols and for l != 0.
+constexpr uint32_t kFastLShift = 5, kFastTShift = 10, kFastR1Shift = 21, kFastLenShift = 27;
 
 struct DevHuff {
     uint32_t fast[1 << kFastBits];    // code + magnitude in one probe when both fit in kFastBits
