@@ -687,6 +687,8 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     // serial dependency chain with few warps to hide an L1 miss — stage the
     // tables in shared memory
     p.smem_tables = (b->n_huff <= kMaxSmemTables && sub < uint64_t(kK1Threads) * 148 * 4) ? b->n_huff : 0;
+    if (const char* e = getenv("PJG_SMEM_TABLES"))  // override (A/B experiments)
+        p.smem_tables = (atoi(e) && b->n_huff <= kMaxSmemTables) ? b->n_huff : 0;
     p.k1_ctas = b->k1_ctas;
     p.n_huff = b->n_huff;
     // grids that do not fill the GPU are latency-bound: a stale CTA start is

@@ -7,7 +7,7 @@ from bench import make_corpus  # noqa: E402
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "3"
 _, blob, offs, sizes = make_corpus(cfgname, 0, pinned=False)
 dec = pj.Decoder(0)
-b = dec.batch((blob, offs, sizes), pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved)
+b = dec.batch((blob, offs, sizes), pj.DecodeConfig(subsequence_bits=int(os.environ.get("SB", "1024"))), pj.OutputColorspace.RGBInterleaved)
 b.upload()
 for _ in range(4):
     b.decode()
