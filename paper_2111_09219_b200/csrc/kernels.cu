@@ -911,8 +911,32 @@ struct DecState {
 
 struct NullSink {
     static constexpr bool kWrite = false;
+    static constexpr bool kStore = false;
     __device__ __forceinline__ void put(uint32_t, int32_t) {}
     __device__ __forceinline__ void block_end(uint32_t) {}
+    __device__ __forceinline__ void sym(uint32_t) {}
+};
+
+// Sync-mode sink that also keeps the decoded symbols of one subsequence for
+// K3 to replay instead of decoding again: 16 bits per symbol, run << 12 |
+// (coefficient & 0xFFF) — DC (z == 0 on replay): the difference; AC: run and
+// the value (nonzero), EOB: run 0 value 0, ZRL: run 15 value 0.  Symbol i of
+// global subsequence g sits at [i * stride + g] (a warp of consecutive
+// subsequences reads symbol i as one 64-byte row); symbols past `cap` are
+// dropped (the tag then says so).
+struct SymSink {
+    static constexpr bool kWrite = false;
+    static constexpr bool kStore = true;
+    uint16_t* dst;     // &sym[g]
+    uint64_t stride;   // subsequences per symbol row
+    uint32_t cap;
+    uint32_t n = 0;
+    __device__ __forceinline__ void put(uint32_t, int32_t) {}
+    __device__ __forceinline__ void block_end(uint32_t) {}
+    __device__ __forceinline__ void sym(uint32_t w) {
+        if (n < cap) dst[uint64_t(n) * stride] = uint16_t(w);
+        ++n;
+    }
 };
 
 // decode_subsequence (parallel_decode.hpp:122-164) with decode_next_symbol
@@ -1025,6 +1049,7 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
                 const uint32_t r1 = (fe >> kFastR1Shift) & 63u;  // run + 1 (0: EOB)
                 step = r1 ? r1 : 64u - z;
                 coefk = (dcs || t != 0) ? 1u : 0u;
+                if (Sink::kStore) sink.sym(((r1 ? r1 - 1u : 0u) << 12) | (uint32_t(coef) & 0xFFFu));
             } else {
                 const DevHuff* t = ST ? ic.huff + (dcs ? tdc : tac) / TabStride<ST>::value
                                       : reinterpret_cast<const DevHuff*>(ic.fast + (dcs ? tdc : tac));
@@ -1080,6 +1105,7 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
                 }
                 len = clen + l;
                 step = eob ? 64u - z : run + 1u;
+                if (Sink::kStore) sink.sym((run << 12) | (uint32_t(coef) & 0xFFFu));
             }
             if (Sink::kWrite && n + step > cap) {  // phantom tail past the true end
                 stop = true;
@@ -1177,20 +1203,33 @@ __device__ __forceinline__ DcSums pack_dc(int32_t a0, int32_t a1, int32_t a2) {
 }
 
 // Sync-mode decode from (p, c, z) of the symbols starting before end_bit.
-template <bool ST = false>
-__device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t end_bit, uint64_t p, uint32_t c, uint32_t z,
-                                            Entry& e, DcSums& d) {
+template <bool ST, class Sink>
+__device__ __forceinline__ void sync_decode_sink(const ImgCtx& ic, uint64_t end_bit, uint64_t p, uint32_t c,
+                                                 uint32_t z, Entry& e, DcSums& d, Sink& sink) {
     DecState s;
     s.p = p;
     s.c = c;
     s.z = z;
     s.dc0 = s.dc1 = s.dc2 = 0;
-    NullSink sink;
-    decode_range<NullSink, ST>(ic, s, end_bit, 0, sink);
+    decode_range<Sink, ST>(ic, s, end_bit, 0, sink);
     e.p = s.p;
     e.n = s.n;
     e.czd = pack_czd(s.c, s.z, s.div);
     d = pack_dc(s.dc0, s.dc1, s.dc2);
+}
+template <bool ST = false>
+__device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t end_bit, uint64_t p, uint32_t c, uint32_t z,
+                                            Entry& e, DcSums& d) {
+    NullSink sink;
+    sync_decode_sink<ST>(ic, end_bit, p, c, z, e, d, sink);
+}
+
+// Replay tags (one per global subsequence): the start state the stored
+// symbols were decoded from, their count and the decode epoch.  K3 replays a
+// subsequence's symbols when its true start state equals the tag's: the
+// decode from one state is unique, so who produced them does not matter.
+__device__ __forceinline__ uint4 make_tag(uint64_t p, uint32_t c, uint32_t z, uint32_t nsym, uint32_t epoch) {
+    return make_uint4(uint32_t(p), uint32_t(p >> 32), c | (z << 8) | (nsym << 16), epoch);
 }
 
 // ======================================================== K1: sync pass ====
@@ -1304,7 +1343,17 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
             }
             Entry e2;
             DcSums d2;
-            sync_decode<ST>(ic, s_hi[nt], ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
+            // the chain keeps its symbols for K3 (tagged with its start state)
+            const uint64_t gt = uint64_t(cta) * TO + nt - 1;
+            SymSink ss;
+            ss.dst = P.sym + gt;
+            ss.stride = P.sym_stride;
+            ss.cap = P.sym_cap;
+            sync_decode_sink<ST>(ic, s_hi[nt], ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2, ss);
+            if (P.sym_cap)
+                reinterpret_cast<uint4*>(P.tag)[gt] =
+                    make_tag(ch.p, czd_c(ch.czd), czd_z(ch.czd), ss.n,
+                             !czd_div(e2.czd) && ss.n <= P.sym_cap ? P.epoch : 0u);
             const bool synced = sync_equal(e2.p, e2.czd, s_p[nt], s_czd[nt]);
             s_p[nt] = e2.p;
             s_n[nt] = e2.n;  // the overflow's n is authoritative (:211)
@@ -1720,6 +1769,8 @@ constexpr uint32_t kMetaNonDc = 1u << 8;
 
 struct BlockSink {
     static constexpr bool kWrite = true;
+    static constexpr bool kStore = false;
+    __device__ __forceinline__ void sym(uint32_t) {}
     const uint32_t* zt;  // smem, per zig-zag k: column-major index | (column bit | nonDC) << 8
     const float* wq3[3]; // wq rows of the image's components
     int16_t* buf;        // this thread's smem block
@@ -1791,7 +1842,7 @@ struct BlockSink {
     }
 };
 
-template <bool ST>
+template <bool ST, bool REPLAY>
 __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     __shared__ __align__(16) int16_t s_blk[kK3Threads * kBlkStride];
     __shared__ uint32_t s_zt[64];
@@ -1824,32 +1875,45 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     load_ctx<ST>(P, D, L, ic, ST ? stage_tables(P, s_fast_k3, tid, kK3Threads) : nullptr);
     ic.sacc = nullptr;  // write mode keeps its DC accumulators in registers
     ic.sacc_stride = 0;
-    {
+    DecState s;
+    s.p = 0;
+    s.c = s.z = 0;
+    if (active) {
+        if (si.j == 0) {  // segment start: the known state (restart: c = z = 0, DC reset)
+            s.p = si.lo;
+        } else {
+            Entry e = P.ent[g - 1];
+            s.p = e.p;
+            s.c = czd_c(e.czd);
+            s.z = czd_z(e.czd);
+        }
+    }
+    // symbols kept by the K1 chain that decoded this subsequence from this
+    // very start state: replay them instead of decoding
+    uint32_t nsym = 0;
+    bool replay = false;
+    if (REPLAY && active) {
+        const uint4 tg = __ldg(reinterpret_cast<const uint4*>(P.tag) + g);
+        replay = tg.w == P.epoch && tg.x == uint32_t(s.p) && tg.y == uint32_t(s.p >> 32) &&
+                 (tg.z & 0xFFFFu) == (s.c | (s.z << 8));
+        nsym = replay ? tg.z >> 16 : 0u;
+    }
+    const bool decode = active && !replay;
+    if (!REPLAY || __syncthreads_or(decode)) {  // some thread decodes: stage the CTA's scan bytes
         __shared__ int4 s_stage[kStageBytes / 16];
         __shared__ StageSmem s_sm;
         // this subsequence's bits start at entries[g-1].p (inside [lo, hi)); stage from lo
-        const uint64_t lo = active ? D.raw_off + (si.lo >> 3) : 1;
-        const uint64_t hi = active ? D.raw_off + ((si.hi + 7) >> 3) + 24 : 0;
+        const uint64_t lo = decode ? D.raw_off + (si.lo >> 3) : 1;
+        const uint64_t hi = decode ? D.raw_off + ((si.hi + 7) >> 3) + 24 : 0;
         stage_scan(P.ubuf, lo, hi, k, tid, kK3Threads, s_stage, s_sm);
         set_stage(ic, s_stage, s_sm, k);
     }
-    if (!active) return;
-    DecState s;
-    if (si.j == 0) {  // segment start: the known state (restart: c = z = 0, DC reset)
-        s.p = si.lo;
-        s.c = 0;
-        s.z = 0;
-    } else {
-        Entry e = P.ent[g - 1];
-        s.p = e.p;
-        s.c = czd_c(e.czd);
-        s.z = czd_z(e.czd);
-    }
-    const DcSums pd = P.pred[g];
+    if (!REPLAY && !active) return;
+    const DcSums pd = active ? P.pred[g] : DcSums{0, 0};
     s.dc0 = int16_t(pd.lo & 0xFFFFu);
     s.dc1 = int16_t(pd.lo >> 16);
     s.dc2 = int16_t(pd.hi & 0xFFFFu);
-    const uint64_t o = P.off[g];
+    const uint64_t o = active ? P.off[g] : 0;
     BlockSink sink;
     sink.zt = s_zt;
     {
@@ -1867,12 +1931,84 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     sink.mflags = 0;
     sink.mS = 0.f;
     sink.set_comp(uint32_t(D.du_comp >> (4 * ((o >> 6) % D.dpm))) & 15u);
-    decode_range<BlockSink, ST>(ic, s, si.hi, cap, sink);
-    if (s.err) {
-        set_status(P.ist + k, s.err);  // write mode rethrows (parallel_decode.hpp:142)
-        return;
+
+    // Replay, warp-cooperative: the warp's 32 consecutive subsequences read
+    // symbol i as one 64-byte row; rows arrive 8 at a time by cp.async, two
+    // tiles ahead, into a 3-tile ring (all lanes consume one symbol per step,
+    // so the rows are read in lockstep).
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    const uint32_t maxn = REPLAY ? __reduce_max_sync(0xFFFFFFFFu, nsym) : 0u;
+    if (REPLAY && maxn) {
+        __shared__ __align__(16) uint16_t s_rt[kK3Threads / 32][3][8 * 32];
+        const uint16_t* base = P.sym + (g - lane);
+        auto issue = [&](uint32_t kt) {
+            const uint32_t row = kt * 8 + (lane >> 2);
+            if (row < maxn)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&s_rt[warp][kt % 3][(lane >> 2) * 32 + (lane & 3) * 8])),
+                             "l"(base + uint64_t(row) * P.sym_stride + (lane & 3) * 8)
+                             : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        issue(0);
+        issue(1);
+        uint32_t c = s.c, z = s.z, n = 0;
+        int32_t a0 = s.dc0, a1 = s.dc1, a2 = s.dc2;
+        uint32_t comp = (ic.duc >> (2 * c)) & 3u;
+        int32_t acur = comp == 0 ? a0 : (comp == 1 ? a1 : a2);
+        bool live = replay;
+        for (uint32_t kt = 0; kt * 8 < maxn; ++kt) {
+            issue(kt + 2);
+            asm volatile("cp.async.wait_group 2;" ::: "memory");
+            __syncwarp();
+            const uint16_t* tile = s_rt[warp][kt % 3];
+#pragma unroll 1
+            for (uint32_t r = 0; r < 8; ++r) {
+                const uint32_t ix = kt * 8 + r;
+                live = live && ix < nsym && n < cap;
+                if (!live) continue;
+                const uint32_t w = tile[r * 32 + lane];
+                int32_t coef = int32_t(w << 20) >> 20;
+                const uint32_t run = (w >> 12) & 15u;
+                const bool dcs = z == 0;
+                // DC: one slot; AC value: run + 1; ZRL (run 15, value 0): 16; EOB: the rest
+                const uint32_t step = dcs ? 1u : (coef != 0 ? run + 1u : (run ? 16u : 64u - z));
+                if (n + step > cap) {  // phantom tail past the true end
+                    live = false;
+                    continue;
+                }
+                if (dcs) {
+                    acur += coef;
+                    coef = acur;
+                }
+                if (dcs || coef != 0) sink.put(z + step - 1, coef);
+                n += step;
+                z += step;
+                if (z >= 64) {
+                    if (comp == 0)
+                        a0 = acur;
+                    else if (comp == 1)
+                        a1 = acur;
+                    else
+                        a2 = acur;
+                    z = 0;
+                    c = (c + 1 == ic.dpm) ? 0 : c + 1;
+                    comp = (ic.duc >> (2 * c)) & 3u;
+                    acur = comp == 0 ? a0 : (comp == 1 ? a1 : a2);
+                    sink.block_end(comp);
+                }
+            }
+            __syncwarp();  // the tile is consumed before issue(kt + 3) refills its slot
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    sink.finish();
+    if (decode) {
+        decode_range<BlockSink, ST>(ic, s, si.hi, cap, sink);
+        if (s.err) {
+            set_status(P.ist + k, s.err);  // write mode rethrows (parallel_decode.hpp:142)
+            return;
+        }
+    }
+    if (active) sink.finish();
 }
 
 // ============================================ K4: IDCT + upsample + RGB ====
@@ -2757,18 +2893,24 @@ void launch_k1c_fixup(const Params& p, void* stream) {
 void launch_k2_scan(const Params& p, void* stream) {
     if (p.k2_tiles) k2_scan<<<p.k2_tiles, kK2Threads, 0, (cudaStream_t)stream>>>(p);
 }
-void launch_k3_write(const Params& p, void* stream) {
-    if (!p.total_subs) return;
+template <bool ST, bool REPLAY>
+static void launch_k3_variant(const Params& p, unsigned grid, cudaStream_t s) {
     static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k3_write<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemTables * kFastWords * 4);
+    if (ST && !attr) {
+        cudaFuncSetAttribute(k3_write<ST, REPLAY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kMaxSmemTables * kFastWords * 4);
         attr = true;
     }
+    k3_write<ST, REPLAY><<<grid, kK3Threads, ST ? size_t(p.smem_tables) * kFastWords * 4 : 0, s>>>(p);
+}
+void launch_k3_write(const Params& p, void* stream) {
+    if (!p.total_subs) return;
     const unsigned grid = unsigned((p.total_subs + kK3Threads - 1) / kK3Threads);
+    cudaStream_t s = (cudaStream_t)stream;
     if (p.smem_tables)
-        k3_write<true><<<grid, kK3Threads, size_t(p.smem_tables) * kFastWords * 4, (cudaStream_t)stream>>>(p);
+        p.sym_cap ? launch_k3_variant<true, true>(p, grid, s) : launch_k3_variant<true, false>(p, grid, s);
     else
-        k3_write<false><<<grid, kK3Threads, 0, (cudaStream_t)stream>>>(p);
+        p.sym_cap ? launch_k3_variant<false, true>(p, grid, s) : launch_k3_variant<false, false>(p, grid, s);
 }
 void launch_k4_transform(const Params& p, void* stream) {
     if (!p.k4_tiles) return;

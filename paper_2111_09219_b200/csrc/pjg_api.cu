@@ -90,7 +90,7 @@ struct pjg_ctx {
     bool busy = false;
     double basis[64];
     cudaEvent_t ev[kNumEvents] = {};
-    DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out, segs,
+    DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out, segs, sym, tag,
         counters, k0_flag, k0_agg, k2_flag, k2_agg, stats;
     HostBuf stage, meta_host, status_host, desc_host;
     // Per-image host arrays, lent to the live batch and taken back at destroy:
@@ -255,7 +255,7 @@ int pjg_ctx_create(int device, pjg_ctx** out) {
     CU(cudaSetDevice(device), "cudaSetDevice");
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : c->ev) CU(cudaEventCreate(&e), "cudaEventCreate");
-    c->k0_flag.zero = c->k2_flag.zero = c->k1_flag.zero = true;
+    c->k0_flag.zero = c->k2_flag.zero = c->k1_flag.zero = c->tag.zero = true;
     // IdctBasis (transform.hpp:93-108): the same host libm expression.
     for (int u = 0; u < 8; ++u) {
         double cu = u == 0 ? 1.0 / std::sqrt(2.0) : 1.0;
@@ -271,7 +271,7 @@ void pjg_ctx_destroy(pjg_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->raw, &c->ubuf, &c->meta, &c->blkmeta, &c->ent, &c->dcs, &c->off, &c->cap, &c->pred,
                       &c->cta_end, &c->cta_start, &c->k1_flag, &c->coef, &c->out, &c->counters,
-                      &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats, &c->segs})
+                      &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats, &c->segs, &c->sym, &c->tag})
         b->release();
     c->stage.release();
     c->meta_host.release();
@@ -649,6 +649,28 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     CU(ctx->pred.ensure(subs * sizeof(DcSums)), "cudaMalloc(pred)");
     CU(ctx->cta_end.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_end)");
     CU(ctx->cta_start.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_start)");
+    // K1 chains keep their decoded symbols for K3 to replay (16 bits each, up
+    // to sb/4 per subsequence: 4 bytes of scratch per compressed byte) when it
+    // pays: measured break-even — many symbols per data unit
+    // (K3's decode dominates its block work) but a stream that syncs in few
+    // rounds (K1 stores each chain's symbols once per round): 64..160 scan
+    // bits per data unit.  PJG_REPLAY=0/1 forces it.
+    bool replay_on = false;
+    {
+        uint64_t bits = 0;
+        for (size_t i = 0; i < n; ++i)
+            if (b->host_status[i] == kOk) bits += desc[i].raw_len * 8;
+        const uint64_t per_du = du ? bits / du : 0;
+        replay_on = per_du >= 64 && per_du <= 160;
+        if (const char* e = getenv("PJG_REPLAY")) replay_on = atoi(e) != 0;
+        if (getenv("PJG_NO_REPLAY")) replay_on = false;
+    }
+    const uint32_t sym_cap = (!replay_on || sb > 65536) ? 0u : uint32_t(sb / 4);
+    const uint64_t sym_stride = align_up(subs, 64);
+    if (sym_cap) {
+        CU(ctx->sym.ensure(sym_stride * sym_cap * 2), "cudaMalloc(sym)");
+        CU(ctx->tag.ensure(subs * 16), "cudaMalloc(tag)");
+    }
     CU(ctx->k1_flag.ensure((b->k1_ctas + 1) * 4), "cudaMalloc(k1_flag)");
     CU(ctx->coef.ensure(std::max<uint64_t>(du, 1) * 128), "cudaMalloc(coef)");
     CU(ctx->segs.ensure(std::max<uint64_t>(seg_total, 1) * sizeof(uint2)), "cudaMalloc(segs)");
@@ -706,6 +728,10 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.pred = ctx->pred.as<DcSums>();
     p.cta_end = ctx->cta_end.as<Entry>();
     p.cta_start = ctx->cta_start.as<Entry>();
+    p.sym = sym_cap ? ctx->sym.as<uint16_t>() : nullptr;
+    p.tag = sym_cap ? ctx->tag.as<uint32_t>() : nullptr;
+    p.sym_stride = sym_stride;
+    p.sym_cap = sym_cap;
     p.k1_flag = ctx->k1_flag.as<uint32_t>();
     p.k2_tiles = b->k2_tiles;
     p.k4_tiles = k4t;

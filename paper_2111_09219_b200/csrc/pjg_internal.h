@@ -199,6 +199,10 @@ struct Params {
     DcSums* pred;                  // DC predictor at the start of each subsequence
     Entry* cta_end;                // K1: each CTA's last entry after intra sync
     Entry* cta_start;              // K1: start state each CTA's inter overflow used
+    uint16_t* sym;                 // K1 chains' decoded symbols: symbol i of subsequence g at [i * sym_stride + g]
+    uint32_t* tag;                 // 4 words per subsequence: start state / count / epoch of its stored symbols
+    uint64_t sym_stride;           // >= total_subs, multiple of 64
+    uint32_t sym_cap;              // symbols kept per subsequence (0: K3 always decodes)
     uint32_t* k1_flag;
     uint32_t k2_tiles;
     uint32_t k4_tiles;

@@ -54,12 +54,15 @@ def test_acceptance_corpus_rgb_bit_exact(decoder):
             assert np.array_equal(got, ref.data), (w, h, q, s, int((got != ref.data).sum()))
 
 
+@pytest.mark.parametrize("replay", ["on", "off"])
 @pytest.mark.parametrize("hop", ["0", "1"])
 @pytest.mark.parametrize("sb", [128, 256, 1024, 4096])
-def test_acceptance_corpus_entropy_and_states(decoder, sb, hop, monkeypatch):
+def test_acceptance_corpus_entropy_and_states(decoder, sb, hop, replay, monkeypatch):
     # both K1 inter-CTA modes: speculative starts checked by K1c's parallel
-    # first pass (hop=0, full grids) and the in-kernel re-chain (hop=1, small grids)
+    # first pass (hop=0, full grids) and the in-kernel re-chain (hop=1, small
+    # grids); K3 replaying K1's kept symbols or decoding every subsequence
     monkeypatch.setenv("PJG_K1_HOP", hop)
+    monkeypatch.setenv("PJG_REPLAY", "1" if replay == "on" else "0")
     corpus = acceptance_corpus()
     files = [f for _, f in corpus]
     with decoder.batch(files, pj.DecodeConfig(subsequence_bits=sb), pj.OutputColorspace.YCbCrPlanes) as b:
