@@ -110,6 +110,19 @@ void* pjg_ctx_stream(pjg_ctx* ctx);       /* the context's cudaStream_t */
 /* ---- header-only inspection (parse(), parser.hpp:264-347, host) ------- */
 int pjg_inspect(const uint8_t* file, size_t size, uint32_t output, pjg_image_info* info);
 
+/* The parsed frame/tables as the reference CLI's `inspect` prints them
+ * (pjpeg_cli.cpp:99-125: FrameInfo, parser.hpp:56-85, and table presence). */
+typedef struct pjg_header_info {
+    uint32_t width, height, num_components;
+    uint32_t comp_id[3], comp_h[3], comp_v[3], comp_tq[3], comp_td[3], comp_ta[3];
+    uint32_t mcu_width, mcu_height, mcus_x, mcus_y, data_units_per_mcu;
+    uint64_t total_data_units;
+    uint32_t quant_tables, dc_tables, ac_tables; /* tables present */
+    uint32_t restart_interval;                   /* DRI Ri (only with allow_dri) */
+    uint64_t scan_offset;                        /* first entropy-coded byte */
+} pjg_header_info;
+int pjg_inspect_header(const uint8_t* file, size_t size, int allow_dri, pjg_header_info* out);
+
 /* ---- one-shot host API ------------------------------------------------ */
 /* decode_single (pipeline.hpp:103-143) [+ upsample_and_convert (:167-201)
  * when cfg->output == PJG_OUT_RGB]: host file in, host output out. */

@@ -219,7 +219,7 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "pjg_ctx_create", "pjg_ctx_destroy", "pjg_last_error", "pjg_status_name", "pjg_default_config",
-    "pjg_ctx_stream", "pjg_inspect", "pjg_decode", "pjg_decode_batch", "pjg_batch_create",
+    "pjg_ctx_stream", "pjg_inspect", "pjg_inspect_header", "pjg_decode", "pjg_decode_batch", "pjg_batch_create",
     "pjg_batch_upload", "pjg_batch_decode", "pjg_batch_synchronize", "pjg_batch_download",
     "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_copy_outputs", "pjg_batch_scan_bits", "pjg_batch_kernel_launches", "pjg_batch_download_all", "pjg_batch_download_all_async", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
     "pjg_batch_sync_stats", "pjg_batch_destroy", "pjg_batch_dump_coefficients",

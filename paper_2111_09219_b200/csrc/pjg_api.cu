@@ -293,6 +293,37 @@ int pjg_inspect(const uint8_t* file, size_t size, uint32_t output, pjg_image_inf
     return h.status;
 }
 
+int pjg_inspect_header(const uint8_t* file, size_t size, int allow_dri, pjg_header_info* out) {
+    if (!file || !out) return PJG_INVALID_ARGUMENT;
+    std::memset(out, 0, sizeof(*out));
+    const Header h = parse_header(file, size, allow_dri != 0);
+    out->width = h.width;
+    out->height = h.height;
+    out->num_components = uint32_t(h.comps.size());
+    for (size_t c = 0; c < h.comps.size() && c < 3; ++c) {
+        out->comp_id[c] = h.comps[c].id;
+        out->comp_h[c] = h.comps[c].h;
+        out->comp_v[c] = h.comps[c].v;
+        out->comp_tq[c] = h.comps[c].tq;
+        out->comp_td[c] = h.comps[c].td;
+        out->comp_ta[c] = h.comps[c].ta;
+    }
+    out->mcu_width = 8 * h.h_max;
+    out->mcu_height = 8 * h.v_max;
+    out->mcus_x = h.mcus_x;
+    out->mcus_y = h.mcus_y;
+    out->data_units_per_mcu = h.dpm;
+    out->total_data_units = h.total_dus();
+    for (int t = 0; t < 4; ++t) {
+        out->quant_tables += h.quant_present[t] ? 1u : 0u;
+        out->dc_tables += h.dc[t].present ? 1u : 0u;
+        out->ac_tables += h.ac[t].present ? 1u : 0u;
+    }
+    out->restart_interval = h.restart_interval;
+    out->scan_offset = h.scan_start;
+    return h.status;
+}
+
 int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const size_t* sizes,
                      const pjg_config* cfg, pjg_batch** out) {
     if (!ctx || !out || (n && (!files || !sizes))) return PJG_INVALID_ARGUMENT;

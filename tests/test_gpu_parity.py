@@ -247,6 +247,43 @@ def test_cpp_dropin_binary_matches_reference(tmp_path):
     assert ("IDENTICAL" in r.stdout) or ("ref:" not in r.stdout)
 
 
+def test_cli_decode_inspect_bench(tmp_path):
+    """The reference CLI's commands (tools/pjpeg_cli.cpp) over the GPU decoder:
+    decode writes the reference's RGB as PPM, inspect prints the parsed frame,
+    bench prints the reference's row keys (+ RGB GB/s)."""
+    import json
+    import subprocess
+    from tests.test_host import _cli
+    exe = _cli()
+    f = ref_jpeg(333, 257, 6, 95, "422")
+    src = tmp_path / "a.jpg"
+    src.write_bytes(f)
+    out = tmp_path / "a.ppm"
+    r = subprocess.run([exe, "decode", str(src), str(out)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    data = out.read_bytes()
+    header = b"P6\n333 257\n255\n"
+    assert data.startswith(header)
+    ref = Ref.decode(f, rgb=True)
+    assert np.array_equal(np.frombuffer(data[len(header):], np.uint8).reshape(ref.data.shape), ref.data)
+    r = subprocess.run([exe, "inspect", str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    info = pj.inspect(f)
+    assert "size: 333x257" in r.stdout and "components: 3" in r.stdout
+    assert f"total data units: {info['data_units']}" in r.stdout
+    assert "partition (s*32=1024, b=256): N=" in r.stdout
+    bdir = tmp_path / "corpus"
+    bdir.mkdir()
+    for k in range(3):
+        (bdir / f"{k}.jpg").write_bytes(ref_jpeg(96 + 16 * k, 80, 100 + k, 75, "420"))
+    r = subprocess.run([exe, "bench", str(bdir), "--iterations", "2"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    row = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("batch", "config", "wall_ms", "stages", "mb_per_s", "checksum", "rgb_gb_s", "images_per_s"):
+        assert key in row, key
+    assert row["batch"] == 3 and "failures" not in row
+
+
 def test_decode_to_cuda_tensors():
     """CUDA uint8 torch tensors straight from the device output (D2D copies on
     the decoder's stream), equal to the reference; failed files give None."""

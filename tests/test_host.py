@@ -160,3 +160,26 @@ def _build_dropin(tmp_path):
 
 def test_cpp_dropin_header_builds_and_links(tmp_path):
     assert os.path.exists(_build_dropin(tmp_path))
+
+
+def _cli():
+    """The pjpeg_gpu CLI (tools/pjpeg_gpu_cli.cpp), built by the library Makefile."""
+    import subprocess
+    exe = os.path.join(ROOT, "paper_2111_09219_b200", "pjpeg_gpu")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "paper_2111_09219_b200", "csrc")], check=True,
+                       capture_output=True)
+    return exe
+
+
+def test_cli_usage_and_exit_codes(tmp_path):
+    """pjpeg_cli.cpp's conventions: usage errors, 10 + Errc on failures (no GPU needed)."""
+    import subprocess
+    exe = _cli()
+    assert subprocess.run([exe], capture_output=True).returncode == 2
+    assert subprocess.run([exe, "frobnicate"], capture_output=True).returncode == 2
+    r = subprocess.run([exe, "decode", str(tmp_path / "missing.jpg"), str(tmp_path / "o.ppm")],
+                       capture_output=True, text=True)
+    assert r.returncode == 10 + 10, r.stderr  # Errc::IoError
+    r = subprocess.run([exe, "bench", str(tmp_path)], capture_output=True, text=True)
+    assert r.returncode == 10 + 9, r.stderr  # Errc::EmptyCorpus
