@@ -514,7 +514,9 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         n_ok += W.n_ok;
     }
     // K0 tile size: 32 KB windows when the scans are large on average, else 8 KB
-    const uint32_t k0_bpt = (n_ok && raw_sum / n_ok >= 48 * 1024) ? kK0BigBpt : kK0SmallBpt;
+    uint32_t k0_bpt = (n_ok && raw_sum / n_ok >= 48 * 1024) ? kK0BigBpt : kK0SmallBpt;
+    if (const char* e = getenv("PJG_K0_BPT"))  // override (A/B experiments): 16 or 64
+        k0_bpt = atoi(e) == int(kK0BigBpt) ? kK0BigBpt : kK0SmallBpt;
     const uint64_t k0_tile = uint64_t(kK0Threads) * k0_bpt;
     // raw extent: contiguous user region or pack
     b->packed = !(lo && uint64_t(hi - lo) <= raw_sum + raw_sum / 2 + (1u << 20));

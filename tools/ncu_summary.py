@@ -35,6 +35,13 @@ def main(path, segments=True):
             print(f"{name:70s} {v[h.index(name)]:>20s} {u[h.index(name)]}")
     if not segments:
         return
+    try:
+        segments_table(path)
+    except Exception as e:  # the source page differs between kernels/ncu versions
+        print(f"(per-segment table unavailable: {type(e).__name__})")
+
+
+def segments_table(path):
     src = list(csv.reader(io.StringIO(run([path] + KERNEL + ["--page", "source", "--csv", "--print-source=sass"]))))
     hdr, data = src[1], src[2:]
     iA, iS, iE = hdr.index("Address"), hdr.index("Source"), hdr.index("Instructions Executed")
