@@ -779,7 +779,6 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.k2_agg = ctx->k2_agg.as<uint64_t>();
     p.stats = ctx->stats.as<unsigned long long>();
     mark("reserve");
-    p.debug = getenv("PJG_K4_DEBUG") ? uint32_t(atoi(getenv("PJG_K4_DEBUG"))) : 0u;
 
     ctx->busy = true;
     *out = b.release();

@@ -219,7 +219,6 @@ struct Params {
     uint64_t* k2_agg;              // 4 x uint64 per tile: aggregate (n|head, dc), inclusive (n, dc)
     // stats
     unsigned long long* stats;     // see StatIndex
-    uint32_t debug;                // K4 ablation bits (PJG_K4_DEBUG), 0 in production
     uint32_t pad3;
 };
 
