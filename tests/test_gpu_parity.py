@@ -297,3 +297,25 @@ def test_decode_to_cuda_tensors():
         ref = Ref.decode(f, rgb=True).data
         assert tuple(t.shape) == ref.shape
         assert np.array_equal(t.cpu().numpy(), ref)
+
+
+def test_large_thumbnail_batch_parallel_planner(decoder):
+    """A batch large enough for the multi-threaded host planner (contiguous
+    per-worker chunks, per-worker table dedup merged afterwards): 1,536 small
+    files with three quality/sampling mixes (distinct tables), in one region and
+    packed from separate buffers; every image RGB-exact against the C oracle."""
+    from paper_2111_09219_b200.synth import synth_batch
+    files = []
+    for q, smp, seed in ((50, "420", 1), (75, "444", 2), (95, "gray", 3)):
+        blob, offs, sizes = synth_batch(512, 40, 24, 7000 + 1000 * seed, q, smp)
+        files += [blob[int(o): int(o) + int(s)].tobytes() for o, s in zip(offs, sizes)]
+    order = np.random.default_rng(5).permutation(len(files))
+    files = [files[i] for i in order]
+    with decoder.batch(files, pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved) as b:
+        st = b.run()
+        assert (st == 0).all(), np.unique(st)
+        outs = b.download()
+    for i, f in enumerate(files):
+        want = Orc.decode(f, rgb=True)
+        assert want.status == 0
+        assert np.array_equal(outs[i][: want.data.size], want.data.reshape(-1)), i
