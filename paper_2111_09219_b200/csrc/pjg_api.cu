@@ -194,23 +194,6 @@ bool validate_cfg(pjg_ctx* ctx, const pjg_config* cfg, int* st) {
     return true;
 }
 
-void parallel_memcpy(uint8_t* dst, const std::vector<std::pair<const uint8_t*, size_t>>& src,
-                     const std::vector<size_t>& dst_off) {
-    size_t total = 0;
-    for (auto& s : src) total += s.second;
-    unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    if (total < (8u << 20) || hw == 1) {
-        for (size_t i = 0; i < src.size(); ++i) std::memcpy(dst + dst_off[i], src[i].first, src[i].second);
-        return;
-    }
-    std::vector<std::thread> th;
-    for (unsigned w = 0; w < hw; ++w)
-        th.emplace_back([&, w] {
-            for (size_t i = w; i < src.size(); i += hw) std::memcpy(dst + dst_off[i], src[i].first, src[i].second);
-        });
-    for (auto& t : th) t.join();
-}
-
 }  // namespace
 
 // ====================================================================== API
@@ -520,66 +503,143 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     const uint64_t k0_tile = uint64_t(kK0Threads) * k0_bpt;
     // raw extent: contiguous user region or pack
     b->packed = !(lo && uint64_t(hi - lo) <= raw_sum + raw_sum / 2 + (1u << 20));
-    uint64_t sub = 0, du = 0, outb = 0, seg_total = 0;
-    std::vector<uint32_t> dri;  // images with restart intervals
-    uint32_t k0t = 0, k4t = 0;
+    // Per image: global table ids, the restart-interval check, and its counts
+    // (K0 tiles, subsequences, data units, K4 tiles, output bytes, segments,
+    // packed bytes) — pass 1, per worker chunk; chunk totals are scanned
+    // serially; pass 2 assigns every image its offsets (and copies its scan
+    // into the pinned stage when packing).
+    struct Counts {
+        uint64_t pack = 0, sub = 0, du = 0, outb = 0, seg = 0;
+        uint32_t k0t = 0, k4t = 0, ndri = 0;
+    };
+    std::vector<Counts> ctot(nw + 1);
     std::vector<uint32_t> k0_first(n + 1), tile_first(n + 1);
     std::vector<uint64_t> sub_first(n + 1);
-    uint64_t pack_off = 0;
-    std::vector<std::pair<const uint8_t*, size_t>> pk_src;
-    std::vector<size_t> pk_dst;
-    for (size_t i = 0; i < n; ++i) {
-        ImgDesc& d = desc[i];
-        k0_first[i] = k0t;
-        tile_first[i] = k4t;
-        sub_first[i] = sub;
-        d.sub_first = sub;
-        d.du_first = du;
-        d.out_off = outb;
-        if (b->host_status[i] != kOk) continue;
-        const size_t rl = d.raw_len;
-        const uint8_t* s = reinterpret_cast<const uint8_t*>(uintptr_t(d.raw_off));
-        if (b->packed) {
-            d.raw_off = pack_off;
-            pk_src.emplace_back(s, rl);
-            pk_dst.push_back(pack_off);
-            pack_off = align_up(pack_off + rl, 16);
-        } else {
-            d.raw_off = uint64_t(s - lo);
-        }
-        const unsigned w = unsigned(i / chunk);
-        for (uint32_t c = 0; c < d.ncomp; ++c) {
-            if (d.deferred == kOk) {
-                d.dc_tab[c] = huff_map[w][d.dc_tab[c]];
-                d.ac_tab[c] = huff_map[w][d.ac_tab[c]];
+    auto pass1 = [&](unsigned w) {
+        Counts t;
+        const size_t i1 = std::min(n, (w + 1) * chunk);
+        for (size_t i = w * chunk; i < i1; ++i) {
+            ImgDesc& d = desc[i];
+            if (b->host_status[i] != kOk) continue;
+            const size_t rl = d.raw_len;
+            const uint8_t* s = reinterpret_cast<const uint8_t*>(uintptr_t(d.raw_off));
+            if (!b->packed) d.raw_off = uint64_t(s - lo);  // packed: assigned in pass 2 (16-aligned)
+            for (uint32_t c = 0; c < d.ncomp; ++c) {
+                if (d.deferred == kOk) {
+                    d.dc_tab[c] = huff_map[w][d.dc_tab[c]];
+                    d.ac_tab[c] = huff_map[w][d.ac_tab[c]];
+                }
+                d.q_tab[c] = quant_map[w][d.q_tab[c]];
             }
-            d.q_tab[c] = quant_map[w][d.q_tab[c]];
+            if (b->packed) t.pack += align_up(rl, 16);
+            // K0 tiles always run (scan checks precede table errors); 16-byte-grid windows
+            t.k0t += uint32_t((((b->packed ? 0 : d.raw_off) & 15) + rl + k0_tile - 1) / k0_tile);
+            if (d.deferred != kOk) continue;
+            if (d.n_int > 1) {
+                // restart intervals: one subsequence partition per interval (K0b), at
+                // most ceil(bits / sb) + intervals subsequences; segment bit offsets
+                // are 32-bit
+                if (uint64_t(rl) * 8 >= (1ull << 32)) {
+                    b->host_status[i] = kUnsupportedFeature;
+                    d.n_int = 1;
+                    d.ri = 0;
+                    d.expected = 0;
+                    d.mcus_per_tile = 0;
+                    d.tiles_x = 0;
+                    d.pad1 = 1;  // placed in pass 2 like an accepted scan (K0 still runs)
+                    continue;
+                }
+                t.seg += d.n_int + 1;
+                d.sub_count += d.n_int;
+                ++t.ndri;
+            }
+            t.sub += d.sub_count;
+            t.du += d.expected / 64;
+            t.k4t += d.tiles_x * d.mcus_y;
+            t.outb += align_up(b->info[i].output_bytes, 256);
         }
-        // K0 tiles always run (scan checks precede table errors)
-        k0t += uint32_t(((d.raw_off & 15) + rl + k0_tile - 1) / k0_tile);  // 16-byte-grid windows
-        if (d.deferred != kOk) continue;
-        if (d.n_int > 1) {
-            // restart intervals: one subsequence partition per interval (K0b), at
-            // most ceil(bits / sb) + intervals subsequences; segment bit offsets are
-            // 32-bit
-            if (uint64_t(rl) * 8 >= (1ull << 32)) {
-                b->host_status[i] = kUnsupportedFeature;
-                d.n_int = 1;
-                d.ri = 0;
-                d.expected = 0;
-                d.mcus_per_tile = 0;
-                d.tiles_x = 0;
+        ctot[w] = t;
+    };
+    auto run_chunks = [&](auto&& fn) {
+        if (nw > 1) {
+            std::vector<std::thread> th;
+            for (unsigned w = 0; w < nw; ++w) th.emplace_back(fn, w);
+            for (auto& t : th) t.join();
+        } else {
+            fn(0u);
+        }
+    };
+    run_chunks(pass1);
+    // exclusive scan of the chunk totals
+    Counts run;
+    for (unsigned w = 0; w <= nw; ++w) {
+        const Counts t = w < nw ? ctot[w] : Counts{};
+        ctot[w] = run;
+        run.pack += t.pack;
+        run.sub += t.sub;
+        run.du += t.du;
+        run.outb += t.outb;
+        run.seg += t.seg;
+        run.k0t += t.k0t;
+        run.k4t += t.k4t;
+        run.ndri += t.ndri;
+    }
+    const uint64_t pack_off = run.pack, sub = run.sub, du = run.du, outb = run.outb, seg_total = run.seg;
+    const uint32_t k0t = run.k0t, k4t = run.k4t;
+    std::vector<uint32_t> dri(run.ndri);  // images with restart intervals
+    if (b->packed) CU(ctx->stage.ensure(pack_off + 64), "cudaMallocHost(stage)");
+    uint8_t* const stage = b->packed ? static_cast<uint8_t*>(ctx->stage.p) : nullptr;
+    std::vector<const uint8_t*> srcp(b->packed ? n : 0, nullptr);  // packed: each scan's source
+    auto pass2 = [&](unsigned w) {
+        Counts t = ctot[w];
+        const size_t i1 = std::min(n, (w + 1) * chunk);
+        for (size_t i = w * chunk; i < i1; ++i) {
+            ImgDesc& d = desc[i];
+            k0_first[i] = t.k0t;
+            tile_first[i] = t.k4t;
+            sub_first[i] = t.sub;
+            d.sub_first = t.sub;
+            d.du_first = t.du;
+            d.out_off = t.outb;
+            if (b->host_status[i] != kOk) {
+                if (d.pad1) {  // a restart-interval scan rejected in pass 1 still runs K0
+                    d.pad1 = 0;
+                    const size_t rl = d.raw_len;
+                    if (b->packed) {
+                        srcp[i] = reinterpret_cast<const uint8_t*>(uintptr_t(d.raw_off));
+                        d.raw_off = t.pack;
+                        t.pack += align_up(rl, 16);
+                    }
+                    t.k0t += uint32_t(((d.raw_off & 15) + rl + k0_tile - 1) / k0_tile);
+                }
                 continue;
             }
-            d.seg_first = seg_total;
-            seg_total += d.n_int + 1;
-            d.sub_count += d.n_int;
-            dri.push_back(uint32_t(i));
+            const size_t rl = d.raw_len;
+            if (b->packed) {
+                srcp[i] = reinterpret_cast<const uint8_t*>(uintptr_t(d.raw_off));
+                d.raw_off = t.pack;
+                t.pack += align_up(rl, 16);
+            }
+            t.k0t += uint32_t(((d.raw_off & 15) + rl + k0_tile - 1) / k0_tile);
+            if (d.deferred != kOk) continue;
+            if (d.n_int > 1) {
+                d.seg_first = t.seg;
+                t.seg += d.n_int + 1;
+                dri[t.ndri++] = uint32_t(i);
+            }
+            t.sub += d.sub_count;
+            t.du += d.expected / 64;
+            t.k4t += d.tiles_x * d.mcus_y;
+            t.outb += align_up(b->info[i].output_bytes, 256);
         }
-        sub += d.sub_count;
-        du += d.expected / 64;
-        k4t += d.tiles_x * d.mcus_y;
-        outb = align_up(outb + b->info[i].output_bytes, 256);
+    };
+    run_chunks(pass2);
+    if (b->packed) {  // the scans into the pinned stage, images interleaved across workers
+        auto copy = [&](unsigned w) {
+            for (size_t i = w; i < n; i += nw)
+                if (srcp[i]) std::memcpy(stage + desc[i].raw_off, srcp[i], desc[i].raw_len);
+        };
+        run_chunks(copy);
     }
     k0_first[n] = k0t;
     tile_first[n] = k4t;
@@ -598,11 +658,9 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     b->k2_tiles = uint32_t((sub + kK2Threads - 1) / kK2Threads);
     mark("layout");
 
-    // ---- raw bytes: user region or pinned staging
+    // ---- raw bytes: user region or the pinned stage (filled in pass 2)
     if (b->packed) {
-        CU(ctx->stage.ensure(pack_off + 64), "cudaMallocHost(stage)");
-        parallel_memcpy(static_cast<uint8_t*>(ctx->stage.p), pk_src, pk_dst);
-        b->raw_src = static_cast<const uint8_t*>(ctx->stage.p);
+        b->raw_src = stage;
         b->raw_bytes = pack_off;
     } else {
         b->raw_src = lo;
@@ -610,6 +668,9 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     }
 
     mark("raw");
+    if (timing)
+        fprintf(stderr, "pjg_batch_create packed=%d raw_bytes=%llu pinned=%d\n", int(b->packed),
+                (unsigned long long)b->raw_bytes, int(b->raw_src == ctx->stage.p));
     // ---- meta blob
     size_t o = 0;
     b->m_desc = o;
@@ -687,14 +748,16 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     // pays: measured break-even — many symbols per data unit
     // (K3's decode dominates its block work) but a stream that syncs in few
     // rounds (K1 stores each chain's symbols once per round): 64..160 scan
-    // bits per data unit.  PJG_REPLAY=0/1 forces it.
+    // bits per data unit, in images of >= 64 subsequences on average.
+    // PJG_REPLAY=0/1 forces it.
     bool replay_on = false;
     {
         uint64_t bits = 0;
         for (size_t i = 0; i < n; ++i)
             if (b->host_status[i] == kOk) bits += desc[i].raw_len * 8;
         const uint64_t per_du = du ? bits / du : 0;
-        replay_on = per_du >= 64 && per_du <= 160;
+        // (and large images: a few subsequences per image keep K3 cheap)
+        replay_on = per_du >= 64 && per_du <= 160 && n_ok && sub / n_ok >= 64;
         if (const char* e = getenv("PJG_REPLAY")) replay_on = atoi(e) != 0;
         if (getenv("PJG_NO_REPLAY")) replay_on = false;
     }
