@@ -17,6 +17,10 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -80,6 +84,76 @@ struct HostBuf {  // pinned
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Host worker threads of a context, started once: batch planning runs a few
+// parallel passes per batch, and spawning threads for each cost more than the
+// passes themselves on thumbnail batches.
+class WorkerPool {
+public:
+    ~WorkerPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    // fn(0..n-1), the calling thread taking part; returns when all are done
+    void run(unsigned n, const std::function<void(unsigned)>& fn) {
+        if (n <= 1) {
+            if (n) fn(0);
+            return;
+        }
+        start(n - 1);
+        {
+            std::lock_guard<std::mutex> g(m_);
+            job_ = &fn;
+            njobs_ = n;
+            next_.store(0);
+            pending_ = n;
+            ++gen_;
+        }
+        cv_.notify_all();
+        work();
+        std::unique_lock<std::mutex> g(m_);
+        done_.wait(g, [&] { return pending_ == 0; });
+        job_ = nullptr;
+    }
+
+private:
+    void start(unsigned want) {
+        while (th_.size() < want) th_.emplace_back([this] { loop(); });
+    }
+    void work() {
+        for (;;) {
+            const unsigned i = next_.fetch_add(1);
+            if (i >= njobs_) return;
+            (*job_)(i);
+            std::lock_guard<std::mutex> g(m_);
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+            }
+            work();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(unsigned)>* job_ = nullptr;
+    unsigned njobs_ = 0, pending_ = 0;
+    std::atomic<unsigned> next_{0};
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
 }  // namespace
 
 struct pjg_ctx {
@@ -93,6 +167,7 @@ struct pjg_ctx {
     DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out, segs, sym, tag,
         counters, k0_flag, k0_agg, k2_flag, k2_agg, stats;
     HostBuf stage, meta_host, status_host, desc_host;
+    WorkerPool pool_threads;
     // Per-image host arrays, lent to the live batch and taken back at destroy:
     // thumbnail batches hold tens of thousands of images, and fresh vectors
     // would be mmap'd and page-faulted again on every batch.
@@ -431,13 +506,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
             d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
         }
     };
-    if (nw > 1) {
-        std::vector<std::thread> th;
-        for (unsigned w = 0; w < nw; ++w) th.emplace_back(phase_a, w);
-        for (auto& t : th) t.join();
-    } else {
-        phase_a(0);
-    }
+    ctx->pool_threads.run(nw, phase_a);
     mark("parse");
 
     // ---- tables: merge the workers' unique lists (batches almost always share
@@ -560,15 +629,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         }
         ctot[w] = t;
     };
-    auto run_chunks = [&](auto&& fn) {
-        if (nw > 1) {
-            std::vector<std::thread> th;
-            for (unsigned w = 0; w < nw; ++w) th.emplace_back(fn, w);
-            for (auto& t : th) t.join();
-        } else {
-            fn(0u);
-        }
-    };
+    auto run_chunks = [&](const std::function<void(unsigned)>& fn) { ctx->pool_threads.run(nw, fn); };
     run_chunks(pass1);
     // exclusive scan of the chunk totals
     Counts run;
