@@ -26,6 +26,7 @@
 // fl(s + (+-0)) == s for s != -0 and s starts at +0); rounding is lround
 // (half away from zero) followed by +128, as transform.hpp:141.
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <stdint.h>
 
 #include <algorithm>
@@ -1345,12 +1346,18 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
             DcSums d2;
             // the chain keeps its symbols for K3 (tagged with its start state)
             const uint64_t gt = uint64_t(cta) * TO + nt - 1;
-            SymSink ss;
-            ss.dst = P.sym + gt;
-            ss.stride = P.sym_stride;
-            ss.cap = P.sym_cap;
+            // (small batches, ST: never replayed — the planner enables replay only
+            // for large ones; the plain sink also compiles better there)
+            using ChainSink = typename std::conditional<ST, NullSink, SymSink>::type;
+            ChainSink ss;
+            if constexpr (!ST) {
+                ss.dst = P.sym + gt;
+                ss.stride = P.sym_stride;
+                ss.cap = P.sym_cap;
+            }
             sync_decode_sink<ST>(ic, s_hi[nt], ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2, ss);
-            if (P.sym_cap)
+            if constexpr (!ST)
+                if (P.sym_cap)
                 reinterpret_cast<uint4*>(P.tag)[gt] =
                     make_tag(ch.p, czd_c(ch.czd), czd_z(ch.czd), ss.n,
                              !czd_div(e2.czd) && ss.n <= P.sym_cap ? P.epoch : 0u);

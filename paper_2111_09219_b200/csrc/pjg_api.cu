@@ -811,6 +811,14 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     // rounds (K1 stores each chain's symbols once per round): 64..160 scan
     // bits per data unit, in images of >= 64 subsequences on average.
     // PJG_REPLAY=0/1 forces it.
+    // small batches (under ~4 K1 CTAs per SM): the decoders' table probes sit on a
+    // serial dependency chain with few warps to hide an L1 miss — stage the
+    // tables in shared memory
+    uint32_t smem_tables =
+        (huffs.size() <= kMaxSmemTables && sub < uint64_t(kK1Threads) * 148 * 4) ? uint32_t(huffs.size()) : 0u;
+    if (const char* e = getenv("PJG_SMEM_TABLES"))  // override (A/B experiments)
+        smem_tables = (atoi(e) && huffs.size() <= kMaxSmemTables) ? uint32_t(huffs.size()) : 0u;
+    const bool st_tables = smem_tables != 0;
     bool replay_on = false;
     {
         uint64_t bits = 0;
@@ -818,8 +826,10 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
             if (b->host_status[i] == kOk) bits += desc[i].raw_len * 8;
         const uint64_t per_du = du ? bits / du : 0;
         // (and large images: a few subsequences per image keep K3 cheap)
-        replay_on = per_du >= 64 && per_du <= 160 && n_ok && sub / n_ok >= 64;
-        if (const char* e = getenv("PJG_REPLAY")) replay_on = atoi(e) != 0;
+        // (large batches only: K1's shared-memory-table variant for small ones
+        // does not keep symbols)
+        replay_on = per_du >= 64 && per_du <= 160 && n_ok && sub / n_ok >= 64 && !st_tables;
+        if (const char* e = getenv("PJG_REPLAY")) replay_on = atoi(e) != 0 && !st_tables;
         if (getenv("PJG_NO_REPLAY")) replay_on = false;
     }
     const uint32_t sym_cap = (!replay_on || sb > 65536) ? 0u : uint32_t(sb / 4);
@@ -862,12 +872,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     p.n_dri = uint32_t(dri.size());
     p.k0_tiles = k0t;
     p.k0_bpt = k0_bpt;
-    // small batches (under ~4 K1 CTAs per SM): the decoders' table probes sit on a
-    // serial dependency chain with few warps to hide an L1 miss — stage the
-    // tables in shared memory
-    p.smem_tables = (b->n_huff <= kMaxSmemTables && sub < uint64_t(kK1Threads) * 148 * 4) ? b->n_huff : 0;
-    if (const char* e = getenv("PJG_SMEM_TABLES"))  // override (A/B experiments)
-        p.smem_tables = (atoi(e) && b->n_huff <= kMaxSmemTables) ? b->n_huff : 0;
+    p.smem_tables = smem_tables;
     p.k1_ctas = b->k1_ctas;
     p.n_huff = b->n_huff;
     // grids that do not fill the GPU are latency-bound: a stale CTA start is

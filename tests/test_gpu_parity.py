@@ -63,6 +63,8 @@ def test_acceptance_corpus_entropy_and_states(decoder, sb, hop, replay, monkeypa
     # grids); K3 replaying K1's kept symbols or decoding every subsequence
     monkeypatch.setenv("PJG_K1_HOP", hop)
     monkeypatch.setenv("PJG_REPLAY", "1" if replay == "on" else "0")
+    if replay == "on":  # replay runs with K1's large-batch (global-table) variant
+        monkeypatch.setenv("PJG_SMEM_TABLES", "0")
     corpus = acceptance_corpus()
     files = [f for _, f in corpus]
     with decoder.batch(files, pj.DecodeConfig(subsequence_bits=sb), pj.OutputColorspace.YCbCrPlanes) as b:
