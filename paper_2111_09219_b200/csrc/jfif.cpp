@@ -52,9 +52,23 @@ void parse_dqt(Reader& r, uint16_t len, Header& h) {
         uint8_t prec = pq >> 4, id = pq & 15;
         if (id > 3) throw Fail{kMalformedHeader, "quant table id > 3"};
         if (prec > 1) throw Fail{kMalformedHeader, "bad quant precision"};
-        for (int i = 0; i < 64; ++i) h.quant[id][i] = prec ? s.u16() : s.u8();
-        for (int i = 0; i < 64; ++i)
-            if (h.quant[id][i] == 0) throw Fail{kMalformedHeader, "zero quantizer entry"};
+        // one bounds check per table, then a plain (vectorisable) conversion
+        const Reader q = s.take(prec ? 128 : 64);
+        const uint8_t* b = q.ptr();
+        uint16_t* dst = h.quant[id].data();
+        uint32_t any_zero = 0;
+        if (prec) {
+            for (int i = 0; i < 64; ++i) {
+                dst[i] = uint16_t((b[2 * i] << 8) | b[2 * i + 1]);
+                any_zero |= dst[i] == 0;
+            }
+        } else {
+            for (int i = 0; i < 64; ++i) {
+                dst[i] = b[i];
+                any_zero |= b[i] == 0;
+            }
+        }
+        if (any_zero) throw Fail{kMalformedHeader, "zero quantizer entry"};
         h.quant_present[id] = true;
     }
 }
@@ -68,11 +82,10 @@ void parse_dht(Reader& r, uint16_t len, Header& h) {
         if (cls > 1) throw Fail{kUnsupportedFeature, "huffman table class > 1"};
         if (id > 3) throw Fail{kMalformedHeader, "huffman table id > 3"};
         HuffSpec sp;
+        const Reader cr = s.take(16);
+        std::memcpy(sp.counts.data(), cr.ptr(), 16);
         size_t total = 0;
-        for (int i = 0; i < 16; ++i) {
-            sp.counts[i] = s.u8();
-            total += sp.counts[i];
-        }
+        for (int i = 0; i < 16; ++i) total += sp.counts[i];
         if (total > 256) throw Fail{kMalformedHeader, "more than 256 huffman symbols"};
         Reader syms = s.take(total);
         sp.symbols.p = syms.ptr();

@@ -58,7 +58,7 @@ struct Header {
     SmallVec<Component, 3> comps;
     uint32_t h_max = 1, v_max = 1, mcus_x = 0, mcus_y = 0, dpm = 0;
     SmallVec<uint8_t, 16> du_seq;
-    std::array<std::array<uint16_t, 64>, 4> quant{};
+    std::array<std::array<uint16_t, 64>, 4> quant;  // valid where quant_present (not zeroed: per-file cost)
     std::array<bool, 4> quant_present{};
     std::array<HuffSpec, 4> dc, ac;
     size_t scan_start = 0;  // offset of the first entropy-coded byte
