@@ -1235,9 +1235,9 @@ __device__ __forceinline__ uint4 make_tag(uint64_t p, uint32_t c, uint32_t z, ui
 
 // ======================================================== K1: sync pass ====
 // CTA j owns the kK1Own global subsequences [j*kK1Own, (j+1)*kK1Own); thread
-// t >= 1 owns subsequence j*kK1Own + t - 1.  Thread 0 re-decodes the
-// predecessor CTA's last subsequence from its origin (round 0 only) and its
-// overflow chain carries that speculative state into this CTA — the
+// t >= kK1Spec owns subsequence j*kK1Own + t - kK1Spec.  Threads 0..kK1Spec-1
+// re-decode the predecessor CTA's last subsequences (round 0, and the chain
+// between them), and their overflow chain carries that speculative state into this CTA — the
 // inter-sequence overflow of sync_inter_sequence (parallel_decode.hpp:247-270)
 // started without waiting for the predecessor.  After the intra rounds the
 // speculative start is checked against the predecessor's published
@@ -1278,7 +1278,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     __syncthreads();
     // ticket order: a predecessor started earlier and is never waiting on this CTA
     const uint32_t cta = s_cta;
-    const int64_t gs = int64_t(cta) * TO + tid - 1;
+    const int64_t gs = int64_t(cta) * TO + tid - kK1Spec;
     const bool inb = gs >= 0 && uint64_t(gs) < P.total_subs;
     const uint64_t g = inb ? uint64_t(gs) : (gs < 0 ? 0 : P.total_subs - 1);
     const uint32_t k = find_img(P, g);
@@ -1345,7 +1345,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
             Entry e2;
             DcSums d2;
             // the chain keeps its symbols for K3 (tagged with its start state)
-            const uint64_t gt = uint64_t(cta) * TO + nt - 1;
+            // (only owned targets: a speculative one is the predecessor CTA's)
+            const bool owned_t = nt >= uint32_t(kK1Spec);
+            const uint64_t gt = uint64_t(cta) * TO + nt - kK1Spec;
             // (small batches, ST: never replayed — the planner enables replay only
             // for large ones; the plain sink also compiles better there)
             using ChainSink = typename std::conditional<ST, NullSink, SymSink>::type;
@@ -1353,11 +1355,11 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
             if constexpr (!ST) {
                 ss.dst = P.sym + gt;
                 ss.stride = P.sym_stride;
-                ss.cap = P.sym_cap;
+                ss.cap = owned_t ? P.sym_cap : 0u;
             }
             sync_decode_sink<ST>(ic, s_hi[nt], ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2, ss);
             if constexpr (!ST)
-                if (P.sym_cap)
+                if (P.sym_cap && owned_t)
                 reinterpret_cast<uint4*>(P.tag)[gt] =
                     make_tag(ch.p, czd_c(ch.czd), czd_z(ch.czd), ss.n,
                              !czd_div(e2.czd) && ss.n <= P.sym_cap ? P.epoch : 0u);
@@ -1388,7 +1390,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
         __threadfence();
         st_release(P.k1_flag + cta, P.epoch);
     }
-    // Inter-CTA check: the speculative start (thread 0's round-0 entry) against
+    // Inter-CTA check: the speculative start (the last speculative thread's entry) against
     // the predecessor's published post-intra last entry; where they differ,
     // the first owned thread re-chains from the published entry (in its own
     // image context) until it meets an entry it agrees with.  HOP waits for
@@ -1396,7 +1398,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     // has already published (usually: it started earlier) and the start stays
     // speculative if not.  K1c compares the start used with the predecessor's
     // FINAL last entry.
-    if (tid == 1) {
+    if (tid == kK1Spec) {
         Entry start;
         start.p = 0;
         start.n = 0;
@@ -1407,9 +1409,9 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
                 while (ld_acquire(P.k1_flag + cta - 1) != P.epoch) spin_pause();
             ready = HOP || ld_acquire(P.k1_flag + cta - 1) == P.epoch;
             if (!ready) {  // K1c's first pass checks the speculative start
-                start.p = s_p[0];
-                start.n = s_n[0];
-                start.czd = s_czd[0] | kBoundaryBit;
+                start.p = s_p[kK1Spec - 1];
+                start.n = s_n[kK1Spec - 1];
+                start.czd = s_czd[kK1Spec - 1] | kBoundaryBit;
             }
         }
         if (ready) {
@@ -1417,7 +1419,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
             const uint64_t nc = __ldcg(reinterpret_cast<const unsigned long long*>(&P.cta_end[cta - 1]) + 1);
             start.n = uint32_t(nc);
             start.czd = uint32_t(nc >> 32);
-            if (!sync_equal(start.p, start.czd, s_p[0], s_czd[0]) && !czd_div(start.czd)) {
+            if (!sync_equal(start.p, start.czd, s_p[kK1Spec - 1], s_czd[kK1Spec - 1]) && !czd_div(start.czd)) {
                 Entry ch = start;
                 uint64_t ii = i;
                 uint32_t hops = 0;
@@ -1425,7 +1427,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
                     load_ctx<ST>(P, D, L, ic, sfast);
                     set_stage(ic, s_stage, s_sm, k);
                 }
-                for (int tt = 1; tt < T && ii < si.seg_sub1; ++tt, ++ii) {
+                for (int tt = kK1Spec; tt < T && ii < si.seg_sub1; ++tt, ++ii) {
                     Entry e2;
                     DcSums d2;
                     sync_decode<ST>(ic, s_hi[tt], ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2);
@@ -1445,7 +1447,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
         P.cta_start[cta] = start;
     }
     __syncthreads();
-    if (inb && tid >= 1) {
+    if (inb && tid >= kK1Spec) {
         Entry o;
         o.p = s_p[tid];
         o.n = s_n[tid];
