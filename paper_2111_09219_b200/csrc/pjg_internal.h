@@ -152,7 +152,7 @@ constexpr uint32_t kMaxSmemTables = 4;  // fast tables K1/K3 stage in shared mem
 constexpr int kK0Threads = 512;
 constexpr uint32_t kK0BigBpt = 64, kK0SmallBpt = 16;  // bytes per K0 thread: 32 KB or 8 KB tiles
 constexpr int kK1Threads = 128;                          // threads per K1 CTA
-constexpr int kK1Spec = 2;                               // K1 threads re-decoding the predecessor CTA's last subsequences
+constexpr int kK1Spec = 4;                               // K1 threads re-decoding the predecessor CTA's last subsequences
 constexpr int kK1Own = kK1Threads - kK1Spec;             // subsequences owned per K1 CTA
 constexpr int kK2Threads = 256;
 constexpr int kK3Threads = 128;
