@@ -33,8 +33,12 @@ CASES = [(64, 48, 75, "420", 1), (200, 120, 85, "444", 3), (333, 257, 90, "422",
          (801, 61, 60, "gray", 5), (1024, 512, 95, "420", 64), (640, 480, 80, "444", 40), (96, 96, 50, "420", 1000)]
 
 
+@pytest.mark.parametrize("replay", ["default", "on"])
 @pytest.mark.parametrize("sb", [1024, 128])
-def test_restart_twins_bit_exact(decoder, sb):
+def test_restart_twins_bit_exact(decoder, sb, replay, monkeypatch):
+    if replay == "on":  # K3 replaying K1's kept symbols inside restart-interval segments
+        monkeypatch.setenv("PJG_REPLAY", "1")
+        monkeypatch.setenv("PJG_SMEM_TABLES", "0")
     pairs = [(c, *_twins(*c, 7000 + k)) for k, c in enumerate(CASES)]
     cfg = pj.DecodeConfig(subsequence_bits=sb, restart_intervals=True)
     with decoder.batch([p for _, p, _ in pairs], pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved) as b0:
