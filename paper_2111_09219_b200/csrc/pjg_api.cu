@@ -195,6 +195,7 @@ struct pjg_batch {
     uint32_t n_huff = 0, n_quant = 0;
     uint32_t k0_tiles = 0, k4_tiles = 0, k1_ctas = 0, k2_tiles = 0;
     uint64_t total_subs = 0, total_dus = 0, out_bytes = 0, seg_total = 0;
+    uint64_t sb_int = 0;  // internal subsequence size (divides cfg.subsequence_bits)
     Params prm{};
     bool uploaded = false, decoded = false, synced = false;
     std::vector<ImgState> dev_state;  // fetched at synchronize
@@ -422,7 +423,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         std::vector<std::array<uint16_t, 64>> quant;
         const uint8_t* lo = nullptr;
         const uint8_t* hi = nullptr;
-        uint64_t raw_sum = 0, n_ok = 0;
+        uint64_t raw_sum = 0, n_ok = 0, n_dri = 0;
     };
     auto same_spec = [](const HuffSpec& a, const HuffSpec& c) {
         return a.counts == c.counts && a.symbols.size() == c.symbols.size() &&
@@ -498,6 +499,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
             if (h.table_status != kOk) continue;
             d.sub_count = (uint64_t(rl) * 8 + sb - 1) / sb;
             if (h.restart_interval && h.intervals() > 1) {
+                ++W.n_dri;
                 d.n_int = uint32_t(h.intervals());  // checked and finished in phase B
                 d.ri = h.restart_interval;
             }
@@ -558,13 +560,33 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     // ---- phase B (serial prefix sums): raw placement, global table ids, layout
     const uint8_t* lo = nullptr;
     const uint8_t* hi = nullptr;
-    uint64_t raw_sum = 0, n_ok = 0;
+    uint64_t raw_sum = 0, n_ok = 0, n_dri = 0;
     for (const Worker& W : wk) {
         if (W.lo && (!lo || W.lo < lo)) lo = W.lo;
         if (W.hi && (!hi || W.hi > hi)) hi = W.hi;
         raw_sum += W.raw_sum;
         n_ok += W.n_ok;
+        n_dri += W.n_dri;
     }
+    // Internal subsequence size: a batch too small to give half the SMs a K1
+    // CTA is decoded at sb / 2^k (>= 256 bits, a multiple of 32 dividing sb) — more
+    // threads for a latency-bound decode.  The decomposition is unique, so the
+    // results do not change; every boundary at the configured sb is also one at
+    // the internal size, and the sync-state dump aggregates back to the
+    // configured partition.  Restart-interval batches keep sb (their
+    // per-interval partitions are dumped as is).  PJG_SB_AUTO=0 turns it off.
+    uint64_t sb_int = sb;
+    {
+        const char* e = getenv("PJG_SB_AUTO");
+        if (!n_dri && !(e && atoi(e) == 0)) {
+            uint64_t est = raw_sum * 8 / sb;
+            while (est < uint64_t(kK1Threads) * 148 / 2 && sb_int / 2 >= 256 && (sb_int / 2) % 32 == 0) {
+                sb_int /= 2;
+                est *= 2;
+            }
+        }
+    }
+    b->sb_int = sb_int;
     // K0 tile size: 32 KB windows when the scans are large on average, else 8 KB
     uint32_t k0_bpt = (n_ok && raw_sum / n_ok >= 48 * 1024) ? kK0BigBpt : kK0SmallBpt;
     if (const char* e = getenv("PJG_K0_BPT"))  // override (A/B experiments): 16 or 64
@@ -604,6 +626,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
             // K0 tiles always run (scan checks precede table errors); 16-byte-grid windows
             t.k0t += uint32_t((((b->packed ? 0 : d.raw_off) & 15) + rl + k0_tile - 1) / k0_tile);
             if (d.deferred != kOk) continue;
+            if (sb_int != sb) d.sub_count = (uint64_t(rl) * 8 + sb_int - 1) / sb_int;
             if (d.n_int > 1) {
                 // restart intervals: one subsequence partition per interval (K0b), at
                 // most ceil(bits / sb) + intervals subsequences; segment bit offsets
@@ -832,7 +855,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
         if (const char* e = getenv("PJG_REPLAY")) replay_on = atoi(e) != 0 && !st_tables;
         if (getenv("PJG_NO_REPLAY")) replay_on = false;
     }
-    const uint32_t sym_cap = (!replay_on || sb > 65536) ? 0u : uint32_t(sb / 4);
+    const uint32_t sym_cap = (!replay_on || sb_int > 65536) ? 0u : uint32_t(sb_int / 4);
     const uint64_t sym_stride = align_up(subs, 64);
     if (sym_cap) {
         CU(ctx->sym.ensure(sym_stride * sym_cap * 2), "cudaMalloc(sym)");
@@ -880,7 +903,7 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     // leave the (few) stale starts to K1c's parallel first pass
     p.k1_hop = b->k1_ctas < 2 * 148 ? 1u : 0u;
     if (const char* e = getenv("PJG_K1_HOP")) p.k1_hop = atoi(e) ? 1u : 0u;  // override (tests, A/B)
-    p.sb = sb;
+    p.sb = sb_int;
     p.sub_first = reinterpret_cast<const uint64_t*>(md + b->m_sub);
     p.total_subs = sub;
     p.ent = ctx->ent.as<Entry>();
@@ -1181,7 +1204,8 @@ int pjg_batch_dump_sync_states(const pjg_batch* b, size_t i, pjg_sync_entry* out
     if (st) return st;
     if (b->host_status[i] != 0) return b->host_status[i];
     const uint64_t L = b->dev_state[i].bit_length;
-    uint64_t N = (L + b->cfg.subsequence_bits - 1) / b->cfg.subsequence_bits;
+    const uint64_t sbu = b->cfg.subsequence_bits, f = b->sb_int ? sbu / b->sb_int : 1;
+    uint64_t N = (L + sbu - 1) / sbu;
     if (b->desc[i].n_int > 1) {  // restart intervals: the subsequences in use (K0b)
         uint2 last;
         CU(cudaMemcpy(&last, ctx->segs.as<uint2>() + b->desc[i].seg_first + b->desc[i].n_int, sizeof(uint2),
@@ -1192,19 +1216,27 @@ int pjg_batch_dump_sync_states(const pjg_batch* b, size_t i, pjg_sync_entry* out
     *n_out = N;
     if (!out) return PJG_OK;
     if (cap < N) return fail(ctx, PJG_CAPACITY, "sync state buffer too small");
-    std::vector<Entry> ents(N);
-    std::vector<uint32_t> caps(N);
+    // internal subsequences (f per configured one when sb was split)
+    const uint64_t Ni = b->desc[i].n_int > 1 ? N : (L + b->sb_int - 1) / b->sb_int;
+    std::vector<Entry> ents(Ni);
+    std::vector<uint32_t> caps(Ni);
     const uint64_t g0 = b->desc[i].sub_first;
-    if (N) {
-        CU(cudaMemcpy(ents.data(), ctx->ent.as<Entry>() + g0, N * sizeof(Entry), cudaMemcpyDeviceToHost), "D2H ent");
-        CU(cudaMemcpy(caps.data(), ctx->cap.as<uint32_t>() + g0, N * 4, cudaMemcpyDeviceToHost), "D2H cap");
+    if (Ni) {
+        CU(cudaMemcpy(ents.data(), ctx->ent.as<Entry>() + g0, Ni * sizeof(Entry), cudaMemcpyDeviceToHost), "D2H ent");
+        CU(cudaMemcpy(caps.data(), ctx->cap.as<uint32_t>() + g0, Ni * 4, cudaMemcpyDeviceToHost), "D2H cap");
     }
+    const uint64_t fk = b->desc[i].n_int > 1 ? 1 : f;
     for (uint64_t k = 0; k < N; ++k) {
-        out[k].p = ents[k].p;
-        out[k].n = caps[k];
-        out[k].c = czd_c(ents[k].czd);
-        out[k].z = czd_z(ents[k].czd);
-        out[k].divergent = czd_div(ents[k].czd) ? 1 : 0;
+        // the configured subsequence k = internal ones [k f, min((k+1) f, Ni)):
+        // its entry is the last one's (same boundary), its slots their sum
+        const uint64_t last = std::min((k + 1) * fk, Ni) - 1;
+        uint64_t nn = 0;
+        for (uint64_t j = k * fk; j <= last; ++j) nn += caps[j];
+        out[k].p = ents[last].p;
+        out[k].n = nn;
+        out[k].c = czd_c(ents[last].czd);
+        out[k].z = czd_z(ents[last].czd);
+        out[k].divergent = czd_div(ents[last].czd) ? 1 : 0;
         out[k].pad = 0;
     }
     return PJG_OK;
