@@ -903,6 +903,14 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     // leave the (few) stale starts to K1c's parallel first pass
     p.k1_hop = b->k1_ctas < 2 * 148 ? 1u : 0u;
     if (const char* e = getenv("PJG_K1_HOP")) p.k1_hop = atoi(e) ? 1u : 0u;  // override (tests, A/B)
+    {  // every image 4:2:0 colour to RGB: K4's specialised variant
+        bool all420 = cfg->output == PJG_OUT_RGB && n_ok > 0;
+        for (size_t i = 0; i < n && all420; ++i)
+            if (b->host_status[i] == kOk)
+                all420 = desc[i].ncomp == 3 && desc[i].h_max == 2 && desc[i].v_max == 2;
+        p.k4_layout = all420 ? 1u : 0u;
+        if (const char* e = getenv("PJG_K4_LAYOUT")) p.k4_layout = atoi(e) == 1 && all420 ? 1u : 0u;  // A/B
+    }
     p.sb = sb_int;
     p.sub_first = reinterpret_cast<const uint64_t*>(md + b->m_sub);
     p.total_subs = sub;

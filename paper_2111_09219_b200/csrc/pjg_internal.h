@@ -189,6 +189,7 @@ struct Params {
     uint32_t smem_tables;          // K1/K3 stage this many fast tables in shared memory (0: read global)
     uint32_t n_huff;               // unique Huffman tables of the batch
     uint32_t k1_hop;               // K1 re-chains stale CTA starts in-kernel (small grids); else K1c first pass
+    uint32_t k4_layout;            // 1: every image is 4:2:0 colour to RGB (specialised K4); 0: any
     // subsequences
     uint64_t sb;                   // subsequence_bits
     const uint64_t* sub_first;     // n_img + 1 prefix
