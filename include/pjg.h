@@ -137,9 +137,18 @@ int pjg_decode_batch(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
 
 /* ---- staged device pipeline (output stays in HBM) --------------------- */
 /* Host header parse + layout plan + device reservation.  The file bytes are
- * read at upload time, so they must stay alive until pjg_batch_upload. */
+ * read at upload time, so they must stay alive until pjg_batch_upload.
+ * Files in separate buffers: the scans are packed into the context's pinned
+ * stage (only the callers' own bytes are ever read). */
 int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const size_t* sizes,
                      const pjg_config* cfg, pjg_batch** out);
+/* Same for files laid out in ONE caller allocation blob[0, blob_bytes) (file i
+ * at blob + offsets[i]): the upload is a single H2D of the scans' extent in
+ * the blob (pinned blob => no staging copy).  decode_batch's input vector
+ * (pipeline.hpp:147) flattened; InvalidArgument if a file leaves the blob. */
+int pjg_batch_create_blob(pjg_ctx* ctx, const uint8_t* blob, size_t blob_bytes, size_t n,
+                          const uint64_t* offsets, const size_t* sizes, const pjg_config* cfg,
+                          pjg_batch** out);
 /* One H2D of the compressed bytes (+ one of the descriptor blob), async. */
 int pjg_batch_upload(pjg_batch* b);
 /* K0..K4 on the context stream, async; output stays on the device. */
@@ -164,7 +173,8 @@ uint64_t pjg_batch_scan_bits(const pjg_batch* b);
 uint32_t pjg_batch_kernel_launches(const pjg_batch* b);
 /* Device-to-device copy of every decoded image i with dst[i] != NULL into
  * caller device buffers (e.g. torch CUDA tensors), ordered on the context's
- * stream after the decode; no host round trip. */
+ * stream after the decode; no pixel crosses the host.  Waits for the decode's
+ * per-image statuses first: images that failed are not copied. */
 int pjg_batch_copy_outputs(pjg_batch* b, void* const* dst, const size_t* caps);
 uint64_t pjg_batch_output_bytes(const pjg_batch* b);
 int pjg_batch_stage_times(const pjg_batch* b, double* ms /* PJG_NUM_STAGES */);

@@ -182,6 +182,9 @@ def lib():
             L.pjg_batch_create.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(u8p),
                                            C.POINTER(C.c_size_t), C.POINTER(_Config),
                                            C.POINTER(C.c_void_p)]
+            L.pjg_batch_create_blob.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
+                                                C.POINTER(C.c_uint64), C.POINTER(C.c_size_t),
+                                                C.POINTER(_Config), C.POINTER(C.c_void_p)]
             for fn in ("pjg_batch_upload", "pjg_batch_decode"):
                 getattr(L, fn).argtypes = [C.c_void_p]
             L.pjg_batch_synchronize.argtypes = [C.c_void_p, C.c_void_p]
@@ -220,7 +223,7 @@ def lib():
 EXPORTED_SYMBOLS = [
     "pjg_ctx_create", "pjg_ctx_destroy", "pjg_last_error", "pjg_status_name", "pjg_default_config",
     "pjg_ctx_stream", "pjg_inspect", "pjg_inspect_header", "pjg_decode", "pjg_decode_batch", "pjg_batch_create",
-    "pjg_batch_upload", "pjg_batch_decode", "pjg_batch_synchronize", "pjg_batch_download",
+    "pjg_batch_create_blob", "pjg_batch_upload", "pjg_batch_decode", "pjg_batch_synchronize", "pjg_batch_download",
     "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_copy_outputs", "pjg_batch_scan_bits", "pjg_batch_kernel_launches", "pjg_batch_download_all", "pjg_batch_download_all_async", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
     "pjg_batch_sync_stats", "pjg_batch_destroy", "pjg_batch_dump_coefficients",
     "pjg_batch_dump_sync_states", "pjg_batch_dump_segment", "pjg_upsample_and_convert",
@@ -287,16 +290,19 @@ class Batch:
     def __init__(self, dec: Decoder, files, config=None, output=None):
         self.dec = dec
         self.config = config or DecodeConfig()
+        blob_args = None
         if isinstance(files, tuple):
+            # one caller allocation: (blob uint8 array, offsets, sizes)
             blob, offsets, sizes = files
-            base = blob.ctypes.data if isinstance(blob, np.ndarray) else int(blob)
+            blob = np.asarray(blob, np.uint8).reshape(-1)
             self._keep = [blob]
             n = len(sizes)
-            pa = (np.asarray(offsets, np.uint64) + np.uint64(base)).astype(np.uint64)
-            sa = np.asarray(sizes, np.uint64)
-            self._keep += [pa, sa]
-            ptrs = pa.ctypes.data_as(C.POINTER(u8p))
-            szs = sa.ctypes.data_as(C.POINTER(C.c_size_t))
+            oa = np.ascontiguousarray(offsets, np.uint64)
+            sa = np.ascontiguousarray(sizes, np.uint64)
+            self._keep += [oa, sa]
+            blob_args = (C.c_void_p(blob.ctypes.data), blob.size, n,
+                         oa.ctypes.data_as(C.POINTER(C.c_uint64)),
+                         sa.ctypes.data_as(C.POINTER(C.c_size_t)))
         else:
             self._keep = [np.frombuffer(f, np.uint8) if not isinstance(f, np.ndarray) else f
                           for f in files]
@@ -307,7 +313,10 @@ class Batch:
         self._h = C.c_void_p()
         cfg = _cfg(self.config, output)
         self.output = cfg.output
-        st = lib().pjg_batch_create(dec.handle, n, ptrs, szs, C.byref(cfg), C.byref(self._h))
+        if blob_args is not None:
+            st = lib().pjg_batch_create_blob(dec.handle, *blob_args, C.byref(cfg), C.byref(self._h))
+        else:
+            st = lib().pjg_batch_create(dec.handle, n, ptrs, szs, C.byref(cfg), C.byref(self._h))
         if st:
             raise Error(st, dec.last_error())
         self._infos = None

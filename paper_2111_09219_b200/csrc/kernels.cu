@@ -30,6 +30,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include "pjg_internal.h"
 
@@ -2827,6 +2829,33 @@ void launch_k5_color(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, uin
 }
 
 // ------------------------------------------------------------ launchers --
+// Per-(device, kernel) launch setup: the dynamic shared-memory opt-in is a
+// per-device/context attribute, and the K4 grid cap depends on the device's
+// SM count.  Several contexts on several devices (or host threads) may launch
+// concurrently, so the cache is keyed by device and guarded by a mutex; the
+// returned value is the kernel's resident CTAs per SM x SMs (0 when the
+// caller did not ask for it).
+static int launch_setup(const void* fn, int dyn_smem, int threads, bool want_grid) {
+    static std::mutex mu;
+    static std::unordered_map<uint64_t, int> done;  // (device, fn) -> grid cap + 1
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t key = (uint64_t(reinterpret_cast<uintptr_t>(fn)) << 8) ^ uint64_t(dev);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = done.find(key);
+    if (it != done.end()) return it->second - 1;
+    if (dyn_smem > 0) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+    int cap = 0;
+    if (want_grid) {
+        int sms = 0, per_sm = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, dyn_smem);
+        cap = std::max(1, sms * std::max(per_sm, 1));
+    }
+    done.emplace(key, cap + 1);
+    return cap;
+}
+
 uint32_t kernel_launches(const Params& p) {
     // mirrors the launch conditions of the launchers below
     return (p.k0_tiles ? 1u : 0u) + (p.n_dri ? 1u : 0u) + (p.k1_ctas ? 1u : 0u) + (p.k1_ctas > 1 ? (p.k1_hop ? 1u : 2u) : 0u) +
@@ -2834,19 +2863,16 @@ uint32_t kernel_launches(const Params& p) {
 }
 void launch_k0_unstuff(const Params& p, void* stream) {
     if (!p.k0_tiles) return;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k0_unstuff<true, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (kK0Threads * 64 + 32));
-        cudaFuncSetAttribute(k0_unstuff<false, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (kK0Threads * 64 + 32));
-        attr = true;
-    }
     const int dyn = 2 * (kK0Threads * int(p.k0_bpt) + 32);
     cudaStream_t s = (cudaStream_t)stream;
     if (p.k0_bpt == 64) {
-        if (p.n_dri)
+        if (p.n_dri) {
+            launch_setup((const void*)k0_unstuff<true, 64>, dyn, kK0Threads, false);
             k0_unstuff<true, 64><<<p.k0_tiles, kK0Threads, dyn, s>>>(p);
-        else
+        } else {
+            launch_setup((const void*)k0_unstuff<false, 64>, dyn, kK0Threads, false);
             k0_unstuff<false, 64><<<p.k0_tiles, kK0Threads, dyn, s>>>(p);
+        }
     } else {
         if (p.n_dri)
             k0_unstuff_small<true><<<p.k0_tiles, kK0Threads, 0, s>>>(p);
@@ -2859,12 +2885,7 @@ void launch_k0b_segments(const Params& p, void* stream) {
 }
 template <bool DRI, bool ST, bool HOP>
 static void launch_k1_variant(const Params& p, size_t dyn, cudaStream_t s) {
-    static bool attr = false;
-    if (ST && !attr) {
-        cudaFuncSetAttribute(k1_sync<DRI, ST, HOP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kMaxSmemTables * kFastWords * 4);
-        attr = true;
-    }
+    if (ST) launch_setup((const void*)k1_sync<DRI, ST, HOP>, kMaxSmemTables * kFastWords * 4, kK1Threads, false);
     k1_sync<DRI, ST, HOP><<<p.k1_ctas, kK1Threads, dyn, s>>>(p);
 }
 template <bool DRI, bool ST>
@@ -2895,12 +2916,7 @@ void launch_k1c_fixup(const Params& p, void* stream) {
     if (!p.k1_hop) {
         const unsigned grid = (p.k1_ctas - 1 + 127) / 128;
         if (p.n_huff <= kMaxSmemTables) {
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k1c_first<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kMaxSmemTables * kFastWords * 4);
-                attr = true;
-            }
+            launch_setup((const void*)k1c_first<true>, kMaxSmemTables * kFastWords * 4, 128, false);
             k1c_first<true><<<grid, 128, size_t(p.n_huff) * kFastWords * 4, (cudaStream_t)stream>>>(p);
         } else {
             k1c_first<false><<<grid, 128, 0, (cudaStream_t)stream>>>(p);
@@ -2913,12 +2929,7 @@ void launch_k2_scan(const Params& p, void* stream) {
 }
 template <bool ST, bool REPLAY>
 static void launch_k3_variant(const Params& p, unsigned grid, cudaStream_t s) {
-    static bool attr = false;
-    if (ST && !attr) {
-        cudaFuncSetAttribute(k3_write<ST, REPLAY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kMaxSmemTables * kFastWords * 4);
-        attr = true;
-    }
+    if (ST) launch_setup((const void*)k3_write<ST, REPLAY>, kMaxSmemTables * kFastWords * 4, kK3Threads, false);
     k3_write<ST, REPLAY><<<grid, kK3Threads, ST ? size_t(p.smem_tables) * kFastWords * 4 : 0, s>>>(p);
 }
 void launch_k3_write(const Params& p, void* stream) {
@@ -2932,16 +2943,8 @@ void launch_k3_write(const Params& p, void* stream) {
 }
 template <int LAYOUT>
 static void launch_k4_variant(const Params& p, cudaStream_t s) {
-    static int grid_cap = 0;
     constexpr size_t dyn = sizeof(WarpSmem) * kK4Warps;
-    if (!grid_cap) {
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k4_transform<LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4_transform<LAYOUT>, kK4Threads, dyn);
-        grid_cap = std::max(1, sms * std::max(per_sm, 1));
-    }
+    const int grid_cap = launch_setup((const void*)k4_transform<LAYOUT>, int(dyn), kK4Threads, true);
     const uint64_t want = (uint64_t(p.k4_tiles) + kK4Threads / 32 - 1) / (kK4Threads / 32);
     const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(grid_cap)));
     k4_transform<LAYOUT><<<grid, kK4Threads, dyn, s>>>(p);

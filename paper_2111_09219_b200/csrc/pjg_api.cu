@@ -38,6 +38,7 @@ struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
     bool zero = false;  // zero-fill on (re)allocation (lookback flag arrays)
+    cudaStream_t zs = nullptr;  // the owning context's stream: the fill is ordered before its kernels
 
     cudaError_t ensure(size_t n) {
         if (n <= cap && p) return cudaSuccess;
@@ -48,7 +49,7 @@ struct DevBuf {
         cudaError_t e = cudaMalloc(&p, want);
         if (e != cudaSuccess) return e;
         cap = want;
-        if (zero) e = cudaMemset(p, 0, want);
+        if (zero) e = cudaMemsetAsync(p, 0, want, zs);
         return e;
     }
     template <class T>
@@ -315,6 +316,7 @@ int pjg_ctx_create(int device, pjg_ctx** out) {
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : c->ev) CU(cudaEventCreate(&e), "cudaEventCreate");
     c->k0_flag.zero = c->k2_flag.zero = c->k1_flag.zero = c->tag.zero = true;
+    for (DevBuf* b : {&c->k0_flag, &c->k2_flag, &c->k1_flag, &c->tag}) b->zs = c->stream;
     // IdctBasis (transform.hpp:93-108): the same host libm expression.
     for (int u = 0; u < 8; ++u) {
         double cu = u == 0 ? 1.0 / std::sqrt(2.0) : 1.0;
@@ -383,9 +385,13 @@ int pjg_inspect_header(const uint8_t* file, size_t size, int allow_dri, pjg_head
     return h.status;
 }
 
-int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const size_t* sizes,
-                     const pjg_config* cfg, pjg_batch** out) {
-    if (!ctx || !out || (n && (!files || !sizes))) return PJG_INVALID_ARGUMENT;
+namespace {
+// blob_lo/blob_hi: the one caller allocation every file lies in (the blob
+// API), or null — then the scans are copied from the caller's buffers only
+// (packed into the pinned stage), except for a single file, whose scan is
+// one range of that file.
+int batch_create_impl(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const size_t* sizes,
+                      const pjg_config* cfg, const uint8_t* blob_lo, const uint8_t* blob_hi, pjg_batch** out) {
     *out = nullptr;
     int st = 0;
     if (!validate_cfg(ctx, cfg, &st)) return st;
@@ -592,8 +598,11 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     if (const char* e = getenv("PJG_K0_BPT"))  // override (A/B experiments): 16 or 64
         k0_bpt = atoi(e) == int(kK0BigBpt) ? kK0BigBpt : kK0SmallBpt;
     const uint64_t k0_tile = uint64_t(kK0Threads) * k0_bpt;
-    // raw extent: contiguous user region or pack
-    b->packed = !(lo && uint64_t(hi - lo) <= raw_sum + raw_sum / 2 + (1u << 20));
+    // raw extent: one copy of the caller's region [lo, hi) when it lies in
+    // memory the caller owns (a single file, or a declared blob) and is not
+    // much larger than the scans; otherwise pack the scans into the stage
+    const bool owned = n_ok <= 1 || (blob_lo && lo >= blob_lo && hi <= blob_hi);
+    b->packed = !(lo && owned && uint64_t(hi - lo) <= raw_sum + raw_sum / 2 + (1u << 20));
     // Per image: global table ids, the restart-interval check, and its counts
     // (K0 tiles, subsequences, data units, K4 tiles, output bytes, segments,
     // packed bytes) — pass 1, per worker chunk; chunk totals are scanned
@@ -945,6 +954,26 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
     return PJG_OK;
 }
 
+}  // namespace
+
+int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const size_t* sizes,
+                     const pjg_config* cfg, pjg_batch** out) {
+    if (!ctx || !out || (n && (!files || !sizes))) return PJG_INVALID_ARGUMENT;
+    return batch_create_impl(ctx, n, files, sizes, cfg, nullptr, nullptr, out);
+}
+
+int pjg_batch_create_blob(pjg_ctx* ctx, const uint8_t* blob, size_t blob_bytes, size_t n, const uint64_t* offsets,
+                          const size_t* sizes, const pjg_config* cfg, pjg_batch** out) {
+    if (!ctx || !out || (n && (!blob || !offsets || !sizes))) return PJG_INVALID_ARGUMENT;
+    std::vector<const uint8_t*> files(n);
+    for (size_t i = 0; i < n; ++i) {
+        if (offsets[i] > blob_bytes || sizes[i] > blob_bytes - offsets[i])
+            return fail(ctx, PJG_INVALID_ARGUMENT, "file outside the blob");
+        files[i] = blob + offsets[i];
+    }
+    return batch_create_impl(ctx, n, files.data(), sizes, cfg, blob, blob + blob_bytes, out);
+}
+
 int pjg_batch_upload(pjg_batch* b) {
     if (!b) return PJG_INVALID_ARGUMENT;
     pjg_ctx* ctx = b->ctx;
@@ -1100,7 +1129,7 @@ int pjg_batch_info(const pjg_batch* b, size_t i, pjg_image_info* info) {
 }
 
 const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i) {
-    if (!b || i >= b->n) return nullptr;
+    if (!b || i >= b->n || b->host_status[i] != 0 || b->desc[i].deferred != 0) return nullptr;
     return b->ctx->out.as<uint8_t>() + b->desc[i].out_off;
 }
 
@@ -1123,13 +1152,15 @@ uint32_t pjg_batch_kernel_launches(const pjg_batch* b) {
 int pjg_batch_copy_outputs(pjg_batch* b, void* const* dst, const size_t* caps) {
     if (!b || !dst || !caps) return PJG_INVALID_ARGUMENT;
     pjg_ctx* ctx = b->ctx;
-    if (!b->decoded) return fail(ctx, PJG_NOT_DECODED, "batch not decoded");
-    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    // only images that decoded: device failures (and deferred table errors,
+    // which reserve no output) are known after the batch finished
+    int st = pjg_batch_synchronize(b, nullptr);
+    if (st) return st;
     for (size_t i = 0; i < b->n; ++i) {
         if (!dst[i]) continue;
         const uint64_t nb = b->info[i].output_bytes;
         if (caps[i] < nb) return fail(ctx, PJG_CAPACITY, "device output buffer too small");
-        if (b->host_status[i] != 0 || nb == 0) continue;
+        if (b->host_status[i] != 0 || b->dev_state[i].status != 0 || b->desc[i].deferred != 0 || nb == 0) continue;
         CU(cudaMemcpyAsync(dst[i], ctx->out.as<uint8_t>() + b->desc[i].out_off, nb, cudaMemcpyDeviceToDevice,
                            ctx->stream),
            "D2D output");

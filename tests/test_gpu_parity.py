@@ -237,16 +237,21 @@ def test_random_shapes_batch_bit_exact(decoder):
 
 
 def test_cpp_dropin_binary_matches_reference(tmp_path):
-    """The C++ shim (include/pjpeg_gpu.hpp) and the reference in one binary:
-    identical planes checksum and RGB."""
+    """The C++ shim (include/pjpeg_gpu.hpp) and the reference in ONE binary
+    (oracle/_ref/cpp_dropin_check, prebuilt with the reference headers where
+    they exist and shipped to the GPU box): identical planes checksum and RGB."""
+    import os
     import subprocess
-    from tests.test_host import _build_dropin
-    exe = _build_dropin(tmp_path)
-    f = tmp_path / "img.jpg"
-    f.write_bytes(ref_jpeg(333, 257, 6, 95, "422"))
-    r = subprocess.run([exe, str(f)], capture_output=True, text=True)
-    assert r.returncode == 0, r.stdout + r.stderr
-    assert ("IDENTICAL" in r.stdout) or ("ref:" not in r.stdout)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "oracle", "_ref", "cpp_dropin_check")
+    assert os.path.exists(exe), "build() prebuilds oracle/_ref/cpp_dropin_check next to the reference"
+    for k, (w, h, q, s) in enumerate([(333, 257, 95, "422"), (512, 512, 85, "444"), (500, 375, 75, "420"),
+                                      (161, 97, 50, "gray")]):
+        f = tmp_path / f"img{k}.jpg"
+        f.write_bytes(ref_jpeg(w, h, 6 + k, q, s))
+        r = subprocess.run([exe, str(f)], capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "IDENTICAL" in r.stdout, r.stdout
 
 
 def test_cli_decode_inspect_bench(tmp_path):
@@ -321,3 +326,51 @@ def test_large_thumbnail_batch_parallel_planner(decoder):
         want = Orc.decode(f, rgb=True)
         assert want.status == 0
         assert np.array_equal(outs[i][: want.data.size], want.data.reshape(-1)), i
+
+
+def test_unstuffed_segment_byte_exact(decoder):
+    """K0's unstuffed entropy segment (FF00 -> FF compaction up to the first
+    marker) byte for byte against the reference's extract_scan + unstuff
+    (parser.hpp:238-258, bitstream.hpp:56-76): the acceptance corpus, forged
+    scans dense in 0xFF bytes, and the unstuff KAT (test_bitstream.cpp:26-32)."""
+    import json
+    import os
+    from oracle.oracle import example_jpeg
+    from tests.test_gpu_adversarial import CASES, _forge
+    kat = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_kats.json")))["unstuff"]
+    files = [f for _, f in acceptance_corpus()] + [_forge(*c, 300 + i) for i, c in enumerate(CASES)]
+    files.append(example_jpeg(bytes(kat["in"])))
+    with decoder.batch(files, pj.DecodeConfig(), pj.OutputColorspace.YCbCrPlanes) as b:
+        b.run()
+        for i, f in enumerate(files):
+            want = Ref.segment(f)
+            got = b.segment(i)
+            assert got == want, (i, len(got), len(want))
+    assert got == bytes(kat["out"]) and len(got) * 8 == kat["bit_length"]
+    assert sum(f.count(b"\xff\x00") for f in files) > 1000  # the stuffing path ran
+
+
+def test_partition_kats(decoder):
+    """partition() KATs (test_parallel_decode.cpp:42-63): N = ceil(bits / sb)
+    subsequences, through the sync-state dump of scans of those exact lengths."""
+    import json
+    import os
+    from oracle.oracle import example_jpeg
+    kat = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_kats.json")))["partition"]
+    for bits, sb, b_, N, B in kat["cases"]:
+        if bits % 8:
+            continue  # scans are whole bytes
+        scan = bytes([0x00]) * (bits // 8)  # DC "0" codes: decodable
+        f = example_jpeg(scan)
+        with decoder.batch([f], pj.DecodeConfig(subsequence_bits=sb, sequence_length_b=b_),
+                           pj.OutputColorspace.YCbCrPlanes) as bt:
+            bt.run()
+            n = C_count(bt)
+        assert n == N, (bits, sb, n, N)
+
+
+def C_count(bt):
+    import ctypes as C
+    n = C.c_size_t()
+    pj.lib().pjg_batch_dump_sync_states(bt._h, 0, None, 0, C.byref(n))
+    return n.value
