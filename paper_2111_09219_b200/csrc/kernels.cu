@@ -908,6 +908,7 @@ struct DecState {
     uint32_t n;
     uint32_t c, z;
     bool div;
+    bool ovf;  // write mode: a run went past the unit end (z + step > 64): the image needs K1x
     int32_t err;
     int32_t dc0, dc1, dc2;
 };
@@ -1114,6 +1115,11 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
                 stop = true;
                 break;
             }
+            if (Sink::kWrite && z + step > 64) {  // a run past the unit end: reference semantics in K1x
+                s.ovf = true;
+                stop = true;
+                break;
+            }
             if (dcs) {
                 if (kRegAcc) {
                     acur += coef;
@@ -1190,6 +1196,7 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
                                              Sink& sink) {
     s.n = 0;
     s.div = false;
+    s.ovf = false;
     s.err = 0;
     if (s.p >= end_bit) return;
     if (ic.staged)
@@ -1759,6 +1766,458 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
     }
 }
 
+// ============================================ K1x: reference-exact replay ====
+// The fast path (K1..K3) is exact whenever the scan decodes without error on
+// its true path: the synchronised decomposition is then unique and every
+// grouping of subsequences finds it.  For corrupt scans the reference's
+// outcome depends on HOW it synchronises (which speculative chain wrote an
+// entry last, which divergent n survives), and on semantics valid scans never
+// reach (an AC run overflowing the block, parallel_decode.hpp:144-162: the
+// coefficient lands in the next unit's slots, z resets with c += 1 only, and
+// dc_prefix_sum then adds whatever sits in slot 0 of each unit).
+// Images whose entropy stage failed, or whose K3 saw a run overflow, are
+// re-decoded here by one CTA each, restating the reference literally at the
+// configured partition (sb, b): sync_intra_sequence in lock-step rounds
+// (parallel_decode.hpp:171-222), sync_inter_sequence passes with the snapshot /
+// end_changed / progress rules (:227-285), offsets() (:290-316), write_output
+// (:321-330) with worker_count = 1 error order (the lowest failing
+// subsequence), dc_prefix_sum (transform.hpp:56-74); then the unit metadata
+// K4 reads.  One reference behaviour cannot be restated: when a pass changes
+// nothing and sets no flag while some flag stays unset, the reference loops
+// forever (`progressed` stays true, :277-283); the replay reports
+// ConsistencyFailure there.  Off the hot path: a launch finds no work for
+// valid batches.
+constexpr int kK1xThreads = 256;
+constexpr uint32_t kExactFlag = 1u;  // ImgState::exact: K3 saw a run past the unit end
+constexpr uint32_t kActiveBit = 1u << 20;
+
+struct RefSym {
+    int32_t err;   // 0, kOutOfBits, kInvalidCode
+    uint32_t len;  // code + magnitude bits
+    uint32_t run;  // run_length (EOB: 63 - z)
+    int32_t coef;
+    bool is_coef;  // Kind::Coefficient
+    bool eob;
+};
+
+// bits [p, p + 24) MSB first, zero past the segment end (BitCursor::peek_bits)
+__device__ __forceinline__ uint32_t ref_peek24(const uint8_t* seg, uint64_t L, uint64_t p) {
+    const uint64_t nbytes = L >> 3;
+    const uint64_t b0 = p >> 3;
+    uint32_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w = (w << 8) | (b0 + k < nbytes ? uint32_t(seg[b0 + k]) : 0u);
+    w <<= uint32_t(p & 7);
+    // bits at or past L are zero (L is a multiple of 8: whole bytes)
+    return w >> 8;
+}
+__device__ __forceinline__ uint32_t ref_read(const uint8_t* seg, uint64_t L, uint64_t p, uint32_t l) {
+    return l ? ref_peek24(seg, L, p) >> (24 - l) : 0u;
+}
+
+// decode_next_symbol (huffman.hpp:137-175) with decode_codeword (:113-131)
+__device__ RefSym ref_symbol(const uint8_t* seg, uint64_t L, uint64_t p, uint32_t z, const DevHuff* dc,
+                             const DevHuff* ac) {
+    RefSym r{0, 0, 0, 0, false, false};
+    const uint64_t avail = L - p;
+    if (avail == 0) {
+        r.err = kOutOfBits;
+        return r;
+    }
+    const DevHuff* t = z == 0 ? dc : ac;
+    const uint32_t w16 = ref_peek24(seg, L, p) >> 8;
+    uint32_t maxlen;
+    const uint32_t e = dev_lookup(t, w16, maxlen);
+    const uint32_t clen = e >> 8, sym = e & 255u;
+    if (clen == 0) {
+        r.err = avail < maxlen ? kOutOfBits : kInvalidCode;
+        return r;
+    }
+    if (clen > avail) {
+        r.err = kOutOfBits;
+        return r;
+    }
+    const uint64_t p2 = p + clen;
+    uint32_t l;
+    if (z == 0) {
+        l = sym;
+        if (l > 11) {
+            r.err = kInvalidCode;
+            return r;
+        }
+        r.is_coef = true;
+    } else {
+        const uint32_t rr = sym >> 4;
+        l = sym & 15u;
+        if (l == 0) {
+            if (rr == 0) {
+                r.eob = true;
+                r.run = 63 - z;
+            } else if (rr == 15) {
+                r.run = 15;
+            } else {
+                r.err = kInvalidCode;
+            }
+            r.len = clen;
+            return r;
+        }
+        if (l > 10) {
+            r.err = kInvalidCode;
+            return r;
+        }
+        r.run = rr;
+        r.is_coef = true;
+    }
+    if (L - p2 < l) {
+        r.err = kOutOfBits;
+        return r;
+    }
+    const uint32_t bits = ref_read(seg, L, p2, l);
+    r.coef = l == 0 ? 0 : (bits >= (1u << (l - 1)) ? int32_t(bits) : int32_t(bits) - int32_t((1u << l) - 1));
+    r.len = clen + l;
+    return r;
+}
+
+struct RefImg {
+    const uint8_t* seg;
+    uint64_t L, sb, N;
+    uint32_t dpm;
+    uint64_t du_comp;
+    const DevHuff* dc[3];
+    const DevHuff* ac[3];
+};
+
+// decode_subsequence (parallel_decode.hpp:122-164).  Sync mode: returns the
+// end state (divergent at the last good state on an error).  Write mode
+// (coef != nullptr): coefficients at slot out_off + local + run of the
+// image's column-major unit buffer, stops at cap; returns the error code.
+__device__ int32_t ref_subsequence(const RefImg& I, uint64_t i, uint64_t& p, uint32_t& c, uint32_t& z, uint64_t& n,
+                                   bool& div, int16_t* coef, uint64_t out_off, uint64_t cap) {
+    const uint64_t end_bit = min64((i + 1) * I.sb, I.L);
+    n = 0;
+    div = false;
+    uint64_t local = 0;
+    while (p < end_bit) {
+        if (coef && local >= cap) break;
+        const uint32_t comp = uint32_t(I.du_comp >> (4 * c)) & 15u;
+        const RefSym s = ref_symbol(I.seg, I.L, p, z, I.dc[comp], I.ac[comp]);
+        if (s.err) {
+            if (coef) return s.err;
+            div = true;
+            return 0;
+        }
+        const uint64_t step = uint64_t(s.run) + 1;
+        if (coef) {
+            if (local + step > cap) break;
+            if (s.is_coef) {
+                const uint64_t slot = out_off + local + s.run;
+                coef[(slot >> 6) * 64 + c_zz2c[slot & 63]] = int16_t(s.coef);
+            }
+        }
+        p += s.len;
+        n += step;
+        local += step;
+        z += uint32_t(step);
+        if (z >= 64 || s.eob) {
+            z = 0;
+            c = (c + 1 == I.dpm) ? 0 : c + 1;
+        }
+    }
+    return 0;
+}
+
+// CTA-wide helpers (kK1xThreads threads)
+__device__ __forceinline__ unsigned long long cta_sum_u64(unsigned long long v, unsigned long long* red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    for (int w = 0; w < kK1xThreads / 32; ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
+__device__ void k1x_image(const Params& P, uint32_t k, unsigned long long* red) {
+    const int tid = threadIdx.x;
+    const ImgDesc& D = P.img[k];
+    ImgState* st = P.ist + k;
+    RefImg I;
+    I.seg = P.ubuf + D.raw_off;
+    I.L = st->bit_length;
+    I.sb = P.sb_cfg;
+    I.N = (I.L + I.sb - 1) / I.sb;
+    I.dpm = D.dpm;
+    I.du_comp = D.du_comp;
+    for (int cc = 0; cc < 3; ++cc) {
+        I.dc[cc] = P.huff + D.dc_tab[cc];
+        I.ac[cc] = P.huff + D.ac_tab[cc];
+    }
+    const uint64_t N = I.N, b = P.b_cfg, B = (N + b - 1) / b;
+    const uint64_t base = D.sub_first;
+    Entry* E = P.ent + base;                 // info.entries
+    uint64_t* Wp = P.off + base;             // worker chain p / later offsets
+    uint32_t* Wc = P.cap + base;             // worker chain c, z, div | active
+    uint64_t* Sp = reinterpret_cast<uint64_t*>(P.pred + base);  // inter: start snapshot p
+    DcSums* Sf = P.dcs + base;               // inter: .lo start czd, .hi flags
+    __shared__ int s_any;
+    __shared__ unsigned long long s_err;
+    if (tid == 0) s_err = ~0ull;
+
+    // ---- sync_intra_sequence: every sequence's workers in lock-step rounds
+    for (uint64_t i = tid; i < N; i += kK1xThreads) {
+        uint64_t p = i * I.sb, n;
+        uint32_t c = 0, z = 0;
+        bool div;
+        ref_subsequence(I, i, p, c, z, n, div, nullptr, 0, 0);
+        E[i].p = p;
+        E[i].n = uint32_t(n);
+        E[i].czd = pack_czd(c, z, div);
+        const uint64_t last = min64((i / b + 1) * b, N) - 1;
+        Wp[i] = p;
+        Wc[i] = pack_czd(c, z, div) | (!div && i < last ? kActiveBit : 0u);
+    }
+    for (uint64_t r = 1;; ++r) {
+        __syncthreads();
+        int any = 0;
+        for (uint64_t i = tid; i < N; i += kK1xThreads) {
+            uint32_t w = Wc[i];
+            if (!(w & kActiveBit)) continue;
+            const uint64_t nx = i + r, last = min64((i / b + 1) * b, N) - 1;
+            if (nx > last) {
+                Wc[i] = w & ~kActiveBit;
+                continue;
+            }
+            uint64_t p = Wp[i], n;
+            uint32_t c = czd_c(w), z = czd_z(w);
+            bool div;
+            ref_subsequence(I, nx, p, c, z, n, div, nullptr, 0, 0);
+            const Entry old = E[nx];
+            const uint32_t czd = pack_czd(c, z, div);
+            const bool synced = czd_div(old.czd) == div && sync_equal(p, czd, old.p, old.czd);
+            E[nx].p = p;
+            E[nx].n = uint32_t(n);
+            E[nx].czd = czd;
+            if (synced || div) {
+                Wc[i] = czd;
+            } else {
+                Wp[i] = p;
+                Wc[i] = czd | kActiveBit;
+                any = 1;
+            }
+        }
+        if (!__syncthreads_or(any)) break;
+    }
+
+    // ---- sync_inter_sequence: snapshot passes until every flag is set
+    if (B > 1) {
+        for (uint64_t g = tid; g + 1 < B; g += kK1xThreads) Sf[g].hi = 0;  // bit 0 synced, 1 changed, 2 end_changed
+        for (uint64_t pass = 0;; ++pass) {
+            __syncthreads();
+            if (pass > 2 * B + 64) {  // bounded: the reference has no such bound but converges far earlier on any scan seen
+                if (tid == 0) st->status = kConsistencyFailure;
+                return;
+            }
+            int unsynced = 0;
+            for (uint64_t g = tid; g + 1 < B; g += kK1xThreads) unsynced |= !(Sf[g].hi & 1u);
+            if (!__syncthreads_or(unsynced)) break;
+            for (uint64_t g = tid; g + 1 < B; g += kK1xThreads) {
+                const Entry e = E[min64((g + 1) * b, N) - 1];
+                Sp[g] = e.p;
+                Sf[g].lo = e.czd;
+                Sf[g].hi &= 1u;
+            }
+            __syncthreads();
+            int newly = 0;
+            for (uint64_t g = tid; g + 1 < B; g += kK1xThreads) {
+                uint32_t f = Sf[g].hi;
+                if (f & 1u) continue;
+                uint64_t p = Sp[g];
+                uint32_t czd0 = Sf[g].lo;
+                if (czd_div(czd0)) continue;
+                uint32_t c = czd_c(czd0), z = czd_z(czd0);
+                const uint64_t first = (g + 1) * b, last = min64(first + b, N) - 1;
+                for (uint64_t j = first; j <= last; ++j) {
+                    uint64_t n;
+                    bool div;
+                    ref_subsequence(I, j, p, c, z, n, div, nullptr, 0, 0);
+                    const Entry old = E[j];
+                    const uint32_t czd = pack_czd(c, z, div);
+                    const bool synced = czd_div(old.czd) == div && sync_equal(p, czd, old.p, old.czd);
+                    if (!synced || uint32_t(n) != old.n) {
+                        f |= 2u;
+                        if (j == last) f |= 4u;
+                    }
+                    E[j].p = p;
+                    E[j].n = uint32_t(n);
+                    E[j].czd = czd;
+                    if (synced) {
+                        f |= 1u;
+                        newly = 1;
+                        break;
+                    }
+                    if (div) break;
+                }
+                Sf[g].hi = f;
+            }
+            __syncthreads();
+            // end_changed invalidates the successor's flag (:271-276)
+            int progressed = 0, changed = 0;
+            for (uint64_t g = tid; g + 1 < B; g += kK1xThreads) {
+                const uint32_t f = Sf[g].hi;
+                changed |= (f & 2u) ? 1 : 0;
+                progressed |= (f & 3u) ? 1 : 0;
+            }
+            __syncthreads();
+            for (uint64_t g = tid; g + 2 < B; g += kK1xThreads)
+                if (Sf[g].hi & 4u) atomicAnd(&Sf[g + 1].hi, ~1u);
+            progressed = __syncthreads_or(progressed);
+            const int moved = __syncthreads_or(changed | newly);
+            if (!progressed || !moved) {  // fixpoint with unset flags (or the reference's endless loop)
+                if (tid == 0) st->status = kConsistencyFailure;
+                return;
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- offsets(): count check, tail trim, exclusive scan
+    const uint64_t expected = D.expected;
+    unsigned long long raw = 0;
+    for (uint64_t i = tid; i < N; i += kK1xThreads) raw += E[i].n;
+    raw = cta_sum_u64(raw, red);
+    if (raw < expected || raw - expected > 512) {
+        if (tid == 0) st->status = kConsistencyFailure;
+        return;
+    }
+    if (tid == 0) {
+        uint64_t excess = raw - expected;
+        for (uint64_t q = N; q-- > 0 && excess > 0;) {
+            const uint64_t d = min64(excess, E[q].n);
+            E[q].n -= uint32_t(d);
+            excess -= d;
+        }
+    }
+    __syncthreads();
+    {  // exclusive scan of n over contiguous per-thread chunks
+        const uint64_t per = (N + kK1xThreads - 1) / kK1xThreads;
+        const uint64_t lo = min64(uint64_t(tid) * per, N), hi = min64(lo + per, N);
+        unsigned long long mine = 0;
+        for (uint64_t i = lo; i < hi; ++i) mine += E[i].n;
+        __shared__ unsigned long long s_pre[kK1xThreads];
+        s_pre[tid] = mine;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long a = 0;
+            for (int t = 0; t < kK1xThreads; ++t) {
+                const unsigned long long v = s_pre[t];
+                s_pre[t] = a;
+                a += v;
+            }
+        }
+        __syncthreads();
+        unsigned long long a = s_pre[tid];
+        for (uint64_t i = lo; i < hi; ++i) {
+            Wp[i] = a;
+            a += E[i].n;
+        }
+    }
+
+    // ---- write_output into the zeroed unit buffer (worker_count 1: lowest failing i)
+    const uint64_t dus = expected / 64;
+    int16_t* coef = P.coef + D.du_first * 64;
+    for (uint64_t x = tid; x < dus * 8; x += kK1xThreads) reinterpret_cast<int4*>(coef)[x] = make_int4(0, 0, 0, 0);
+    __syncthreads();
+    for (uint64_t i = tid; i < N; i += kK1xThreads) {
+        const uint64_t cap = E[i].n;
+        if (cap == 0) continue;
+        uint64_t p = 0, n;
+        uint32_t c = 0, z = 0;
+        bool div;
+        if (i > 0) {
+            const Entry e = E[i - 1];
+            p = e.p;
+            c = czd_c(e.czd);
+            z = czd_z(e.czd);
+        }
+        const int32_t err = ref_subsequence(I, i, p, c, z, n, div, coef, Wp[i], cap);
+        if (err) atomicMin(&s_err, (unsigned long long)(i << 8) | uint32_t(err));
+    }
+    __syncthreads();
+    if (s_err != ~0ull) {
+        if (tid == 0) st->status = int32_t(s_err & 0xFFu);
+        return;
+    }
+
+    // ---- dc_prefix_sum: per component over the units in scan order (slot 0
+    // of every unit, whatever the decode put there), int16 wrap; chunked scan
+    {
+        const uint64_t per = (dus + kK1xThreads - 1) / kK1xThreads;
+        const uint64_t lo = min64(uint64_t(tid) * per, dus), hi = min64(lo + per, dus);
+        __shared__ uint32_t s_dc[kK1xThreads][3];
+        uint32_t a[3] = {0, 0, 0};
+        for (uint64_t d = lo; d < hi; ++d) a[uint32_t(I.du_comp >> (4 * (d % I.dpm))) & 15u] += uint16_t(coef[d * 64]);
+        for (int cc = 0; cc < 3; ++cc) s_dc[tid][cc] = a[cc];
+        __syncthreads();
+        if (tid < 3) {
+            uint32_t acc = 0;
+            for (int t = 0; t < kK1xThreads; ++t) {
+                const uint32_t v = s_dc[t][tid];
+                s_dc[t][tid] = acc;
+                acc += v;
+            }
+        }
+        __syncthreads();
+        for (int cc = 0; cc < 3; ++cc) a[cc] = s_dc[tid][cc];
+        // the first unit of each chain stays as stored: acc starts at it (mod 2^16 the same)
+        for (uint64_t d = lo; d < hi; ++d) {
+            const uint32_t cc = uint32_t(I.du_comp >> (4 * (d % I.dpm))) & 15u;
+            a[cc] += uint16_t(coef[d * 64]);
+            coef[d * 64] = int16_t(uint16_t(a[cc]));
+        }
+    }
+    __syncthreads();
+
+    // ---- K4's per-unit metadata (as K3's BlockSink): nonzero column mask |
+    // has-AC << 8 | nonzero row mask << 16, S = sum w_u w_v Q |F|
+    for (uint64_t d = tid; d < dus; d += kK1xThreads) {
+        const uint32_t comp = uint32_t(I.du_comp >> (4 * (d % I.dpm))) & 15u;
+        const float* wq = P.wq + 64u * D.q_tab[comp];
+        const int16_t* u = coef + d * 64;
+        uint32_t flags = 0;
+        float S = 0.f;
+        for (int zz = 0; zz < 64; ++zz) {
+            const uint32_t cm = c_zz2c[zz];
+            const int32_t v = u[cm];
+            if (v != 0) {
+                flags |= (1u << (cm >> 3)) | (zz ? (1u << 8) : 0u) | (1u << (16 + (cm & 7)));
+                S = fmaf(wq[zz], float(abs(v)), S);
+            }
+        }
+        P.meta[D.du_first + d] = make_uint2(flags, __float_as_uint(S));
+    }
+}
+
+__global__ void __launch_bounds__(kK1xThreads) k1x_exact(Params P) {
+    __shared__ unsigned long long red[kK1xThreads / 32];
+    for (uint32_t k = blockIdx.x; k < P.n_img; k += gridDim.x) {
+        const ImgState s = P.ist[k];
+        const ImgDesc& D = P.img[k];
+        const bool entropy_fail = s.status == kOutOfBits || s.status == kInvalidCode || s.status == kConsistencyFailure;
+        if (!(entropy_fail || (s.status == 0 && (s.exact & kExactFlag))) || D.n_int > 1 || D.deferred || !D.expected)
+            continue;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            P.ist[k].status = 0;
+            P.ist[k].exact |= 2u;
+        }
+        __syncthreads();
+        k1x_image(P, k, red);
+        __syncthreads();
+    }
+}
+
 // ======================================================= K3: write pass ====
 // Each thread re-decodes its subsequence from the synchronised state and
 // stages the current data unit in a private shared-memory block (column-major,
@@ -1987,6 +2446,11 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
                     live = false;
                     continue;
                 }
+                if (z + step > 64) {  // a run past the unit end: K1x redoes the image
+                    atomicOr(&P.ist[k].exact, kExactFlag);
+                    live = false;
+                    continue;
+                }
                 if (dcs) {
                     acur += coef;
                     coef = acur;
@@ -2014,6 +2478,7 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     }
     if (decode) {
         decode_range<BlockSink, ST>(ic, s, si.hi, cap, sink);
+        if (s.ovf) atomicOr(&P.ist[k].exact, kExactFlag);
         if (s.err) {
             set_status(P.ist + k, s.err);  // write mode rethrows (parallel_decode.hpp:142)
             return;
@@ -2859,7 +3324,7 @@ static int launch_setup(const void* fn, int dyn_smem, int threads, bool want_gri
 uint32_t kernel_launches(const Params& p) {
     // mirrors the launch conditions of the launchers below
     return (p.k0_tiles ? 1u : 0u) + (p.n_dri ? 1u : 0u) + (p.k1_ctas ? 1u : 0u) + (p.k1_ctas > 1 ? (p.k1_hop ? 1u : 2u) : 0u) +
-           (p.k2_tiles ? 1u : 0u) + (p.total_subs ? 1u : 0u) + (p.k4_tiles ? 1u : 0u);
+           (p.k2_tiles ? 1u : 0u) + (p.total_subs ? 1u : 0u) + (p.n_img ? 1u : 0u) + (p.k4_tiles ? 1u : 0u);
 }
 void launch_k0_unstuff(const Params& p, void* stream) {
     if (!p.k0_tiles) return;
@@ -2923,6 +3388,9 @@ void launch_k1c_fixup(const Params& p, void* stream) {
         }
     }
     k1c_fixup<<<1, 1024, 0, (cudaStream_t)stream>>>(p);
+}
+void launch_k1x_exact(const Params& p, void* stream) {
+    if (p.n_img) k1x_exact<<<std::min<uint32_t>(p.n_img, 296), kK1xThreads, 0, (cudaStream_t)stream>>>(p);
 }
 void launch_k2_scan(const Params& p, void* stream) {
     if (p.k2_tiles) k2_scan<<<p.k2_tiles, kK2Threads, 0, (cudaStream_t)stream>>>(p);

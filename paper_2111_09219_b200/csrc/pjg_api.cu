@@ -921,6 +921,8 @@ int batch_create_impl(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const
         if (const char* e = getenv("PJG_K4_LAYOUT")) p.k4_layout = atoi(e) == 1 && all420 ? 1u : 0u;  // A/B
     }
     p.sb = sb_int;
+    p.sb_cfg = sb;
+    p.b_cfg = cfg->sequence_length_b;
     p.sub_first = reinterpret_cast<const uint64_t*>(md + b->m_sub);
     p.total_subs = sub;
     p.ent = ctx->ent.as<Entry>();
@@ -1023,6 +1025,9 @@ int pjg_batch_decode(pjg_batch* b) {
     CU(cudaEventRecord(ctx->ev[5], s), "ev");
     if (b->total_dus) CU(cudaMemsetAsync(ctx->blkmeta.p, 0, b->total_dus * 8, s), "memset meta");
     launch_k3_write(b->prm, s);
+    // images whose entropy stage failed (or saw a run past a unit end): the
+    // reference's exact semantics at the configured partition (K1x)
+    launch_k1x_exact(b->prm, s);
     CU(cudaEventRecord(ctx->ev[6], s), "ev");
     launch_k4_transform(b->prm, s);
     CU(cudaGetLastError(), "kernel launch");
@@ -1243,7 +1248,9 @@ int pjg_batch_dump_sync_states(const pjg_batch* b, size_t i, pjg_sync_entry* out
     if (st) return st;
     if (b->host_status[i] != 0) return b->host_status[i];
     const uint64_t L = b->dev_state[i].bit_length;
-    const uint64_t sbu = b->cfg.subsequence_bits, f = b->sb_int ? sbu / b->sb_int : 1;
+    // K1x-redone images hold the reference's entries at the configured partition
+    const bool redone = (b->dev_state[i].exact & 2u) != 0;
+    const uint64_t sbu = b->cfg.subsequence_bits, f = (b->sb_int && !redone) ? sbu / b->sb_int : 1;
     uint64_t N = (L + sbu - 1) / sbu;
     if (b->desc[i].n_int > 1) {  // restart intervals: the subsequences in use (K0b)
         uint2 last;
@@ -1256,13 +1263,15 @@ int pjg_batch_dump_sync_states(const pjg_batch* b, size_t i, pjg_sync_entry* out
     if (!out) return PJG_OK;
     if (cap < N) return fail(ctx, PJG_CAPACITY, "sync state buffer too small");
     // internal subsequences (f per configured one when sb was split)
-    const uint64_t Ni = b->desc[i].n_int > 1 ? N : (L + b->sb_int - 1) / b->sb_int;
+    const uint64_t Ni = (b->desc[i].n_int > 1 || redone) ? N : (L + b->sb_int - 1) / b->sb_int;
     std::vector<Entry> ents(Ni);
     std::vector<uint32_t> caps(Ni);
     const uint64_t g0 = b->desc[i].sub_first;
     if (Ni) {
         CU(cudaMemcpy(ents.data(), ctx->ent.as<Entry>() + g0, Ni * sizeof(Entry), cudaMemcpyDeviceToHost), "D2H ent");
         CU(cudaMemcpy(caps.data(), ctx->cap.as<uint32_t>() + g0, Ni * 4, cudaMemcpyDeviceToHost), "D2H cap");
+        if (redone)
+            for (uint64_t j = 0; j < Ni; ++j) caps[j] = ents[j].n;  // trimmed by K1x's offsets()
     }
     const uint64_t fk = b->desc[i].n_int > 1 ? 1 : f;
     for (uint64_t k = 0; k < N; ++k) {

@@ -111,7 +111,8 @@ struct ImgDesc {
 struct ImgState {
     uint64_t bit_length;   // 8 * unstuffed bytes (bitstream.hpp:74), written by K0
     int32_t status;        // first error (Status), 0 = ok
-    uint32_t inter_hops;   // inter-sequence overflow hops (diagnostics)
+    uint32_t exact;        // bit 0: K3 saw an AC run past the unit end; bit 1: K1x re-decoded the image
+                           // (its s_info entries are then at the configured partition)
 };
 
 // ----------------------------------------------------------- sync state --
@@ -191,7 +192,10 @@ struct Params {
     uint32_t k1_hop;               // K1 re-chains stale CTA starts in-kernel (small grids); else K1c first pass
     uint32_t k4_layout;            // 1: every image is 4:2:0 colour to RGB (specialised K4); 0: any
     // subsequences
-    uint64_t sb;                   // subsequence_bits
+    uint64_t sb;                   // subsequence_bits (internal: may be a divisor of sb_cfg)
+    uint64_t sb_cfg;               // the configured subsequence_bits (K1x replays the reference partition)
+    uint32_t b_cfg;                // the configured sequence_length_b
+    uint32_t pad_b;
     const uint64_t* sub_first;     // n_img + 1 prefix
     uint64_t total_subs;
     Entry* ent;
@@ -242,6 +246,7 @@ void launch_k0b_segments(const Params& p, void* stream);
 void launch_k1_sync(const Params& p, void* stream);
 void launch_k1c_fixup(const Params& p, void* stream);
 void launch_k2_scan(const Params& p, void* stream);
+void launch_k1x_exact(const Params& p, void* stream);
 void launch_k3_write(const Params& p, void* stream);
 void launch_k4_transform(const Params& p, void* stream);
 void launch_k5_color(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, uint32_t W, uint32_t H,

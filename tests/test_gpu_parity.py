@@ -147,12 +147,7 @@ def test_error_codes_match_reference(decoder):
         st = b.run()
     for (name, f), s in zip(cases.items(), st):
         ref = Ref.decode(f, rgb=True)
-        if ref.status == 0:
-            assert s == 0, name
-        else:
-            assert s != 0, name
-            if name != "scan_cut":  # mid-scan truncation: both fail; the stage may differ
-                assert s == ref.status, (name, s, ref.status)
+        assert s == ref.status, (name, s, ref.status)  # corrupt scans: K1x replays the reference
 
 
 def test_upsample_and_convert_kats(decoder):
