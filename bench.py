@@ -1,20 +1,35 @@
 #!/usr/bin/env python3
 """Benchmark: JPEG decode GB/s (RGB out) & images/s on B200 vs the CPU reference.
 
-Workload (BASELINE.json configs[2], the batch the metric's 1/2/4/8-GPU scaling
-is quoted on): 4096 synthetic 500x375 4:2:0 q75 baseline JPEGs per GPU
-(weak scaling: every rank decodes its own 4096-image batch, no collective on
-the data path).  ``--config`` selects the other BASELINE shapes.
+Workload (default ``--config 3``, BASELINE.json configs[2], the batch the
+metric's 1/2/4/8-GPU scaling is quoted on): the SURVEY.md §8(d) corpus —
+4096 files oracle_encode(make_test_image(500, 375, seed), 75, 4:2:0), seeds
+1000..5095, produced natively and byte-identical to the reference encoder
+(paper_2111_09219_b200/synth.py, pinned by tests/test_synth.py).  Under
+torchrun the ONE batch is split across the ranks by compressed bytes
+(dist.shard_by_bytes), one process and two contexts
+(streams) per GPU, no collective on the data path; single-image configs run
+as replicas.
 
-One step = one full batch decode: K0 unstuff -> K1 sync -> K1c fix-up ->
-K2 scan -> K3 write -> K4 IDCT+upsample+RGB, inputs already resident in HBM
-(``value``), RGB left in HBM.  ``e2e`` = the same batch through the C-ABI
-from pinned HOST JPEG bytes to pinned HOST RGB: header parse + H2D + decode +
-D2H inside the timed region.
+One step = one decode of the rank's shard: K0 unstuff -> K1 sync -> K1c
+fix-up -> K2 scan -> K3 write -> K1x (idle on valid scans) -> K4 IDCT +
+upsample + RGB, RGB left in HBM.  Reported:
+
+  value             device-resident: compressed bytes already in HBM, L2
+                    flushed between steps (untimed), CUDA events on the
+                    decode streams, max over ranks
+  metric_of_record  SURVEY.md §8(d) / PAPER.md:341-342: host header parse ->
+                    H2D of the compressed bytes (pinned) -> K0..K4, output in
+                    HBM; host wall clock from a start barrier to the last
+                    GPU's completion, median and best of the steps
+  e2e               through the C-ABI from pinned HOST JPEG bytes to pinned
+                    HOST RGB (parse + H2D + decode + D2H), max over ranks
+  weak_scaling      (N > 1) every rank decodes the whole batch
+  roofline          K4 (+ K0/K3 in stage_rooflines) against MEASURED_PEAKS
 
 ``--impl reference`` times the reference's own CPU decoder (pjpeg headers
-compiled in place: oracle/_ref, decode_batch + upsample_and_convert) on a
-bounded sample of the same workload with all host threads.
+compiled in place: oracle/_ref, decode_batch + upsample_and_convert) on the
+same corpus with all host threads, rank 0 only.
 """
 from __future__ import annotations
 
@@ -30,27 +45,42 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "JPEG decode GB/s (RGB out)"
+CORPUS = "oracle_encode(make_test_image(w, h, seed)) per SURVEY.md §8(d); native byte-identical generator"
+
+# name: (images, w, h, quality, sampling, restart_interval (MCUs), first seed)
 CONFIGS = {
-    # name: (n images, w, h, quality, sampling, restart_interval)
-    "1": (1, 512, 512, 85, "444", 0),
-    "2": (1, 3840, 2160, 90, "420", 0),
-    "3": (4096, 500, 375, 75, "420", 0),
-    "4": (1, 16384, 16384, 95, "444", 0),
-    "5": (1, 8192, 8192, 75, "420", 0),
-    "5r": (1, 8192, 8192, 75, "420", 512),  # one MCU row per restart interval (DRI extension)
-    "5g": (1, 8192, 8192, 75, "gray", 0),
-    "5q": (1, 8192, 8192, 100, "444", 0),
+    "1": (1, 512, 512, 85, "444", 0, 1),
+    "2": (1, 3840, 2160, 90, "420", 0, 2),
+    "3": (4096, 500, 375, 75, "420", 0, 1000),
+    "4": (1, 16384, 16384, 95, "444", 0, 4),
 }
 CONFIG_NAMES = {
     "1": "single 512x512 4:4:4 q85",
     "2": "single 3840x2160 4:2:0 q90",
-    "3": "batch 4096 x 500x375 4:2:0 q75 per GPU",
+    "3": "batch 4096 x 500x375 4:2:0 q75",
     "4": "single 16384x16384 4:4:4 q95",
-    "5": "single 8192x8192 4:2:0 q75",
-    "5r": "single 8192x8192 4:2:0 q75, DRI one MCU row per interval",
-    "5g": "single 8192x8192 grayscale q75",
-    "5q": "single 8192x8192 4:4:4 q100",
 }
+# config 5: the 8192^2 sweep, "5-q<Q>-<420|444|gray>[-dri]" (DRI: one restart
+# interval per MCU row, decoded with the restart-interval extension)
+for _q in (50, 60, 70, 75, 80, 85, 90, 95, 100):
+    for _s in ("420", "444", "gray"):
+        _mx = 8192 // (16 if _s == "420" else 8)
+        CONFIGS[f"5-q{_q}-{_s}"] = (1, 8192, 8192, _q, _s, 0, 5000 + _q)
+        CONFIG_NAMES[f"5-q{_q}-{_s}"] = f"single 8192x8192 {_s} q{_q}"
+        CONFIGS[f"5-q{_q}-{_s}-dri"] = (1, 8192, 8192, _q, _s, _mx, 5000 + _q)
+        CONFIG_NAMES[f"5-q{_q}-{_s}-dri"] = f"single 8192x8192 {_s} q{_q}, DRI one MCU row per interval"
+for _alias, _k in (("5", "5-q75-420"), ("5r", "5-q75-420-dri"), ("5g", "5-q75-gray"), ("5q", "5-q100-444")):
+    CONFIGS[_alias] = CONFIGS[_k]
+    CONFIG_NAMES[_alias] = CONFIG_NAMES[_k]
+
+
+def config_dict(key, sb):
+    """The workload description — identical in both arms."""
+    n, w, h, q, s, ri, seed = CONFIGS[key]
+    return {"workload": CONFIG_NAMES[key], "images": n, "width": w, "height": h, "quality": q, "sampling": s,
+            "restart_interval": ri, "seed0": seed, "corpus": CORPUS, "subsequence_bits": sb,
+            "sequence_length_b": 256}
 
 
 def load_peaks():
@@ -62,8 +92,19 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 class ClockSampler:
-    """SM clock + throttle reasons sampled through NVML every 10 ms during
+    """SM clock + throttle reasons sampled through NVML every 5 ms during
     the timed region (the recipe's clocks line, B200_PROFILING.md)."""
 
     def __init__(self, index):
@@ -92,8 +133,6 @@ class ClockSampler:
             time.sleep(0.005)
 
     def start(self):
-        # the NVML handle is taken here, so the sampling thread samples from
-        # the first millisecond of the timed region
         try:
             import pynvml as N
             N.nvmlInit()
@@ -109,29 +148,32 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
         self.stop_evt.set()
         self.t.join(timeout=2)
-        if not self.samples:  # a timed region shorter than one sampling period
+        if not self.samples:
             self._sample()
         return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 def profiled_traffic(cfg_key):
-    """dram__bytes_read.sum + dram__bytes_write.sum of K4 from the committed
-    ncu --set full capture of the same workload (config 3), bytes per launch."""
+    """dram__bytes_read.sum + dram__bytes_write.sum of K4 per launch, from the
+    committed ncu --set full capture of the same workload (config 3)."""
     if cfg_key != "3":
-        return None
-    try:
-        vals = {}
-        with open(os.path.join(ROOT, "profiles", "round1", "ncu_k4_transform.txt")) as f:
-            for line in f:
-                parts = line.split()
-                if len(parts) >= 2 and parts[0].startswith("dram__bytes_"):
-                    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(
-                        parts[2] if len(parts) > 2 else "Gbyte", 1e9)
-                    vals[parts[0]] = float(parts[1]) * scale
-        return int(vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
-    except Exception:
-        return None
+        return None, None
+    for rnd in ("round2", "round1"):
+        path = os.path.join(ROOT, "profiles", rnd, "ncu_k4_transform.txt")
+        try:
+            vals = {}
+            with open(path) as f:
+                for line in f:
+                    parts = line.split()
+                    if len(parts) >= 2 and parts[0].startswith("dram__bytes_"):
+                        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(
+                            parts[2] if len(parts) > 2 else "Gbyte", 1e9)
+                        vals[parts[0]] = float(parts[1]) * scale
+            return int(vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]), os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
 
 
 def dist_env():
@@ -139,49 +181,47 @@ def dist_env():
     return rank_env()
 
 
-def make_corpus(cfg_key, rank, pinned=True, no_restart=False):
-    """no_restart: the DRI-free twin (the reference rejects DRI)."""
-    from paper_2111_09219_b200.synth import synth_batch
-    n, w, h, q, s, ri = CONFIGS[cfg_key]
-    if no_restart:
-        ri = 0
-    blob, offs, sizes = synth_batch(n, w, h, 100000 * (rank + 1), q, s, ri)
-    if pinned:
-        import torch
-        pb = torch.empty(blob.size + 64, dtype=torch.uint8).pin_memory()
-        pn = pb.numpy()
-        pn[: blob.size] = blob
-        return pb, pn[: blob.size], offs, sizes
-    return None, blob, offs, sizes
+def make_corpus(key, no_restart=False, threads=None):
+    """(blob, offsets, sizes) of the configuration's files; no_restart: the
+    DRI-free twin (the reference rejects DRI)."""
+    from paper_2111_09219_b200.synth import synth_ref_batch
+    n, w, h, q, s, ri, seed = CONFIGS[key]
+    return synth_ref_batch(n, w, h, seed, q, s, 0 if no_restart else ri, threads=threads)
+
+
+def pinned_copy(arr):
+    import torch
+    t = torch.empty(arr.size + 64, dtype=torch.uint8).pin_memory()
+    v = t.numpy()
+    v[: arr.size] = arr
+    return t, v[: arr.size]
 
 
 def cpu_reference_sample(blob, offs, sizes, target_s, threads):
-    """Reference decode_batch + upsample_and_convert on a bounded sample."""
+    """The reference's decode_batch + upsample_and_convert on a bounded sample
+    (about target_s seconds of work)."""
     from oracle.oracle import Ref
     files = [blob[o: o + s].tobytes() for o, s in zip(offs, sizes)]
     n_all = len(files)
-    # calibrate on a small prefix, then size the sample for ~target_s seconds
     k = min(n_all, max(1, threads))
     t0 = time.perf_counter()
-    st, outs = Ref.decode_batch_rgb(files[:k], threads)
+    st, _ = Ref.decode_batch_rgb(files[:k], threads)
     dt = time.perf_counter() - t0
     assert (st == 0).all(), st
     per = dt / k
     m = int(min(n_all, max(k, target_s / max(per, 1e-9))))
-    sample = [files[i % n_all] for i in range(m)] if n_all > 1 else files
+    sample = files[:m]
     t0 = time.perf_counter()
-    reps = 0
-    rgb_bytes = 0
+    reps = rgb_bytes = 0
     while True:
         st, outs = Ref.decode_batch_rgb(sample, threads)
         assert (st == 0).all()
         rgb_bytes += sum(o.size for o in outs)
         reps += 1
-        if time.perf_counter() - t0 >= target_s * 0.5 or n_all == 1 and reps >= 1:
+        if time.perf_counter() - t0 >= target_s * 0.5:
             break
     el = time.perf_counter() - t0
-    nimg = reps * len(sample)
-    return {"gbs": rgb_bytes / el / 1e9, "img_s": nimg / el, "seconds": el, "images": nimg,
+    return {"gbs": rgb_bytes / el / 1e9, "img_s": reps * len(sample) / el, "seconds": el,
             "sample": f"{len(sample)} of {n_all} images x {reps} reps"}
 
 
@@ -190,26 +230,25 @@ def run_reference(args, rank, world):
         return 0
     from oracle.oracle import Ref
     threads = Ref.hardware_concurrency()
-    _, blob, offs, sizes = make_corpus(args.config, 0, pinned=False, no_restart=True)
-    n, w, h, q, s, _ = CONFIGS[args.config]
-    target = 6.0 if args.config in ("1", "2", "3") else 60.0
+    blob, offs, sizes = make_corpus(args.config, no_restart=True)
+    n = CONFIGS[args.config][0]
+    target = 6.0 if n > 1 or CONFIGS[args.config][1] * CONFIGS[args.config][2] < 10_000_000 else 20.0
     for _ in range(args.warmup):
-        cpu_reference_sample(blob, offs, sizes[:], 1.0, threads)
-    vals = []
-    for _ in range(args.steps):
-        r = cpu_reference_sample(blob, offs, sizes, target / max(1, args.steps) * 2, threads)
-        vals.append(r)
-    gbs = float(np.mean([v["gbs"] for v in vals]))
-    ims = float(np.mean([v["img_s"] for v in vals]))
+        cpu_reference_sample(blob, offs, sizes, 1.0, threads)
+    vals = [cpu_reference_sample(blob, offs, sizes, target / max(1, args.steps) * 2, threads)
+            for _ in range(args.steps)]
+    gbs = float(np.median([v["gbs"] for v in vals]))
+    ims = float(np.median([v["img_s"] for v in vals]))
     rec = {
-        "impl": "reference", "metric": "JPEG decode GB/s (RGB out)", "value": round(gbs, 4), "unit": "GB/s",
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
         "images_per_s": round(ims, 2), "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1000 * float(np.mean([v["seconds"] for v in vals])), 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8 in / f64 IDCT+colour / u8 out",
-        "data": "synthetic", "config": {"workload": CONFIG_NAMES[args.config], "images": n, "width": w, "height": h,
-                                        "quality": q, "sampling": s},
+        "ms_per_step": round(1000 * float(np.median([v["seconds"] for v in vals])), 3),
+        "higher_is_better": True, "scaling": "strong" if n > 1 else "weak", "vs_baseline": None,
+        "dtype": "u8 in / f64 IDCT+colour / u8 out", "data": "synthetic",
+        "config": config_dict(args.config, args.sb),
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": vals[-1]["sample"]},
+                         "cpu_model": cpu_model(), "sample": vals[-1]["sample"]
+                         + (" (DRI-free twin: the reference rejects DRI)" if CONFIGS[args.config][5] else "")},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(rec), flush=True)
@@ -225,9 +264,10 @@ def main():
     ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
     ap.add_argument("--sb", type=int, default=1024, help="subsequence_bits")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-weak", action="store_true", help="skip the N > 1 weak-scaling leg")
     ap.add_argument("--chunk", type=int, default=512, help="images per pipelined e2e chunk")
-    ap.add_argument("--check", action="store_true", help="verify a few images against the reference")
     args = ap.parse_args()
+    args.steps = max(1, args.steps)
     rank, world, local = dist_env()
 
     if args.impl == "reference":
@@ -235,166 +275,197 @@ def main():
 
     import torch
     import paper_2111_09219_b200 as pj
+    from paper_2111_09219_b200 import dist as pdist
 
     # PJG_BENCH_ONE_DEVICE=1: every rank on cuda:0 with gloo plumbing — exercises
-    # the N > 1 path (barrier, max-over-ranks, rank-0 line) on a one-GPU box
+    # the N > 1 path (sharding, barrier, max-over-ranks, rank-0 line) on one GPU
     one_dev = os.environ.get("PJG_BENCH_ONE_DEVICE") == "1"
     if one_dev:
         local = 0
     torch.cuda.set_device(local)
-    from paper_2111_09219_b200 import dist as pdist
     dist = pdist.init("gloo" if one_dev else "nccl", local) if world > 1 else None
-    dev = torch.device("cpu") if one_dev else torch.device("cuda", local)  # reduction tensors
+    rdev = torch.device("cpu") if one_dev else torch.device("cuda", local)  # reduction tensors
 
-    n, w, h, q, s, _ = CONFIGS[args.config]
-    pinned_t, blob, offs, sizes = make_corpus(args.config, rank)
+    n_all, W, H, Q, S, RI, _ = CONFIGS[args.config]
+    cfgd = config_dict(args.config, args.sb)
+    # ---- corpus: generated once (rank 0, all host threads) and shared
+    if rank == 0:
+        blob, offs, sizes = make_corpus(args.config)
+    else:
+        blob = offs = sizes = np.zeros(0, np.uint8)
+    if world > 1:
+        blob = pdist.broadcast_array(np.asarray(blob, np.uint8), 0, rdev)
+        offs = pdist.broadcast_array(np.asarray(offs, np.int64), 0, rdev)
+        sizes = pdist.broadcast_array(np.asarray(sizes, np.int64), 0, rdev)
+    batch_mode = n_all > 1
+    if batch_mode:  # §8(e): the one batch split by compressed bytes
+        mine = pdist.shard_by_bytes(sizes, world)[rank]
+        scaling = "strong"
+    else:  # single images: replicas
+        mine = list(range(n_all))
+        scaling = "weak"
+    sblob, soffs, ssizes = pdist.shard_blob(blob, offs, sizes, mine)
+    pin_t, pblob = pinned_copy(sblob)
+    n = len(mine)
+
     dec = pj.Decoder(local)
-    cfg = pj.DecodeConfig(subsequence_bits=args.sb, restart_intervals=CONFIGS[args.config][5] > 0)
+    dec2 = pj.Decoder(local)
+    decs = [dec, dec2]
+    cfg = pj.DecodeConfig(subsequence_bits=args.sb, restart_intervals=RI > 0)
     out_kind = pj.OutputColorspace.RGBInterleaved
-    stream = torch.cuda.ExternalStream(dec.stream(), device=torch.device("cuda", local))
-    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
+    dev = torch.device("cuda", local)
+    streams = [torch.cuda.ExternalStream(d.stream(), device=dev) for d in decs]
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    # ---------------- device-resident timing (value) ----------------------
-    b = dec.batch((blob, offs, sizes), cfg, out_kind)
+    def parts_of(k):  # the shard as k concurrent parts on the two contexts
+        if k <= 1 or n < 2:
+            return [(0, n)]
+        return [(0, n // 2), (n // 2, n)]
+
+    # ---- (1) one stream: per-stage CUDA-event times (rooflines)
+    b = dec.batch((pblob, soffs, ssizes), cfg, out_kind)
     b.upload()
     st = b.decode().synchronize()
     assert (st == 0).all(), f"decode failed: {np.unique(st)}"
     rgb_bytes = sum(int(i.output_bytes) for i in b.infos)
     dus = sum(int(i.data_units) for i in b.infos)
-    comp_bytes = int(sum(sizes))
-    if args.check:
-        from oracle.oracle import Ref
-        outs = b.download()
-        _, tb, to, ts = make_corpus(args.config, rank, pinned=False, no_restart=True)  # DRI-free twin
-        for i in list(range(min(4, n))) + ([n - 1] if n > 4 else []):
-            f = tb[to[i]: to[i] + ts[i]].tobytes()
-            ref = Ref.decode(f, rgb=True)
-            assert np.array_equal(outs[i][: ref.data.size], ref.data.reshape(-1)), f"mismatch image {i}"
-        print(f"# check: {min(4, n) + (1 if n > 4 else 0)} images bit-exact vs reference", file=sys.stderr)
-
-    def one_step():
-        with torch.cuda.stream(stream):
-            flush_buf.zero_()  # untimed L2 flush
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
+    comp_bytes = int(np.sum(ssizes))
+    stage_runs = []
+    for it in range(args.warmup + args.steps):
+        with torch.cuda.stream(streams[0]):
+            flush_buf.zero_()
         b.decode()
-        with torch.cuda.stream(stream):
-            e1.record(stream)
         b.synchronize()
-        return e0.elapsed_time(e1), b.stage_times()
-
-    # (a) one stream: per-stage CUDA-event times for the rooflines
-    for _ in range(args.warmup):
-        one_step()
-    torch.cuda.synchronize()
-    single_ms, stages = [], []
-    for _ in range(args.steps):
-        ms, stt = one_step()
-        single_ms.append(ms)
-        stages.append(stt)
-    torch.cuda.synchronize()
+        if it >= args.warmup:
+            stage_runs.append(b.stage_times())
+    st_mean = {k: float(np.mean([getattr(x, k) for x in stage_runs])) for k in
+               ("unstuff", "sync", "scan", "write", "idct")}
     sync_stats = b.sync_stats()
     scan_bits = b.scan_bits()
-    st_mean = {k: float(np.mean([getattr(x, k) for x in stages])) for k in
-               ("unstuff", "sync", "scan", "write", "idct")}
-    if n >= 2:
-        b.close()
+    single_launches = b.kernel_launches()
+    b.close()
 
-    # (b) the step as deployed: the batch as two concurrent half-batches on two
-    # contexts (streams), so one half's latency-bound Huffman kernels overlap the
-    # other half's bandwidth-bound transform; timed from one event to the join
-    dec2 = pj.Decoder(local)
-    halves = []
-    if n >= 2:
-        h = n // 2
-        for lo, hi, d in ((0, h, dec), (h, n, dec2)):
-            bb = d.batch((blob, offs[lo:hi], sizes[lo:hi]), cfg, out_kind)
-            bb.upload()
-            assert (bb.decode().synchronize() == 0).all()
-            halves.append(bb)
-    stream2 = torch.cuda.ExternalStream(dec2.stream(), device=torch.device("cuda", local))
+    # ---- (2) value: device-resident step, the shard as two concurrent parts
+    parts = []
+    for (lo, hi), d in zip(parts_of(2), decs):
+        bb = d.batch((pblob, soffs[lo:hi], ssizes[lo:hi]), cfg, out_kind)
+        bb.upload()
+        assert (bb.decode().synchronize() == 0).all()
+        parts.append(bb)
+    launches_per_step = sum(x.kernel_launches() for x in parts)
 
-    def two_stream_step():
-        with torch.cuda.stream(stream):
+    def device_step():
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(streams[0]):
             flush_buf.zero_()  # untimed L2 flush
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(streams[0])
+        for s_ in streams[1:]:
+            s_.wait_event(e0)
+        for bb in parts:
+            bb.decode()
+        for s_ in streams[1:len(parts)]:
             j = torch.cuda.Event()
-            e0.record(stream)
-        stream2.wait_event(e0)
-        halves[0].decode()
-        halves[1].decode()
-        j.record(stream2)
-        stream.wait_event(j)
-        with torch.cuda.stream(stream):
-            e1.record(stream)
-        halves[0].synchronize()
-        halves[1].synchronize()
+            j.record(s_)
+            streams[0].wait_event(j)
+        e1.record(streams[0])
+        for bb in parts:
+            bb.synchronize()
         return e0.elapsed_time(e1)
 
-    step_fn = two_stream_step if halves else (lambda: one_step()[0])
-    # our kernels per timed step (the library's own count of its launches)
-    launches_per_step = sum(x.kernel_launches() for x in halves) if halves else b.kernel_launches()
     for _ in range(args.warmup):
-        step_fn()
+        device_step()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     clk.start()
-    step_ms = [step_fn() for _ in range(args.steps)]
+    dev_ms = [device_step() for _ in range(args.steps)]
     torch.cuda.synchronize()
     clocks = clk.stop()
-    for bb in halves:
+    for bb in parts:
         bb.close()
-    if not halves:
-        b.close()
-    tot_ms = pdist.max_over_ranks(float(np.sum(step_ms)), dev)
-    ms_per_step = tot_ms / args.steps
-    value = world * rgb_bytes / (ms_per_step / 1e3) / 1e9
-    img_s = world * n / (ms_per_step / 1e3)
-    single_tot = pdist.max_over_ranks(float(np.sum(single_ms)), dev)
-    single_value = world * rgb_bytes / (single_tot / args.steps / 1e3) / 1e9
+    step_max = [pdist.max_over_ranks(x, rdev) for x in dev_ms]  # per step: the slowest rank
+    tot_rgb = pdist.sum_over_ranks(rgb_bytes, rdev)
+    tot_img = pdist.sum_over_ranks(n, rdev)
+    ms_per_step = float(np.mean(step_max))
+    value = tot_rgb / (ms_per_step / 1e3) / 1e9
 
-    # ---------------- end-to-end through the C-ABI with host buffers ------
+    # ---- (3) metric of record: host parse -> H2D -> K0..K4, output in HBM
+    def record_step():
+        bs = []
+        t0 = time.perf_counter()
+        for (lo, hi), d in zip(parts_of(2), decs):
+            bb = d.batch((pblob, soffs[lo:hi], ssizes[lo:hi]), cfg, out_kind)  # header parse + plan
+            bb.upload()  # one H2D of the compressed bytes
+            bb.decode()
+            bs.append(bb)
+        for bb in bs:
+            bb.synchronize()
+        t1 = time.perf_counter()
+        for bb in bs:
+            bb.close()
+        return (t1 - t0) * 1e3
+
+    for _ in range(args.warmup):
+        record_step()
+    rec_ms = []
+    for _ in range(args.steps):
+        if dist:
+            dist.barrier()
+        rec_ms.append(pdist.max_over_ranks(record_step(), rdev))
+    rec_med, rec_best = float(np.median(rec_ms)), float(np.min(rec_ms))
+
+    # ---- (4) e2e through the C-ABI with host buffers (D2H included)
     host_out = torch.empty(rgb_bytes + n * 256 + 4096, dtype=torch.uint8).pin_memory()
-    host_ptr = host_out.data_ptr()
-    e2e_ms = []
-    h2d = d2h = 0
-
-    decs = [dec, dec2]
 
     def e2e_step():
-        # the public API a host caller uses: pinned JPEG bytes in, pinned RGB
-        # out, chunked so D2H of one chunk overlaps decode of the next
         t0 = time.perf_counter()
-        st, _, ob = pj.decode_to_host_pipelined(decs, blob, offs, sizes, host_ptr, host_out.numel(), cfg,
-                                                out_kind, chunk=args.chunk)
+        st_, _, ob = pj.decode_to_host_pipelined(decs, pblob, soffs, ssizes, host_out.data_ptr(), host_out.numel(),
+                                                 cfg, out_kind, chunk=args.chunk)
         t1 = time.perf_counter()
-        assert (st == 0).all()
+        assert (st_ == 0).all()
         return (t1 - t0) * 1e3, ob
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
-    if dist:
-        dist.barrier()
+    e2e_ms = []
+    d2h = 0
     for _ in range(args.steps):
-        ms, ob = e2e_step()
-        e2e_ms.append(ms)
-        d2h = ob
-    h2d = comp_bytes
-    e2e_tot = pdist.max_over_ranks(float(np.sum(e2e_ms)), dev)
-    e2e_val = world * rgb_bytes / (e2e_tot / args.steps / 1e3) / 1e9
+        if dist:
+            dist.barrier()
+        ms, d2h = e2e_step()
+        e2e_ms.append(pdist.max_over_ranks(ms, rdev))
+    e2e_med = float(np.median(e2e_ms))
+    e2e_val = tot_rgb / (e2e_med / 1e3) / 1e9
 
-    # ---------------- roofline of the dominant HBM-bound stage (K4) -------
+    # ---- (5) weak scaling (N > 1): every rank decodes the whole batch
+    weak = None
+    if world > 1 and batch_mode and not args.no_weak:
+        fpin, fblob = pinned_copy(np.asarray(blob, np.uint8))
+        wparts = []
+        half = n_all // 2
+        for (lo, hi), d in zip(((0, half), (half, n_all)), decs):
+            bb = d.batch((fblob, offs[lo:hi], sizes[lo:hi]), cfg, out_kind)
+            bb.upload()
+            assert (bb.decode().synchronize() == 0).all()
+            wparts.append(bb)
+        full_rgb = sum(x.output_bytes() for x in wparts)
+        parts = wparts
+        for _ in range(args.warmup):
+            device_step()
+        dist.barrier()
+        wms = [pdist.max_over_ranks(device_step(), rdev) for _ in range(args.steps)]
+        for bb in wparts:
+            bb.close()
+        weak = {"value": round(world * full_rgb / (float(np.mean(wms)) / 1e3) / 1e9, 3), "unit": "GB/s",
+                "ms_per_step": round(float(np.mean(wms)), 4), "images_per_gpu": n_all}
+
+    # ---- rooflines (K4 dominant HBM-bound stage; K0 / K3 beside it)
     peak, peak_kind = load_peaks()
     k4_bytes = dus * 128 + rgb_bytes  # int16 coefficient read + RGB write
     k4_ms = st_mean["idct"]
     achieved = k4_bytes / (k4_ms / 1e3) / 1e9
-    dominant = max(st_mean, key=st_mean.get)
-    # the other bandwidth-bound stages against the same peak:
-    # K0 reads + writes the scan (2 C), K3 reads it and writes the coefficients
     stage_roof = {
         "k0_unstuff": {"algorithmic_bytes": 2 * comp_bytes, "ms": st_mean["unstuff"]},
         "k3_write": {"algorithmic_bytes": comp_bytes + dus * 128, "ms": st_mean["write"]},
@@ -404,59 +475,79 @@ def main():
         v["achieved_gbs"] = round(v["algorithmic_bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 else None
         v["frac"] = round(v["achieved_gbs"] / peak, 4) if v["achieved_gbs"] else None
         v["ms"] = round(v["ms"], 4)
-    traffic = profiled_traffic(args.config)
+    traffic, traffic_src = profiled_traffic(args.config)
+    per_rank = pdist.all_over_ranks(float(np.mean(dev_ms)), rdev)
 
+    # ---- CPU baseline: the reference on this host's cores (rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle.oracle import Ref
             threads = Ref.hardware_concurrency()
             cb, co, cs = blob, offs, sizes
-            if CONFIGS[args.config][5]:  # the reference rejects DRI: time the DRI-free twin
-                _, cb, co, cs = make_corpus(args.config, rank, pinned=False, no_restart=True)
-            r = cpu_reference_sample(cb, co, cs, 10.0 if args.config in ("1", "2", "3") else 30.0, threads)
+            if RI:  # the reference rejects DRI: time the DRI-free twin
+                cb, co, cs = make_corpus(args.config, no_restart=True)
+            big = W * H >= 10_000_000
+            r = cpu_reference_sample(cb, co, cs, 20.0 if big else 10.0, threads)
             cpu = {"value": round(r["gbs"], 4), "unit": "GB/s", "cores": threads, "kind": "reference",
-                   "images_per_s": round(r["img_s"], 2), "sample": r["sample"]
-                   + (" (DRI-free twin: the reference rejects DRI)" if CONFIGS[args.config][5] else "")}
+                   "cpu_model": cpu_model(), "images_per_s": round(r["img_s"], 2),
+                   "sample": r["sample"] + (" (DRI-free twin: the reference rejects DRI)" if RI else "")
+                   + ("; decode_batch in a parallel_for over files" if batch_mode else
+                      "; decode_single(worker_count = cores) + upsample_and_convert")}
+            if not batch_mode:  # §8(d): single images also at worker_count = 1
+                r1 = cpu_reference_sample(cb, co, cs, 30.0 if big else 5.0, 1)
+                cpu["w1"] = {"value": round(r1["gbs"], 4), "cores": 1, "images_per_s": round(r1["img_s"], 3),
+                             "sample": r1["sample"]}
         except Exception as ex:  # pragma: no cover
             cpu = {"value": None, "unit": "GB/s", "cores": None, "kind": "reference", "sample": f"failed: {ex}"}
 
     if rank == 0:
         rec = {
-            "metric": "JPEG decode GB/s (RGB out)", "value": round(value, 3), "unit": "GB/s",
-            "images_per_s": round(img_s, 1), "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8 in / f64 IDCT+colour / u8 out", "data": "synthetic",
-            "config": {"workload": CONFIG_NAMES[args.config], "images_per_gpu": n, "width": w, "height": h,
-                       "quality": q, "sampling": s, "subsequence_bits": args.sb,
-                       "compressed_bytes_per_gpu": comp_bytes, "rgb_bytes_per_gpu": rgb_bytes,
-                       "l2": "flushed between steps (256 MB write, untimed)",
-                       "streams": 2 if halves else 1},
-            "single_stream_value": round(single_value, 3),
-            "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_tot / args.steps, 3),
-                    "path": "decode_to_host_pipelined: per chunk pjg_batch_create+upload+decode+download_all_async "
-                            "over 2 contexts (pinned host in/out)", "chunk_images": args.chunk},
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+            "images_per_s": round(tot_img / (ms_per_step / 1e3), 1), "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "ms_per_step_median": round(float(np.median(step_max)), 4),
+            "ms_per_step_best": round(float(np.min(step_max)), 4),
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "u8 in / f64 IDCT+colour / u8 out", "data": "synthetic",
+            "config": cfgd,
+            "l2": "flushed between steps (256 MB write, untimed)",
+            "sharding": ("the one batch split by compressed bytes (dist.shard_by_bytes), 2 contexts per GPU"
+                         if batch_mode else "replicas: every GPU decodes the image"),
+            "per_rank_ms": [round(x, 4) for x in per_rank],
+            "metric_of_record": {
+                "value": round(tot_rgb / (rec_med / 1e3) / 1e9, 3), "unit": "GB/s",
+                "best": round(tot_rgb / (rec_best / 1e3) / 1e9, 3),
+                "ms_median": round(rec_med, 4), "ms_best": round(rec_best, 4),
+                "images_per_s": round(tot_img / (rec_med / 1e3), 1),
+                "compressed_mb_per_s": round(pdist.sum_over_ranks(comp_bytes, rdev) / (rec_med / 1e3) / 1e6, 1),
+                "timed": "host wall clock, start barrier -> last GPU done: header parse + plan, H2D of the "
+                         "compressed bytes (pinned), K0..K4; RGB left in HBM (SURVEY.md §8(d), PAPER.md:341-342)"},
+            "e2e": {"value": round(e2e_val, 3), "unit": "GB/s", "h2d_bytes_per_step": comp_bytes,
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_med, 3),
+                    "path": "decode_to_host_pipelined: per chunk pjg_batch_create_blob + upload + decode + "
+                            "download_all_async over 2 contexts (pinned host in/out)", "chunk_images": args.chunk},
             "roofline": {"bound": "hbm", "kernel": "k4_transform", "achieved": round(achieved, 1),
                          "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_kind": peak_kind, "algorithmic_bytes": k4_bytes,
-                         "traffic_source": "profiles/round1/ncu_k4_transform.txt (dram read + write, one launch)"
-                         if traffic else None},
+                         "traffic_source": f"{traffic_src} (dram read + write, one launch)" if traffic else None},
             "stage_rooflines": stage_roof,
             "stages_ms": {k: round(v, 4) for k, v in st_mean.items()},
-            "dominant_stage": dominant,
+            "dominant_stage": max(st_mean, key=st_mean.get),
             "sync": sync_stats,
-            # Huffman stages (not roofline stages): bits of entropy-coded data
-            # decoded per second (K1 decodes each bit >= twice: round 0 + overflow)
             "huffman": {"scan_bits_per_gpu": scan_bits,
                         "k1_sync_gbit_s": round(scan_bits / (st_mean["sync"] / 1e3) / 1e9, 1),
                         "k3_write_gbit_s": round(scan_bits / (st_mean["write"] / 1e3) / 1e9, 1),
-                        "intra_rounds_per_cta": round(sync_stats["intra_rounds_sum"] / max(1, -(-scan_bits // (args.sb * 127))), 2)},
-            "compressed_mb_per_s": round(world * comp_bytes / (ms_per_step / 1e3) / 1e6, 1),
+                        "intra_rounds_per_cta": round(sync_stats["intra_rounds_sum"]
+                                                      / max(1, -(-scan_bits // (args.sb * 124))), 2)},
+            "compressed_mb_per_s": round(pdist.sum_over_ranks(comp_bytes, rdev) / (ms_per_step / 1e3) / 1e6, 1),
             "gpu_launches": launches_per_step * args.steps,
+            "single_stream_launches_per_step": single_launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
         }
+        if weak:
+            rec["weak_scaling"] = weak
         print(json.dumps(rec), flush=True)
     if dist:
         dist.barrier()

@@ -56,3 +56,53 @@ def sum_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def all_over_ranks(value: float, device=None) -> list:
+    """Every rank's value (per-rank times in the bench line)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return [float(value)]
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [float(x.item()) for x in out]
+
+
+def broadcast_array(arr, src: int = 0, device=None):
+    """Rank `src`'s 1-D numpy array on every rank (the batch is generated once
+    and shared; setup only, never inside a timed region)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return arr
+    me = dist.get_rank()
+    meta = torch.zeros(2, dtype=torch.int64, device=device)
+    if me == src:
+        meta[0] = arr.size
+        meta[1] = {np.dtype(np.uint8): 0, np.dtype(np.int64): 1}[arr.dtype]
+    dist.broadcast(meta, src)
+    n, kind = int(meta[0].item()), int(meta[1].item())
+    dt = torch.uint8 if kind == 0 else torch.int64
+    t = torch.from_numpy(np.ascontiguousarray(arr)).to(device) if me == src else torch.empty(n, dtype=dt, device=device)
+    dist.broadcast(t, src)
+    return t.cpu().numpy()
+
+
+def shard_blob(blob, offsets, sizes, idx):
+    """The files `idx` of a contiguous batch as their own contiguous blob:
+    (blob, offsets, sizes) of the shard."""
+    import numpy as np
+    idx = list(idx)
+    sz = np.array([int(sizes[i]) for i in idx], np.int64)
+    out = np.empty(int(sz.sum()), np.uint8)
+    offs = np.zeros(len(idx), np.int64)
+    o = 0
+    for k, i in enumerate(idx):
+        a = int(offsets[i])
+        out[o: o + sz[k]] = blob[a: a + sz[k]]
+        offs[k] = o
+        o += int(sz[k])
+    return out, offs, sz
