@@ -38,32 +38,52 @@ def main(path, segments=True):
     try:
         segments_table(path)
     except Exception as e:  # the source page differs between kernels/ncu versions
-        print(f"(per-segment table unavailable: {type(e).__name__})")
+        print(f"(per-segment table unavailable: {type(e).__name__}: {e})")
 
 
 def segments_table(path):
-    src = list(csv.reader(io.StringIO(run([path] + KERNEL + ["--page", "source", "--csv", "--print-source=sass"]))))
-    hdr, data = src[1], src[2:]
+    """Stall-reason totals over the kernel's SASS (warp-state samples), then
+    per barrier-delimited segment.  The source page repeats a 'Kernel Name'
+    row per kernel; only rows with the full header width are SASS lines."""
+    out = run([path] + KERNEL + ["--page", "source", "--csv", "--print-source=sass"])
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, data = None, []
+    for r in rows:
+        if r and r[0] == "Address":
+            if hdr is not None:
+                break  # first kernel only
+            hdr = r
+            continue
+        if hdr is not None and len(r) == len(hdr):
+            data.append(r)
     iA, iS, iE = hdr.index("Address"), hdr.index("Source"), hdr.index("Instructions Executed")
     cols = {x: i for i, x in enumerate(hdr)}
+    reasons = [x for x in REASONS if x in cols]
+    tot = {x: 0 for x in reasons}
     base = int(data[0][iA], 16)
-    segs, seg, tot = {}, 0, 0
+    segs, seg, inst = {}, 0, 0
     for r in data:
         e = int(r[iE]) if r[iE].isdigit() else 0
-        tot += e
+        inst += e
         if "BAR.SYNC" in r[iS] or "EXIT" in r[iS]:
             seg += 1
         d = segs.setdefault(seg, {"e": 0, "off": int(r[iA], 16) - base})
         d["e"] += e
-        for rs in REASONS:
+        for rs in reasons:
             x = r[cols[rs]]
-            d[rs] = d.get(rs, 0) + (int(x) if x.isdigit() else 0)
+            v = int(x) if x.isdigit() else 0
+            d[rs] = d.get(rs, 0) + v
+            tot[rs] += v
+    T = max(1, sum(tot.values()))
+    print("stall reasons (warp-state samples, whole kernel):")
+    for rs, v in sorted(tot.items(), key=lambda x: -x[1])[:10]:
+        print(f"  {rs:28s} {v:10d} {100 * v / T:5.1f}%")
     print(f"{'segment':>8} {'start':>6} {'inst':>12} {'share':>6}  top stalls (samples)")
     for k, d in segs.items():
         if d["e"] == 0:
             continue
-        top = sorted([(d[rs], rs) for rs in REASONS], reverse=True)[:4]
-        print(f"{k:8d} {d['off']:06x} {d['e']:12d} {100 * d['e'] / max(tot, 1):5.1f}%  " +
+        top = sorted([(d[rs], rs) for rs in reasons], reverse=True)[:4]
+        print(f"{k:8d} {d['off']:06x} {d['e']:12d} {100 * d['e'] / max(inst, 1):5.1f}%  " +
               ", ".join(f"{n[6:]}={c}" for c, n in top))
 
 

@@ -14,9 +14,11 @@ ap.add_argument("--config", default="3")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--sb", type=int, default=1024)
 a = ap.parse_args()
-_, blob, offs, sizes = make_corpus(a.config, 0, pinned=False)
+blob, offs, sizes = make_corpus(a.config)
 dec = pj.Decoder(0)
-b = dec.batch((blob, offs, sizes), pj.DecodeConfig(subsequence_bits=a.sb), pj.OutputColorspace.RGBInterleaved)
+ri = CONFIGS[a.config][5]
+b = dec.batch((blob, offs, sizes), pj.DecodeConfig(subsequence_bits=a.sb, restart_intervals=ri > 0),
+              pj.OutputColorspace.RGBInterleaved)
 b.upload()
 for _ in range(a.reps):
     st = b.decode().synchronize()
