@@ -269,6 +269,11 @@ def main():
     args = ap.parse_args()
     args.steps = max(1, args.steps)
     rank, world, local = dist_env()
+    trace_on = os.environ.get("PJG_BENCH_TRACE") == "1"
+
+    def trace(what):  # phase markers on stderr (diagnosing multi-rank runs)
+        if trace_on:
+            print(f"[rank {rank}] {time.strftime('%H:%M:%S')} {what}", file=sys.stderr, flush=True)
 
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -288,6 +293,7 @@ def main():
 
     n_all, W, H, Q, S, RI, _ = CONFIGS[args.config]
     cfgd = config_dict(args.config, args.sb)
+    trace("init done")
     # ---- corpus: generated once (rank 0, all host threads) and shared
     if rank == 0:
         blob, offs, sizes = make_corpus(args.config)
@@ -322,6 +328,7 @@ def main():
             return [(0, n)]
         return [(0, n // 2), (n // 2, n)]
 
+    trace(f"corpus shared, shard of {n} images")
     # ---- (1) one stream: per-stage CUDA-event times (rooflines)
     b = dec.batch((pblob, soffs, ssizes), cfg, out_kind)
     b.upload()
@@ -345,6 +352,7 @@ def main():
     single_launches = b.kernel_launches()
     b.close()
 
+    trace("stage runs done")
     # ---- (2) value: device-resident step, the shard as two concurrent parts
     parts = []
     for (lo, hi), d in zip(parts_of(2), decs):
@@ -391,6 +399,7 @@ def main():
     ms_per_step = float(np.mean(step_max))
     value = tot_rgb / (ms_per_step / 1e3) / 1e9
 
+    trace("device steps done")
     # ---- (3) metric of record: host parse -> H2D -> K0..K4, output in HBM
     def record_step():
         bs = []
@@ -416,6 +425,7 @@ def main():
         rec_ms.append(pdist.max_over_ranks(record_step(), rdev))
     rec_med, rec_best = float(np.median(rec_ms)), float(np.min(rec_ms))
 
+    trace("record steps done")
     # ---- (4) e2e through the C-ABI with host buffers (D2H included)
     host_out = torch.empty(rgb_bytes + n * 256 + 4096, dtype=torch.uint8).pin_memory()
 
@@ -439,6 +449,7 @@ def main():
     e2e_med = float(np.median(e2e_ms))
     e2e_val = tot_rgb / (e2e_med / 1e3) / 1e9
 
+    trace("e2e done")
     # ---- (5) weak scaling (N > 1): every rank decodes the whole batch
     weak = None
     if world > 1 and batch_mode and not args.no_weak:
@@ -461,6 +472,7 @@ def main():
         weak = {"value": round(world * full_rgb / (float(np.mean(wms)) / 1e3) / 1e9, 3), "unit": "GB/s",
                 "ms_per_step": round(float(np.mean(wms)), 4), "images_per_gpu": n_all}
 
+    trace("weak leg done")
     # ---- rooflines (K4 dominant HBM-bound stage; K0 / K3 beside it)
     peak, peak_kind = load_peaks()
     k4_bytes = dus * 128 + rgb_bytes  # int16 coefficient read + RGB write

@@ -149,6 +149,17 @@ int pjg_batch_create(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const 
 int pjg_batch_create_blob(pjg_ctx* ctx, const uint8_t* blob, size_t blob_bytes, size_t n,
                           const uint64_t* offsets, const size_t* sizes, const pjg_config* cfg,
                           pjg_batch** out);
+/* Device-planned batch: same inputs as pjg_batch_create_blob
+ * (blob may be host or device memory).  The files are copied to the device
+ * whole, in one transfer; the JFIF marker walk (parse, parser.hpp:264-347),
+ * Huffman/quantisation table dedup + construction (build_table,
+ * huffman.hpp:60-93) and the batch layout run as kernels, and the host only
+ * reads back a small totals record — no per-file host work.  Statuses,
+ * outputs and every other batch call are identical to the host-planned
+ * batch; pjg_batch_upload is a no-op for it. */
+int pjg_batch_create_device(pjg_ctx* ctx, const uint8_t* blob, size_t blob_bytes, size_t n,
+                            const uint64_t* offsets, const size_t* sizes, const pjg_config* cfg,
+                            pjg_batch** out);
 /* One H2D of the compressed bytes (+ one of the descriptor blob), async. */
 int pjg_batch_upload(pjg_batch* b);
 /* K0..K4 on the context stream, async; output stays on the device. */

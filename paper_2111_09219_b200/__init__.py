@@ -185,6 +185,7 @@ def lib():
             L.pjg_batch_create_blob.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t,
                                                 C.POINTER(C.c_uint64), C.POINTER(C.c_size_t),
                                                 C.POINTER(_Config), C.POINTER(C.c_void_p)]
+            L.pjg_batch_create_device.argtypes = L.pjg_batch_create_blob.argtypes
             for fn in ("pjg_batch_upload", "pjg_batch_decode"):
                 getattr(L, fn).argtypes = [C.c_void_p]
             L.pjg_batch_synchronize.argtypes = [C.c_void_p, C.c_void_p]
@@ -223,7 +224,7 @@ def lib():
 EXPORTED_SYMBOLS = [
     "pjg_ctx_create", "pjg_ctx_destroy", "pjg_last_error", "pjg_status_name", "pjg_default_config",
     "pjg_ctx_stream", "pjg_inspect", "pjg_inspect_header", "pjg_decode", "pjg_decode_batch", "pjg_batch_create",
-    "pjg_batch_create_blob", "pjg_batch_upload", "pjg_batch_decode", "pjg_batch_synchronize", "pjg_batch_download",
+    "pjg_batch_create_blob", "pjg_batch_create_device", "pjg_batch_upload", "pjg_batch_decode", "pjg_batch_synchronize", "pjg_batch_download",
     "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_copy_outputs", "pjg_batch_scan_bits", "pjg_batch_kernel_launches", "pjg_batch_download_all", "pjg_batch_download_all_async", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
     "pjg_batch_sync_stats", "pjg_batch_destroy", "pjg_batch_dump_coefficients",
     "pjg_batch_dump_sync_states", "pjg_batch_dump_segment", "pjg_upsample_and_convert",
@@ -277,17 +278,19 @@ class Decoder:
         except Exception:
             pass
 
-    def batch(self, files, config: DecodeConfig | None = None, output=None) -> "Batch":
-        return Batch(self, files, config, output)
+    def batch(self, files, config: DecodeConfig | None = None, output=None, device_plan=False) -> "Batch":
+        return Batch(self, files, config, output, device_plan)
 
 
 class Batch:
     """A planned batch on the device: create → upload → decode → synchronize
     → download / taps.  ``files`` is a list of bytes-like objects, or a tuple
     (blob: np.uint8 array, offsets, sizes) for files laid out contiguously
-    (e.g. in pinned host memory) so the upload is one copy."""
+    (e.g. in pinned host memory) so the upload is one copy.  ``device_plan``:
+    plan on the device (pjg_batch_create_device: header parse, tables and
+    layout as kernels; whole files uploaded)."""
 
-    def __init__(self, dec: Decoder, files, config=None, output=None):
+    def __init__(self, dec: Decoder, files, config=None, output=None, device_plan=False):
         self.dec = dec
         self.config = config or DecodeConfig()
         blob_args = None
@@ -303,6 +306,18 @@ class Batch:
             blob_args = (C.c_void_p(blob.ctypes.data), blob.size, n,
                          oa.ctypes.data_as(C.POINTER(C.c_uint64)),
                          sa.ctypes.data_as(C.POINTER(C.c_size_t)))
+        elif device_plan:  # one contiguous copy of the files
+            arrs = [np.frombuffer(f, np.uint8) if not isinstance(f, np.ndarray) else f for f in files]
+            sizes = np.array([a.size for a in arrs], np.uint64)
+            offs = np.zeros(len(arrs), np.uint64)
+            if len(arrs):
+                offs[1:] = np.cumsum(sizes)[:-1]
+            blob = np.concatenate(arrs) if arrs else np.zeros(1, np.uint8)
+            self._keep = [blob, offs, sizes]
+            n = len(arrs)
+            blob_args = (C.c_void_p(blob.ctypes.data), blob.size, n,
+                         offs.ctypes.data_as(C.POINTER(C.c_uint64)),
+                         sizes.ctypes.data_as(C.POINTER(C.c_size_t)))
         else:
             self._keep = [np.frombuffer(f, np.uint8) if not isinstance(f, np.ndarray) else f
                           for f in files]
@@ -314,7 +329,8 @@ class Batch:
         cfg = _cfg(self.config, output)
         self.output = cfg.output
         if blob_args is not None:
-            st = lib().pjg_batch_create_blob(dec.handle, *blob_args, C.byref(cfg), C.byref(self._h))
+            fn = lib().pjg_batch_create_device if device_plan else lib().pjg_batch_create_blob
+            st = fn(dec.handle, *blob_args, C.byref(cfg), C.byref(self._h))
         else:
             st = lib().pjg_batch_create(dec.handle, n, ptrs, szs, C.byref(cfg), C.byref(self._h))
         if st:

@@ -2516,6 +2516,9 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
 //     arithmetic on the decimal constants, ties replayed in FP64
 //     (pipeline.hpp:190-197).  Saturating byte packs, 3 x 32-bit stores per
 //     4 pixels.
+#ifndef PJG_K4_PAIRCOL
+#define PJG_K4_PAIRCOL 1
+#endif
 constexpr float kM128 = 12583040.0f;  // 1.5 * 2^23 + 128: round(acc) + 128 in the low mantissa bits
 constexpr int kMagicBits = 0x4B400000;
 constexpr int kK4Warps = kK4Threads / 32;
@@ -2673,22 +2676,27 @@ __device__ __forceinline__ void walk_enter_image(const Params& P, uint32_t t, Ti
 //   G: m = ga[Cb] + gb[Cr] = -344136 cb - 714136 cr + 500000 + 2e8 (+1 when Cb
 //   is a B tie; m is otherwise even), oG = floor(m / 1e6) - 200; a G tie is
 //   m == 0 mod 1e6, so (m mod 1e6) == 0 or odd flags any tie.
+// The division is pre-split: with ga = qa 1e6 + ra, gb = qb 1e6 + rb (0 <= r
+// < 1e6) the tables hold (qa - 200) << 20 | (ra + 2^20 - 1e6) and qb << 20 | rb,
+// so one add carries exactly when ra + rb >= 1e6: oG = sum >> 20 and the low
+// 20 bits are m mod 1e6 (carry) or m mod 1e6 + 48576 (no carry — then m mod
+// 1e6 is never 0: that needs rb = 0, i.e. cr = 0, and ra(0) = 500000), so a
+// tie is "low 20 bits odd or zero".  Each half is loaded with its R / B
+// offset as one 64-bit word.
 struct ColourLut {
-    int32_t r[256];
-    int32_t b[256];
-    int32_t ga[256];
-    int32_t gb[256];
+    int2 cb[256];  // (G word of Cb, B offset)
+    int2 cr[256];  // (G word of Cr, R offset)
 };
 
 __device__ __forceinline__ void chroma_off(const ColourLut& L, uint32_t cb, uint32_t cr, int& oR, int& oG, int& oB,
                                            uint32_t& tie) {
-    oR = L.r[cr];
-    oB = L.b[cb];
-    const uint32_t m = uint32_t(L.ga[cb] + L.gb[cr]);
-    const uint32_t q = m / 1000000u;
-    const uint32_t rem = m - q * 1000000u;
-    tie |= (rem & 1u) | uint32_t(rem == 0u);
-    oG = int(q) - 200;
+    const int2 a = L.cb[cb], b = L.cr[cr];
+    oR = b.y;
+    oB = a.y;
+    const uint32_t m = uint32_t(a.x) + uint32_t(b.x);
+    const uint32_t lo = m & 0xFFFFFu;
+    tie |= (lo & 1u) | uint32_t(lo == 0u);
+    oG = int32_t(m) >> 20;
 }
 
 __device__ __forceinline__ int ybyte(uint32_t y4, int i) { return int((y4 >> (8 * i)) & 0xFFu); }
@@ -2784,11 +2792,21 @@ __device__ __forceinline__ void colour_tile(const WarpImg& I, const uint8_t* pl,
     }
 }
 
-// Whole 32-pixel-wide, full-height tile with 4-byte-aligned rows: two fixed
-// items per lane, no bounds checks.
+// Whole 64-pixel-wide, full-height tile with 4-byte-aligned rows: two fixed
+// items per lane, no bounds checks.  The tile's RGB rows (192 bytes each) are
+// assembled in shared memory (`stg`, the IDCT's F tile, dead by now) at the
+// 16-byte phase of their global address, then leave as 16-byte stores: a row
+// touches 12 aligned chunks (13 when misaligned: a ragged head and tail
+// written word by word).  Staging row stride 208 = 13 chunks, so item i of
+// the write-out reads smem chunk i — conflict-free, and consecutive lanes
+// store consecutive 16-byte chunks of a row.
+constexpr uint32_t kStgRow = 208;
+#ifndef PJG_K4_STAGE
+#define PJG_K4_STAGE 1
+#endif
 template <int HS, bool PAIR>
 __device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl, const ColourLut& L, uint8_t* out,
-                                            uint32_t X0, uint32_t Y0, int lane) {
+                                            uint8_t* stg, uint32_t X0, uint32_t Y0, uint32_t rows, int lane) {
     const uint32_t W = I.width;
     const uint32_t gx = (lane % kGroups) * 4, jr0 = lane / kGroups;
     const uint32_t cgx = HS == 2 ? gx >> 1 : gx;
@@ -2797,7 +2815,8 @@ __device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl,
     const uint8_t* crb = pl + I.poff[2];
     const uint32_t pst0 = I.pst[0], pst1 = I.pst[1];
     const uint64_t orow = uint64_t(W) * 3;
-    uint8_t* ob = out + I.out_off + (uint64_t(Y0) * W + X0 + gx) * 3;
+    uint8_t* ob0 = out + I.out_off + (uint64_t(Y0) * W + X0) * 3;  // row 0 of the tile
+    const uint32_t m0 = uint32_t(reinterpret_cast<uintptr_t>(ob0)) & 15u, mstep = uint32_t(orow) & 15u;
 #pragma unroll
     for (int h = 0; h < 8 * kGroups / 32; ++h) {
         const uint32_t jr = jr0 + (32 / kGroups) * h;
@@ -2828,24 +2847,46 @@ __device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl,
         {
             const uint32_t y4 = *reinterpret_cast<const uint32_t*>(yb + r0 * pst0);
             const uint3 w = tie ? rgb4_exact(y4, cbrow, crrow, cx) : rgb4(y4, oR, oG, oB);
-            uint32_t* d = reinterpret_cast<uint32_t*>(ob + r0 * orow);
+            uint32_t* d = PJG_K4_STAGE ? reinterpret_cast<uint32_t*>(stg + r0 * kStgRow + ((m0 + r0 * mstep) & 15u) + gx * 3)
+                                       : reinterpret_cast<uint32_t*>(ob0 + r0 * orow + gx * 3);
             d[0] = w.x;
             d[1] = w.y;
             d[2] = w.z;
         }
         if (PAIR) {
-            const uint32_t y4 = *reinterpret_cast<const uint32_t*>(yb + (r0 + 1) * pst0);
+            const uint32_t r1 = r0 + 1;
+            const uint32_t y4 = *reinterpret_cast<const uint32_t*>(yb + r1 * pst0);
             const uint3 w = tie ? rgb4_exact(y4, cbrow, crrow, cx) : rgb4(y4, oR, oG, oB);
-            uint32_t* d = reinterpret_cast<uint32_t*>(ob + (r0 + 1) * orow);
+            uint32_t* d = PJG_K4_STAGE ? reinterpret_cast<uint32_t*>(stg + r1 * kStgRow + ((m0 + r1 * mstep) & 15u) + gx * 3)
+                                       : reinterpret_cast<uint32_t*>(ob0 + r1 * orow + gx * 3);
             d[0] = w.x;
             d[1] = w.y;
             d[2] = w.z;
+        }
+    }
+    if (!PJG_K4_STAGE) return;
+    __syncwarp();
+    // write-out: item = (row r, aligned chunk c of 13)
+    for (uint32_t it = lane; it < rows * 13u; it += 32) {
+        const uint32_t r = it / 13u, c = it - r * 13u;
+        const uint32_t m = (m0 + r * mstep) & 15u;
+        uint8_t* g = ob0 + r * orow - m + 16u * c;  // 16-byte aligned
+        const uint4 v = *reinterpret_cast<const uint4*>(stg + 16u * it);
+        if ((c != 0 || m == 0) && c != 12) {
+            *reinterpret_cast<uint4*>(g) = v;
+        } else if (m != 0) {  // ragged head (bytes m..15) or tail (bytes 0..m-1), 4-byte granular
+            const uint32_t lo = c == 0 ? m >> 2 : 0u, hi = c == 0 ? 4u : m >> 2;
+            const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+                if (k >= lo && k < hi) reinterpret_cast<uint32_t*>(g)[k] = vw[k];
         }
     }
 }
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 static_assert(sizeof(WarpSmem) * kK4Warps + 4864 + 1024 <= 228 * 1024 / 4, "K4 must fit 4 CTAs per SM");
+static_assert(sizeof(WarpSmem::F) >= 16 * kStgRow, "RGB row staging lives in the F tile");
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
     unsigned long long r;
     asm("sub.rn.f32x2 %0, %1, %2;"
@@ -2874,11 +2915,14 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
     for (int c = tid; c < 256; c += kK4Threads) {
         const int v = c - 128;
         // round(k v) for decimal k, exactly: floor((1000 k v + 500) / 1000)
-        s_lut.r[c] = int((1402 * v + 500 + 200000) / 1000) - 200;
+        const int oR = int((1402 * v + 500 + 200000) / 1000) - 200;
         const int mB = 1772 * v + 500 + 300000;
-        s_lut.b[c] = mB / 1000 - 300;
-        s_lut.ga[c] = -344136 * v + 500000 + 200000000 + ((mB % 1000) == 0 ? 1 : 0);
-        s_lut.gb[c] = -714136 * v;
+        const int ga = -344136 * v + 500000 + 200000000 + ((mB % 1000) == 0 ? 1 : 0);  // > 0
+        const int gb = -714136 * v;
+        const int qa = ga / 1000000, ra = ga - qa * 1000000;
+        const int qb = (gb >= 0 ? gb : gb - 999999) / 1000000, rb = gb - qb * 1000000;  // floor
+        s_lut.cb[c] = make_int2(int(uint32_t(qa - 200) << 20) + ra + (1048576 - 1000000), mB / 1000 - 300);
+        s_lut.cr[c] = make_int2(int(uint32_t(qb) << 20) + rb, oR);
     }
     __syncthreads();
 
@@ -3087,11 +3131,56 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
             float2 acc[8];
 #pragma unroll
             for (int y = 0; y < 8; ++y) acc[y] = make_float2(0.f, 0.f);
+#if PJG_K4_PAIRCOL
+            // two columns per step: two independent column-sum chains (the
+            // 8-deep FFMA2 chain of one column was the kernel's top fixed-
+            // latency stall).  An odd count pairs the last column with one
+            // outside the union: zero in every unit of the pass, so its terms
+            // add exact zeros and the error bound is unchanged.
+            for (uint32_t m = ucols; m;) {
+                const uint32_t v = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t w2 = m ? __ffs(m) - 1 : __ffs(~ucols) - 1;
+                m &= m - 1;
+                const float4 f0 = *reinterpret_cast<const float4*>(F + v * 8);
+                const float4 f1 = *reinterpret_cast<const float4*>(F + v * 8 + 4);
+                const float4 g0 = *reinterpret_cast<const float4*>(F + w2 * 8);
+                const float4 g1 = *reinterpret_cast<const float4*>(F + w2 * 8 + 4);
+                // s = sum_u (b[u][q], b[u][q+4]) F[u][v]
+                float2 sv = __fmul2_rn(bq[0], f2(f0.x));
+                float2 sw = __fmul2_rn(bq[0], f2(g0.x));
+                sv = __ffma2_rn(bq[1], f2(f0.y), sv);
+                sw = __ffma2_rn(bq[1], f2(g0.y), sw);
+                sv = __ffma2_rn(bq[2], f2(f0.z), sv);
+                sw = __ffma2_rn(bq[2], f2(g0.z), sw);
+                sv = __ffma2_rn(bq[3], f2(f0.w), sv);
+                sw = __ffma2_rn(bq[3], f2(g0.w), sw);
+                sv = __ffma2_rn(bq[4], f2(f1.x), sv);
+                sw = __ffma2_rn(bq[4], f2(g1.x), sw);
+                sv = __ffma2_rn(bq[5], f2(f1.y), sv);
+                sw = __ffma2_rn(bq[5], f2(g1.y), sw);
+                sv = __ffma2_rn(bq[6], f2(f1.z), sv);
+                sw = __ffma2_rn(bq[6], f2(g1.z), sw);
+                sv = __ffma2_rn(bq[7], f2(f1.w), sv);
+                sw = __ffma2_rn(bq[7], f2(g1.w), sw);
+                const float4 b0 = *reinterpret_cast<const float4*>(s_b32 + v * 8);
+                const float4 b1 = *reinterpret_cast<const float4*>(s_b32 + v * 8 + 4);
+                const float4 c0 = *reinterpret_cast<const float4*>(s_b32 + w2 * 8);
+                const float4 c1 = *reinterpret_cast<const float4*>(s_b32 + w2 * 8 + 4);
+                acc[0] = __ffma2_rn(f2(c0.x), sw, __ffma2_rn(f2(b0.x), sv, acc[0]));
+                acc[1] = __ffma2_rn(f2(c0.y), sw, __ffma2_rn(f2(b0.y), sv, acc[1]));
+                acc[2] = __ffma2_rn(f2(c0.z), sw, __ffma2_rn(f2(b0.z), sv, acc[2]));
+                acc[3] = __ffma2_rn(f2(c0.w), sw, __ffma2_rn(f2(b0.w), sv, acc[3]));
+                acc[4] = __ffma2_rn(f2(c1.x), sw, __ffma2_rn(f2(b1.x), sv, acc[4]));
+                acc[5] = __ffma2_rn(f2(c1.y), sw, __ffma2_rn(f2(b1.y), sv, acc[5]));
+                acc[6] = __ffma2_rn(f2(c1.z), sw, __ffma2_rn(f2(b1.z), sv, acc[6]));
+                acc[7] = __ffma2_rn(f2(c1.w), sw, __ffma2_rn(f2(b1.w), sv, acc[7]));
+            }
+#else
             for (uint32_t m = ucols; m; m &= m - 1) {
                 const uint32_t v = __ffs(m) - 1;
                 const float4 f0 = *reinterpret_cast<const float4*>(F + v * 8);
                 const float4 f1 = *reinterpret_cast<const float4*>(F + v * 8 + 4);
-                // s = sum_u (b[u][q], b[u][q+4]) F[u][v]
                 float2 sv = __fmul2_rn(bq[0], f2(f0.x));
                 sv = __ffma2_rn(bq[1], f2(f0.y), sv);
                 sv = __ffma2_rn(bq[2], f2(f0.z), sv);
@@ -3111,6 +3200,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 acc[6] = __ffma2_rn(f2(b1.z), sv, acc[6]);
                 acc[7] = __ffma2_rn(f2(b1.w), sv, acc[7]);
             }
+#endif
             // round: v = acc + M holds round(acc) + 128 in its low bits
             int o0[8], o1[8];
             float mx = 0.f;
@@ -3192,19 +3282,20 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
         const uint32_t X0 = cur_mx0 * cur_mcuw, Y0 = cur_my * cur_mcuh;
         const uint32_t cols = min(cur_nm * cur_mcuw, I.width - X0), rws = min(cur_mcuh, I.height - Y0);
         const bool full = cols == uint32_t(kTileW) && rws == cur_mcuh && (I.width & 3) == 0 && (I.out_off & 3) == 0;
+        uint8_t* stg = reinterpret_cast<uint8_t*>(S.F);  // RGB row staging (F is dead after the IDCT)
         if constexpr (LAYOUT == 1) {
             if (full)
-                colour_full<2, true>(I, S.pl, s_lut, P.out, X0, Y0, lane);
+                colour_full<2, true>(I, S.pl, s_lut, P.out, stg, X0, Y0, rws, lane);
             else
                 colour_tile<2, true>(I, S.pl, s_lut, P.out, X0, Y0, cols, rws, lane);
         } else if (I.rgb && full) {
             if (I.h_max == 2) {
                 if (I.v_max == 2)
-                    colour_full<2, true>(I, S.pl, s_lut, P.out, X0, Y0, lane);
+                    colour_full<2, true>(I, S.pl, s_lut, P.out, stg, X0, Y0, rws, lane);
                 else
-                    colour_full<2, false>(I, S.pl, s_lut, P.out, X0, Y0, lane);
+                    colour_full<2, false>(I, S.pl, s_lut, P.out, stg, X0, Y0, rws, lane);
             } else {
-                colour_full<1, false>(I, S.pl, s_lut, P.out, X0, Y0, lane);
+                colour_full<1, false>(I, S.pl, s_lut, P.out, stg, X0, Y0, rws, lane);
             }
         } else if (I.rgb) {
             if (I.h_max == 2) {

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/pjg.h"
+#include "devplan.h"
 #include "jfif.hpp"
 #include "pjg_internal.h"
 
@@ -166,8 +167,8 @@ struct pjg_ctx {
     double basis[64];
     cudaEvent_t ev[kNumEvents] = {};
     DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out, segs, sym, tag,
-        counters, k0_flag, k0_agg, k2_flag, k2_agg, stats;
-    HostBuf stage, meta_host, status_host, desc_host;
+        counters, k0_flag, k0_agg, k2_flag, k2_agg, stats, plan, meta2;
+    HostBuf stage, meta_host, status_host, desc_host, plan_host;
     WorkerPool pool_threads;
     // Per-image host arrays, lent to the live batch and taken back at destroy:
     // thumbnail batches hold tens of thousands of images, and fresh vectors
@@ -199,6 +200,11 @@ struct pjg_batch {
     uint64_t sb_int = 0;  // internal subsequence size (divides cfg.subsequence_bits)
     Params prm{};
     bool uploaded = false, decoded = false, synced = false;
+    // device-planned batch (pjg_batch_create_device): descriptors, statuses and
+    // image infos live on the device; the host copies are fetched on first use
+    bool devplan = false, host_view = false;
+    const ImgState* state0 = nullptr;      // device: initial per-image statuses
+    const pjg_image_info* dinfo = nullptr; // device: per-image infos
     std::vector<ImgState> dev_state;  // fetched at synchronize
     void swap_pool(pjg_ctx::Scratch& p) {
         host_status.swap(p.host_status);
@@ -332,12 +338,13 @@ void pjg_ctx_destroy(pjg_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->raw, &c->ubuf, &c->meta, &c->blkmeta, &c->ent, &c->dcs, &c->off, &c->cap, &c->pred,
                       &c->cta_end, &c->cta_start, &c->k1_flag, &c->coef, &c->out, &c->counters,
-                      &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats, &c->segs, &c->sym, &c->tag})
+                      &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats, &c->segs, &c->sym, &c->tag, &c->plan, &c->meta2})
         b->release();
     c->stage.release();
     c->meta_host.release();
     c->desc_host.release();
     c->status_host.release();
+    c->plan_host.release();
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -386,6 +393,158 @@ int pjg_inspect_header(const uint8_t* file, size_t size, int allow_dri, pjg_head
 }
 
 namespace {
+// smallest internal subsequence size for small batches (PJG_SB_MIN overrides, A/B)
+uint64_t sb_floor() {
+    const char* e = getenv("PJG_SB_MIN");
+    const long v = e ? atol(e) : 0;
+    return (v >= 32 && v % 32 == 0) ? uint64_t(v) : 256u;
+}
+
+// Per-batch totals of a plan (host planner or devplan.cu) and where its
+// device-side tables live: everything the buffer reservation and the kernel
+// parameters need.
+struct PlanSummary {
+    size_t n = 0;
+    uint64_t sub = 0, du = 0, outb = 0, seg_total = 0, bits = 0, n_ok = 0, sb = 0, sb_int = 0;
+    uint32_t k0t = 0, k4t = 0, ndri = 0, n_huff = 0, n_quant = 0, k0_bpt = 0;
+    bool all420 = false;
+};
+struct MetaPtrs {
+    uint8_t *desc, *state, *huff, *quant, *wq, *basis, *k0, *tile, *sub, *k0img, *subimg, *dri;
+};
+
+int finish_plan(pjg_ctx* ctx, pjg_batch* b, const PlanSummary& S, const MetaPtrs& M) {
+    b->n_huff = S.n_huff;
+    b->n_quant = S.n_quant;
+    b->k0_tiles = S.k0t;
+    b->k4_tiles = S.k4t;
+    b->total_subs = S.sub;
+    b->total_dus = S.du;
+    b->seg_total = S.seg_total;
+    b->out_bytes = S.outb;
+    b->sb_int = S.sb_int;
+    b->k1_ctas = uint32_t((S.sub + kK1Own - 1) / kK1Own);
+    b->k2_tiles = uint32_t((S.sub + kK2Threads - 1) / kK2Threads);
+    // ---- device reservation
+    CU(ctx->raw.ensure(b->raw_bytes + 64), "cudaMalloc(raw)");
+    CU(ctx->ubuf.ensure(b->raw_bytes + 64), "cudaMalloc(ubuf)");
+    const size_t subs = std::max<uint64_t>(S.sub, 1);
+    CU(ctx->ent.ensure(subs * sizeof(Entry)), "cudaMalloc(ent)");
+    CU(ctx->dcs.ensure(subs * sizeof(DcSums)), "cudaMalloc(dcs)");
+    CU(ctx->off.ensure(subs * 8), "cudaMalloc(off)");
+    CU(ctx->cap.ensure(subs * 4), "cudaMalloc(cap)");
+    CU(ctx->pred.ensure(subs * sizeof(DcSums)), "cudaMalloc(pred)");
+    CU(ctx->cta_end.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_end)");
+    CU(ctx->cta_start.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_start)");
+    // K1 chains keep their decoded symbols for K3 to replay (16 bits each, up
+    // to sb/4 per subsequence: 4 bytes of scratch per compressed byte) when it
+    // pays: measured break-even (DESIGN.md §5) — many symbols per data unit
+    // (K3's decode dominates its block work) but a stream that syncs in few
+    // rounds (K1 stores each chain's symbols once per round): 64..160 scan
+    // bits per data unit, in images of >= 64 subsequences on average.
+    // PJG_REPLAY=0/1 forces it.
+    // small batches (under ~4 K1 CTAs per SM): the decoders' table probes sit on a
+    // serial dependency chain with few warps to hide an L1 miss — stage the
+    // tables in shared memory
+    uint32_t smem_tables =
+        (S.n_huff <= kMaxSmemTables && S.sub < uint64_t(kK1Threads) * 148 * 4) ? S.n_huff : 0u;
+    if (const char* e = getenv("PJG_SMEM_TABLES"))  // override (A/B experiments)
+        smem_tables = (atoi(e) && S.n_huff <= kMaxSmemTables) ? S.n_huff : 0u;
+    const bool st_tables = smem_tables != 0;
+    bool replay_on = false;
+    {
+        const uint64_t per_du = S.du ? S.bits / S.du : 0;
+        // (and large images: a few subsequences per image keep K3 cheap)
+        // (large batches only: K1's shared-memory-table variant for small ones
+        // does not keep symbols)
+        replay_on = per_du >= 64 && per_du <= 160 && S.n_ok && S.sub / S.n_ok >= 64 && !st_tables;
+        if (const char* e = getenv("PJG_REPLAY")) replay_on = atoi(e) != 0 && !st_tables;
+        if (getenv("PJG_NO_REPLAY")) replay_on = false;
+    }
+    const uint32_t sym_cap = (!replay_on || S.sb_int > 65536) ? 0u : uint32_t(S.sb_int / 4);
+    const uint64_t sym_stride = align_up(subs, 64);
+    if (sym_cap) {
+        CU(ctx->sym.ensure(sym_stride * sym_cap * 2), "cudaMalloc(sym)");
+        CU(ctx->tag.ensure(subs * 16), "cudaMalloc(tag)");
+    }
+    CU(ctx->k1_flag.ensure((b->k1_ctas + 1) * 4), "cudaMalloc(k1_flag)");
+    CU(ctx->coef.ensure(std::max<uint64_t>(S.du, 1) * 128), "cudaMalloc(coef)");
+    CU(ctx->segs.ensure(std::max<uint64_t>(S.seg_total, 1) * sizeof(uint2)), "cudaMalloc(segs)");
+    CU(ctx->blkmeta.ensure(std::max<uint64_t>(S.du, 1) * 8), "cudaMalloc(blkmeta)");
+    CU(ctx->out.ensure(std::max<uint64_t>(S.outb, 1)), "cudaMalloc(out)");
+    CU(ctx->counters.ensure(kNumCounters * 4), "cudaMalloc(counters)");
+    CU(ctx->stats.ensure(kNumStats * 8), "cudaMalloc(stats)");
+    CU(ctx->k0_flag.ensure((S.k0t + 1) * 4), "cudaMalloc(k0_flag)");
+    CU(ctx->k0_agg.ensure((S.k0t + 1) * 32), "cudaMalloc(k0_agg)");
+    CU(ctx->k2_flag.ensure((b->k2_tiles + 1) * 4), "cudaMalloc(k2_flag)");
+    CU(ctx->k2_agg.ensure((b->k2_tiles + 1) * 64), "cudaMalloc(k2_agg)");
+    CU(ctx->status_host.ensure(S.n * sizeof(ImgState) + 64 + kNumStats * 8), "cudaMallocHost(status)");
+
+    // ---- kernel parameters
+    Params& p = b->prm;
+    p.img = reinterpret_cast<const ImgDesc*>(M.desc);
+    p.ist = reinterpret_cast<ImgState*>(M.state);
+    p.n_img = uint32_t(S.n);
+    p.huff = reinterpret_cast<const DevHuff*>(M.huff);
+    p.quant_raster = reinterpret_cast<const uint16_t*>(M.quant);
+    p.basis = reinterpret_cast<const double*>(M.basis);
+    p.wq = reinterpret_cast<const float*>(M.wq);
+    p.n_quant = S.n_quant;
+    p.raw = ctx->raw.as<uint8_t>();
+    p.ubuf = ctx->ubuf.as<uint8_t>();
+    p.k0_first = reinterpret_cast<const uint32_t*>(M.k0);
+    p.k0_img = reinterpret_cast<const uint32_t*>(M.k0img);
+    p.sub_img = reinterpret_cast<const uint32_t*>(M.subimg);
+    p.segs = ctx->segs.as<uint2>();
+    p.dri_img = reinterpret_cast<const uint32_t*>(M.dri);
+    p.n_dri = S.ndri;
+    p.k0_tiles = S.k0t;
+    p.k0_bpt = S.k0_bpt;
+    p.smem_tables = smem_tables;
+    p.k1_ctas = b->k1_ctas;
+    p.n_huff = b->n_huff;
+    // grids that do not fill the GPU are latency-bound: a stale CTA start is
+    // re-chained inside K1 from shared memory; full grids skip the wait and
+    // leave the (few) stale starts to K1c's parallel first pass
+    p.k1_hop = b->k1_ctas < 2 * 148 ? 1u : 0u;
+    if (const char* e = getenv("PJG_K1_HOP")) p.k1_hop = atoi(e) ? 1u : 0u;  // override (tests, A/B)
+    {  // every image 4:2:0 colour to RGB: K4's specialised variant
+        const bool all420 = S.all420 && b->cfg.output == PJG_OUT_RGB;
+        p.k4_layout = all420 ? 1u : 0u;
+        if (const char* e = getenv("PJG_K4_LAYOUT")) p.k4_layout = atoi(e) == 1 && all420 ? 1u : 0u;  // A/B
+    }
+    p.sb = S.sb_int;
+    p.sb_cfg = S.sb;
+    p.b_cfg = b->cfg.sequence_length_b;
+    p.sub_first = reinterpret_cast<const uint64_t*>(M.sub);
+    p.total_subs = S.sub;
+    p.ent = ctx->ent.as<Entry>();
+    p.dcs = ctx->dcs.as<DcSums>();
+    p.off = ctx->off.as<uint64_t>();
+    p.cap = ctx->cap.as<uint32_t>();
+    p.pred = ctx->pred.as<DcSums>();
+    p.cta_end = ctx->cta_end.as<Entry>();
+    p.cta_start = ctx->cta_start.as<Entry>();
+    p.sym = sym_cap ? ctx->sym.as<uint16_t>() : nullptr;
+    p.tag = sym_cap ? ctx->tag.as<uint32_t>() : nullptr;
+    p.sym_stride = sym_stride;
+    p.sym_cap = sym_cap;
+    p.k1_flag = ctx->k1_flag.as<uint32_t>();
+    p.k2_tiles = b->k2_tiles;
+    p.k4_tiles = S.k4t;
+    p.tile_first = reinterpret_cast<const uint32_t*>(M.tile);
+    p.coef = ctx->coef.as<int16_t>();
+    p.meta = ctx->blkmeta.as<uint2>();
+    p.out = ctx->out.as<uint8_t>();
+    p.counters = ctx->counters.as<uint32_t>();
+    p.k0_flag = ctx->k0_flag.as<uint32_t>();
+    p.k0_agg = ctx->k0_agg.as<uint64_t>();
+    p.k2_flag = ctx->k2_flag.as<uint32_t>();
+    p.k2_agg = ctx->k2_agg.as<uint64_t>();
+    p.stats = ctx->stats.as<unsigned long long>();
+    return PJG_OK;
+}
+
 // blob_lo/blob_hi: the one caller allocation every file lies in (the blob
 // API), or null — then the scans are copied from the caller's buffers only
 // (packed into the pinned stage), except for a single file, whose scan is
@@ -586,7 +745,7 @@ int batch_create_impl(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const
         const char* e = getenv("PJG_SB_AUTO");
         if (!n_dri && !(e && atoi(e) == 0)) {
             uint64_t est = raw_sum * 8 / sb;
-            while (est < uint64_t(kK1Threads) * 148 / 2 && sb_int / 2 >= 256 && (sb_int / 2) % 32 == 0) {
+            while (est < uint64_t(kK1Threads) * 148 / 2 && sb_int / 2 >= sb_floor() && (sb_int / 2) % 32 == 0) {
                 sb_int /= 2;
                 est *= 2;
             }
@@ -824,131 +983,36 @@ int batch_create_impl(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const
     }
 
     mark("meta");
-    // ---- device reservation
     CU(ctx->meta.ensure(o), "cudaMalloc(meta)");
-    CU(ctx->raw.ensure(b->raw_bytes + 64), "cudaMalloc(raw)");
-    CU(ctx->ubuf.ensure(b->raw_bytes + 64), "cudaMalloc(ubuf)");
-    const size_t subs = std::max<uint64_t>(sub, 1);
-    CU(ctx->ent.ensure(subs * sizeof(Entry)), "cudaMalloc(ent)");
-    CU(ctx->dcs.ensure(subs * sizeof(DcSums)), "cudaMalloc(dcs)");
-    CU(ctx->off.ensure(subs * 8), "cudaMalloc(off)");
-    CU(ctx->cap.ensure(subs * 4), "cudaMalloc(cap)");
-    CU(ctx->pred.ensure(subs * sizeof(DcSums)), "cudaMalloc(pred)");
-    CU(ctx->cta_end.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_end)");
-    CU(ctx->cta_start.ensure((b->k1_ctas + 1) * sizeof(Entry)), "cudaMalloc(cta_start)");
-    // K1 chains keep their decoded symbols for K3 to replay (16 bits each, up
-    // to sb/4 per subsequence: 4 bytes of scratch per compressed byte) when it
-    // pays: measured break-even (DESIGN.md §5) — many symbols per data unit
-    // (K3's decode dominates its block work) but a stream that syncs in few
-    // rounds (K1 stores each chain's symbols once per round): 64..160 scan
-    // bits per data unit, in images of >= 64 subsequences on average.
-    // PJG_REPLAY=0/1 forces it.
-    // small batches (under ~4 K1 CTAs per SM): the decoders' table probes sit on a
-    // serial dependency chain with few warps to hide an L1 miss — stage the
-    // tables in shared memory
-    uint32_t smem_tables =
-        (huffs.size() <= kMaxSmemTables && sub < uint64_t(kK1Threads) * 148 * 4) ? uint32_t(huffs.size()) : 0u;
-    if (const char* e = getenv("PJG_SMEM_TABLES"))  // override (A/B experiments)
-        smem_tables = (atoi(e) && huffs.size() <= kMaxSmemTables) ? uint32_t(huffs.size()) : 0u;
-    const bool st_tables = smem_tables != 0;
-    bool replay_on = false;
     {
-        uint64_t bits = 0;
+        PlanSummary S;
+        S.n = n;
+        S.sub = sub;
+        S.du = du;
+        S.outb = outb;
+        S.seg_total = seg_total;
+        S.k0t = k0t;
+        S.k4t = k4t;
+        S.ndri = uint32_t(dri.size());
+        S.n_huff = uint32_t(huffs.size());
+        S.n_quant = uint32_t(quants.size());
+        S.k0_bpt = k0_bpt;
+        S.sb = sb;
+        S.sb_int = sb_int;
+        S.n_ok = n_ok;
+        S.bits = 0;
         for (size_t i = 0; i < n; ++i)
-            if (b->host_status[i] == kOk) bits += desc[i].raw_len * 8;
-        const uint64_t per_du = du ? bits / du : 0;
-        // (and large images: a few subsequences per image keep K3 cheap)
-        // (large batches only: K1's shared-memory-table variant for small ones
-        // does not keep symbols)
-        replay_on = per_du >= 64 && per_du <= 160 && n_ok && sub / n_ok >= 64 && !st_tables;
-        if (const char* e = getenv("PJG_REPLAY")) replay_on = atoi(e) != 0 && !st_tables;
-        if (getenv("PJG_NO_REPLAY")) replay_on = false;
-    }
-    const uint32_t sym_cap = (!replay_on || sb_int > 65536) ? 0u : uint32_t(sb_int / 4);
-    const uint64_t sym_stride = align_up(subs, 64);
-    if (sym_cap) {
-        CU(ctx->sym.ensure(sym_stride * sym_cap * 2), "cudaMalloc(sym)");
-        CU(ctx->tag.ensure(subs * 16), "cudaMalloc(tag)");
-    }
-    CU(ctx->k1_flag.ensure((b->k1_ctas + 1) * 4), "cudaMalloc(k1_flag)");
-    CU(ctx->coef.ensure(std::max<uint64_t>(du, 1) * 128), "cudaMalloc(coef)");
-    CU(ctx->segs.ensure(std::max<uint64_t>(seg_total, 1) * sizeof(uint2)), "cudaMalloc(segs)");
-    CU(ctx->blkmeta.ensure(std::max<uint64_t>(du, 1) * 8), "cudaMalloc(blkmeta)");
-    CU(ctx->out.ensure(std::max<uint64_t>(outb, 1)), "cudaMalloc(out)");
-    CU(ctx->counters.ensure(kNumCounters * 4), "cudaMalloc(counters)");
-    CU(ctx->stats.ensure(kNumStats * 8), "cudaMalloc(stats)");
-    CU(ctx->k0_flag.ensure((k0t + 1) * 4), "cudaMalloc(k0_flag)");
-    CU(ctx->k0_agg.ensure((k0t + 1) * 32), "cudaMalloc(k0_agg)");
-    CU(ctx->k2_flag.ensure((b->k2_tiles + 1) * 4), "cudaMalloc(k2_flag)");
-    CU(ctx->k2_agg.ensure((b->k2_tiles + 1) * 64), "cudaMalloc(k2_agg)");
-    CU(ctx->status_host.ensure(n * sizeof(ImgState) + 64 + kNumStats * 8), "cudaMallocHost(status)");
-
-    // ---- kernel parameters
-    Params& p = b->prm;
-    uint8_t* md = ctx->meta.as<uint8_t>();
-    p.img = reinterpret_cast<const ImgDesc*>(md + b->m_desc);
-    p.ist = reinterpret_cast<ImgState*>(md + b->m_state);
-    p.n_img = uint32_t(n);
-    p.huff = reinterpret_cast<const DevHuff*>(md + b->m_huff);
-    p.quant_raster = reinterpret_cast<const uint16_t*>(md + b->m_quant);
-    p.basis = reinterpret_cast<const double*>(md + b->m_basis);
-    p.wq = reinterpret_cast<const float*>(md + b->m_wq);
-    p.n_quant = uint32_t(quants.size());
-    p.raw = ctx->raw.as<uint8_t>();
-    p.ubuf = ctx->ubuf.as<uint8_t>();
-    p.k0_first = reinterpret_cast<const uint32_t*>(md + b->m_k0);
-    p.k0_img = reinterpret_cast<const uint32_t*>(md + b->m_k0img);
-    p.sub_img = reinterpret_cast<const uint32_t*>(md + b->m_subimg);
-    p.segs = ctx->segs.as<uint2>();
-    p.dri_img = reinterpret_cast<const uint32_t*>(md + b->m_dri);
-    p.n_dri = uint32_t(dri.size());
-    p.k0_tiles = k0t;
-    p.k0_bpt = k0_bpt;
-    p.smem_tables = smem_tables;
-    p.k1_ctas = b->k1_ctas;
-    p.n_huff = b->n_huff;
-    // grids that do not fill the GPU are latency-bound: a stale CTA start is
-    // re-chained inside K1 from shared memory; full grids skip the wait and
-    // leave the (few) stale starts to K1c's parallel first pass
-    p.k1_hop = b->k1_ctas < 2 * 148 ? 1u : 0u;
-    if (const char* e = getenv("PJG_K1_HOP")) p.k1_hop = atoi(e) ? 1u : 0u;  // override (tests, A/B)
-    {  // every image 4:2:0 colour to RGB: K4's specialised variant
-        bool all420 = cfg->output == PJG_OUT_RGB && n_ok > 0;
-        for (size_t i = 0; i < n && all420; ++i)
+            if (b->host_status[i] == kOk) S.bits += desc[i].raw_len * 8;
+        S.all420 = cfg->output == PJG_OUT_RGB && n_ok > 0;
+        for (size_t i = 0; i < n && S.all420; ++i)
             if (b->host_status[i] == kOk)
-                all420 = desc[i].ncomp == 3 && desc[i].h_max == 2 && desc[i].v_max == 2;
-        p.k4_layout = all420 ? 1u : 0u;
-        if (const char* e = getenv("PJG_K4_LAYOUT")) p.k4_layout = atoi(e) == 1 && all420 ? 1u : 0u;  // A/B
+                S.all420 = desc[i].ncomp == 3 && desc[i].h_max == 2 && desc[i].v_max == 2;
+        uint8_t* md = ctx->meta.as<uint8_t>();
+        MetaPtrs M{md + b->m_desc, md + b->m_state, md + b->m_huff, md + b->m_quant, md + b->m_wq,
+                   md + b->m_basis, md + b->m_k0, md + b->m_tile, md + b->m_sub, md + b->m_k0img,
+                   md + b->m_subimg, md + b->m_dri};
+        if ((st = finish_plan(ctx, b.get(), S, M))) return st;
     }
-    p.sb = sb_int;
-    p.sb_cfg = sb;
-    p.b_cfg = cfg->sequence_length_b;
-    p.sub_first = reinterpret_cast<const uint64_t*>(md + b->m_sub);
-    p.total_subs = sub;
-    p.ent = ctx->ent.as<Entry>();
-    p.dcs = ctx->dcs.as<DcSums>();
-    p.off = ctx->off.as<uint64_t>();
-    p.cap = ctx->cap.as<uint32_t>();
-    p.pred = ctx->pred.as<DcSums>();
-    p.cta_end = ctx->cta_end.as<Entry>();
-    p.cta_start = ctx->cta_start.as<Entry>();
-    p.sym = sym_cap ? ctx->sym.as<uint16_t>() : nullptr;
-    p.tag = sym_cap ? ctx->tag.as<uint32_t>() : nullptr;
-    p.sym_stride = sym_stride;
-    p.sym_cap = sym_cap;
-    p.k1_flag = ctx->k1_flag.as<uint32_t>();
-    p.k2_tiles = b->k2_tiles;
-    p.k4_tiles = k4t;
-    p.tile_first = reinterpret_cast<const uint32_t*>(md + b->m_tile);
-    p.coef = ctx->coef.as<int16_t>();
-    p.meta = ctx->blkmeta.as<uint2>();
-    p.out = ctx->out.as<uint8_t>();
-    p.counters = ctx->counters.as<uint32_t>();
-    p.k0_flag = ctx->k0_flag.as<uint32_t>();
-    p.k0_agg = ctx->k0_agg.as<uint64_t>();
-    p.k2_flag = ctx->k2_flag.as<uint32_t>();
-    p.k2_agg = ctx->k2_agg.as<uint64_t>();
-    p.stats = ctx->stats.as<unsigned long long>();
     mark("reserve");
 
     ctx->busy = true;
@@ -976,8 +1040,249 @@ int pjg_batch_create_blob(pjg_ctx* ctx, const uint8_t* blob, size_t blob_bytes, 
     return batch_create_impl(ctx, n, files.data(), sizes, cfg, blob, blob + blob_bytes, out);
 }
 
+// Device-side planning (devplan.cu): the files go up whole
+// in one copy; the marker walk, table dedup/build and layout run as kernels;
+// the host reads back one small totals record to size the decode.
+int pjg_batch_create_device(pjg_ctx* ctx, const uint8_t* blob, size_t blob_bytes, size_t n,
+                            const uint64_t* offsets, const size_t* sizes, const pjg_config* cfg, pjg_batch** out) {
+    if (!ctx || !out || (n && (!blob || !offsets || !sizes))) return PJG_INVALID_ARGUMENT;
+    *out = nullptr;
+    int st = 0;
+    if (!validate_cfg(ctx, cfg, &st)) return st;
+    if (ctx->busy) return fail(ctx, PJG_INVALID_ARGUMENT, "one live batch per context");
+    uint64_t tot = 0;
+    for (size_t i = 0; i < n; ++i) {
+        if (offsets[i] > blob_bytes || sizes[i] > blob_bytes - offsets[i])
+            return fail(ctx, PJG_INVALID_ARGUMENT, "file outside the blob");
+        tot += sizes[i];
+    }
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = ctx->stream;
+    auto b = std::make_unique<pjg_batch>();
+    b->ctx = ctx;
+    b->cfg = *cfg;
+    b->n = n;
+    b->devplan = true;
+    b->swap_pool(ctx->pool);
+    b->dev_state.clear();
+    b->host_status.assign(n, 0);
+    b->info.resize(n);
+    // the host planner's heuristics on the files' bytes (scans are ~all of them)
+    const uint64_t sb = cfg->subsequence_bits;
+    uint64_t sb_int = sb;
+    {
+        const char* e = getenv("PJG_SB_AUTO");
+        if (!cfg->restart_intervals && !(e && atoi(e) == 0)) {
+            uint64_t est = tot * 8 / sb;
+            while (est < uint64_t(kK1Threads) * 148 / 2 && sb_int / 2 >= sb_floor() && (sb_int / 2) % 32 == 0) {
+                sb_int /= 2;
+                est *= 2;
+            }
+        }
+    }
+    uint32_t k0_bpt = (n && tot / n >= 48 * 1024) ? kK0BigBpt : kK0SmallBpt;
+    if (const char* e = getenv("PJG_K0_BPT")) k0_bpt = atoi(e) == int(kK0BigBpt) ? kK0BigBpt : kK0SmallBpt;
+
+    // ---- device layout: meta (desc, state, basis, prefix arrays, DRI list),
+    // plan scratch (inputs, headers, dedup table, uniques, counts, totals)
+    const size_t nn = std::max<size_t>(n, 1);
+    size_t o = 0;
+    b->m_desc = o;
+    o = align_up(o + nn * sizeof(ImgDesc), 16);
+    b->m_state = o;
+    o = align_up(o + nn * sizeof(ImgState), 16);
+    b->m_basis = o;
+    o = align_up(o + 64 * sizeof(double), 16);
+    b->m_k0 = o;
+    o = align_up(o + (nn + 1) * 4, 16);
+    b->m_tile = o;
+    o = align_up(o + (nn + 1) * 4, 16);
+    b->m_sub = o;
+    o = align_up(o + (nn + 1) * 8, 16);
+    b->m_dri = o;
+    o = align_up(o + (nn + 1) * 4, 16);
+    b->m_total = o;
+    CU(ctx->meta.ensure(o), "cudaMalloc(meta)");
+    const uint64_t refs = 9 * uint64_t(nn) + 16;
+    uint64_t H = 64;
+    while (H < 2 * refs) H <<= 1;
+    const uint32_t nblk = uint32_t((nn + 255) / 256);
+    size_t q = 0;
+    const size_t p_off = q;
+    q = align_up(q + nn * 8, 16);
+    const size_t p_size = q;
+    q = align_up(q + nn * 8, 16);
+    const size_t p_hdr = q;
+    q = align_up(q + nn * sizeof(DevHdr), 16);
+    const size_t p_hkeys = q;
+    q = align_up(q + H * 8, 16);
+    const size_t p_hval = q;
+    q = align_up(q + H * 4, 16);
+    const size_t p_cnts = q;
+    q = align_up(q + kPlanCounters * 4, 16);
+    const size_t p_tot = q;
+    q = align_up(q + sizeof(PlanTotals), 16);
+    const size_t zero_end = q;  // [p_hkeys, zero_end) is zeroed per plan
+    const size_t p_hrep = q;
+    q = align_up(q + H * sizeof(TabRep), 16);
+    const size_t p_uh = q;
+    q = align_up(q + refs * sizeof(TabRep), 16);
+    const size_t p_uq = q;
+    q = align_up(q + refs * sizeof(TabRep), 16);
+    const size_t p_state0 = q;
+    q = align_up(q + nn * sizeof(ImgState), 16);
+    const size_t p_info = q;
+    q = align_up(q + nn * sizeof(pjg_image_info), 16);
+    const size_t p_cnt = q;
+    q = align_up(q + nn * sizeof(Cnt), 16);
+    const size_t p_blk = q;
+    q = align_up(q + (nblk + 1) * sizeof(Cnt), 16);
+    CU(ctx->plan.ensure(q), "cudaMalloc(plan)");
+    CU(ctx->raw.ensure(blob_bytes + 64), "cudaMalloc(raw)");
+    CU(ctx->ubuf.ensure(blob_bytes + 64), "cudaMalloc(ubuf)");
+    // pinned staging: offsets, sizes, basis; totals come back here
+    const size_t h_tot = align_up(nn * 16 + 64 * sizeof(double), 16);
+    CU(ctx->plan_host.ensure(h_tot + sizeof(PlanTotals)), "cudaMallocHost(plan)");
+    uint8_t* ph = static_cast<uint8_t*>(ctx->plan_host.p);
+    std::memcpy(ph, offsets, n * 8);
+    for (size_t i = 0; i < n; ++i) reinterpret_cast<uint64_t*>(ph + nn * 8)[i] = sizes[i];
+    std::memcpy(ph + nn * 16, ctx->basis, 64 * sizeof(double));
+
+    uint8_t* pd = ctx->plan.as<uint8_t>();
+    uint8_t* md = ctx->meta.as<uint8_t>();
+    cudaPointerAttributes pa{};
+    const bool dev_blob = cudaPointerGetAttributes(&pa, blob) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    CU(cudaEventRecord(ctx->ev[0], s), "ev");
+    if (blob_bytes)
+        CU(cudaMemcpyAsync(ctx->raw.p, blob, blob_bytes, dev_blob ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s),
+           "H2D files");
+    CU(cudaMemcpyAsync(pd + p_off, ph, nn * 16, cudaMemcpyHostToDevice, s), "H2D offsets");  // offsets, sizes
+    CU(cudaMemcpyAsync(md + b->m_basis, ph + nn * 16, 64 * sizeof(double), cudaMemcpyHostToDevice, s), "H2D basis");
+    CU(cudaEventRecord(ctx->ev[1], s), "ev");
+    CU(cudaMemsetAsync(pd + p_hkeys, 0, zero_end - p_hkeys, s), "memset plan");
+
+    PlanParams P{};
+    P.raw = ctx->raw.as<uint8_t>();
+    P.offsets = reinterpret_cast<const uint64_t*>(pd + p_off);
+    P.sizes = reinterpret_cast<const uint64_t*>(pd + p_size);
+    P.n = uint32_t(n);
+    P.allow_dri = cfg->restart_intervals != 0;
+    P.out_mode = cfg->output;
+    P.k0_bpt = k0_bpt;
+    P.sb_int = sb_int;
+    P.hdr = reinterpret_cast<DevHdr*>(pd + p_hdr);
+    P.hkeys = reinterpret_cast<uint64_t*>(pd + p_hkeys);
+    P.hval = reinterpret_cast<uint32_t*>(pd + p_hval);
+    P.hrep = reinterpret_cast<TabRep*>(pd + p_hrep);
+    P.hmask = uint32_t(H - 1);
+    P.counters = reinterpret_cast<uint32_t*>(pd + p_cnts);
+    P.uh = reinterpret_cast<TabRep*>(pd + p_uh);
+    P.uq = reinterpret_cast<TabRep*>(pd + p_uq);
+    P.desc = reinterpret_cast<ImgDesc*>(md + b->m_desc);
+    P.state = reinterpret_cast<ImgState*>(md + b->m_state);
+    P.state0 = reinterpret_cast<ImgState*>(pd + p_state0);
+    P.info = reinterpret_cast<pjg_image_info*>(pd + p_info);
+    P.k0_first = reinterpret_cast<uint32_t*>(md + b->m_k0);
+    P.tile_first = reinterpret_cast<uint32_t*>(md + b->m_tile);
+    P.sub_first = reinterpret_cast<uint64_t*>(md + b->m_sub);
+    P.dri = reinterpret_cast<uint32_t*>(md + b->m_dri);
+    P.totals = reinterpret_cast<PlanTotals*>(pd + p_tot);
+    P.cnt = reinterpret_cast<Cnt*>(pd + p_cnt);
+    P.blk = reinterpret_cast<Cnt*>(pd + p_blk);
+    if (n) {
+        launch_plan_parse(P, s);
+        CU(cudaGetLastError(), "plan launch");
+    }
+    PlanTotals T{};
+    CU(cudaMemcpyAsync(ph + h_tot, pd + p_tot, sizeof(PlanTotals), cudaMemcpyDeviceToHost, s), "D2H totals");
+    CU(cudaStreamSynchronize(s), "plan");
+    std::memcpy(&T, ph + h_tot, sizeof(T));
+
+    // ---- unique tables and lookup tables (sized by the totals)
+    const uint32_t nh = std::max<uint32_t>(T.n_huff, 1), nq = std::max<uint32_t>(T.n_quant, 1);
+    const uint64_t n_subimg = ((T.sub + (1u << kSubImgShift) - 1) >> kSubImgShift) + 2;
+    size_t r = 0;
+    b->m_huff = r;
+    r = align_up(r + nh * sizeof(DevHuff), 16);
+    b->m_quant = r;
+    r = align_up(r + nq * 128, 16);
+    b->m_wq = r;
+    r = align_up(r + nq * 64 * sizeof(float), 16);
+    b->m_k0img = r;
+    r = align_up(r + (uint64_t(T.k0t) + 1) * 4, 16);
+    b->m_subimg = r;
+    r = align_up(r + n_subimg * 4, 16);
+    CU(ctx->meta2.ensure(r), "cudaMalloc(meta2)");
+    uint8_t* m2 = ctx->meta2.as<uint8_t>();
+    TableOut TO{reinterpret_cast<DevHuff*>(m2 + b->m_huff), reinterpret_cast<uint16_t*>(m2 + b->m_quant),
+                reinterpret_cast<float*>(m2 + b->m_wq), T.n_huff, T.n_quant};
+    launch_plan_finish(P, TO, reinterpret_cast<uint32_t*>(m2 + b->m_k0img), reinterpret_cast<uint32_t*>(m2 + b->m_subimg),
+                       n_subimg, s);
+    CU(cudaGetLastError(), "plan launch");
+
+    PlanSummary S;
+    S.n = n;
+    S.sub = T.sub;
+    S.du = T.du;
+    S.outb = T.outb;
+    S.seg_total = T.seg;
+    S.k0t = T.k0t;
+    S.k4t = T.k4t;
+    S.ndri = T.ndri;
+    S.n_huff = nh;
+    S.n_quant = nq;
+    S.k0_bpt = k0_bpt;
+    S.sb = sb;
+    S.sb_int = sb_int;
+    S.n_ok = T.n_ok;
+    S.bits = T.bits;
+    S.all420 = T.all420 != 0;
+    MetaPtrs M{md + b->m_desc, md + b->m_state, m2 + b->m_huff, m2 + b->m_quant, m2 + b->m_wq,
+               md + b->m_basis, md + b->m_k0, md + b->m_tile, md + b->m_sub, m2 + b->m_k0img,
+               m2 + b->m_subimg, md + b->m_dri};
+    b->raw_src = nullptr;
+    b->raw_bytes = blob_bytes;
+    b->packed = false;
+    if ((st = finish_plan(ctx, b.get(), S, M))) return st;
+    b->state0 = reinterpret_cast<const ImgState*>(pd + p_state0);
+    b->dinfo = reinterpret_cast<const pjg_image_info*>(pd + p_info);
+    b->uploaded = true;
+    ctx->busy = true;
+    *out = b.release();
+    return PJG_OK;
+}
+
+namespace {
+// Host copies of a device-planned batch's descriptors, header statuses and
+// image infos (for the per-image API calls); a no-op for host-planned ones.
+int host_view(const pjg_batch* cb) {
+    pjg_batch* b = const_cast<pjg_batch*>(cb);
+    if (!b->devplan || b->host_view) return PJG_OK;
+    pjg_ctx* ctx = b->ctx;
+    CU(cudaSetDevice(ctx->device), "cudaSetDevice");
+    CU(ctx->desc_host.ensure(b->n * sizeof(ImgDesc) + 16), "cudaMallocHost(desc)");
+    std::vector<ImgState> s0(b->n);
+    if (b->n) {
+        CU(cudaMemcpyAsync(ctx->desc_host.p, ctx->meta.as<uint8_t>() + b->m_desc, b->n * sizeof(ImgDesc),
+                           cudaMemcpyDeviceToHost, ctx->stream),
+           "D2H desc");
+        CU(cudaMemcpyAsync(b->info.data(), b->dinfo, b->n * sizeof(pjg_image_info), cudaMemcpyDeviceToHost, ctx->stream),
+           "D2H info");
+        CU(cudaMemcpyAsync(s0.data(), b->state0, b->n * sizeof(ImgState), cudaMemcpyDeviceToHost, ctx->stream),
+           "D2H status");
+    }
+    CU(cudaStreamSynchronize(ctx->stream), "host view");
+    b->desc = static_cast<const ImgDesc*>(ctx->desc_host.p);
+    for (size_t i = 0; i < b->n; ++i) b->host_status[i] = s0[i].status;
+    b->host_view = true;
+    return PJG_OK;
+}
+}  // namespace
+
 int pjg_batch_upload(pjg_batch* b) {
     if (!b) return PJG_INVALID_ARGUMENT;
+    if (b->devplan) return PJG_OK;  // the files went up with the plan
     pjg_ctx* ctx = b->ctx;
     CU(cudaSetDevice(ctx->device), "cudaSetDevice");
     CU(cudaEventRecord(ctx->ev[0], ctx->stream), "cudaEventRecord");
@@ -1003,7 +1308,12 @@ int pjg_batch_decode(pjg_batch* b) {
     CU(cudaSetDevice(ctx->device), "cudaSetDevice");
     cudaStream_t s = ctx->stream;
     // status words are re-initialised so decode can be re-run on the same upload
-    {
+    if (b->devplan) {
+        if (b->n)
+            CU(cudaMemcpyAsync(ctx->meta.as<uint8_t>() + b->m_state, b->state0, b->n * sizeof(ImgState),
+                               cudaMemcpyDeviceToDevice, s),
+               "D2D status");
+    } else {
         uint8_t* mh = static_cast<uint8_t*>(ctx->meta_host.p);
         CU(cudaMemcpyAsync(ctx->meta.as<uint8_t>() + b->m_state, mh + b->m_state, b->n * sizeof(ImgState),
                            cudaMemcpyHostToDevice, s),
@@ -1072,6 +1382,7 @@ int pjg_batch_synchronize(pjg_batch* b, int32_t* statuses) {
 
 int pjg_batch_download(pjg_batch* b, uint8_t* const* outs, const size_t* caps) {
     if (!b || !outs) return PJG_INVALID_ARGUMENT;
+    if (int hv = host_view(b)) return hv;
     pjg_ctx* ctx = b->ctx;
     int st = pjg_batch_synchronize(b, nullptr);
     if (st) return st;
@@ -1124,16 +1435,19 @@ int pjg_batch_download_all_async(pjg_batch* b, void* host, size_t cap) {
 
 uint64_t pjg_batch_output_offset(const pjg_batch* b, size_t i) {
     if (!b || i >= b->n) return 0;
+    if (host_view(b)) return 0;
     return b->desc[i].out_off;
 }
 
 int pjg_batch_info(const pjg_batch* b, size_t i, pjg_image_info* info) {
     if (!b || i >= b->n || !info) return PJG_INVALID_ARGUMENT;
+    if (int hv = host_view(b)) return hv;
     *info = b->info[i];
     return b->host_status[i];
 }
 
 const uint8_t* pjg_batch_device_output(const pjg_batch* b, size_t i) {
+    if (!b || i >= b->n || host_view(b)) return nullptr;
     if (!b || i >= b->n || b->host_status[i] != 0 || b->desc[i].deferred != 0) return nullptr;
     return b->ctx->out.as<uint8_t>() + b->desc[i].out_off;
 }
@@ -1142,6 +1456,7 @@ uint64_t pjg_batch_output_bytes(const pjg_batch* b) { return b ? b->out_bytes : 
 
 uint64_t pjg_batch_scan_bits(const pjg_batch* b) {
     if (!b || !b->synced) return 0;
+    if (host_view(b)) return 0;
     uint64_t bits = 0;
     for (size_t i = 0; i < b->n; ++i)
         if (b->host_status[i] == 0 && i < b->dev_state.size() && b->dev_state[i].status == 0)
@@ -1156,6 +1471,7 @@ uint32_t pjg_batch_kernel_launches(const pjg_batch* b) {
 
 int pjg_batch_copy_outputs(pjg_batch* b, void* const* dst, const size_t* caps) {
     if (!b || !dst || !caps) return PJG_INVALID_ARGUMENT;
+    if (int hv = host_view(b)) return hv;
     pjg_ctx* ctx = b->ctx;
     // only images that decoded: device failures (and deferred table errors,
     // which reserve no output) are known after the batch finished
@@ -1203,6 +1519,7 @@ void pjg_batch_destroy(pjg_batch* b) {
 
 int pjg_batch_dump_coefficients(const pjg_batch* b, size_t i, int pre_dc_zigzag, int16_t* out, size_t count) {
     if (!b || i >= b->n || !out) return PJG_INVALID_ARGUMENT;
+    if (int hv = host_view(b)) return hv;
     pjg_ctx* ctx = b->ctx;
     const ImgDesc& d = b->desc[i];
     const uint64_t dus = uint64_t(d.mcus_x) * d.mcus_y * d.dpm;
@@ -1243,6 +1560,7 @@ int pjg_batch_dump_coefficients(const pjg_batch* b, size_t i, int pre_dc_zigzag,
 
 int pjg_batch_dump_sync_states(const pjg_batch* b, size_t i, pjg_sync_entry* out, size_t cap, size_t* n_out) {
     if (!b || i >= b->n || !n_out) return PJG_INVALID_ARGUMENT;
+    if (int hv = host_view(b)) return hv;
     pjg_ctx* ctx = b->ctx;
     int st = pjg_batch_synchronize(const_cast<pjg_batch*>(b), nullptr);
     if (st) return st;
@@ -1292,6 +1610,7 @@ int pjg_batch_dump_sync_states(const pjg_batch* b, size_t i, pjg_sync_entry* out
 
 int pjg_batch_dump_segment(const pjg_batch* b, size_t i, uint8_t* out, size_t cap, size_t* n_out) {
     if (!b || i >= b->n || !n_out) return PJG_INVALID_ARGUMENT;
+    if (int hv = host_view(b)) return hv;
     pjg_ctx* ctx = b->ctx;
     int st = pjg_batch_synchronize(const_cast<pjg_batch*>(b), nullptr);
     if (st) return st;

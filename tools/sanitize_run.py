@@ -1,0 +1,37 @@
+"""Small decodes for compute-sanitizer (racecheck / synccheck / memcheck):
+the spin-wait lookbacks of K0, K1 and K2 run across many CTAs, images and
+restart intervals.  Usage: compute-sanitizer --tool racecheck python
+tools/sanitize_run.py  (exit 0 = every decode bit-exact vs the oracle)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_2111_09219_b200 as pj  # noqa: E402
+from oracle.oracle import Orc  # noqa: E402
+from paper_2111_09219_b200.synth import synth_ref_batch  # noqa: E402
+
+cases = [
+    # (n, w, h, seed, q, sampling, restart interval, sb)
+    (24, 500, 375, 1000, 75, "420", 0, 1024),   # batch: K0 multi-tile lookback, K1 CTAs spanning images
+    (1, 1024, 768, 7, 95, "444", 0, 256),        # one image, many K1 CTAs (inter-CTA chaining, K1c)
+    (2, 640, 480, 9, 90, "420", 40, 512),        # restart intervals: K0 RST strip, K0b segments
+    (3, 333, 211, 11, 60, "gray", 0, 128),       # ragged, gray
+]
+dec = pj.Decoder(0)
+for n, w, h, seed, q, s, ri, sb in cases:
+    blob, offs, sizes = synth_ref_batch(n, w, h, seed, q, s, ri)
+    files = [blob[o: o + z].tobytes() for o, z in zip(offs, sizes)]
+    cfg = pj.DecodeConfig(subsequence_bits=sb, restart_intervals=ri > 0)
+    with dec.batch(files, cfg, pj.OutputColorspace.RGBInterleaved) as b:
+        st = b.run()
+        assert (st == 0).all(), st
+        outs = b.download()
+    if ri == 0:
+        for i, f in enumerate(files):
+            want = Orc.decode(f, rgb=True)
+            assert np.array_equal(outs[i][: want.data.size], want.data.reshape(-1)), (n, w, h, i)
+    print(f"ok {n}x{w}x{h} q{q} {s} dri={ri} sb={sb}")
+dec.close()
+print("sanitize_run: all decodes ok")
