@@ -214,6 +214,10 @@ int pjg_upsample_and_convert(pjg_ctx* ctx, uint32_t width, uint32_t height, uint
                              const uint8_t* const* planes, uint8_t* out_rgb);
 
 /* ---- test hooks (host emulation of device table logic) ---------------- */
+/* The device planner's header parse (pjg_batch_create_device) run on the
+ * host: out = {status, table_status, width, height, components, units per MCU,
+ * scan offset} (tests pin it against the host parser and the reference). */
+int pjg_debug_device_parse(const uint8_t* file, size_t size, int allow_dri, int64_t* out);
 /* Builds the device Huffman table for a DHT spec and decodes a 16-bit
  * window with it: returns (len << 8) | symbol, 0 = no code, or -(status). */
 int pjg_debug_huff_decode(const uint8_t* counts16, const uint8_t* symbols, size_t nsym,

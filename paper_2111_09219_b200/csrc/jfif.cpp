@@ -272,12 +272,21 @@ int32_t build_dev_huff(const HuffSpec& spec, DevHuff* out) {
     if (si != spec.symbols.size()) return kMalformedHeader;
     if (maxlen == 0) return kMalformedHeader;
     out->maxlen = maxlen;
+    uint32_t n2 = 0;
     for (size_t k = 0; k < si; ++k) {
-        if (lens[k] > kPrimaryBits) continue;
-        uint32_t shift = kPrimaryBits - lens[k];
-        uint32_t first = uint32_t(codes[k]) << shift, count = 1u << shift;
-        for (uint32_t i = 0; i < count; ++i)
-            out->lut[first + i] = uint16_t((uint32_t(lens[k]) << 8) | spec.symbols[k]);
+        const uint16_t e = uint16_t((uint32_t(lens[k]) << 8) | spec.symbols[k]);
+        if (lens[k] <= kPrimaryBits) {
+            uint32_t shift = kPrimaryBits - lens[k];
+            uint32_t first = uint32_t(codes[k]) << shift, count = 1u << shift;
+            for (uint32_t i = 0; i < count; ++i) out->lut[first + i] = e;
+        } else {  // second level of the code's 9-bit prefix (allocated in code order)
+            const uint32_t pre = uint32_t(codes[k]) >> (lens[k] - kPrimaryBits);
+            if (out->lut[pre] == 0 && n2 < uint32_t(kL2Tables)) out->lut[pre] = uint16_t(kL2Flag | n2++);
+            if (!(out->lut[pre] & kL2Flag)) continue;  // out of second-level tables: maxcode walk
+            const uint32_t shift = 16 - lens[k];
+            const uint32_t first = (uint32_t(codes[k]) << shift) & ((1u << (16 - kPrimaryBits)) - 1);
+            for (uint32_t i = 0; i < (1u << shift); ++i) out->lut2[out->lut[pre] & 0x7FFFu][first + i] = e;
+        }
     }
     return kOk;
 }

@@ -63,6 +63,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void spin_pause() { __nanosleep(32); }
+// griddepcontrol.wait: the predecessor grid (programmatic launch) has completed
+// and its memory is visible; a no-op for ordinary launches
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // largest k < n with first[k] <= g (first[] ascending, first[0] == 0)
 template <class T>
@@ -186,6 +189,7 @@ __device__ __forceinline__ uint32_t movemask4(uint32_t x) { return (x * 0x002040
 // edge chunks a tile shares with its neighbours go byte-wise).
 template <bool DRI, int BPT>
 __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
+    pdl_wait();
     constexpr int kTile = kK0Threads * BPT;
     extern __shared__ __align__(16) uint8_t k0_dyn[];
     uint8_t* s_b = k0_dyn;                 // s_b[16 + i] = raw byte win0 + i; [15] before, [16 + tile] after
@@ -460,6 +464,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff(Params P) {
 // (only the two edge chunks a tile shares with its neighbours go byte-wise).
 template <bool DRI>
 __global__ void __launch_bounds__(kK0Threads) k0_unstuff_small(Params P) {
+    pdl_wait();
     constexpr int kSmallTile = kK0Threads * 16;
     __shared__ uint32_t s_tile;
     // s_b[16 + i] = raw byte win0 + i; s_b[15] = byte before the window,
@@ -704,6 +709,7 @@ __global__ void __launch_bounds__(kK0Threads) k0_unstuff_small(Params P) {
 // and is non-empty, and partitions each interval into ceil(bits / sb)
 // subsequences (y = exclusive prefix; y_n = subsequences in use).
 __global__ void __launch_bounds__(256) k0b_segments(Params P) {
+    pdl_wait();
     __shared__ uint32_t s_w[8];
     __shared__ uint32_t s_carry;
     __shared__ int s_bad;
@@ -894,6 +900,7 @@ __device__ __forceinline__ void set_stage(ImgCtx& ic, const int4* s_stage, const
 __device__ __forceinline__ uint32_t dev_lookup(const DevHuff* t, uint32_t w16, uint32_t& maxlen) {
     maxlen = __ldg(&t->maxlen);
     uint32_t e = __ldg(&t->lut[w16 >> (16 - kPrimaryBits)]);
+    if (e & kL2Flag) return __ldg(&t->lut2[e & 0x7FFFu][w16 & ((1u << (16 - kPrimaryBits)) - 1)]);
     if (e != 0) return e;
     for (uint32_t len = kPrimaryBits + 1; len <= maxlen; ++len) {
         int32_t code = int32_t(w16 >> (16 - len));
@@ -1268,6 +1275,7 @@ struct K1Chain {
 };
 template <bool DRI, bool ST, bool HOP>
 __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
+    pdl_wait();
     constexpr int T = kK1Threads;
     constexpr int TO = kK1Own;
     __shared__ uint64_t s_p[T];
@@ -1517,6 +1525,7 @@ __device__ __forceinline__ void k1c_redo(const Params& P, uint32_t cta, Entry st
 // serial dependency chain, and this kernel's L1 starts cold).
 template <bool ST>
 __global__ void __launch_bounds__(128) k1c_first(Params P) {
+    pdl_wait();
     const uint32_t cta = 1 + blockIdx.x * blockDim.x + threadIdx.x;
     __shared__ int32_t s_acc[3 * 128];
     extern __shared__ uint32_t s_fast_k1c[];
@@ -1539,6 +1548,7 @@ __global__ void __launch_bounds__(128) k1c_first(Params P) {
 
 // Fix-point passes (one CTA): repeat until no boundary is stale.
 __global__ void __launch_bounds__(1024) k1c_fixup(Params P) {
+    pdl_wait();
     constexpr int TO = kK1Own;
     __shared__ int s_any;
     __shared__ int32_t s_acc[3 * 1024];
@@ -1599,6 +1609,7 @@ __device__ __forceinline__ ScanVal scan_op(const ScanVal& a, const ScanVal& b) {
 }
 
 __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
+    pdl_wait();
     constexpr int T = kK2Threads;
     __shared__ uint32_t s_tile;
     __shared__ ScanVal s_w[T / 32];
@@ -2200,6 +2211,7 @@ __device__ void k1x_image(const Params& P, uint32_t k, unsigned long long* red) 
 }
 
 __global__ void __launch_bounds__(kK1xThreads) k1x_exact(Params P) {
+    pdl_wait();
     __shared__ unsigned long long red[kK1xThreads / 32];
     for (uint32_t k = blockIdx.x; k < P.n_img; k += gridDim.x) {
         const ImgState s = P.ist[k];
@@ -2242,7 +2254,8 @@ struct BlockSink {
     static constexpr bool kStore = false;
     __device__ __forceinline__ void sym(uint32_t) {}
     const uint32_t* zt;  // smem, per zig-zag k: column-major index | (column bit | nonDC) << 8
-    const float* wq3[3]; // wq rows of the image's components
+    const float* wqb;    // the batch's wq rows
+    uint64_t qrow;       // per component (21 bits each): its wq row
     int16_t* buf;        // this thread's smem block
     int16_t* coef;       // batch coefficient buffer
     uint2* meta;         // batch per-unit metadata
@@ -2254,7 +2267,7 @@ struct BlockSink {
     uint32_t mflags;     // metadata of the current unit (owned part)
     float mS;
 
-    __device__ __forceinline__ void set_comp(uint32_t comp) { wqc = comp == 0 ? wq3[0] : (comp == 1 ? wq3[1] : wq3[2]); }
+    __device__ __forceinline__ void set_comp(uint32_t comp) { wqc = wqb + 64u * uint32_t((qrow >> (21 * comp)) & 0x1FFFFFu); }
     __device__ __forceinline__ void put(uint32_t k, int32_t v) {
         const uint32_t t = zt[k];
         buf[t & 0xFFu] = int16_t(v);
@@ -2314,6 +2327,7 @@ struct BlockSink {
 
 template <bool ST, bool REPLAY>
 __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
+    pdl_wait();
     __shared__ __align__(16) int16_t s_blk[kK3Threads * kBlkStride];
     __shared__ uint32_t s_zt[64];
     __shared__ float s_wq[kK3SmemQuant * 64];  // the batch's metadata weights when they fit
@@ -2387,9 +2401,8 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     BlockSink sink;
     sink.zt = s_zt;
     {
-        const float* wqb = wq_smem ? s_wq : P.wq;
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) sink.wq3[cc] = wqb + 64u * D.q_tab[cc];
+        sink.wqb = wq_smem ? s_wq : P.wq;
+        sink.qrow = uint64_t(D.q_tab[0]) | (uint64_t(D.q_tab[1]) << 21) | (uint64_t(D.q_tab[2]) << 42);
     }
     sink.buf = buf;
     sink.coef = P.coef;
@@ -2517,7 +2530,7 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
 //     (pipeline.hpp:190-197).  Saturating byte packs, 3 x 32-bit stores per
 //     4 pixels.
 #ifndef PJG_K4_PAIRCOL
-#define PJG_K4_PAIRCOL 1
+#define PJG_K4_PAIRCOL 0
 #endif
 constexpr float kM128 = 12583040.0f;  // 1.5 * 2^23 + 128: round(acc) + 128 in the low mantissa bits
 constexpr int kMagicBits = 0x4B400000;
@@ -2802,7 +2815,7 @@ __device__ __forceinline__ void colour_tile(const WarpImg& I, const uint8_t* pl,
 // store consecutive 16-byte chunks of a row.
 constexpr uint32_t kStgRow = 208;
 #ifndef PJG_K4_STAGE
-#define PJG_K4_STAGE 1
+#define PJG_K4_STAGE 0
 #endif
 template <int HS, bool PAIR>
 __device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl, const ColourLut& L, uint8_t* out,
@@ -2925,6 +2938,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
         s_lut.cr[c] = make_int2(int(uint32_t(qb) << 20) + rb, oR);
     }
     __syncthreads();
+    pdl_wait();  // the LUT and basis above are batch constants
 
     WarpSmem& S = s_w[warp];
     const uint32_t gw = blockIdx.x * kK4Warps + warp, nw = gridDim.x * kK4Warps;
@@ -3391,6 +3405,31 @@ void launch_k5_color(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, uin
 // concurrently, so the cache is keyed by device and guarded by a mutex; the
 // returned value is the kernel's resident CTAs per SM x SMs (0 when the
 // caller did not ask for it).
+// Programmatic dependent launch: a kernel may be scheduled while its
+// predecessor's last CTAs drain; every kernel starts with griddepcontrol.wait
+// (pdl_wait) before touching its predecessors' results, so ordering is that
+// of the stream.  PJG_PDL=0 turns the attribute off.
+static bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("PJG_PDL");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+static void launch_pdl(void (*k)(Params), unsigned grid, unsigned block, size_t smem, cudaStream_t s, const Params& p) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, p);
+}
+
 static int launch_setup(const void* fn, int dyn_smem, int threads, bool want_grid) {
     static std::mutex mu;
     static std::unordered_map<uint64_t, int> done;  // (device, fn) -> grid cap + 1
@@ -3424,25 +3463,25 @@ void launch_k0_unstuff(const Params& p, void* stream) {
     if (p.k0_bpt == 64) {
         if (p.n_dri) {
             launch_setup((const void*)k0_unstuff<true, 64>, dyn, kK0Threads, false);
-            k0_unstuff<true, 64><<<p.k0_tiles, kK0Threads, dyn, s>>>(p);
+            launch_pdl(k0_unstuff<true, 64>, p.k0_tiles, kK0Threads, dyn, s, p);
         } else {
             launch_setup((const void*)k0_unstuff<false, 64>, dyn, kK0Threads, false);
-            k0_unstuff<false, 64><<<p.k0_tiles, kK0Threads, dyn, s>>>(p);
+            launch_pdl(k0_unstuff<false, 64>, p.k0_tiles, kK0Threads, dyn, s, p);
         }
     } else {
         if (p.n_dri)
-            k0_unstuff_small<true><<<p.k0_tiles, kK0Threads, 0, s>>>(p);
+            launch_pdl(k0_unstuff_small<true>, p.k0_tiles, kK0Threads, 0, s, p);
         else
-            k0_unstuff_small<false><<<p.k0_tiles, kK0Threads, 0, s>>>(p);
+            launch_pdl(k0_unstuff_small<false>, p.k0_tiles, kK0Threads, 0, s, p);
     }
 }
 void launch_k0b_segments(const Params& p, void* stream) {
-    if (p.n_dri) k0b_segments<<<p.n_dri, 256, 0, (cudaStream_t)stream>>>(p);
+    if (p.n_dri) launch_pdl(k0b_segments, p.n_dri, 256, 0, (cudaStream_t)stream, p);
 }
 template <bool DRI, bool ST, bool HOP>
 static void launch_k1_variant(const Params& p, size_t dyn, cudaStream_t s) {
     if (ST) launch_setup((const void*)k1_sync<DRI, ST, HOP>, kMaxSmemTables * kFastWords * 4, kK1Threads, false);
-    k1_sync<DRI, ST, HOP><<<p.k1_ctas, kK1Threads, dyn, s>>>(p);
+    launch_pdl(k1_sync<DRI, ST, HOP>, p.k1_ctas, kK1Threads, dyn, s, p);
 }
 template <bool DRI, bool ST>
 static void launch_k1_hop(const Params& p, size_t dyn, cudaStream_t s) {
@@ -3473,23 +3512,23 @@ void launch_k1c_fixup(const Params& p, void* stream) {
         const unsigned grid = (p.k1_ctas - 1 + 127) / 128;
         if (p.n_huff <= kMaxSmemTables) {
             launch_setup((const void*)k1c_first<true>, kMaxSmemTables * kFastWords * 4, 128, false);
-            k1c_first<true><<<grid, 128, size_t(p.n_huff) * kFastWords * 4, (cudaStream_t)stream>>>(p);
+            launch_pdl(k1c_first<true>, grid, 128, size_t(p.n_huff) * kFastWords * 4, (cudaStream_t)stream, p);
         } else {
-            k1c_first<false><<<grid, 128, 0, (cudaStream_t)stream>>>(p);
+            launch_pdl(k1c_first<false>, grid, 128, 0, (cudaStream_t)stream, p);
         }
     }
-    k1c_fixup<<<1, 1024, 0, (cudaStream_t)stream>>>(p);
+    launch_pdl(k1c_fixup, 1, 1024, 0, (cudaStream_t)stream, p);
 }
 void launch_k1x_exact(const Params& p, void* stream) {
-    if (p.n_img) k1x_exact<<<std::min<uint32_t>(p.n_img, 296), kK1xThreads, 0, (cudaStream_t)stream>>>(p);
+    if (p.n_img) launch_pdl(k1x_exact, std::min<uint32_t>(p.n_img, 296), kK1xThreads, 0, (cudaStream_t)stream, p);
 }
 void launch_k2_scan(const Params& p, void* stream) {
-    if (p.k2_tiles) k2_scan<<<p.k2_tiles, kK2Threads, 0, (cudaStream_t)stream>>>(p);
+    if (p.k2_tiles) launch_pdl(k2_scan, p.k2_tiles, kK2Threads, 0, (cudaStream_t)stream, p);
 }
 template <bool ST, bool REPLAY>
 static void launch_k3_variant(const Params& p, unsigned grid, cudaStream_t s) {
     if (ST) launch_setup((const void*)k3_write<ST, REPLAY>, kMaxSmemTables * kFastWords * 4, kK3Threads, false);
-    k3_write<ST, REPLAY><<<grid, kK3Threads, ST ? size_t(p.smem_tables) * kFastWords * 4 : 0, s>>>(p);
+    launch_pdl(k3_write<ST, REPLAY>, grid, kK3Threads, ST ? size_t(p.smem_tables) * kFastWords * 4 : 0, s, p);
 }
 void launch_k3_write(const Params& p, void* stream) {
     if (!p.total_subs) return;
@@ -3506,7 +3545,7 @@ static void launch_k4_variant(const Params& p, cudaStream_t s) {
     const int grid_cap = launch_setup((const void*)k4_transform<LAYOUT>, int(dyn), kK4Threads, true);
     const uint64_t want = (uint64_t(p.k4_tiles) + kK4Threads / 32 - 1) / (kK4Threads / 32);
     const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(grid_cap)));
-    k4_transform<LAYOUT><<<grid, kK4Threads, dyn, s>>>(p);
+    launch_pdl(k4_transform<LAYOUT>, grid, kK4Threads, dyn, s, p);
 }
 void launch_k4_transform(const Params& p, void* stream) {
     if (!p.k4_tiles) return;

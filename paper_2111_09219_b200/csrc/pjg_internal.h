@@ -37,7 +37,9 @@ enum Status : int32_t {
 // ------------------------------------------------------- Huffman tables --
 // Two-level canonical decoder reproducing the reference's flat 2^maxlen LUT
 // (huffman.hpp:60-93, 113-130) bit for bit: a 9-bit primary table resolves
-// codes of length <= 9; longer codes walk per-length maxcode (Annex F.2.2.3).
+// codes of length <= 9; a code of 10..16 bits is found in the 128-entry
+// second-level table of its 9-bit prefix (up to kL2Tables prefixes; beyond
+// that the per-length maxcode walk of Annex F.2.2.3).
 constexpr int kPrimaryBits = 9;
 
 constexpr int kFastBits = 11;
@@ -50,9 +52,13 @@ constexpr uint32_t kFastWords = 1u << kFastBits;
 //   length.  A coefficient is written for DC symbols and for l != 0.
 constexpr uint32_t kFastLShift = 5, kFastTShift = 10, kFastR1Shift = 21, kFastLenShift = 27;
 
+constexpr int kL2Tables = 16;  // second-level tables (codes of 10..16 bits) per Huffman table
+constexpr uint32_t kL2Flag = 0x8000u;
+
 struct DevHuff {
     uint32_t fast[1 << kFastBits];    // code + magnitude in one probe when both fit in kFastBits
-    uint16_t lut[1 << kPrimaryBits];  // (length << 8) | symbol; length 0 = unresolved
+    uint16_t lut[1 << kPrimaryBits];  // (length << 8) | symbol; 0 = unresolved; kL2Flag | k: second level k
+    uint16_t lut2[kL2Tables][1 << (16 - kPrimaryBits)];  // by the 7 bits after a 9-bit prefix of long codes
     int32_t maxcode[18];              // per length 1..16 ([17] unused), -1 when no code has that length
     int32_t valoff[18];               // symbol index = code + valoff[len]
     uint8_t symbols[256];
@@ -66,6 +72,7 @@ static_assert(sizeof(DevHuff) % 16 == 0, "DevHuff must stay 16-byte aligned");
 // the reference's `e.length == 0`.
 PJG_HD uint32_t huff_lookup(const DevHuff& t, uint32_t w16) {
     uint32_t e = t.lut[w16 >> (16 - kPrimaryBits)];
+    if (e & kL2Flag) return t.lut2[e & 0x7FFFu][w16 & ((1u << (16 - kPrimaryBits)) - 1)];
     if (e != 0) return e;
     for (uint32_t len = kPrimaryBits + 1; len <= t.maxlen; ++len) {
         int32_t code = int32_t(w16 >> (16 - len));

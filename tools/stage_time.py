@@ -19,14 +19,22 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 b = dec.batch((blob, offs, sizes), pj.DecodeConfig(restart_intervals=CONFIGS[cfg_key][5] > 0),
               pj.OutputColorspace.RGBInterleaved)
 b.upload()
-runs = []
+runs, steps = [], []
+ext = torch.cuda.ExternalStream(dec.stream(), device=torch.device("cuda", 0))
 for r in range(reps + 3):
     flush.zero_()
     torch.cuda.synchronize()
-    st = b.decode().synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    b.decode()
+    e1.record(ext)
+    st = b.synchronize()
     assert (st == 0).all()
     if r >= 3:
         runs.append(b.stage_times())
+        steps.append(e0.elapsed_time(e1))
 keys = ("unstuff", "sync", "scan", "write", "idct")
-print(json.dumps({"lib": os.environ.get("PJG_LIB", "libpjg.so"), "config": cfg_key,
+env = {k: os.environ[k] for k in ("PJG_GRAPH", "PJG_PDL", "PJG_SB_MIN") if k in os.environ}
+print(json.dumps({"lib": os.environ.get("PJG_LIB", "libpjg.so"), "config": cfg_key, "env": env,
+                  "step_ms": round(float(np.median(steps)), 4),
                   **{k: round(float(np.mean([getattr(x, k) for x in runs])), 4) for k in keys}}))
