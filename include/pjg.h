@@ -190,8 +190,10 @@ int pjg_batch_copy_outputs(pjg_batch* b, void* const* dst, const size_t* caps);
 uint64_t pjg_batch_output_bytes(const pjg_batch* b);
 int pjg_batch_stage_times(const pjg_batch* b, double* ms /* PJG_NUM_STAGES */);
 /* Decode diagnostics: intra rounds (sum, max), inter-CTA hops, fix-up passes,
- * K4 samples replayed in FP64 (near-tie or wide units), K4 units with AC terms. */
-#define PJG_NUM_SYNC_STATS 6
+ * K4 samples replayed in FP64 (near-tie or wide units), K4 units with AC terms,
+ * compact K3->K4 entries written (0 when the batch used the dense buffer),
+ * 1 when the batch used the compact interface. */
+#define PJG_NUM_SYNC_STATS 8
 int pjg_batch_sync_stats(const pjg_batch* b, uint64_t* stats /* PJG_NUM_SYNC_STATS */);
 void pjg_batch_destroy(pjg_batch* b);
 

@@ -440,11 +440,12 @@ class Batch:
         return StageTimings(*[float(v) for v in ms])
 
     def sync_stats(self) -> dict:
-        s = (C.c_uint64 * 6)()
+        s = (C.c_uint64 * 8)()
         self._check(lib().pjg_batch_sync_stats(self._h, s))
         return {"intra_rounds_sum": int(s[0]), "intra_rounds_max": int(s[1]),
                 "inter_hops": int(s[2]), "fixup_passes": int(s[3]),
-                "k4_fp64_replayed_samples": int(s[4]), "k4_ac_units": int(s[5])}
+                "k4_fp64_replayed_samples": int(s[4]), "k4_ac_units": int(s[5]),
+                "compact_entries": int(s[6]), "compact": bool(s[7])}
 
     # ---- parity taps ----------------------------------------------------
     def coefficients(self, i, pre_dc_zigzag=True) -> np.ndarray:

@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(kLayThreads) kp_counts(PlanParams P) {
                     d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
                     c.sub = d.sub_count;
                     c.du = d.expected / 64;
+                    atomicMax(reinterpret_cast<unsigned long long*>(&P.totals->max_du), (unsigned long long)c.du);
                     c.k4t = d.tiles_x * h.mcus_y;
                     c.outb = aup(info.output_bytes, 256);
                 }

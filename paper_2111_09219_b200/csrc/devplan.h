@@ -32,7 +32,7 @@ struct TabRep {
 };
 
 struct PlanTotals {
-    uint64_t sub, du, outb, seg, bits, raw, n_ok;
+    uint64_t sub, du, outb, seg, bits, raw, n_ok, max_du;
     uint32_t k0t, k4t, ndri, all420, n_huff, n_quant;
 };
 

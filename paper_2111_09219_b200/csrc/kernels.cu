@@ -913,6 +913,7 @@ __device__ __forceinline__ uint32_t dev_lookup(const DevHuff* t, uint32_t w16, u
 struct DecState {
     uint64_t p;
     uint32_t n;
+    uint32_t k;  // sync mode: coded coefficients (DC symbols + nonzero AC) — the compact entries K3 writes
     uint32_t c, z;
     bool div;
     bool ovf;  // write mode: a run went past the unit end (z + step > 64): the image needs K1x
@@ -1007,7 +1008,7 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
     wi += 2;
     uint32_t nw = W(wi);  // the word after w1
     uint64_t p = s.p;
-    uint32_t c = s.c, z = s.z, n = 0;
+    uint32_t c = s.c, z = s.z, n = 0, kc = 0;
     int32_t a0 = s.dc0, a1 = s.dc1, a2 = s.dc2;
     uint32_t comp = (ic.duc >> (2 * c)) & 3u;
     uint32_t tdc = comp == 0 ? ic.tdc[0] : (comp == 1 ? ic.tdc[1] : ic.tdc[2]);
@@ -1147,6 +1148,7 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
             nw = W(wi);
             rem -= int32_t(len);
             n += step;
+            if (!Sink::kWrite) kc += coefk;
             z += step;
             if (z >= 64) {
                 if (kRegAcc) {
@@ -1191,6 +1193,7 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
     }
     s.p = p;
     s.n = n;
+    s.k = kc;
     s.c = c;
     s.z = z;
     s.dc0 = a0;
@@ -1202,6 +1205,7 @@ template <class Sink, bool ST = false>
 __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint64_t end_bit, uint32_t cap,
                                              Sink& sink) {
     s.n = 0;
+    s.k = 0;
     s.div = false;
     s.ovf = false;
     s.err = 0;
@@ -1212,10 +1216,13 @@ __device__ __forceinline__ void decode_range(const ImgCtx& ic, DecState& s, uint
         decode_core<Sink, ST, false>(ic, s, end_bit, cap, sink);
 }
 
-__device__ __forceinline__ DcSums pack_dc(int32_t a0, int32_t a1, int32_t a2) {
+// DC sums mod 2^16 per component; the high half of .hi carries the entry
+// count k (<= subsequence bits: every coded coefficient takes >= 1 bit; the
+// compact interface needs sb <= 65535)
+__device__ __forceinline__ DcSums pack_dc(int32_t a0, int32_t a1, int32_t a2, uint32_t k) {
     DcSums d;
     d.lo = (uint32_t(a0) & 0xFFFFu) | (uint32_t(a1) << 16);
-    d.hi = uint32_t(a2) & 0xFFFFu;
+    d.hi = (uint32_t(a2) & 0xFFFFu) | (min(k, 0xFFFFu) << 16);
     return d;
 }
 
@@ -1232,7 +1239,7 @@ __device__ __forceinline__ void sync_decode_sink(const ImgCtx& ic, uint64_t end_
     e.p = s.p;
     e.n = s.n;
     e.czd = pack_czd(s.c, s.z, s.div);
-    d = pack_dc(s.dc0, s.dc1, s.dc2);
+    d = pack_dc(s.dc0, s.dc1, s.dc2, s.k);
 }
 template <bool ST = false>
 __device__ __forceinline__ void sync_decode(const ImgCtx& ic, uint64_t end_bit, uint64_t p, uint32_t c, uint32_t z,
@@ -1595,6 +1602,7 @@ __global__ void __launch_bounds__(1024) k1c_fixup(Params P) {
 struct ScanVal {
     uint64_t n;     // bit 63: segment head
     uint32_t lo, hi;
+    uint32_t ek;    // coded coefficients (compact entries)
 };
 constexpr uint64_t kHead = 1ull << 63;
 
@@ -1605,6 +1613,7 @@ __device__ __forceinline__ ScanVal scan_op(const ScanVal& a, const ScanVal& b) {
     r.n = ((a.n & ~kHead) + b.n) | (a.n & kHead);
     r.lo = __vadd2(a.lo, b.lo);
     r.hi = __vadd2(a.hi, b.hi);
+    r.ek = a.ek + b.ek;
     return r;
 }
 
@@ -1632,15 +1641,16 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
     if (dri) real = P.ist[k].status == 0 && sub_info(P, D, P.ist[k].bit_length, i, si);
     ScanVal v;
     v.n = 0;
-    v.lo = v.hi = 0;
+    v.lo = v.hi = v.ek = 0;
     if (inb) {
         Entry e = P.ent[g];
         DcSums d = P.dcs[g];
         v.n = e.n;
         v.lo = d.lo;
-        v.hi = d.hi;
+        v.hi = d.hi & 0xFFFFu;
+        v.ek = d.hi >> 16;
         if (!dri ? i == 0 : (!real || si.j == 0)) v.n |= kHead;
-        if (!real) v.n = kHead, v.lo = v.hi = 0;
+        if (!real) v.n = kHead, v.lo = v.hi = v.ek = 0;
     }
     // warp inclusive segmented scan
     ScanVal x = v;
@@ -1649,13 +1659,14 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
         y.n = __shfl_up_sync(0xFFFFFFFFu, x.n, o);
         y.lo = __shfl_up_sync(0xFFFFFFFFu, x.lo, o);
         y.hi = __shfl_up_sync(0xFFFFFFFFu, x.hi, o);
+        y.ek = __shfl_up_sync(0xFFFFFFFFu, x.ek, o);
         if (lane >= o) x = scan_op(y, x);
     }
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
     ScanVal wpre;  // exclusive prefix of earlier warps in this tile
     wpre.n = 0;
-    wpre.lo = wpre.hi = 0;
+    wpre.lo = wpre.hi = wpre.ek = 0;
     bool have_wpre = false;
     for (int w = 0; w < warp; ++w) {
         wpre = have_wpre ? scan_op(wpre, s_w[w]) : s_w[w];
@@ -1672,17 +1683,19 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
         uint64_t* agg = P.k2_agg + 8ull * t;
         ScanVal ex;
         ex.n = 0;
-        ex.lo = ex.hi = 0;
+        ex.lo = ex.hi = ex.ek = 0;
         const bool own_prefix = (incl.n & kHead) != 0;
         const bool need = t > 0 && !s_first_head;
         if (own_prefix || !need) {
             agg[4] = incl.n;
             agg[5] = (uint64_t(incl.hi) << 32) | incl.lo;
+            agg[6] = incl.ek;
             __threadfence();
             st_release(P.k2_flag + t, (P.epoch << 2) | 2u);
         } else {
             agg[0] = incl.n;
             agg[1] = (uint64_t(incl.hi) << 32) | incl.lo;
+            agg[2] = incl.ek;
             __threadfence();
             st_release(P.k2_flag + t, (P.epoch << 2) | 1u);
         }
@@ -1701,6 +1714,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
                 uint64_t dd = __ldcg(src + 1);
                 pv.lo = uint32_t(dd);
                 pv.hi = uint32_t(dd >> 32);
+                pv.ek = uint32_t(__ldcg(src + 2));
                 ex = first ? pv : scan_op(pv, ex);
                 first = false;
                 if ((f & 3u) == 2u || (pv.n & kHead)) break;
@@ -1710,6 +1724,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
                 ScanVal ti = scan_op(ex, incl);
                 agg[4] = ti.n;
                 agg[5] = (uint64_t(ti.hi) << 32) | ti.lo;
+                agg[6] = ti.ek;
                 __threadfence();
                 st_release(P.k2_flag + t, (P.epoch << 2) | 2u);
             }
@@ -1727,9 +1742,10 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
         xup.n = __shfl_up_sync(0xFFFFFFFFu, x.n, 1);
         xup.lo = __shfl_up_sync(0xFFFFFFFFu, x.lo, 1);
         xup.hi = __shfl_up_sync(0xFFFFFFFFu, x.hi, 1);
+        xup.ek = __shfl_up_sync(0xFFFFFFFFu, x.ek, 1);
         bool have = false;
         wx.n = 0;
-        wx.lo = wx.hi = 0;
+        wx.lo = wx.hi = wx.ek = 0;
         if (have_wpre) {
             wx = wpre;
             have = true;
@@ -1742,7 +1758,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
     }
     if (v.n & kHead) {
         before.n = 0;
-        before.lo = before.hi = 0;
+        before.lo = before.hi = before.ek = 0;
     }
     // trimmed offsets (offsets(), parallel_decode.hpp:290-316), per segment:
     // a restart interval expects 64 * dpm * (its MCUs) slots at slot base
@@ -1754,6 +1770,7 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
             P.off[g] = 0;
             P.cap[g] = 0;
             P.pred[g] = DcSums{0, 0};
+            if (P.compact) P.eoff[g] = 0;
             return;
         }
         const uint64_t mcus = uint64_t(D.mcus_x) * D.mcus_y;
@@ -1767,6 +1784,8 @@ __global__ void __launch_bounds__(kK2Threads) k2_scan(Params P) {
     const uint64_t o = min(pre, E);
     P.off[g] = base + o;
     P.cap[g] = uint32_t(min(pre + n, E) - o);
+    // entries of a restart interval start at its slot base (entries <= slots)
+    if (P.compact) P.eoff[g] = uint32_t(base) + before.ek;
     DcSums pd;
     pd.lo = before.lo;
     pd.hi = before.hi;
@@ -2198,15 +2217,22 @@ __device__ void k1x_image(const Params& P, uint32_t k, unsigned long long* red) 
         const int16_t* u = coef + d * 64;
         uint32_t flags = 0;
         float S = 0.f;
+        // compact batches: this unit's entries at the fixed slot range [64 d, 64 d + 64)
+        uint32_t* ce = P.compact ? P.ents + (D.du_first + d) * 64 : nullptr;
+        uint32_t ne = 0;
         for (int zz = 0; zz < 64; ++zz) {
             const uint32_t cm = c_zz2c[zz];
             const int32_t v = u[cm];
+            if (ce && (v != 0 || zz == 0)) ce[ne++] = (cm << 16) | (uint32_t(v) & 0xFFFFu);
             if (v != 0) {
                 flags |= (1u << (cm >> 3)) | (zz ? (1u << 8) : 0u) | (1u << (16 + (cm & 7)));
                 S = fmaf(wq[zz], float(abs(v)), S);
             }
         }
-        P.meta[D.du_first + d] = make_uint2(flags, __float_as_uint(S));
+        if (ce)
+            P.umeta[D.du_first + d] = make_uint4(uint32_t(64 * d), uint32_t(64 * d) + ne, flags, __float_as_uint(S));
+        else
+            P.meta[D.du_first + d] = make_uint2(flags, __float_as_uint(S));
     }
 }
 
@@ -2325,10 +2351,72 @@ struct BlockSink {
     }
 };
 
-template <bool ST, bool REPLAY>
+// Compact interface (Params::compact): one 32-bit entry per coded coefficient
+// (col-major index << 16 | value; DC absolute, written even when 0 so that
+// it marks the unit start), written sequentially from the subsequence's
+// entry offset (K2), plus per unit (first entry, end entry, flags, S).  A
+// unit split between subsequences: the DC owner writes the first entry, the
+// thread owning slot 63 the end; flags and S combine through atomics (the
+// metadata buffer is zeroed before K3).  No staging block, no zero slots.
+struct EntrySink {
+    static constexpr bool kWrite = true;
+    static constexpr bool kStore = false;
+    __device__ __forceinline__ void sym(uint32_t) {}
+    const uint32_t* zt;  // smem, per zig-zag k: column-major index | (column bit | nonDC | row bit) << 8
+    const float* wqb;
+    uint64_t qrow;
+    const float* wqc;
+    uint32_t* ent;       // the image's entries (ents + 64 du_first)
+    uint4* um;           // the image's unit metadata
+    uint32_t u;          // image-relative current unit
+    uint32_t pos;        // image-relative next entry
+    uint32_t ustart;     // entry of the current unit's DC (klo == 0)
+    uint64_t slot0;      // image-relative slot of the current unit's first coefficient
+    uint64_t own_hi;     // owned slots end (image-relative)
+    uint32_t klo;        // first owned zig-zag position of the current unit
+    uint32_t mflags;
+    float mS;
+
+    __device__ __forceinline__ void set_comp(uint32_t comp) { wqc = wqb + 64u * uint32_t((qrow >> (21 * comp)) & 0x1FFFFFu); }
+    __device__ __forceinline__ void put(uint32_t k, int32_t v) {
+        const uint32_t t = zt[k];
+        if (k == 0) ustart = pos;
+        ent[pos++] = ((t & 0xFFu) << 16) | (uint32_t(v) & 0xFFFFu);
+        if (v != 0) {
+            mflags |= t >> 8;
+            mS = fmaf(wqc[k], float(abs(v)), mS);
+        }
+    }
+    // the owned part of the current unit ends (complete: through slot 63)
+    __device__ __forceinline__ void close(bool complete) {
+        uint4* m = um + u;
+        if (klo == 0 && complete) {
+            *m = make_uint4(ustart, pos, mflags, __float_as_uint(mS));
+        } else {
+            if (klo == 0) m->x = ustart;
+            if (complete) m->y = pos;
+            if (mflags) atomicOr(&m->z, mflags);
+            if (mS != 0.f) atomicAdd(reinterpret_cast<float*>(&m->w), mS);
+        }
+        mflags = 0;
+        mS = 0.f;
+        klo = 0;
+        ++u;
+        slot0 += 64;
+    }
+    __device__ __forceinline__ void block_end(uint32_t next_comp) {
+        close(true);
+        set_comp(next_comp);
+    }
+    __device__ __forceinline__ void finish() {
+        while (slot0 < own_hi) close(own_hi - slot0 >= 64);
+    }
+};
+
+template <bool ST, bool REPLAY, bool CMP>
 __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     pdl_wait();
-    __shared__ __align__(16) int16_t s_blk[kK3Threads * kBlkStride];
+    __shared__ __align__(16) int16_t s_blk[CMP ? 8 : kK3Threads * kBlkStride];
     __shared__ uint32_t s_zt[64];
     __shared__ float s_wq[kK3SmemQuant * 64];  // the batch's metadata weights when they fit
     const int tid = threadIdx.x;
@@ -2339,8 +2427,8 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     const bool wq_smem = P.n_quant <= kK3SmemQuant;
     if (wq_smem)
         for (uint32_t x = tid; x < P.n_quant * 64; x += kK3Threads) s_wq[x] = P.wq[x];
-    int16_t* buf = s_blk + tid * kBlkStride;
-    {
+    int16_t* buf = s_blk + (CMP ? 0 : tid * kBlkStride);
+    if (!CMP) {
         const int4 zero = make_int4(0, 0, 0, 0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(buf)[q] = zero;
@@ -2356,7 +2444,7 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     const bool active = inb && cap != 0 && P.ist[k].status == 0 && sub_info(P, D, L, i, si);
     extern __shared__ uint32_t s_fast_k3[];
     ImgCtx ic;
-    load_ctx<ST>(P, D, L, ic, ST ? stage_tables(P, s_fast_k3, tid, kK3Threads) : nullptr);
+    load_ctx<ST>(P, D, L, ic, ST ? stage_tables(P, s_fast_k3, tid, kK3Threads, P.k3_tables) : nullptr);
     ic.sacc = nullptr;  // write mode keeps its DC accumulators in registers
     ic.sacc_stride = 0;
     DecState s;
@@ -2398,16 +2486,25 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
     s.dc1 = int16_t(pd.lo >> 16);
     s.dc2 = int16_t(pd.hi & 0xFFFFu);
     const uint64_t o = active ? P.off[g] : 0;
-    BlockSink sink;
+    using Sink = typename std::conditional<CMP, EntrySink, BlockSink>::type;
+    Sink sink;
     sink.zt = s_zt;
     {
         sink.wqb = wq_smem ? s_wq : P.wq;
         sink.qrow = uint64_t(D.q_tab[0]) | (uint64_t(D.q_tab[1]) << 21) | (uint64_t(D.q_tab[2]) << 42);
     }
-    sink.buf = buf;
-    sink.coef = P.coef;
-    sink.meta = P.meta;
-    sink.du = D.du_first + (o >> 6);
+    if constexpr (CMP) {
+        sink.ent = P.ents + D.du_first * 64;
+        sink.um = P.umeta + D.du_first;
+        sink.u = uint32_t(o >> 6);
+        sink.pos = active ? P.eoff[g] : 0u;
+        sink.ustart = 0;
+    } else {
+        sink.buf = buf;
+        sink.coef = P.coef;
+        sink.meta = P.meta;
+        sink.du = D.du_first + (o >> 6);
+    }
     sink.slot0 = o & ~63ull;
     sink.own_hi = o + cap;
     sink.klo = uint32_t(o & 63);
@@ -2490,7 +2587,7 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
         asm volatile("cp.async.wait_all;" ::: "memory");
     }
     if (decode) {
-        decode_range<BlockSink, ST>(ic, s, si.hi, cap, sink);
+        decode_range<Sink, ST>(ic, s, si.hi, cap, sink);
         if (s.ovf) atomicOr(&P.ist[k].exact, kExactFlag);
         if (s.err) {
             set_status(P.ist + k, s.err);  // write mode rethrows (parallel_decode.hpp:142)
@@ -2498,6 +2595,13 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
         }
     }
     if (active) sink.finish();
+    if constexpr (CMP) {
+        if (P.stats) {  // entries written (bench accounting), one atomic per warp
+            const uint32_t m = __activemask();
+            const uint32_t ne = __reduce_add_sync(m, active ? sink.pos - P.eoff[g] : 0u);
+            if ((tid & 31) == __ffs(m) - 1) atomicAdd(P.stats + kStatEntries, (unsigned long long)ne);
+        }
+    }
 }
 
 // ============================================ K4: IDCT + upsample + RGB ====
@@ -2538,6 +2642,8 @@ constexpr int kK4Warps = kK4Threads / 32;
 constexpr int kTileW = 64;  // pixels per tile row
 constexpr int kGroups = kTileW / 4;  // 4-pixel items per tile row
 constexpr int kFS = 68;     // floats per unit in the F tile
+constexpr uint32_t kK4Win = 512;  // compact: entries prefetched per tile (a q75 4:2:0 tile holds ~150)
+constexpr uint32_t kNoWin = 0xFFFFFFFFu;
 // raw staging row of (unit, column v): rows XOR-swizzled so that reading the
 // same column of different units hits different bank groups
 __device__ __forceinline__ uint32_t raw_row(uint32_t blk, uint32_t v) { return blk * 8 + (v ^ (blk & 7u)); }
@@ -2600,11 +2706,16 @@ struct TileWalk {
     uint64_t du_first;
 };
 
+template <bool CMP>
 struct WarpSmem {
     float F[kK4MaxBlocks * kFS];  // dequantised AC units (float, or int32 bits when big), compact order
-    int4 raw[kK4MaxBlocks * 8];   // next tile's coefficients (cp.async staging)
-    uint2 meta[kK4MaxBlocks];     // next tile's per-unit metadata
-    uint8_t pl[1664];             // sample planes (row stride padded by 4): 4:2:0 needs 68x16 + 2 x 36x8
+    int4 raw[CMP ? 1 : kK4MaxBlocks * 8];   // dense: next tile's coefficients (cp.async staging)
+    uint2 meta[CMP ? 1 : kK4MaxBlocks];     // dense: next tile's per-unit metadata
+    uint4 meta4[CMP ? kK4MaxBlocks : 1];    // compact: next tile's (first entry, end entry, flags, S)
+    int32_t dcv[CMP ? kK4MaxBlocks : 1];    // compact: quantised DC of each unit
+    uint32_t ud[CMP ? kK4MaxBlocks : 1];    // compact: per unit F offset (0xFFFF: DC-only) | qf offset << 16 | big << 24
+    __align__(16) uint32_t win[CMP ? kK4Win : 1];  // compact: next tile's entries (cp.async window)
+    __align__(16) uint8_t pl[1664];             // sample planes (row stride padded by 4): 4:2:0 needs 68x16 + 2 x 36x8
     WarpImg img;
     float lim[kK4MaxBlocks];      // per AC unit: 0.5 - error bound
     uint32_t cm[kK4MaxBlocks];    // per AC unit: column mask | big << 8 | row mask << 16
@@ -2898,8 +3009,8 @@ __device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl,
 }
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
-static_assert(sizeof(WarpSmem) * kK4Warps + 4864 + 1024 <= 228 * 1024 / 4, "K4 must fit 4 CTAs per SM");
-static_assert(sizeof(WarpSmem::F) >= 16 * kStgRow, "RGB row staging lives in the F tile");
+static_assert(sizeof(WarpSmem<false>) * kK4Warps + 4864 + 1024 <= 228 * 1024 / 4, "K4 must fit 4 CTAs per SM");
+static_assert(sizeof(WarpSmem<false>::F) >= 16 * kStgRow, "RGB row staging lives in the F tile");
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
     unsigned long long r;
     asm("sub.rn.f32x2 %0, %1, %2;"
@@ -2911,10 +3022,10 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
 // LAYOUT 1: every image of the batch is 4:2:0 colour to RGB — only that colour
 // path is compiled in (a smaller hot loop for the instruction cache: 3.1 K vs
 // 5.2 K instructions, K4 -4 % on cfg 3; a 4:4:4 variant gained nothing); 0: any.
-template <int LAYOUT>
+template <int LAYOUT, bool CMP>
 __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
     extern __shared__ __align__(16) unsigned char k4_dyn[];  // kK4Warps x WarpSmem
-    WarpSmem* s_w = reinterpret_cast<WarpSmem*>(k4_dyn);
+    WarpSmem<CMP>* s_w = reinterpret_cast<WarpSmem<CMP>*>(k4_dyn);
     __shared__ __align__(16) float s_b32[64];   // basis[u][x]
     __shared__ __align__(16) double s_b64[64];
     __shared__ __align__(16) ColourLut s_lut;
@@ -2940,7 +3051,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
     __syncthreads();
     pdl_wait();  // the LUT and basis above are batch constants
 
-    WarpSmem& S = s_w[warp];
+    WarpSmem<CMP>& S = s_w[warp];
     const uint32_t gw = blockIdx.x * kK4Warps + warp, nw = gridDim.x * kK4Warps;
     const uint32_t t_begin = uint32_t(uint64_t(P.k4_tiles) * gw / nw);
     const uint32_t t_end = uint32_t(uint64_t(P.k4_tiles) * (gw + 1) / nw);
@@ -2969,10 +3080,38 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
     uint32_t cached_k = 0xFFFFFFFFu;
     // prefetch of a tile into the warp's smem staging (cp.async, no registers
     // held): 16-byte columns lane, lane+32, lane+64 of its units + metadata
-    auto issue = [&](const TileWalk& tw) {
+    // compact: the window of entries staged with the tile (kNoWin: none)
+    uint32_t win_pend = kNoWin;
+    const uint64_t ent_total = P.total_dus * 64;
+    auto issue = [&](const TileWalk& tw, uint32_t wstart, uint32_t wlen) {
         const uint32_t mx0 = tw.tx * tw.MT;
         const uint32_t nblk = min(tw.MT, tw.mcus_x - mx0) * tw.dpm;
         const uint64_t du0 = tw.du_first + (uint64_t(tw.my) * tw.mcus_x + mx0) * tw.dpm;
+        if (CMP) {
+            win_pend = kNoWin;
+            if (tw.valid) {
+                if (uint32_t(lane) < nblk)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.meta4[lane])),
+                                 "l"(P.umeta + du0 + lane)
+                                 : "memory");
+                if (wstart != kNoWin) {
+                    // the tile's entries start where the previous tile's ended
+                    // (contiguous runs); 16-byte aligned window of kK4Win entries
+                    win_pend = wstart & ~3u;
+                    const uint64_t g0 = tw.du_first * 64 + win_pend;
+#pragma unroll
+                    for (uint32_t j = 0; j < kK4Win / 128; ++j) {
+                        const uint32_t c = lane + 32 * j;
+                        if (4 * c < wlen && g0 + 4 * c + 4 <= ent_total)
+                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.win[4 * c])),
+                                         "l"(P.ents + g0 + 4 * c)
+                                         : "memory");
+                    }
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            return;
+        }
         const int4* src = reinterpret_cast<const int4*>(P.coef + du0 * 64);
         if (tw.valid) {
 #pragma unroll
@@ -2989,13 +3128,16 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    issue(w);
+    issue(w, kNoWin, 0);
     const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t next_wstart = kNoWin;  // compact: where the next tile's entries start (contiguous runs)
+    uint32_t next_wlen = kK4Win;    // compact: entries to stage (twice the current tile's + slack)
     uint32_t n_replay = 0, n_ac = 0;
     for (uint32_t t = t_begin; t < t_end; ++t) {
         const uint32_t cur_k = w.k, cur_my = w.my, cur_mx0 = w.tx * w.MT;
         const uint32_t cur_nm = min(w.MT, w.mcus_x - cur_mx0);
         const uint32_t cur_valid = w.valid, cur_mcuw = w.mcu_w, cur_mcuh = w.mcu_h;
+        const uint64_t cur_du_first = w.du_first;
         const uint32_t nblk = cur_nm * w.dpm;
         if (cur_valid && cached_k != cur_k) {
             __syncwarp();
@@ -3006,11 +3148,22 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
 
         // 1. classify units (K3 metadata: column mask | has-AC << 8 | big << 9, S)
         asm volatile("cp.async.wait_all;" ::: "memory");
+        const uint32_t win_cur = win_pend;
+        next_wstart = kNoWin;
         __syncwarp();
         uint32_t nac = 0, ndc = 0, ndq = 0;
         if (cur_valid) {
             const bool in = uint32_t(lane) < nblk;
-            const uint2 pm = in ? S.meta[lane] : make_uint2(0, 0);
+            uint2 pm;
+            uint32_t e_lo = 0, e_hi = 0;  // compact: the unit's entries
+            if (CMP) {
+                const uint4 m4 = in ? S.meta4[lane] : make_uint4(0, 0, 0, 0);
+                pm = make_uint2(m4.z, m4.w);
+                e_lo = m4.x;
+                e_hi = m4.y;
+            } else {
+                pm = in ? S.meta[lane] : make_uint2(0, 0);
+            }
             const bool isac = in && (pm.x & kMetaNonDc);
             const uint32_t acm = __ballot_sync(0xFFFFFFFFu, isac);
             const uint32_t dcm = __ballot_sync(0xFFFFFFFFu, in && !isac);
@@ -3033,9 +3186,9 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 float4* Fa = reinterpret_cast<float4*>(S.F + a * kFS);
 #pragma unroll
                 for (uint32_t v = 0; v < 8; ++v) {
-                    if ((pm.x >> v) & 1u) {
+                    if (!CMP && ((pm.x >> v) & 1u)) {
                         S.dq[j++] = uint8_t((a << 3) | v);
-                    } else {
+                    } else {  // compact: every column zero-filled, the entries land on top
                         Fa[2 * v] = make_float4(0.f, 0.f, 0.f, 0.f);
                         Fa[2 * v + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
@@ -3058,12 +3211,63 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
             } else if (in) {
                 S.dcl[__popc(dcm & lt_mask)] = uint8_t(lane);
             }
+            if (CMP && in)
+                S.ud[lane] = (isac ? __popc(acm & lt_mask) * kFS : 0xFFFFu) | ((uint32_t(I.bcomp[lane]) * 64u) << 16) |
+                             (isac && __uint_as_float(pm.y) >= 262144.f ? (1u << 24) : 0u);
             __syncwarp();
+            if constexpr (CMP) {
+                // 2a'. scatter the tile's entries into the zeroed F tiles (dequantised;
+                //      exact-FP64 units keep int32 products); DC values for the
+                //      DC-only units.  Entries of consecutive units are contiguous
+                //      (one range, unit = count of DC entries so far) unless a
+                //      restart interval's end or a K1x image breaks the run.
+                const uint32_t* eb = P.ents + cur_du_first * 64;
+                const float* qf0 = &I.qf[0][0];
+                auto scatter = [&](uint32_t u, uint32_t x) {
+                    const uint32_t idx = (x >> 16) & 63u;
+                    const int32_t v = int32_t(int16_t(x & 0xFFFFu));
+                    const uint32_t d = S.ud[u];
+                    const uint32_t fo = d & 0xFFFFu;
+                    if (fo != 0xFFFFu) {
+                        const float q = qf0[((d >> 16) & 0xFFu) + idx];
+                        S.F[fo + idx] = (d >> 24) ? __int_as_float(v * int32_t(q)) : float(v) * q;
+                    } else if (idx == 0) {
+                        S.dcv[u] = v;
+                    }
+                };
+                const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, e_lo, 1);
+                const bool contiguous = __all_sync(0xFFFFFFFFu, uint32_t(lane) + 1 >= nblk || e_hi == nxt);
+                if (contiguous) {
+                    const uint32_t r0 = __shfl_sync(0xFFFFFFFFu, e_lo, 0);
+                    const uint32_t r1 = __shfl_sync(0xFFFFFFFFu, e_hi, (nblk - 1) & 31u);
+                    const uint32_t le_mask = lt_mask | (1u << lane);
+                    uint32_t ubase = 0;
+#pragma unroll 1
+                    for (uint32_t j0 = r0; j0 < r1; j0 += 32) {
+                        const uint32_t jj = j0 + lane;
+                        const bool ok = jj < r1;
+                        const uint32_t x = !ok ? 0u : (jj - win_cur < kK4Win && win_cur != kNoWin) ? S.win[jj - win_cur] : __ldg(eb + jj);
+                        const uint32_t dm = __ballot_sync(0xFFFFFFFFu, ok && ((x >> 16) & 63u) == 0);
+                        const uint32_t u = min(ubase + __popc(dm & le_mask), nblk) - 1;
+                        ubase += __popc(dm);
+                        if (ok && u < nblk) scatter(u, x);
+                    }
+                    next_wstart = r1;
+                    next_wlen = min(kK4Win, 2 * (r1 - r0) + 64);
+                } else {
+#pragma unroll 1
+                    for (uint32_t u = 0; u < nblk; ++u) {
+                        const uint32_t lo = __shfl_sync(0xFFFFFFFFu, e_lo, u), hi = __shfl_sync(0xFFFFFFFFu, e_hi, u);
+                        for (uint32_t jj = lo + lane; jj < hi; jj += 32) scatter(u, __ldg(eb + jj));
+                    }
+                }
+                __syncwarp();
+            }
             // 2a. dequantise the AC units' nonzero columns: coef * Q in FP32 is exact
             //     (|coef * Q| < 2^21 below the exact-FP64 threshold); exact-FP64
             //     units keep the int32 products
 #pragma unroll 1
-            for (uint32_t it = lane; it < ndq; it += 32) {
+            for (uint32_t it = lane; it < (CMP ? 0u : ndq); it += 32) {
                 const uint32_t e = S.dq[it], a = e >> 3, v = e & 7u;
                 const uint32_t blk = S.acl[a];
                 float4* dst = reinterpret_cast<float4*>(S.F + a * kFS + v * 8);
@@ -3103,7 +3307,8 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
 #pragma unroll 1
             for (uint32_t it = lane; it < ndc * 8; it += 32) {
                 const uint32_t blk = S.dcl[it >> 3], x = it & 7;
-                const int32_t F00 = int32_t(int16_t(uint32_t(S.raw[raw_row(blk, 0)].x) & 0xFFFFu)) * int32_t(I.qf[I.bcomp[blk]][0]);
+                const int32_t F00 = (CMP ? S.dcv[blk] : int32_t(int16_t(uint32_t(S.raw[raw_row(blk, 0)].x) & 0xFFFFu))) *
+                                    int32_t(I.qf[I.bcomp[blk]][0]);
                 int o;
                 if ((F00 & 7) != 4)
                     o = (F00 + 4) >> 3;
@@ -3129,7 +3334,8 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 }
             }
             __syncwarp();  // staging consumed by every lane before it is refilled
-            issue(w);
+            // a new image's entries start at its first unit (entry 0)
+            issue(w, w.k == cur_k ? next_wstart : (w.tx == 0 && w.my == 0 ? 0u : kNoWin), next_wlen);
         }
         if (!cur_valid) continue;
 
@@ -3141,6 +3347,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
             const bool act = a < nac;
             const uint32_t cmw = act ? S.cm[a] : 0u;
             const uint32_t ucols = __reduce_or_sync(0xFFFFFFFFu, cmw & 0xFFu);
+            const bool urows_hi = __reduce_or_sync(0xFFFFFFFFu, cmw & 0xF00000u) != 0;
             const float* F = S.F + (act ? a : 0) * kFS;
             float2 acc[8];
 #pragma unroll
@@ -3193,16 +3400,24 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
 #else
             for (uint32_t m = ucols; m; m &= m - 1) {
                 const uint32_t v = __ffs(m) - 1;
+                // column sum over u in two 4-deep chains (u < 4, u >= 4) joined
+                // by one add — the upper chain only when some unit of the pass
+                // has a nonzero F[u >= 4] (warp-uniform).  Any order of k
+                // nonzero terms rounds each at most k times (zero terms and
+                // the join of a zero chain are exact): the bound is unchanged.
                 const float4 f0 = *reinterpret_cast<const float4*>(F + v * 8);
-                const float4 f1 = *reinterpret_cast<const float4*>(F + v * 8 + 4);
                 float2 sv = __fmul2_rn(bq[0], f2(f0.x));
                 sv = __ffma2_rn(bq[1], f2(f0.y), sv);
                 sv = __ffma2_rn(bq[2], f2(f0.z), sv);
                 sv = __ffma2_rn(bq[3], f2(f0.w), sv);
-                sv = __ffma2_rn(bq[4], f2(f1.x), sv);
-                sv = __ffma2_rn(bq[5], f2(f1.y), sv);
-                sv = __ffma2_rn(bq[6], f2(f1.z), sv);
-                sv = __ffma2_rn(bq[7], f2(f1.w), sv);
+                if (urows_hi) {
+                    const float4 f1 = *reinterpret_cast<const float4*>(F + v * 8 + 4);
+                    float2 sh = __fmul2_rn(bq[4], f2(f1.x));
+                    sh = __ffma2_rn(bq[5], f2(f1.y), sh);
+                    sh = __ffma2_rn(bq[6], f2(f1.z), sh);
+                    sh = __ffma2_rn(bq[7], f2(f1.w), sh);
+                    sv = __fadd2_rn(sv, sh);
+                }
                 const float4 b0 = *reinterpret_cast<const float4*>(s_b32 + v * 8);
                 const float4 b1 = *reinterpret_cast<const float4*>(s_b32 + v * 8 + 4);
                 acc[0] = __ffma2_rn(f2(b0.x), sv, acc[0]);
@@ -3337,8 +3552,9 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 }
             }
         } else {
-            // planes (extract_planes, transform.hpp:165-211)
-            const uint32_t nplanes = I.ncomp;
+            // planes (extract_planes, transform.hpp:165-211); Grayscale output
+            // (out_mode 2) is the Y plane alone — its region holds nothing else
+            const uint32_t nplanes = I.out_mode == 2 ? 1u : I.ncomp;
             uint64_t plane_base = I.out_off;
 #pragma unroll
             for (uint32_t c = 0; c < 3; ++c) {
@@ -3525,34 +3741,75 @@ void launch_k1x_exact(const Params& p, void* stream) {
 void launch_k2_scan(const Params& p, void* stream) {
     if (p.k2_tiles) launch_pdl(k2_scan, p.k2_tiles, kK2Threads, 0, (cudaStream_t)stream, p);
 }
-template <bool ST, bool REPLAY>
+template <bool ST, bool REPLAY, bool CMP>
 static void launch_k3_variant(const Params& p, unsigned grid, cudaStream_t s) {
-    if (ST) launch_setup((const void*)k3_write<ST, REPLAY>, kMaxSmemTables * kFastWords * 4, kK3Threads, false);
-    launch_pdl(k3_write<ST, REPLAY>, grid, kK3Threads, ST ? size_t(p.smem_tables) * kFastWords * 4 : 0, s, p);
+    if (ST) launch_setup((const void*)k3_write<ST, REPLAY, CMP>, kMaxSmemTables * kFastWords * 4, kK3Threads, false);
+    launch_pdl(k3_write<ST, REPLAY, CMP>, grid, kK3Threads, ST ? size_t(p.k3_tables) * kFastWords * 4 : 0, s, p);
+}
+template <bool CMP>
+static void launch_k3_cmp(const Params& p, unsigned grid, cudaStream_t s) {
+    if (p.k3_tables)
+        p.sym_cap ? launch_k3_variant<true, true, CMP>(p, grid, s) : launch_k3_variant<true, false, CMP>(p, grid, s);
+    else
+        p.sym_cap ? launch_k3_variant<false, true, CMP>(p, grid, s) : launch_k3_variant<false, false, CMP>(p, grid, s);
 }
 void launch_k3_write(const Params& p, void* stream) {
     if (!p.total_subs) return;
     const unsigned grid = unsigned((p.total_subs + kK3Threads - 1) / kK3Threads);
     cudaStream_t s = (cudaStream_t)stream;
-    if (p.smem_tables)
-        p.sym_cap ? launch_k3_variant<true, true>(p, grid, s) : launch_k3_variant<true, false>(p, grid, s);
-    else
-        p.sym_cap ? launch_k3_variant<false, true>(p, grid, s) : launch_k3_variant<false, false>(p, grid, s);
+    p.compact ? launch_k3_cmp<true>(p, grid, s) : launch_k3_cmp<false>(p, grid, s);
 }
-template <int LAYOUT>
+template <int LAYOUT, bool CMP>
 static void launch_k4_variant(const Params& p, cudaStream_t s) {
-    constexpr size_t dyn = sizeof(WarpSmem) * kK4Warps;
-    const int grid_cap = launch_setup((const void*)k4_transform<LAYOUT>, int(dyn), kK4Threads, true);
+    constexpr size_t dyn = sizeof(WarpSmem<CMP>) * kK4Warps;
+    const int grid_cap = launch_setup((const void*)k4_transform<LAYOUT, CMP>, int(dyn), kK4Threads, true);
     const uint64_t want = (uint64_t(p.k4_tiles) + kK4Threads / 32 - 1) / (kK4Threads / 32);
     const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(grid_cap)));
-    launch_pdl(k4_transform<LAYOUT>, grid, kK4Threads, dyn, s, p);
+    launch_pdl(k4_transform<LAYOUT, CMP>, grid, kK4Threads, dyn, s, p);
 }
 void launch_k4_transform(const Params& p, void* stream) {
     if (!p.k4_tiles) return;
-    if (p.k4_layout == 1)
-        launch_k4_variant<1>(p, (cudaStream_t)stream);
+    const cudaStream_t s = (cudaStream_t)stream;
+    if (p.compact)
+        p.k4_layout == 1 ? launch_k4_variant<1, true>(p, s) : launch_k4_variant<0, true>(p, s);
     else
-        launch_k4_variant<0>(p, (cudaStream_t)stream);
+        p.k4_layout == 1 ? launch_k4_variant<1, false>(p, s) : launch_k4_variant<0, false>(p, s);
+}
+// Compact batches, coefficient dumps only: expand the entries of every image
+// the fast path wrote (not K1x's — those are dense already) into the dense
+// buffer (column-major int16[64], absolute DC), one warp per unit.
+__global__ void k3d_densify(Params P) {
+    const uint64_t w = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (w >= P.total_dus) return;
+    uint32_t lo = 0, hi = P.n_img;  // image of unit w
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (P.img[mid].du_first <= w)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    const ImgDesc& D = P.img[lo];
+    const ImgState st = P.ist[lo];
+    if (st.status != 0 || (st.exact & 2u) || !D.expected) return;
+    const uint64_t d = w - D.du_first;
+    if (d >= D.expected / 64) return;
+    int16_t* dst = P.coef + w * 64;
+    dst[lane] = 0;
+    dst[lane + 32] = 0;
+    __syncwarp();
+    const uint4 m = P.umeta[w];
+    const uint32_t* e = P.ents + D.du_first * 64;
+    for (uint32_t j = m.x + lane; j < m.y; j += 32) {
+        const uint32_t x = e[j];
+        dst[(x >> 16) & 63u] = int16_t(x & 0xFFFFu);
+    }
+}
+void launch_k3d_densify(const Params& p, void* stream) {
+    if (!p.compact || !p.total_dus) return;
+    const uint64_t threads = p.total_dus * 32;
+    k3d_densify<<<unsigned((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(p);
 }
 
 }  // namespace pjg

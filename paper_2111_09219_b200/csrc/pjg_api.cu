@@ -167,7 +167,7 @@ struct pjg_ctx {
     double basis[64];
     cudaEvent_t ev[kNumEvents] = {};
     DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out, segs, sym, tag,
-        counters, k0_flag, k0_agg, k2_flag, k2_agg, stats, plan, meta2;
+        counters, k0_flag, k0_agg, k2_flag, k2_agg, stats, plan, meta2, ents, umeta, eoff;
     HostBuf stage, meta_host, status_host, desc_host, plan_host;
     WorkerPool pool_threads;
     // Per-image host arrays, lent to the live batch and taken back at destroy:
@@ -339,7 +339,8 @@ void pjg_ctx_destroy(pjg_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (DevBuf* b : {&c->raw, &c->ubuf, &c->meta, &c->blkmeta, &c->ent, &c->dcs, &c->off, &c->cap, &c->pred,
                       &c->cta_end, &c->cta_start, &c->k1_flag, &c->coef, &c->out, &c->counters,
-                      &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats, &c->segs, &c->sym, &c->tag, &c->plan, &c->meta2})
+                      &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats, &c->segs, &c->sym, &c->tag, &c->plan, &c->meta2,
+                      &c->ents, &c->umeta, &c->eoff})
         b->release();
     c->stage.release();
     c->meta_host.release();
@@ -406,7 +407,7 @@ uint64_t sb_floor() {
 // parameters need.
 struct PlanSummary {
     size_t n = 0;
-    uint64_t sub = 0, du = 0, outb = 0, seg_total = 0, bits = 0, n_ok = 0, sb = 0, sb_int = 0;
+    uint64_t sub = 0, du = 0, outb = 0, seg_total = 0, bits = 0, n_ok = 0, sb = 0, sb_int = 0, max_du = 0;
     uint32_t k0t = 0, k4t = 0, ndri = 0, n_huff = 0, n_quant = 0, k0_bpt = 0;
     bool all420 = false;
 };
@@ -470,6 +471,21 @@ int finish_plan(pjg_ctx* ctx, pjg_batch* b, const PlanSummary& S, const MetaPtrs
     }
     CU(ctx->k1_flag.ensure((b->k1_ctas + 1) * 4), "cudaMalloc(k1_flag)");
     CU(ctx->coef.ensure(std::max<uint64_t>(S.du, 1) * 128), "cudaMalloc(coef)");
+    // Compact K3 -> K4 interface (Params::compact): per-subsequence entry counts
+    // ride in 16 bits (sb <= 65535) and entry positions are image-relative 32-bit
+    // (64 x the largest image's units < 2^32).  PJG_COMPACT=0 forces the dense
+    // int16 coefficient buffer (A/B, parity).
+    // Measured: compact wins while units are short — K3 drops its
+    // staging block, K4's per-entry scatter stays cheaper than dense column
+    // dequantisation — and loses on long units (q95+ 4:4:4): <= 64 scan bits
+    // per data unit.
+    bool compact = S.sb_int <= 65535 && S.max_du * 64 < (1ull << 32) && S.du && S.bits <= 64 * S.du;
+    if (const char* e = getenv("PJG_COMPACT")) compact = S.sb_int <= 65535 && S.max_du * 64 < (1ull << 32) && atoi(e) != 0;
+    if (compact) {
+        CU(ctx->ents.ensure(std::max<uint64_t>(S.du, 1) * 256), "cudaMalloc(ents)");
+        CU(ctx->umeta.ensure(std::max<uint64_t>(S.du, 1) * 16), "cudaMalloc(umeta)");
+        CU(ctx->eoff.ensure(subs * 4), "cudaMalloc(eoff)");
+    }
     CU(ctx->segs.ensure(std::max<uint64_t>(S.seg_total, 1) * sizeof(uint2)), "cudaMalloc(segs)");
     CU(ctx->blkmeta.ensure(std::max<uint64_t>(S.du, 1) * 8), "cudaMalloc(blkmeta)");
     CU(ctx->out.ensure(std::max<uint64_t>(S.outb, 1)), "cudaMalloc(out)");
@@ -536,6 +552,16 @@ int finish_plan(pjg_ctx* ctx, pjg_batch* b, const PlanSummary& S, const MetaPtrs
     p.tile_first = reinterpret_cast<const uint32_t*>(M.tile);
     p.coef = ctx->coef.as<int16_t>();
     p.meta = ctx->blkmeta.as<uint2>();
+    p.compact = compact ? 1u : 0u;
+    // K3's table probes sit on the decoder's serial chain: compact K3 (69
+    // registers, no staging block) keeps 4 CTAs per SM even with the tables
+    // in shared memory (cfg 3: 1.37 -> 1.27 ms); dense K3 loses occupancy
+    p.k3_tables = (compact && S.n_huff <= kMaxSmemTables) ? S.n_huff : smem_tables;
+    if (const char* e = getenv("PJG_K3_TABLES")) p.k3_tables = (atoi(e) && S.n_huff <= kMaxSmemTables) ? S.n_huff : 0u;
+    p.ents = compact ? ctx->ents.as<uint32_t>() : nullptr;
+    p.umeta = compact ? ctx->umeta.as<uint4>() : nullptr;
+    p.eoff = compact ? ctx->eoff.as<uint32_t>() : nullptr;
+    p.total_dus = S.du;
     p.out = ctx->out.as<uint8_t>();
     p.counters = ctx->counters.as<uint32_t>();
     p.k0_flag = ctx->k0_flag.as<uint32_t>();
@@ -1003,7 +1029,10 @@ int batch_create_impl(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const
         S.n_ok = n_ok;
         S.bits = 0;
         for (size_t i = 0; i < n; ++i)
-            if (b->host_status[i] == kOk) S.bits += desc[i].raw_len * 8;
+            if (b->host_status[i] == kOk) {
+                S.bits += desc[i].raw_len * 8;
+                S.max_du = std::max<uint64_t>(S.max_du, desc[i].expected / 64);
+            }
         S.all420 = cfg->output == PJG_OUT_RGB && n_ok > 0;
         for (size_t i = 0; i < n && S.all420; ++i)
             if (b->host_status[i] == kOk)
@@ -1237,6 +1266,7 @@ int pjg_batch_create_device(pjg_ctx* ctx, const uint8_t* blob, size_t blob_bytes
     S.sb_int = sb_int;
     S.n_ok = T.n_ok;
     S.bits = T.bits;
+    S.max_du = T.max_du;
     S.all420 = T.all420 != 0;
     MetaPtrs M{md + b->m_desc, md + b->m_state, m2 + b->m_huff, m2 + b->m_quant, m2 + b->m_wq,
                md + b->m_basis, md + b->m_k0, md + b->m_tile, md + b->m_sub, m2 + b->m_k0img,
@@ -1338,7 +1368,12 @@ int enqueue_decode(pjg_batch* b, cudaStream_t s) {
     CU(ev(4), "ev");
     launch_k2_scan(b->prm, s);
     CU(ev(5), "ev");
-    if (b->total_dus) CU(cudaMemsetAsync(ctx->blkmeta.p, 0, b->total_dus * 8, s), "memset meta");
+    if (b->total_dus) {
+        if (b->prm.compact)
+            CU(cudaMemsetAsync(ctx->umeta.p, 0, b->total_dus * 16, s), "memset umeta");
+        else
+            CU(cudaMemsetAsync(ctx->blkmeta.p, 0, b->total_dus * 8, s), "memset meta");
+    }
     launch_k3_write(b->prm, s);
     // images whose entropy stage failed (or saw a run past a unit end): the
     // reference's exact semantics at the configured partition (K1x)
@@ -1544,6 +1579,8 @@ int pjg_batch_sync_stats(const pjg_batch* b, uint64_t* stats) {
     stats[3] = b->stats[kStatFixPasses];
     stats[4] = b->stats[kStatReplays];
     stats[5] = b->stats[kStatAcUnits];
+    stats[6] = b->stats[kStatEntries];
+    stats[7] = b->prm.compact;
     return PJG_OK;
 }
 
@@ -1568,6 +1605,8 @@ int pjg_batch_dump_coefficients(const pjg_batch* b, size_t i, int pre_dc_zigzag,
     uint64_t nco = dus * 64;
     if (count < nco) return fail(ctx, PJG_CAPACITY, "coefficient buffer too small");
     if (b->host_status[i] != 0) return b->host_status[i];
+    // compact batches keep no dense coefficients: expand the entries (debug tap)
+    if (b->prm.compact) launch_k3d_densify(b->prm, ctx->stream);
     CU(cudaStreamSynchronize(ctx->stream), "sync");
     std::vector<int16_t> colmaj(nco), raster(nco);
     CU(cudaMemcpy(colmaj.data(), ctx->coef.as<int16_t>() + d.du_first * 64, nco * 2,

@@ -5,6 +5,7 @@
 #include <stdint.h>
 #ifndef __CUDACC__
 struct uint2 { unsigned int x, y; };
+struct uint4 { unsigned int x, y, z, w; };
 #else
 #include <vector_types.h>
 #endif
@@ -223,6 +224,18 @@ struct Params {
     const uint32_t* tile_first;    // n_img + 1 prefix of K4 tiles
     int16_t* coef;                 // 64 int16 per data unit, raster order, absolute DC
     uint2* meta;                   // per data unit: flags (row mask | has-AC | big), S (K3 -> K4)
+    // compact coefficient interface (compact != 0): K3 emits one 32-bit entry
+    // per coded coefficient (every DC, every nonzero AC) instead of 64 int16
+    // slots per unit — col-major index << 16 | uint16 value (DC absolute) —
+    // at ents[64 * du_first + e], e = the image-relative entry position (K1
+    // counts entries per subsequence, K2 scans them into eoff); per unit
+    // umeta = (first entry, end entry, flags, S) relative to 64 * du_first
+    uint32_t* ents;
+    uint4* umeta;
+    uint32_t* eoff;                // per subsequence: first entry (image-relative), K2 -> K3
+    uint32_t compact;
+    uint32_t k3_tables;            // fast tables K3 stages in shared memory (0: global)
+    uint64_t total_dus;
     uint8_t* out;
     // lookback scratch
     uint32_t* counters;            // tickets (reset per run)
@@ -243,6 +256,7 @@ enum StatIndex {
     kStatFixPasses = 3,    // K1c passes that found work
     kStatReplays = 4,      // K4 samples recomputed in exact FP64
     kStatAcUnits = 5,      // K4 data units with AC terms (FP32 IDCT path)
+    kStatEntries = 6,      // compact entries K3 wrote
     kNumStats = 8
 };
 
@@ -256,6 +270,7 @@ void launch_k2_scan(const Params& p, void* stream);
 void launch_k1x_exact(const Params& p, void* stream);
 void launch_k3_write(const Params& p, void* stream);
 void launch_k4_transform(const Params& p, void* stream);
+void launch_k3d_densify(const Params& p, void* stream);  // compact batches: entries -> coef (dumps)
 void launch_k5_color(const uint8_t* y, const uint8_t* cb, const uint8_t* cr, uint32_t W, uint32_t H,
                      uint32_t pw0, uint32_t pw1, uint32_t ph1, uint32_t pw2, uint32_t ph2, uint8_t* out,
                      void* stream);

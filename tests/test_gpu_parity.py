@@ -208,10 +208,13 @@ def test_contiguous_region_unaligned_offsets(decoder):
             assert np.array_equal(got, ref.data), i
 
 
-def test_random_shapes_batch_bit_exact(decoder):
+@pytest.mark.parametrize("compact", ["1", "0"])
+def test_random_shapes_batch_bit_exact(decoder, compact, monkeypatch):
     """A mixed batch of seeded random shapes, samplings and qualities (full
     and partial K4 tiles, 1-3 IDCT passes per tile, FP64 replays) against the
-    reference decoder, RGB bit-exact."""
+    reference decoder, RGB bit-exact — through the compact K3->K4 entry
+    interface and the dense coefficient buffer."""
+    monkeypatch.setenv("PJG_COMPACT", compact)
     rng = np.random.default_rng(2111)
     cases = []
     for k in range(14):
@@ -369,3 +372,40 @@ def C_count(bt):
     n = C.c_size_t()
     pj.lib().pjg_batch_dump_sync_states(bt._h, 0, None, 0, C.byref(n))
     return n.value
+
+
+@pytest.mark.parametrize("compact", ["1", "0"])
+@pytest.mark.parametrize("sb", [128, 1024])
+def test_compact_interface_entropy_and_states(decoder, sb, compact, monkeypatch):
+    """K3 -> K4 through compact entries (K1 entry counts, K2 entry offsets,
+    per-unit entry ranges; coefficients expanded for the dump) or the dense
+    buffer: coefficients, sync states and planes equal the reference on the
+    acceptance corpus (every sampling, 8- and 16-bit tables)."""
+    monkeypatch.setenv("PJG_COMPACT", compact)
+    corpus = acceptance_corpus()
+    files = [f for _, f in corpus]
+    with decoder.batch(files, pj.DecodeConfig(subsequence_bits=sb), pj.OutputColorspace.YCbCrPlanes) as b:
+        st = b.run()
+        assert (st == 0).all(), st
+        outs = b.download()
+        for i, (_, f) in enumerate(corpus):
+            _check_file(b, i, f, sb)
+            ref = Ref.decode(f, rgb=False)
+            assert np.array_equal(outs[i][: ref.data.size], ref.data)
+
+
+def test_grayscale_output_of_colour_files(decoder):
+    """Grayscale output (the Y plane alone, pipeline.hpp Grayscale) of a batch
+    of colour files: each image's region holds exactly its Y plane — the
+    chroma planes must not spill into the next image's region."""
+    files = [ref_jpeg(40 + 8 * k, 24 + 4 * k, 700 + k, 75, ["420", "444", "422"][k % 3]) for k in range(24)]
+    with decoder.batch(files, pj.DecodeConfig(), pj.OutputColorspace.Grayscale) as b:
+        st = b.run()
+        assert (st == 0).all(), st
+        outs = b.download()
+        for i, f in enumerate(files):
+            ref = Ref.decode(f, rgb=False)
+            inf = b.infos[i]
+            y = ref.data[: inf.width * inf.height]
+            assert outs[i].size == y.size, i
+            assert np.array_equal(outs[i], y), i
