@@ -224,6 +224,11 @@ int pjg_debug_device_parse(const uint8_t* file, size_t size, int allow_dri, int6
  * window with it: returns (len << 8) | symbol, 0 = no code, or -(status). */
 int pjg_debug_huff_decode(const uint8_t* counts16, const uint8_t* symbols, size_t nsym,
                           const uint16_t* windows, size_t nwin, uint32_t* out);
+/* The decoder's one-probe fast entry (after the second-level hop for codes
+ * of 12..16 bits) for each 32-bit MSB-first window: the fields
+ * decode_next_symbol needs (pjg_internal.h kFast*), 0 = exact path.  Test hook. */
+int pjg_debug_fast_entry(const uint8_t* counts16, const uint8_t* symbols, size_t nsym, int dc,
+                         const uint32_t* windows, size_t nwin, uint32_t* out);
 
 #ifdef __cplusplus
 }

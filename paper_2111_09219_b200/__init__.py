@@ -217,6 +217,8 @@ def lib():
                                                    C.POINTER(u8p), u8p]
             L.pjg_debug_huff_decode.argtypes = [u8p, u8p, C.c_size_t, C.POINTER(C.c_uint16),
                                                 C.c_size_t, C.POINTER(C.c_uint32)]
+            L.pjg_debug_fast_entry.argtypes = [u8p, u8p, C.c_size_t, C.c_int, C.POINTER(C.c_uint32),
+                                               C.c_size_t, C.POINTER(C.c_uint32)]
             _lib = L
         return _lib
 
@@ -228,7 +230,7 @@ EXPORTED_SYMBOLS = [
     "pjg_batch_info", "pjg_batch_device_output", "pjg_batch_copy_outputs", "pjg_batch_scan_bits", "pjg_batch_kernel_launches", "pjg_batch_download_all", "pjg_batch_download_all_async", "pjg_batch_output_offset", "pjg_batch_output_bytes", "pjg_batch_stage_times",
     "pjg_batch_sync_stats", "pjg_batch_destroy", "pjg_batch_dump_coefficients",
     "pjg_batch_dump_sync_states", "pjg_batch_dump_segment", "pjg_upsample_and_convert",
-    "pjg_debug_huff_decode",
+    "pjg_debug_huff_decode", "pjg_debug_fast_entry",
 ]
 
 

@@ -410,37 +410,32 @@ __global__ void __launch_bounds__(kTabThreads) kp_tables(PlanParams P, TableOut 
                     }
             }
             __syncthreads();
-            // fast table (jfif.cpp build_fast): decode_next_symbol resolved per 11-bit window
+            // fast table (jfif.cpp build_fast): decode_next_symbol resolved per
+            // 11-bit window; prefixes of longer codes get second-level tables
+            // in prefix order (warp 0 numbers them with a ballot scan)
             const bool dc = rep.kind == 0;
             for (uint32_t wv = threadIdx.x; wv < (1u << kFastBits); wv += kTabThreads) {
-                const uint32_t e = huff_lookup(s_t, wv << (16 - kFastBits));
-                const uint32_t clen = e >> 8, sym = e & 255u;
-                uint32_t f = 0;
-                if (clen != 0 && clen <= uint32_t(kFastBits)) {
-                    uint32_t l = 0, run = 0, kind = 0;
-                    bool ok = true;
-                    if (dc) {
-                        l = sym;
-                        ok = l <= 11;
-                    } else {
-                        run = sym >> 4;
-                        l = sym & 15u;
-                        if (l == 0) {
-                            if (run == 0)
-                                kind = 1;
-                            else if (run == 15)
-                                kind = 2;
-                            else
-                                ok = false;
-                        } else if (l > 10) {
-                            ok = false;
-                        }
-                    }
-                    if (ok)
-                        f = clen | (l << kFastLShift) | (((1u << l) - 1u) << kFastTShift) |
-                            ((kind == 1 ? 0u : run + 1u) << kFastR1Shift) | ((clen + l) << kFastLenShift);
+                const int64_t f = fast_primary(s_t, wv, dc);
+                s_t.fast[wv] = f >= 0 ? uint32_t(f) : 0xFFFFFFFFu;
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                uint32_t n2 = 0;
+                for (uint32_t w0 = 0; w0 < (1u << kFastBits); w0 += 32) {
+                    const uint32_t wv = w0 + threadIdx.x;
+                    const bool lng = s_t.fast[wv] == 0xFFFFFFFFu;
+                    const uint32_t m = __ballot_sync(0xFFFFFFFFu, lng);
+                    const uint32_t k2 = n2 + __popc(m & ((1u << threadIdx.x) - 1u));
+                    if (lng) s_t.fast[wv] = k2 < uint32_t(kL2Fast) ? (kFastL2 | (k2 << 10)) : 0u;
+                    n2 += __popc(m);
                 }
-                s_t.fast[wv] = f;
+            }
+            __syncthreads();
+            for (uint32_t x = threadIdx.x; x < uint32_t(kL2Fast) * 32; x += kTabThreads) s_t.fast2[x >> 5][x & 31] = 0;
+            __syncthreads();
+            for (uint32_t x = threadIdx.x; x < (1u << kFastBits) * 32; x += kTabThreads) {
+                const uint32_t wv = x >> 5, f = s_t.fast[wv];
+                if ((f & 0x3FFu) == kFastL2) s_t.fast2[(f >> 10) & 31u][x & 31] = fast_secondary(s_t, wv, x & 31, dc);
             }
             __syncthreads();
             uint4* dst = reinterpret_cast<uint4*>(T.huff + u);

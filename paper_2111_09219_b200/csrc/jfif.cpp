@@ -297,37 +297,18 @@ int32_t build_dev_huff(const HuffSpec& spec, DevHuff* out) {
 // are left to the exact path so its error order is preserved.  `dc` selects
 // the class semantics the table is used with (DC at z == 0, AC otherwise).
 void build_fast(DevHuff* t, bool dc) {
+    uint32_t n2 = 0;
+    std::memset(t->fast2, 0, sizeof(t->fast2));
     for (uint32_t w = 0; w < (1u << kFastBits); ++w) {
-        const uint32_t e = huff_lookup(*t, w << (16 - kFastBits));
-        const uint32_t clen = e >> 8, sym = e & 255u;
-        uint32_t f = 0;
-        if (clen != 0 && clen <= uint32_t(kFastBits)) {
-            uint32_t l = 0, run = 0, kind = 0;
-            bool ok = true;
-            if (dc) {
-                l = sym;
-                ok = l <= 11;
-            } else {
-                run = sym >> 4;
-                l = sym & 15u;
-                if (l == 0) {
-                    if (run == 0)
-                        kind = 1;
-                    else if (run == 15)
-                        kind = 2;
-                    else
-                        ok = false;
-                } else if (l > 10) {
-                    ok = false;
-                }
-            }
-            // layout: pjg_internal.h (kFast*); slots advanced = run + 1, 0 for EOB
-            // (64 - z, known on the device)
-            if (ok)
-                f = clen | (l << kFastLShift) | (((1u << l) - 1u) << kFastTShift) |
-                    ((kind == 1 ? 0u : run + 1u) << kFastR1Shift) | ((clen + l) << kFastLenShift);
+        const int64_t f = fast_primary(*t, w, dc);
+        if (f >= 0) {
+            t->fast[w] = uint32_t(f);
+        } else if (n2 < uint32_t(kL2Fast)) {  // long codes: second level, in prefix order
+            for (uint32_t s = 0; s < 32; ++s) t->fast2[n2][s] = fast_secondary(*t, w, s, dc);
+            t->fast[w] = kFastL2 | (n2++ << 10);
+        } else {
+            t->fast[w] = 0;
         }
-        t->fast[w] = f;
     }
 }
 

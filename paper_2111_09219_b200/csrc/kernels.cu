@@ -993,6 +993,13 @@ __device__ __forceinline__ uint32_t fast_entry(const ImgCtx& ic, uint32_t tsh, u
     return __ldg(ic.fast + fi);
 }
 
+// second-level fast entry (codes of 12..16 bits): global (L1) in both modes
+template <bool ST>
+__device__ __forceinline__ uint32_t fast_entry2(const ImgCtx& ic, uint32_t tb, uint32_t k2, uint32_t s) {
+    if (ST) return __ldg(&ic.huff[tb / kFastWords].fast2[k2][s]);
+    return __ldg(ic.fast + tb + kFastWords + k2 * 32 + s);
+}
+
 template <class Sink, bool ST, bool SW>
 __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint64_t end_bit, uint32_t cap,
                                             Sink& sink) {
@@ -1045,7 +1052,9 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
             }
             const uint32_t win = __funnelshift_l(w1, w0, bp);
             const bool dcs = z == 0;
-            const uint32_t fe = fast_entry<ST>(ic, tsh, (dcs ? tdc : tac) + (win >> (32 - kFastBits)));
+            const uint32_t tb = dcs ? tdc : tac;
+            uint32_t fe = fast_entry<ST>(ic, tsh, tb + (win >> (32 - kFastBits)));
+            if ((fe & 0x3FFu) == kFastL2) fe = fast_entry2<ST>(ic, tb, (fe >> 10) & 31u, (win >> (32 - kFastBits - 5)) & 31u);
             uint32_t len, step, coefk;
             int32_t coef;
             if ((fe & 31u) != 0 && rem >= rthr) {
@@ -2223,7 +2232,7 @@ __device__ void k1x_image(const Params& P, uint32_t k, unsigned long long* red) 
         for (int zz = 0; zz < 64; ++zz) {
             const uint32_t cm = c_zz2c[zz];
             const int32_t v = u[cm];
-            if (ce && (v != 0 || zz == 0)) ce[ne++] = (cm << 16) | (uint32_t(v) & 0xFFFFu);
+            if (ce && (v != 0 || zz == 0)) ce[ne++] = (uint32_t(d & 0xFFu) << 22) | (cm << 16) | (uint32_t(v) & 0xFFFFu);
             if (v != 0) {
                 flags |= (1u << (cm >> 3)) | (zz ? (1u << 8) : 0u) | (1u << (16 + (cm & 7)));
                 S = fmaf(wq[zz], float(abs(v)), S);
@@ -2381,7 +2390,7 @@ struct EntrySink {
     __device__ __forceinline__ void put(uint32_t k, int32_t v) {
         const uint32_t t = zt[k];
         if (k == 0) ustart = pos;
-        ent[pos++] = ((t & 0xFFu) << 16) | (uint32_t(v) & 0xFFFFu);
+        ent[pos++] = ((u & 0xFFu) << 22) | ((t & 0xFFu) << 16) | (uint32_t(v) & 0xFFFFu);
         if (v != 0) {
             mflags |= t >> 8;
             mS = fmaf(wqc[k], float(abs(v)), mS);
@@ -3138,6 +3147,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
         const uint32_t cur_nm = min(w.MT, w.mcus_x - cur_mx0);
         const uint32_t cur_valid = w.valid, cur_mcuw = w.mcu_w, cur_mcuh = w.mcu_h;
         const uint64_t cur_du_first = w.du_first;
+        const uint64_t du_tile0 = w.du_first + (uint64_t(w.my) * w.mcus_x + cur_mx0) * w.dpm;
         const uint32_t nblk = cur_nm * w.dpm;
         if (cur_valid && cached_k != cur_k) {
             __syncwarp();
@@ -3172,12 +3182,14 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
             // nonzero columns of the AC units -> dequantisation work list
             const uint32_t ncol = isac ? __popc(pm.x & 0xFFu) : 0u;
             uint32_t cincl = ncol;
+            if (!CMP) {  // (compact: no dequantisation list, the entries are scattered)
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, cincl, o);
-                if (lane >= o) cincl += x;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t x = __shfl_up_sync(0xFFFFFFFFu, cincl, o);
+                    if (lane >= o) cincl += x;
+                }
+                ndq = __shfl_sync(0xFFFFFFFFu, cincl, 31);
             }
-            ndq = __shfl_sync(0xFFFFFFFFu, cincl, 31);
             if (isac) {
                 const uint32_t a = __popc(acm & lt_mask);
                 // columns: nonzero ones to the list, zero ones zero-filled (the IDCT
@@ -3240,17 +3252,22 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 if (contiguous) {
                     const uint32_t r0 = __shfl_sync(0xFFFFFFFFu, e_lo, 0);
                     const uint32_t r1 = __shfl_sync(0xFFFFFFFFu, e_hi, (nblk - 1) & 31u);
-                    const uint32_t le_mask = lt_mask | (1u << lane);
-                    uint32_t ubase = 0;
+                    // entries carry their unit's index mod 256 (bits 22-29)
+                    const uint32_t ub = uint32_t(du_tile0 - cur_du_first);
+                    if (win_cur != kNoWin && r0 >= win_cur && r1 - win_cur <= kK4Win) {  // all staged
 #pragma unroll 1
-                    for (uint32_t j0 = r0; j0 < r1; j0 += 32) {
-                        const uint32_t jj = j0 + lane;
-                        const bool ok = jj < r1;
-                        const uint32_t x = !ok ? 0u : (jj - win_cur < kK4Win && win_cur != kNoWin) ? S.win[jj - win_cur] : __ldg(eb + jj);
-                        const uint32_t dm = __ballot_sync(0xFFFFFFFFu, ok && ((x >> 16) & 63u) == 0);
-                        const uint32_t u = min(ubase + __popc(dm & le_mask), nblk) - 1;
-                        ubase += __popc(dm);
-                        if (ok && u < nblk) scatter(u, x);
+                        for (uint32_t jj = r0 - win_cur + lane; jj < r1 - win_cur; jj += 32) {
+                            const uint32_t x = S.win[jj];
+                            const uint32_t u = ((x >> 22) - ub) & 0xFFu;
+                            if (u < nblk) scatter(u, x);
+                        }
+                    } else {
+#pragma unroll 1
+                        for (uint32_t jj = r0 + lane; jj < r1; jj += 32) {
+                            const uint32_t x = (jj - win_cur < kK4Win && win_cur != kNoWin) ? S.win[jj - win_cur] : __ldg(eb + jj);
+                            const uint32_t u = ((x >> 22) - ub) & 0xFFu;
+                            if (u < nblk) scatter(u, x);
+                        }
                     }
                     next_wstart = r1;
                     next_wlen = min(kK4Win, 2 * (r1 - r0) + 64);
@@ -3762,7 +3779,13 @@ void launch_k3_write(const Params& p, void* stream) {
 template <int LAYOUT, bool CMP>
 static void launch_k4_variant(const Params& p, cudaStream_t s) {
     constexpr size_t dyn = sizeof(WarpSmem<CMP>) * kK4Warps;
-    const int grid_cap = launch_setup((const void*)k4_transform<LAYOUT, CMP>, int(dyn), kK4Threads, true);
+    int grid_cap = launch_setup((const void*)k4_transform<LAYOUT, CMP>, int(dyn), kK4Threads, true);
+    if (const char* e = getenv("PJG_K4_OCC")) {  // A/B: K4 CTAs per SM (overlap experiments)
+        int sms = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (atoi(e) > 0) grid_cap = std::min(grid_cap, sms * atoi(e));
+    }
     const uint64_t want = (uint64_t(p.k4_tiles) + kK4Threads / 32 - 1) / (kK4Threads / 32);
     const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(grid_cap)));
     launch_pdl(k4_transform<LAYOUT, CMP>, grid, kK4Threads, dyn, s, p);

@@ -475,11 +475,12 @@ int finish_plan(pjg_ctx* ctx, pjg_batch* b, const PlanSummary& S, const MetaPtrs
     // ride in 16 bits (sb <= 65535) and entry positions are image-relative 32-bit
     // (64 x the largest image's units < 2^32).  PJG_COMPACT=0 forces the dense
     // int16 coefficient buffer (A/B, parity).
-    // Measured: compact wins while units are short — K3 drops its
-    // staging block, K4's per-entry scatter stays cheaper than dense column
-    // dequantisation — and loses on long units (q95+ 4:4:4): <= 64 scan bits
-    // per data unit.
-    bool compact = S.sb_int <= 65535 && S.max_du * 64 < (1ull << 32) && S.du && S.bits <= 64 * S.du;
+    // Measured: compact wins while units are short enough — K3
+    // drops its staging block, K4's per-entry scatter costs about what dense
+    // column dequantisation does (cfg 3, 31 bits/unit: step -6 %; cfg 4, 83:
+    // -4 %) — and loses on very long units (q100 4:4:4, 265 bits/unit: +10 %):
+    // <= 128 scan bits per data unit.
+    bool compact = S.sb_int <= 65535 && S.max_du * 64 < (1ull << 32) && S.du && S.bits <= 128 * S.du;
     if (const char* e = getenv("PJG_COMPACT")) compact = S.sb_int <= 65535 && S.max_du * 64 < (1ull << 32) && atoi(e) != 0;
     if (compact) {
         CU(ctx->ents.ensure(std::max<uint64_t>(S.du, 1) * 256), "cudaMalloc(ents)");
@@ -1808,6 +1809,26 @@ int pjg_debug_huff_decode(const uint8_t* counts16, const uint8_t* symbols, size_
     int32_t st = build_dev_huff(s, &d);
     if (st) return -st;
     for (size_t i = 0; i < nwin; ++i) out[i] = huff_lookup(d, windows[i]);
+    return 0;
+}
+
+int pjg_debug_fast_entry(const uint8_t* counts16, const uint8_t* symbols, size_t nsym, int dc,
+                         const uint32_t* windows, size_t nwin, uint32_t* out) {
+    HuffSpec s;
+    std::memcpy(s.counts.data(), counts16, 16);
+    s.symbols.p = symbols;
+    s.symbols.n = uint32_t(nsym);
+    s.present = true;
+    DevHuff d;
+    int32_t st = build_dev_huff(s, &d);
+    if (st) return -st;
+    build_fast(&d, dc != 0);
+    for (size_t i = 0; i < nwin; ++i) {
+        const uint32_t w = windows[i];
+        uint32_t fe = d.fast[w >> (32 - kFastBits)];
+        if ((fe & 0x3FFu) == kFastL2) fe = d.fast2[(fe >> 10) & 31u][(w >> (32 - kFastBits - 5)) & 31u];
+        out[i] = fe;
+    }
     return 0;
 }
 

@@ -52,12 +52,19 @@ constexpr uint32_t kFastWords = 1u << kFastBits;
 //   offset), 21-26 slots advanced (run + 1; 0 = EOB), 27-31 code + magnitude
 //   length.  A coefficient is written for DC symbols and for l != 0.
 constexpr uint32_t kFastLShift = 5, kFastTShift = 10, kFastR1Shift = 21, kFastLenShift = 27;
+// Codes longer than kFastBits: the fast entry of their 11-bit prefix points
+// (kFastL2 | k << 10, clen 0) at second-level table k of 32 entries indexed by
+// the next 5 window bits, same entry format (code lengths 12..16).  Prefixes
+// beyond kL2Fast tables, and invalid windows, keep 0: the exact path.
+constexpr uint32_t kFastL2 = 1u << 9;
+constexpr int kL2Fast = 16;
 
 constexpr int kL2Tables = 16;  // second-level tables (codes of 10..16 bits) per Huffman table
 constexpr uint32_t kL2Flag = 0x8000u;
 
 struct DevHuff {
-    uint32_t fast[1 << kFastBits];    // code + magnitude in one probe when both fit in kFastBits
+    uint32_t fast[1 << kFastBits];    // decode_next_symbol per kFastBits window (codes <= kFastBits bits)
+    uint32_t fast2[kL2Fast][32];      // second level: codes of 12..16 bits
     uint16_t lut[1 << kPrimaryBits];  // (length << 8) | symbol; 0 = unresolved; kL2Flag | k: second level k
     uint16_t lut2[kL2Tables][1 << (16 - kPrimaryBits)];  // by the 7 bits after a 9-bit prefix of long codes
     int32_t maxcode[18];              // per length 1..16 ([17] unused), -1 when no code has that length
@@ -80,6 +87,51 @@ PJG_HD uint32_t huff_lookup(const DevHuff& t, uint32_t w16) {
         if (code <= t.maxcode[len]) return (len << 8) | t.symbols[code + t.valoff[len]];
     }
     return 0;
+}
+
+// Fast entry of one decoded codeword (e = huff_lookup result, clen >= 1):
+// the fields decode_next_symbol needs, or 0 for symbols the reference
+// rejects (they take the exact path for its error order).
+PJG_HD uint32_t fast_fields(uint32_t e, bool dc) {
+    const uint32_t clen = e >> 8, sym = e & 255u;
+    uint32_t l = 0, run = 0, kind = 0;
+    bool ok = true;
+    if (dc) {
+        l = sym;
+        ok = l <= 11;
+    } else {
+        run = sym >> 4;
+        l = sym & 15u;
+        if (l == 0) {
+            if (run == 0)
+                kind = 1;
+            else if (run == 15)
+                kind = 2;
+            else
+                ok = false;
+        } else if (l > 10) {
+            ok = false;
+        }
+    }
+    // slots advanced = run + 1, 0 for EOB (64 - z, known on the device)
+    return ok ? clen | (l << kFastLShift) | (((1u << l) - 1u) << kFastTShift) |
+                    ((kind == 1 ? 0u : run + 1u) << kFastR1Shift) | ((clen + l) << kFastLenShift)
+              : 0u;
+}
+// Entry of window w11 (top kFastBits bits) of a table whose canonical code
+// is set up (lut/lut2/maxcode): a direct entry, 0, or -1 when the prefix
+// belongs to a code longer than kFastBits (needs a second-level table).
+PJG_HD int64_t fast_primary(const DevHuff& t, uint32_t w11, bool dc) {
+    const uint32_t e = huff_lookup(t, w11 << (16 - kFastBits));
+    const uint32_t clen = e >> 8;
+    if (clen == 0) return 0;
+    if (clen > uint32_t(kFastBits)) return -1;
+    return fast_fields(e, dc);
+}
+// Second-level entry for prefix w11 and the next 5 bits s.
+PJG_HD uint32_t fast_secondary(const DevHuff& t, uint32_t w11, uint32_t s, bool dc) {
+    const uint32_t e = huff_lookup(t, (w11 << (16 - kFastBits)) | s);
+    return (e >> 8) ? fast_fields(e, dc) : 0u;
 }
 
 // -------------------------------------------------------------- images --

@@ -107,6 +107,57 @@ def test_two_level_huffman_table_equals_reference_flat_lut():
         assert np.array_equal(got, want), (counts, syms[:8])
 
 
+def _fast_fields(e, dc):
+    """decode_next_symbol's outcome for a decoded codeword e = (len << 8) | sym
+    (huffman.hpp:137-175) packed like pjg_internal.h kFast*; 0 = rejected."""
+    clen, sym = e >> 8, e & 255
+    run = kind = 0
+    if dc:
+        l = sym
+        if l > 11:
+            return 0
+    else:
+        run, l = sym >> 4, sym & 15
+        if l == 0:
+            if run == 0:
+                kind = 1
+            elif run != 15:
+                return 0
+        elif l > 10:
+            return 0
+    return clen | (l << 5) | (((1 << l) - 1) << 10) | ((0 if kind == 1 else run + 1) << 21) | ((clen + l) << 27)
+
+
+def test_fast_entries_with_second_level_equal_reference_decode():
+    """The decoder's one-probe fast entry (11-bit primary, 5-bit second level
+    for codes of 12..16 bits) resolves every 16-bit window like the
+    reference's flat LUT + decode_next_symbol rules, or defers (0) to the
+    exact path — which then sees the same window."""
+    rng = np.random.default_rng(5)
+    tables = annex_k_tables() + [random_canonical(rng) for _ in range(30)]
+    windows = (np.arange(65536, dtype=np.uint32) << 16) | np.uint32(0x5A5A)
+    for counts, syms in tables:
+        st, want, _ = ref_huff_lut16(counts, syms)
+        if st:
+            continue
+        c = np.array(counts, np.uint8)
+        s = np.array(syms if syms else [0], np.uint8)
+        for dc in (0, 1):
+            got = np.zeros(65536, np.uint32)
+            rc = pj.lib().pjg_debug_fast_entry(c.ctypes.data_as(pj.u8p), s.ctypes.data_as(pj.u8p), len(syms), dc,
+                                               windows.ctypes.data_as(pj.C.POINTER(pj.C.c_uint32)), 65536,
+                                               got.ctypes.data_as(pj.C.POINTER(pj.C.c_uint32)))
+            assert rc == 0
+            exp = np.array([_fast_fields(int(e), dc) if (int(e) >> 8) else 0 for e in want], np.uint32)
+            nz = got != 0
+            assert np.array_equal(got[nz], exp[nz]), (counts, dc)
+            # deferrals only where the reference rejects, or prefixes beyond the
+            # second-level capacity (never for the Annex K tables)
+            deferred = np.flatnonzero(~nz & (exp != 0))
+            if (counts, syms) in annex_k_tables():
+                assert deferred.size == 0, (counts, dc, deferred[:5])
+
+
 def test_oversubscribed_table_rejected_like_reference():
     counts = [3] + [0] * 15  # 3 codes of length 1
     st, _, _ = ref_huff_lut16(counts, [1, 2, 3])

@@ -6,7 +6,7 @@ import torch  # noqa: E402
 import paper_2111_09219_b200 as pj  # noqa: E402
 from bench import make_corpus  # noqa: E402
 
-_, blob, offs, sizes = make_corpus("3", 0, pinned=False)
+blob, offs, sizes = make_corpus("3")
 n = len(sizes)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for k in (1, 2, 3, 4, 6):
