@@ -266,6 +266,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-weak", action="store_true", help="skip the N > 1 weak-scaling leg")
     ap.add_argument("--chunk", type=int, default=512, help="images per pipelined e2e chunk")
+    ap.add_argument("--parts", type=int, default=1, help="concurrent parts (contexts) of the device-resident step")
+    ap.add_argument("--record-parts", type=int, default=4,
+                    help="pipelined parts (contexts) of the metric-of-record step")
+    ap.add_argument("--record-parts-device", type=int, default=2,
+                    help="parts of the device-planned record step (each plan reads its totals back)")
     args = ap.parse_args()
     args.steps = max(1, args.steps)
     rank, world, local = dist_env()
@@ -314,19 +319,20 @@ def main():
     pin_t, pblob = pinned_copy(sblob)
     n = len(mine)
 
-    dec = pj.Decoder(local)
-    dec2 = pj.Decoder(local)
-    decs = [dec, dec2]
+    # contexts: the device-resident step uses --parts of them; the metric of
+    # record pipelines --record-parts parts (host plan + H2D of part j+1 under
+    # the decode of part j); e2e rotates chunks over two
+    decs = [pj.Decoder(local) for _ in range(max(2, args.parts, args.record_parts))]
+    dec = decs[0]
     cfg = pj.DecodeConfig(subsequence_bits=args.sb, restart_intervals=RI > 0)
     out_kind = pj.OutputColorspace.RGBInterleaved
     dev = torch.device("cuda", local)
     streams = [torch.cuda.ExternalStream(d.stream(), device=dev) for d in decs]
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    def parts_of(k):  # the shard as k concurrent parts on the two contexts
-        if k <= 1 or n < 2:
-            return [(0, n)]
-        return [(0, n // 2), (n // 2, n)]
+    def parts_of(k):  # the shard as k contiguous parts (one context each)
+        k = max(1, min(k, n))
+        return [(n * j // k, n * (j + 1) // k) for j in range(k)]
 
     trace(f"corpus shared, shard of {n} images")
     # ---- (1) one stream: per-stage CUDA-event times (rooflines)
@@ -353,9 +359,10 @@ def main():
     b.close()
 
     trace("stage runs done")
-    # ---- (2) value: device-resident step, the shard as two concurrent parts
+    # ---- (2) value: device-resident step, the shard as --parts concurrent parts
+    # (1: one stream measured fastest on cfg 3 since round 2's kernels)
     parts = []
-    for (lo, hi), d in zip(parts_of(2), decs):
+    for (lo, hi), d in zip(parts_of(args.parts), decs):
         bb = d.batch((pblob, soffs[lo:hi], ssizes[lo:hi]), cfg, out_kind)
         bb.upload()
         assert (bb.decode().synchronize() == 0).all()
@@ -404,7 +411,7 @@ def main():
     def record_step():
         bs = []
         t0 = time.perf_counter()
-        for (lo, hi), d in zip(parts_of(2), decs):
+        for (lo, hi), d in zip(parts_of(args.record_parts), decs):
             bb = d.batch((pblob, soffs[lo:hi], ssizes[lo:hi]), cfg, out_kind)  # header parse + plan
             bb.upload()  # one H2D of the compressed bytes
             bb.decode()
@@ -419,7 +426,7 @@ def main():
     def record_step_dev():  # the same with the header parse + plan on the device (§8 f4)
         bs = []
         t0 = time.perf_counter()
-        for (lo, hi), d in zip(parts_of(2), decs):
+        for (lo, hi), d in zip(parts_of(args.record_parts_device), decs):
             bb = d.batch((pblob, soffs[lo:hi], ssizes[lo:hi]), cfg, out_kind, device_plan=True)
             bb.decode()
             bs.append(bb)
@@ -474,8 +481,8 @@ def main():
     if world > 1 and batch_mode and not args.no_weak:
         fpin, fblob = pinned_copy(np.asarray(blob, np.uint8))
         wparts = []
-        half = n_all // 2
-        for (lo, hi), d in zip(((0, half), (half, n_all)), decs):
+        kp = max(1, min(args.parts, n_all))
+        for (lo, hi), d in zip([(n_all * j // kp, n_all * (j + 1) // kp) for j in range(kp)], decs):
             bb = d.batch((fblob, offs[lo:hi], sizes[lo:hi]), cfg, out_kind)
             bb.upload()
             assert (bb.decode().synchronize() == 0).all()
@@ -553,7 +560,8 @@ def main():
             "dtype": "u8 in / f64 IDCT+colour / u8 out", "data": "synthetic",
             "config": cfgd,
             "l2": "flushed between steps (256 MB write, untimed)",
-            "sharding": ("the one batch split by compressed bytes (dist.shard_by_bytes), 2 contexts per GPU"
+            "sharding": (f"the one batch split by compressed bytes (dist.shard_by_bytes); per GPU {args.parts} "
+                         f"part(s) for value, {args.record_parts} pipelined parts for the metric of record"
                          if batch_mode else "replicas: every GPU decodes the image"),
             "per_rank_ms": [round(x, 4) for x in per_rank],
             "metric_of_record": {
