@@ -1289,7 +1289,8 @@ struct K1Chain {
     uint32_t czd;
     uint32_t nt;
 };
-template <bool DRI, bool ST, bool HOP>
+// SYM: the batch replays K1's symbols in K3 (Params::sym_cap != 0; never with ST)
+template <bool DRI, bool ST, bool HOP, bool SYM>
 __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
     pdl_wait();
     constexpr int T = kK1Threads;
@@ -1383,15 +1384,15 @@ __global__ void __launch_bounds__(kK1Threads) k1_sync(Params P) {
             const uint64_t gt = uint64_t(cta) * TO + nt - kK1Spec;
             // (small batches, ST: never replayed — the planner enables replay only
             // for large ones; the plain sink also compiles better there)
-            using ChainSink = typename std::conditional<ST, NullSink, SymSink>::type;
+            using ChainSink = typename std::conditional<SYM && !ST, SymSink, NullSink>::type;
             ChainSink ss;
-            if constexpr (!ST) {
+            if constexpr (SYM && !ST) {
                 ss.dst = P.sym + gt;
                 ss.stride = P.sym_stride;
                 ss.cap = owned_t ? P.sym_cap : 0u;
             }
             sync_decode_sink<ST>(ic, s_hi[nt], ch.p, czd_c(ch.czd), czd_z(ch.czd), e2, d2, ss);
-            if constexpr (!ST)
+            if constexpr (SYM && !ST)
                 if (P.sym_cap && owned_t)
                 reinterpret_cast<uint4*>(P.tag)[gt] =
                     make_tag(ch.p, czd_c(ch.czd), czd_z(ch.czd), ss.n,
@@ -3091,6 +3092,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
     // held): 16-byte columns lane, lane+32, lane+64 of its units + metadata
     // compact: the window of entries staged with the tile (kNoWin: none)
     uint32_t win_pend = kNoWin;
+    uint32_t win_len_pend = 0;  // entries the window holds (only these may be read from it)
     const uint64_t ent_total = P.total_dus * 64;
     auto issue = [&](const TileWalk& tw, uint32_t wstart, uint32_t wlen) {
         const uint32_t mx0 = tw.tx * tw.MT;
@@ -3098,6 +3100,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
         const uint64_t du0 = tw.du_first + (uint64_t(tw.my) * tw.mcus_x + mx0) * tw.dpm;
         if (CMP) {
             win_pend = kNoWin;
+            win_len_pend = 0;
             if (tw.valid) {
                 if (uint32_t(lane) < nblk)
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.meta4[lane])),
@@ -3108,10 +3111,12 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                     // (contiguous runs); 16-byte aligned window of kK4Win entries
                     win_pend = wstart & ~3u;
                     const uint64_t g0 = tw.du_first * 64 + win_pend;
+                    const uint64_t avail = ent_total > g0 ? (ent_total - g0) & ~3ull : 0ull;
+                    win_len_pend = uint32_t(min64(min64((wstart - win_pend + wlen + 3) & ~3u, kK4Win), avail));
 #pragma unroll
                     for (uint32_t j = 0; j < kK4Win / 128; ++j) {
                         const uint32_t c = lane + 32 * j;
-                        if (4 * c < wlen && g0 + 4 * c + 4 <= ent_total)
+                        if (4 * c < win_len_pend)
                             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&S.win[4 * c])),
                                          "l"(P.ents + g0 + 4 * c)
                                          : "memory");
@@ -3158,7 +3163,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
 
         // 1. classify units (K3 metadata: column mask | has-AC << 8 | big << 9, S)
         asm volatile("cp.async.wait_all;" ::: "memory");
-        const uint32_t win_cur = win_pend;
+        const uint32_t win_cur = win_pend, win_len = win_len_pend;
         next_wstart = kNoWin;
         __syncwarp();
         uint32_t nac = 0, ndc = 0, ndq = 0;
@@ -3179,6 +3184,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
             const uint32_t dcm = __ballot_sync(0xFFFFFFFFu, in && !isac);
             nac = __popc(acm);
             ndc = __popc(dcm);
+            const uint32_t a_slot = __popc(acm & lt_mask);
             // nonzero columns of the AC units -> dequantisation work list
             const uint32_t ncol = isac ? __popc(pm.x & 0xFFu) : 0u;
             uint32_t cincl = ncol;
@@ -3191,7 +3197,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 ndq = __shfl_sync(0xFFFFFFFFu, cincl, 31);
             }
             if (isac) {
-                const uint32_t a = __popc(acm & lt_mask);
+                const uint32_t a = a_slot;
                 // columns: nonzero ones to the list, zero ones zero-filled (the IDCT
                 // reads every column any unit of its pass uses)
                 uint32_t j = cincl - ncol;
@@ -3224,7 +3230,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                 S.dcl[__popc(dcm & lt_mask)] = uint8_t(lane);
             }
             if (CMP && in)
-                S.ud[lane] = (isac ? __popc(acm & lt_mask) * kFS : 0xFFFFu) | ((uint32_t(I.bcomp[lane]) * 64u) << 16) |
+                S.ud[lane] = (isac ? a_slot * kFS : 0xFFFFu) | ((uint32_t(I.bcomp[lane]) * 64u) << 16) |
                              (isac && __uint_as_float(pm.y) >= 262144.f ? (1u << 24) : 0u);
             __syncwarp();
             if constexpr (CMP) {
@@ -3254,7 +3260,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                     const uint32_t r1 = __shfl_sync(0xFFFFFFFFu, e_hi, (nblk - 1) & 31u);
                     // entries carry their unit's index mod 256 (bits 22-29)
                     const uint32_t ub = uint32_t(du_tile0 - cur_du_first);
-                    if (win_cur != kNoWin && r0 >= win_cur && r1 - win_cur <= kK4Win) {  // all staged
+                    if (win_cur != kNoWin && r0 >= win_cur && r1 - win_cur <= win_len) {  // all staged
 #pragma unroll 1
                         for (uint32_t jj = r0 - win_cur + lane; jj < r1 - win_cur; jj += 32) {
                             const uint32_t x = S.win[jj];
@@ -3264,7 +3270,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                     } else {
 #pragma unroll 1
                         for (uint32_t jj = r0 + lane; jj < r1; jj += 32) {
-                            const uint32_t x = (jj - win_cur < kK4Win && win_cur != kNoWin) ? S.win[jj - win_cur] : __ldg(eb + jj);
+                            const uint32_t x = (jj - win_cur < win_len && win_cur != kNoWin) ? S.win[jj - win_cur] : __ldg(eb + jj);
                             const uint32_t u = ((x >> 22) - ub) & 0xFFu;
                             if (u < nblk) scatter(u, x);
                         }
@@ -3713,8 +3719,11 @@ void launch_k0b_segments(const Params& p, void* stream) {
 }
 template <bool DRI, bool ST, bool HOP>
 static void launch_k1_variant(const Params& p, size_t dyn, cudaStream_t s) {
-    if (ST) launch_setup((const void*)k1_sync<DRI, ST, HOP>, kMaxSmemTables * kFastWords * 4, kK1Threads, false);
-    launch_pdl(k1_sync<DRI, ST, HOP>, p.k1_ctas, kK1Threads, dyn, s, p);
+    if (ST) launch_setup((const void*)k1_sync<DRI, ST, HOP, false>, kMaxSmemTables * kFastWords * 4, kK1Threads, false);
+    if (!ST && p.sym_cap)
+        launch_pdl(k1_sync<DRI, false, HOP, true>, p.k1_ctas, kK1Threads, dyn, s, p);
+    else
+        launch_pdl(k1_sync<DRI, ST, HOP, false>, p.k1_ctas, kK1Threads, dyn, s, p);
 }
 template <bool DRI, bool ST>
 static void launch_k1_hop(const Params& p, size_t dyn, cudaStream_t s) {

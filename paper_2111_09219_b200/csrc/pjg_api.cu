@@ -402,6 +402,24 @@ uint64_t sb_floor() {
     return (v >= 32 && v % 32 == 0) ? uint64_t(v) : 64u;  // cfg 1: 256 -> 64 bits: 0.19 -> 0.157 ms
 }
 
+// Internal subsequence size: halve sb while the batch would give K1 fewer than
+// `target` subsequences (default: half the GPU's K1 threads at one CTA per SM;
+// PJG_SB_TARGET overrides, PJG_SB_AUTO=0 disables).  Restart-interval batches
+// keep sb (their per-interval partitions are dumped as is).
+uint64_t internal_sb(uint64_t sb, uint64_t bits, bool allowed) {
+    uint64_t sb_int = sb;
+    const char* e = getenv("PJG_SB_AUTO");
+    if (!allowed || (e && atoi(e) == 0)) return sb;
+    uint64_t target = uint64_t(kK1Threads) * 148 / 2;
+    if (const char* t = getenv("PJG_SB_TARGET")) target = std::max<long>(1, atol(t));
+    uint64_t est = bits / sb;
+    while (est < target && sb_int / 2 >= sb_floor() && (sb_int / 2) % 32 == 0) {
+        sb_int /= 2;
+        est *= 2;
+    }
+    return sb_int;
+}
+
 // Per-batch totals of a plan (host planner or devplan.cu) and where its
 // device-side tables live: everything the buffer reservation and the kernel
 // parameters need.
@@ -459,7 +477,10 @@ int finish_plan(pjg_ctx* ctx, pjg_batch* b, const PlanSummary& S, const MetaPtrs
         // (and large images: a few subsequences per image keep K3 cheap)
         // (large batches only: K1's shared-memory-table variant for small ones
         // does not keep symbols)
-        replay_on = per_du >= 64 && per_du <= 160 && S.n_ok && S.sub / S.n_ok >= 64 && !st_tables;
+        // (dense interface only: with the compact one K3 is cheap enough that
+        // K1's symbol stores cost more than the replay saves — cfg 4: step 5.97
+        // ms with replay, 5.60 without)
+        replay_on = per_du > 128 && per_du <= 160 && S.n_ok && S.sub / S.n_ok >= 64 && !st_tables;
         if (const char* e = getenv("PJG_REPLAY")) replay_on = atoi(e) != 0 && !st_tables;
         if (getenv("PJG_NO_REPLAY")) replay_on = false;
     }
@@ -768,17 +789,7 @@ int batch_create_impl(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const
     // the internal size, and the sync-state dump aggregates back to the
     // configured partition.  Restart-interval batches keep sb (their
     // per-interval partitions are dumped as is).  PJG_SB_AUTO=0 turns it off.
-    uint64_t sb_int = sb;
-    {
-        const char* e = getenv("PJG_SB_AUTO");
-        if (!n_dri && !(e && atoi(e) == 0)) {
-            uint64_t est = raw_sum * 8 / sb;
-            while (est < uint64_t(kK1Threads) * 148 / 2 && sb_int / 2 >= sb_floor() && (sb_int / 2) % 32 == 0) {
-                sb_int /= 2;
-                est *= 2;
-            }
-        }
-    }
+    const uint64_t sb_int = internal_sb(sb, raw_sum * 8, n_dri == 0);
     b->sb_int = sb_int;
     // K0 tile size: 32 KB windows when the scans are large on average, else 8 KB
     uint32_t k0_bpt = (n_ok && raw_sum / n_ok >= 48 * 1024) ? kK0BigBpt : kK0SmallBpt;
@@ -1100,17 +1111,7 @@ int pjg_batch_create_device(pjg_ctx* ctx, const uint8_t* blob, size_t blob_bytes
     b->info.resize(n);
     // the host planner's heuristics on the files' bytes (scans are ~all of them)
     const uint64_t sb = cfg->subsequence_bits;
-    uint64_t sb_int = sb;
-    {
-        const char* e = getenv("PJG_SB_AUTO");
-        if (!cfg->restart_intervals && !(e && atoi(e) == 0)) {
-            uint64_t est = tot * 8 / sb;
-            while (est < uint64_t(kK1Threads) * 148 / 2 && sb_int / 2 >= sb_floor() && (sb_int / 2) % 32 == 0) {
-                sb_int /= 2;
-                est *= 2;
-            }
-        }
-    }
+    const uint64_t sb_int = internal_sb(sb, tot * 8, !cfg->restart_intervals);
     uint32_t k0_bpt = (n && tot / n >= 48 * 1024) ? kK0BigBpt : kK0SmallBpt;
     if (const char* e = getenv("PJG_K0_BPT")) k0_bpt = atoi(e) == int(kK0BigBpt) ? kK0BigBpt : kK0SmallBpt;
 

@@ -409,3 +409,24 @@ def test_grayscale_output_of_colour_files(decoder):
             y = ref.data[: inf.width * inf.height]
             assert outs[i].size == y.size, i
             assert np.array_equal(outs[i], y), i
+
+
+@pytest.mark.parametrize("compact", ["1", "0"])
+def test_alternating_density_batch(decoder, compact, monkeypatch):
+    """Files alternating between very sparse (q20) and very dense (q100) scans,
+    so that consecutive K4 tiles of a warp differ by 10x in coded coefficients:
+    the compact interface's per-tile entry window (sized from the previous
+    tile) must fall back to global reads for whatever it did not stage."""
+    monkeypatch.setenv("PJG_COMPACT", compact)
+    files = []
+    for k in range(24):
+        s = ["444", "420", "gray"][k % 3]
+        files.append(ref_jpeg(72 + 8 * (k % 5), 40 + 8 * (k % 3), 900 + k, 20 if k % 2 else 100, s))
+    with decoder.batch(files, pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved) as b:
+        st = b.run()
+        assert (st == 0).all(), st
+        outs = b.download()
+        for i, f in enumerate(files):
+            ref = Ref.decode(f, rgb=True)
+            got = _rgb(outs[i], b.infos[i])
+            assert np.array_equal(got, ref.data), (i, int((got != ref.data).sum()))

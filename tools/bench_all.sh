@@ -4,7 +4,7 @@
 # line.  Parity of every point is the GPU test suite's job
 # (tests/test_gpu_configs.py); the CPU baseline runs on the DRI-free points.
 out=${1:-gpurun_out/bench_all.jsonl}
-: > $out
+mkdir -p "$(dirname "$out")"; : > $out
 for c in 1 2 4 3; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 >> $out 2> ${out%.jsonl}_$c.err || echo "{\"config\": \"$c\", \"failed\": true}" >> $out
 done

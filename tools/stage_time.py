@@ -34,7 +34,8 @@ for r in range(reps + 3):
         runs.append(b.stage_times())
         steps.append(e0.elapsed_time(e1))
 keys = ("unstuff", "sync", "scan", "write", "idct")
-env = {k: os.environ[k] for k in ("PJG_GRAPH", "PJG_PDL", "PJG_SB_MIN") if k in os.environ}
+env = {k: v for k, v in os.environ.items() if k.startswith("PJG_")}
 print(json.dumps({"lib": os.environ.get("PJG_LIB", "libpjg.so"), "config": cfg_key, "env": env,
                   "step_ms": round(float(np.median(steps)), 4),
-                  **{k: round(float(np.mean([getattr(x, k) for x in runs])), 4) for k in keys}}))
+                  **{k: round(float(np.mean([getattr(x, k) for x in runs])), 4) for k in keys},
+                  "stats": b.sync_stats()}))
