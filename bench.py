@@ -334,6 +334,7 @@ def main():
         k = max(1, min(k, n))
         return [(n * j // k, n * (j + 1) // k) for j in range(k)]
 
+
     trace(f"corpus shared, shard of {n} images")
     # ---- (1) one stream: per-stage CUDA-event times (rooflines)
     b = dec.batch((pblob, soffs, ssizes), cfg, out_kind)

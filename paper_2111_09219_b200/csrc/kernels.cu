@@ -924,6 +924,7 @@ struct DecState {
 struct NullSink {
     static constexpr bool kWrite = false;
     static constexpr bool kStore = false;
+    static constexpr bool kSmemAcc = true;
     __device__ __forceinline__ void put(uint32_t, int32_t) {}
     __device__ __forceinline__ void block_end(uint32_t) {}
     __device__ __forceinline__ void sym(uint32_t) {}
@@ -939,6 +940,7 @@ struct NullSink {
 struct SymSink {
     static constexpr bool kWrite = false;
     static constexpr bool kStore = true;
+    static constexpr bool kSmemAcc = true;
     uint16_t* dst;     // &sym[g]
     uint64_t stride;   // subsequences per symbol row
     uint32_t cap;
@@ -1024,7 +1026,7 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
     // per block) updates the current component's, and a block end only moves
     // the address.  Write mode needs each absolute DC at once (the sink): the
     // current component's accumulator is a register, swapped at block ends.
-    constexpr bool kRegAcc = Sink::kWrite;
+    constexpr bool kRegAcc = Sink::kWrite && !Sink::kSmemAcc;
     int32_t* const sa0 = ic.sacc;
     const uint32_t sst = ic.sacc_stride;
     if (!kRegAcc) {
@@ -2288,6 +2290,7 @@ constexpr uint32_t kMetaNonDc = 1u << 8;
 struct BlockSink {
     static constexpr bool kWrite = true;
     static constexpr bool kStore = false;
+    static constexpr bool kSmemAcc = false;  // DC accumulators in registers, swapped at block ends
     __device__ __forceinline__ void sym(uint32_t) {}
     const uint32_t* zt;  // smem, per zig-zag k: column-major index | (column bit | nonDC) << 8
     const float* wqb;    // the batch's wq rows
@@ -2371,6 +2374,7 @@ struct BlockSink {
 struct EntrySink {
     static constexpr bool kWrite = true;
     static constexpr bool kStore = false;
+    static constexpr bool kSmemAcc = false;  // (shared-memory accumulators measured slower: write 1.20 -> 1.25 ms)
     __device__ __forceinline__ void sym(uint32_t) {}
     const uint32_t* zt;  // smem, per zig-zag k: column-major index | (column bit | nonDC | row bit) << 8
     const float* wqb;
@@ -3770,7 +3774,10 @@ void launch_k2_scan(const Params& p, void* stream) {
 template <bool ST, bool REPLAY, bool CMP>
 static void launch_k3_variant(const Params& p, unsigned grid, cudaStream_t s) {
     if (ST) launch_setup((const void*)k3_write<ST, REPLAY, CMP>, kMaxSmemTables * kFastWords * 4, kK3Threads, false);
-    launch_pdl(k3_write<ST, REPLAY, CMP>, grid, kK3Threads, ST ? size_t(p.k3_tables) * kFastWords * 4 : 0, s, p);
+    size_t dyn = ST ? size_t(p.k3_tables) * kFastWords * 4 : 0;
+    if (const char* e = getenv("PJG_K3_EXTRA_SMEM"))  // A/B: occupancy experiments (bytes)
+        if (ST) dyn = std::min<size_t>(dyn + size_t(atol(e)), kMaxSmemTables * kFastWords * 4);
+    launch_pdl(k3_write<ST, REPLAY, CMP>, grid, kK3Threads, dyn, s, p);
 }
 template <bool CMP>
 static void launch_k3_cmp(const Params& p, unsigned grid, cudaStream_t s) {
@@ -3796,7 +3803,9 @@ static void launch_k4_variant(const Params& p, cudaStream_t s) {
         if (atoi(e) > 0) grid_cap = std::min(grid_cap, sms * atoi(e));
     }
     const uint64_t want = (uint64_t(p.k4_tiles) + kK4Threads / 32 - 1) / (kK4Threads / 32);
-    const unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(grid_cap)));
+    unsigned grid = unsigned(std::min<uint64_t>(want, uint64_t(grid_cap)));
+    if (const char* e = getenv("PJG_K4_TPW"))  // A/B: tiles per warp (non-persistent grid, waves)
+        if (atoi(e) > 0) grid = unsigned(std::max<uint64_t>(1, (want + atoi(e) - 1) / atoi(e)));
     launch_pdl(k4_transform<LAYOUT, CMP>, grid, kK4Threads, dyn, s, p);
 }
 void launch_k4_transform(const Params& p, void* stream) {

@@ -9,7 +9,7 @@ from bench import make_corpus  # noqa: E402
 blob, offs, sizes = make_corpus("3")
 n = len(sizes)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for k in (1, 2, 3, 4, 6):
+for k in (1, 2, 4, 8):
     decs = [pj.Decoder(0) for _ in range(k)]
     parts = []
     for j in range(k):
