@@ -231,6 +231,25 @@ inline DecodeSuccess decode_single(std::span<const uint8_t> file_bytes, const De
     return std::move(std::get<DecodeSuccess>(r[0]));
 }
 
+// decode_single + upsample_and_convert in one pass (an extension, not in the
+// reference API): the fused K4 writes interleaved RGB directly, no planes
+// round trip through the host.  Same output as
+// upsample_and_convert(decode_single(file, config).planes).
+inline RgbImage decode_rgb(std::span<const uint8_t> file_bytes, const DecodeConfig& config) {
+    pjg_image_info info;
+    if (int st = pjg_inspect(file_bytes.data(), file_bytes.size(), PJG_OUT_RGB, &info)) detail::raise(st, "decode_rgb");
+    RgbImage img;
+    img.width = info.width;
+    img.height = info.height;
+    img.channels = info.channels;
+    img.pixels.resize(info.output_bytes);
+    const pjg_config cfg = detail::to_c(config, PJG_OUT_RGB);
+    int st = pjg_decode(detail::context(), file_bytes.data(), file_bytes.size(), &cfg, &info, img.pixels.data(),
+                        img.pixels.size());
+    if (st) detail::raise(st, "decode_rgb");
+    return img;
+}
+
 // upsample_and_convert (pipeline.hpp:167-201) on the GPU.
 inline RgbImage upsample_and_convert(const ImagePlanes& planes) {
     RgbImage img;

@@ -167,7 +167,7 @@ struct pjg_ctx {
     double basis[64];
     cudaEvent_t ev[kNumEvents] = {};
     DevBuf raw, ubuf, meta, blkmeta, ent, dcs, off, cap, pred, cta_end, cta_start, k1_flag, coef, out, segs, sym, tag,
-        counters, k0_flag, k0_agg, k2_flag, k2_agg, stats, plan, meta2, ents, umeta, eoff;
+        counters, k0_flag, k0_agg, k2_flag, k2_agg, stats, plan, meta2, ents, umeta, eoff, k5tmp;
     HostBuf stage, meta_host, status_host, desc_host, plan_host;
     WorkerPool pool_threads;
     // Per-image host arrays, lent to the live batch and taken back at destroy:
@@ -340,7 +340,7 @@ void pjg_ctx_destroy(pjg_ctx* c) {
     for (DevBuf* b : {&c->raw, &c->ubuf, &c->meta, &c->blkmeta, &c->ent, &c->dcs, &c->off, &c->cap, &c->pred,
                       &c->cta_end, &c->cta_start, &c->k1_flag, &c->coef, &c->out, &c->counters,
                       &c->k0_flag, &c->k0_agg, &c->k2_flag, &c->k2_agg, &c->stats, &c->segs, &c->sym, &c->tag, &c->plan, &c->meta2,
-                      &c->ents, &c->umeta, &c->eoff})
+                      &c->ents, &c->umeta, &c->eoff, &c->k5tmp})
         b->release();
     c->stage.release();
     c->meta_host.release();
@@ -1757,9 +1757,9 @@ int pjg_upsample_and_convert(pjg_ctx* ctx, uint32_t width, uint32_t height, uint
         sz[c] = uint64_t(plane_w[c]) * plane_h[c];
         tot += align_up(sz[c], 256);
     }
-    DevBuf tmp;
-    CU(tmp.ensure(tot + npx * 3), "cudaMalloc(tmp)");
-    uint8_t* d = tmp.as<uint8_t>();
+    // the context's grow-only scratch (no allocation per call)
+    CU(ctx->k5tmp.ensure(tot + npx * 3), "cudaMalloc(k5tmp)");
+    uint8_t* d = ctx->k5tmp.as<uint8_t>();
     uint8_t* dp[3];
     uint64_t o = 0;
     for (int c = 0; c < 3; ++c) {
@@ -1772,7 +1772,6 @@ int pjg_upsample_and_convert(pjg_ctx* ctx, uint32_t width, uint32_t height, uint
     CU(cudaGetLastError(), "k5 launch");
     CU(cudaMemcpyAsync(out_rgb, d + o, npx * 3, cudaMemcpyDeviceToHost, ctx->stream), "D2H rgb");
     CU(cudaStreamSynchronize(ctx->stream), "colour");
-    tmp.release();
     return PJG_OK;
 }
 

@@ -19,9 +19,13 @@ int main(int argc, char** argv) {
     std::vector<uint8_t> f((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
     pjpeg::gpu::DecodeSuccess g = pjpeg::gpu::decode_single(f, {});
     pjpeg::gpu::RgbImage rgb = pjpeg::gpu::upsample_and_convert(g.planes);
-    std::printf("gpu: %ux%u planes=%zu checksum=%016llx rgb=%zu\n", g.planes.width, g.planes.height,
+    // the fused extension must equal the two-call composition
+    pjpeg::gpu::RgbImage fused = pjpeg::gpu::decode_rgb(f, {});
+    const bool fused_same = fused.pixels == rgb.pixels && fused.width == rgb.width && fused.channels == rgb.channels;
+    std::printf("gpu: %ux%u planes=%zu checksum=%016llx rgb=%zu fused=%s\n", g.planes.width, g.planes.height,
                 g.planes.planes.size(), (unsigned long long)pjpeg::gpu::planes_checksum(g.planes),
-                rgb.pixels.size());
+                rgb.pixels.size(), fused_same ? "same" : "DIFFERENT");
+    if (!fused_same) return 2;
 #ifndef PJPEG_NO_REF
     pjpeg::DecodeSuccess r = pjpeg::decode_single(f, {});
     pjpeg::RgbImage rr = pjpeg::upsample_and_convert(r.planes);

@@ -94,8 +94,14 @@ pg::DecodeConfig config_of(const Args& a, uint64_t sb) {
 int cmd_decode(const Args& a) {
     if (a.pos.size() != 2) throw std::invalid_argument("decode INPUT OUTPUT");
     const auto bytes = read_file(a.pos[0]);
-    const pg::DecodeSuccess res = pg::decode_single(bytes, config_of(a, a.subseq_bits));
     const std::string& out = a.pos[1];
+    if (a.colorspace != "ycbcr" && a.colorspace != "gray") {
+        // RGB (or the Y plane of a gray file): the fused decode, no planes round trip
+        const pg::RgbImage img = pg::decode_rgb(bytes, config_of(a, a.subseq_bits));
+        write_pnm(out, img.width, img.height, img.channels, img.pixels.data());
+        return 0;
+    }
+    const pg::DecodeSuccess res = pg::decode_single(bytes, config_of(a, a.subseq_bits));
     if (a.colorspace == "ycbcr" && res.planes.planes.size() == 3) {
         static const char* names[3] = {".y.pgm", ".cb.pgm", ".cr.pgm"};
         for (size_t i = 0; i < 3; ++i) {
