@@ -3365,6 +3365,9 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
             issue(w, w.k == cur_k ? next_wstart : (w.tx == 0 && w.my == 0 ? 0u : kNoWin), next_wlen);
         }
         if (!cur_valid) continue;
+        // the dequantised F tile (written lane-by-unit above) is read across lanes
+        // below; the syncs around the prefetch only run when a next tile exists
+        __syncwarp();
 
         // 3. IDCT of the AC units, eight per pass: lane = (unit a, rows q, q+4)
         uint64_t pend = 0;  // per pass g: bit 16g + y (row q) / 16g + 8 + y (row q+4) need the FP64 replay
