@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
 import paper_2111_09219_b200 as pj  # noqa: E402
-from oracle.oracle import Orc  # noqa: E402
+from oracle.oracle import Orc, Ref  # noqa: E402
 from paper_2111_09219_b200.synth import synth_ref_batch  # noqa: E402
 
 cases = [
@@ -34,5 +34,28 @@ for n, w, h, seed, q, s, ri, sb in cases:
             want = Orc.decode(f, rgb=True)
             assert np.array_equal(outs[i][: want.data.size], want.data.reshape(-1)), (n, w, h, i)
     print(f"ok {n}x{w}x{h} q{q} {s} dri={ri} sb={sb}")
+# the device-side planner (pjg_batch_create_device: parse, dedup spin-waits,
+# layout scans, table builds) on a mixed-table batch
+blob, offs, sizes = synth_ref_batch(12, 120, 90, 300, 80, "444")
+blob2, offs2, sizes2 = synth_ref_batch(12, 96, 64, 400, 60, "420")
+files = [blob[o: o + z].tobytes() for o, z in zip(offs, sizes)] + [blob2[o: o + z].tobytes() for o, z in zip(offs2, sizes2)]
+with dec.batch(files, pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved, device_plan=True) as b:
+    st = b.run()
+    assert (st == 0).all(), st
+    outs = b.download()
+for i, f in enumerate(files):
+    want = Orc.decode(f, rgb=True)
+    assert np.array_equal(outs[i][: want.data.size], want.data.reshape(-1)), ("devplan", i)
+print("ok device-planned mixed batch")
+# corrupt scans: K1x's reference-exact replay of failed images next to valid ones
+good = files[0]
+sos = good.index(b"\xff\xda")
+bad = [good[: sos + 40], good[: sos + 20] + bytes(range(7, 200)) + good[sos + 200:], good]
+with dec.batch(bad, pj.DecodeConfig(), pj.OutputColorspace.RGBInterleaved) as b:
+    st = b.run()
+for i, f in enumerate(bad):
+    want = Ref.decode(f, rgb=True)  # the reference itself (oracle/_ref, prebuilt)
+    assert int(st[i]) == want.status, (i, int(st[i]), want.status)
+print("ok corrupt scans (statuses equal the reference's)")
 dec.close()
 print("sanitize_run: all decodes ok")
