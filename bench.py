@@ -394,11 +394,14 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    # SM clocks + throttle reasons sampled from here through the metric-of-record
+    # legs (GPU-busy timed regions): the device-step leg alone is ~45 ms, too
+    # short for more than a few 5 ms samples
     clk = ClockSampler(local)
     clk.start()
+    time.sleep(0.02)  # NVML up before the first timed step
     dev_ms = [device_step() for _ in range(args.steps)]
     torch.cuda.synchronize()
-    clocks = clk.stop()
     for bb in parts:
         bb.close()
     step_max = [pdist.max_over_ranks(x, rdev) for x in dev_ms]  # per step: the slowest rank
@@ -448,6 +451,7 @@ def main():
                 dist.barrier()
             ms_.append(pdist.max_over_ranks(fn(), rdev))
         recs[name] = ms_
+    clocks = clk.stop()
     rec_ms = recs["host"]
     rec_med, rec_best = float(np.median(rec_ms)), float(np.min(rec_ms))
     drec_med, drec_best = float(np.median(recs["device"])), float(np.min(recs["device"]))
