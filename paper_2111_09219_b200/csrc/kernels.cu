@@ -1056,7 +1056,13 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
             const bool dcs = z == 0;
             const uint32_t tb = dcs ? tdc : tac;
             uint32_t fe = fast_entry<ST>(ic, tsh, tb + (win >> (32 - kFastBits)));
-            if ((fe & 0x3FFu) == kFastL2) fe = fast_entry2<ST>(ic, tb, (fe >> 10) & 31u, (win >> (32 - kFastBits - 5)) & 31u);
+            if ((fe & 0x3FFu) == kFastL2) {
+                // (the table address only on this path: keep the compiler from
+                // hoisting its 64-bit arithmetic into every symbol)
+                uint32_t tb2 = tb;
+                asm volatile("" : "+r"(tb2));
+                fe = fast_entry2<ST>(ic, tb2, (fe >> 10) & 31u, (win >> (32 - kFastBits - 5)) & 31u);
+            }
             uint32_t len, step, coefk;
             int32_t coef;
             if ((fe & 31u) != 0 && rem >= rthr) {
@@ -1130,20 +1136,19 @@ __device__ __forceinline__ void decode_core(const ImgCtx& ic, DecState& s, uint6
                 step = eob ? 64u - z : run + 1u;
                 if (Sink::kStore) sink.sym((run << 12) | (uint32_t(coef) & 0xFFFu));
             }
-            if (Sink::kWrite && n + step > cap) {  // phantom tail past the true end
+            // write mode: a phantom tail past the true end stops the decode; a run
+            // past the unit end (reference semantics in K1x) also flags it —
+            // one test of both on the per-symbol path
+            if (Sink::kWrite && (n + step > cap || z + step > 64)) {
+                if (n + step <= cap) s.ovf = true;
                 stop = true;
                 break;
             }
-            if (Sink::kWrite && z + step > 64) {  // a run past the unit end: reference semantics in K1x
-                s.ovf = true;
-                stop = true;
-                break;
-            }
-            if (dcs) {
-                if (kRegAcc) {
-                    acur += coef;
-                    coef = acur;
-                } else {
+            if (kRegAcc) {  // branch-free: the DC test diverges across lanes
+                acur += dcs ? coef : 0;
+                coef = dcs ? acur : coef;
+            } else if (dcs) {
+                {
                     coef += *sa;
                     *sa = coef;
                 }
@@ -2393,13 +2398,13 @@ struct EntrySink {
 
     __device__ __forceinline__ void set_comp(uint32_t comp) { wqc = wqb + 64u * uint32_t((qrow >> (21 * comp)) & 0x1FFFFFu); }
     __device__ __forceinline__ void put(uint32_t k, int32_t v) {
+        // branch-free (lanes diverge on every condition here); a zero term adds
+        // +0 to S exactly, and only a DC entry can be zero
         const uint32_t t = zt[k];
-        if (k == 0) ustart = pos;
+        ustart = k == 0 ? pos : ustart;
         ent[pos++] = ((u & 0xFFu) << 22) | ((t & 0xFFu) << 16) | (uint32_t(v) & 0xFFFFu);
-        if (v != 0) {
-            mflags |= t >> 8;
-            mS = fmaf(wqc[k], float(abs(v)), mS);
-        }
+        mflags |= v != 0 ? (t >> 8) : 0u;
+        mS = fmaf(wqc[k], float(abs(v)), mS);
     }
     // the owned part of the current unit ends (complete: through slot 63)
     __device__ __forceinline__ void close(bool complete) {
