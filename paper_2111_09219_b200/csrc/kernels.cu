@@ -2661,7 +2661,28 @@ constexpr int kK4Warps = kK4Threads / 32;
 constexpr int kTileW = 64;  // pixels per tile row
 constexpr int kGroups = kTileW / 4;  // 4-pixel items per tile row
 constexpr int kFS = 68;     // floats per unit in the F tile
-constexpr uint32_t kK4Win = 512;  // compact: entries prefetched per tile (a q75 4:2:0 tile holds ~150)
+// Compact-interface K4: threads per CTA and resident CTAs per SM (its warp
+// state is smaller than the dense variant's: 6 warps x 3 CTAs = 18 warps fit
+// where the dense one fits 4 x 4 = 16)
+#ifndef PJG_K4C_THREADS
+#define PJG_K4C_THREADS 128
+#endif
+#ifndef PJG_K4C_MINB
+#define PJG_K4C_MINB 4
+#endif
+template <bool CMP>
+struct K4Shape {
+    static constexpr int kThreads = CMP ? PJG_K4C_THREADS : kK4Threads;
+    static constexpr int kWarps = kThreads / 32;
+    static constexpr int kMinBlocks = CMP ? PJG_K4C_MINB : 4;
+};
+#ifndef PJG_K4_WIN
+#define PJG_K4_WIN 512
+#endif
+#ifndef PJG_K4_WIN_MUL
+#define PJG_K4_WIN_MUL 2
+#endif
+constexpr uint32_t kK4Win = PJG_K4_WIN;  // compact: entries prefetched per tile (a q75 4:2:0 tile holds ~150)
 constexpr uint32_t kNoWin = 0xFFFFFFFFu;
 // raw staging row of (unit, column v): rows XOR-swizzled so that reading the
 // same column of different units hits different bank groups
@@ -3029,6 +3050,8 @@ __device__ __forceinline__ void colour_full(const WarpImg& I, const uint8_t* pl,
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 static_assert(sizeof(WarpSmem<false>) * kK4Warps + 4864 + 1024 <= 228 * 1024 / 4, "K4 must fit 4 CTAs per SM");
+static_assert(sizeof(WarpSmem<true>) * K4Shape<true>::kWarps + 4864 + 1024 <= 228 * 1024 / K4Shape<true>::kMinBlocks,
+              "compact K4 must fit its CTAs per SM");
 static_assert(sizeof(WarpSmem<false>::F) >= 16 * kStgRow, "RGB row staging lives in the F tile");
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
     unsigned long long r;
@@ -3042,7 +3065,8 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
 // path is compiled in (a smaller hot loop for the instruction cache: 3.1 K vs
 // 5.2 K instructions, K4 -4 % on cfg 3; a 4:4:4 variant gained nothing); 0: any.
 template <int LAYOUT, bool CMP>
-__global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
+__global__ void __launch_bounds__(K4Shape<CMP>::kThreads, K4Shape<CMP>::kMinBlocks) k4_transform(Params P) {
+    constexpr int kK4Threads = K4Shape<CMP>::kThreads, kK4Warps = K4Shape<CMP>::kWarps;
     extern __shared__ __align__(16) unsigned char k4_dyn[];  // kK4Warps x WarpSmem
     WarpSmem<CMP>* s_w = reinterpret_cast<WarpSmem<CMP>*>(k4_dyn);
     __shared__ __align__(16) float s_b32[64];   // basis[u][x]
@@ -3285,7 +3309,7 @@ __global__ void __launch_bounds__(kK4Threads, 4) k4_transform(Params P) {
                         }
                     }
                     next_wstart = r1;
-                    next_wlen = min(kK4Win, 2 * (r1 - r0) + 64);
+                    next_wlen = min(kK4Win, PJG_K4_WIN_MUL * (r1 - r0) + 64);
                 } else {
 #pragma unroll 1
                     for (uint32_t u = 0; u < nblk; ++u) {
@@ -3802,6 +3826,7 @@ void launch_k3_write(const Params& p, void* stream) {
 }
 template <int LAYOUT, bool CMP>
 static void launch_k4_variant(const Params& p, cudaStream_t s) {
+    constexpr int kK4Threads = K4Shape<CMP>::kThreads, kK4Warps = K4Shape<CMP>::kWarps;
     constexpr size_t dyn = sizeof(WarpSmem<CMP>) * kK4Warps;
     int grid_cap = launch_setup((const void*)k4_transform<LAYOUT, CMP>, int(dyn), kK4Threads, true);
     if (const char* e = getenv("PJG_K4_OCC")) {  // A/B: K4 CTAs per SM (overlap experiments)
