@@ -284,9 +284,11 @@ def test_cli_decode_inspect_bench(tmp_path):
     r = subprocess.run([exe, "bench", str(bdir), "--iterations", "2"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     row = json.loads(r.stdout.strip().splitlines()[-1])
-    for key in ("batch", "config", "wall_ms", "stages", "mb_per_s", "checksum", "rgb_gb_s", "images_per_s"):
+    for key in ("batch", "config", "wall_ms", "stages", "mb_per_s", "checksum", "rgb_gb_s", "images_per_s",
+                "gpus", "k4_roofline_frac"):
         assert key in row, key
     assert row["batch"] == 3 and "failures" not in row
+    assert row["gpus"] == 1 and 0 < row["k4_roofline_frac"] < 1
 
 
 def test_decode_to_cuda_tensors():

@@ -55,6 +55,7 @@ struct Args {
     std::string colorspace = "rgb", subseq_list, worker_list, json_path, csv_path;
     unsigned warmup = 1, iterations = 3;
     bool restart = false;
+    double peak_gbs = 6463.0;  // HBM copy bandwidth measured on this pool's B200s (MEASURED_PEAKS.json)
 };
 
 Args parse_args(int argc, char** argv, int first) {
@@ -73,6 +74,7 @@ Args parse_args(int argc, char** argv, int first) {
         else if (k == "--worker-list") a.worker_list = val();
         else if (k == "--warmup") a.warmup = unsigned(std::stoul(val()));
         else if (k == "--iterations") a.iterations = unsigned(std::stoul(val()));
+        else if (k == "--peak-gbs") a.peak_gbs = std::stod(val());
         else if (k == "--json") a.json_path = val();
         else if (k == "--csv") a.csv_path = val();
         else if (k == "--restart-intervals") a.restart = true;
@@ -172,12 +174,18 @@ int cmd_bench(const Args& a) {
         compressed += files.back().size();
     }
     if (files.empty()) throw pg::Error(pg::Errc::EmptyCorpus, "no files in " + a.pos[0]);
+    // data units of the decodable files: K4's SURVEY §8(d) bytes (int16 coefficients + output)
+    uint64_t total_dus = 0;
+    for (const auto& f : files) {
+        pjg_image_info inf;
+        if (pjg_inspect(f.data(), f.size(), PJG_OUT_RGB, &inf) == 0) total_dus += inf.data_units;
+    }
     const std::vector<uint64_t> sweeps = a.subseq_list.empty() ? std::vector<uint64_t>{a.subseq_bits}
                                                                : parse_list(a.subseq_list);
     std::ostringstream json, csv;
     json << "[\n";
     csv << "batch,subseq_bits,b,workers,wall_ms,parse,sync,write,dc,idct,extract,mb_per_s,checksum,"
-           "rgb_gb_s,images_per_s\n";
+           "rgb_gb_s,images_per_s,gpus,k4_roofline_frac\n";
     bool first = true;
     for (const uint64_t sb : sweeps) {
         const pg::DecodeConfig cfg = config_of(a, sb);
@@ -207,16 +215,19 @@ int cmd_bench(const Args& a) {
             rgb_bytes = rgb;
         }
         const double mb = double(compressed) / (1024.0 * 1024.0);
-        char row[1024];
+        // K4 (IDCT + colour, the dominant HBM stage) against the HBM peak
+        const double k4_frac = stages.idct > 0 ? double(total_dus * 128 + rgb_bytes) / (stages.idct / 1e3) / 1e9 / a.peak_gbs : 0.0;
+        char row[1200];
         std::snprintf(row, sizeof(row),
                       "{\"batch\": %zu, \"config\": {\"subseq_bits\": %llu, \"b\": %u, \"workers\": %u}, "
                       "\"wall_ms\": %.4f, \"stages\": {\"parse\": %.4f, \"sync\": %.4f, \"write\": %.4f, "
                       "\"dc\": %.4f, \"idct\": %.4f, \"extract\": %.4f}, \"mb_per_s\": %.3f, \"checksum\": %llu, "
-                      "\"rgb_gb_s\": %.3f, \"images_per_s\": %.1f, \"device\": \"B200 (sm_100a), 1 GPU\"%s}",
+                      "\"rgb_gb_s\": %.3f, \"images_per_s\": %.1f, \"gpus\": 1, \"k4_roofline_frac\": %.4f, "
+                      "\"device\": \"B200 (sm_100a), 1 GPU\"%s}",
                       files.size(), (unsigned long long)sb, a.seq_len, a.workers, best, stages.parse,
                       stages.sync, stages.write, stages.dc, stages.idct, stages.extract, mb / (best / 1e3),
                       (unsigned long long)checksum, double(rgb_bytes) / (best / 1e3) / 1e9,
-                      double(files.size()) / (best / 1e3),
+                      double(files.size()) / (best / 1e3), k4_frac,
                       failures ? (", \"failures\": " + std::to_string(failures)).c_str() : "");
         std::cout << row << "\n";
         json << (first ? "  " : ",\n  ") << row;
@@ -224,7 +235,8 @@ int cmd_bench(const Args& a) {
         csv << files.size() << "," << sb << "," << a.seq_len << "," << a.workers << "," << best << ","
             << stages.parse << "," << stages.sync << "," << stages.write << "," << stages.dc << ","
             << stages.idct << "," << stages.extract << "," << mb / (best / 1e3) << "," << checksum << ","
-            << double(rgb_bytes) / (best / 1e3) / 1e9 << "," << double(files.size()) / (best / 1e3) << "\n";
+            << double(rgb_bytes) / (best / 1e3) / 1e9 << "," << double(files.size()) / (best / 1e3) << ",1,"
+            << k4_frac << "\n";
     }
     json << "\n]\n";
     if (!a.json_path.empty()) std::ofstream(a.json_path) << json.str();
