@@ -269,6 +269,8 @@ def main():
     ap.add_argument("--parts", type=int, default=1, help="concurrent parts (contexts) of the device-resident step")
     ap.add_argument("--record-parts", type=int, default=4,
                     help="pipelined parts (contexts) of the metric-of-record step")
+    ap.add_argument("--record-growth", type=float, default=1.0,
+                    help="size ratio of consecutive metric-of-record parts (1: equal)")
     ap.add_argument("--record-parts-device", type=int, default=2,
                     help="parts of the device-planned record step (each plan reads its totals back)")
     args = ap.parse_args()
@@ -333,6 +335,13 @@ def main():
     def parts_of(k):  # the shard as k contiguous parts (one context each)
         k = max(1, min(k, n))
         return [(n * j // k, n * (j + 1) // k) for j in range(k)]
+
+    def record_parts(k, r):  # pipelined parts growing by r (the host plans + uploads part j+1
+        k = max(1, min(k, n))  # while the GPU decodes parts <= j; r = 1: equal parts)
+        w = [r ** j for j in range(k)]
+        cuts = [0] + [int(round(n * sum(w[: j + 1]) / sum(w))) for j in range(k)]
+        cuts[-1] = n
+        return [(cuts[j], cuts[j + 1]) for j in range(k) if cuts[j + 1] > cuts[j]]
 
 
     trace(f"corpus shared, shard of {n} images")
@@ -415,7 +424,7 @@ def main():
     def record_step():
         bs = []
         t0 = time.perf_counter()
-        for (lo, hi), d in zip(parts_of(args.record_parts), decs):
+        for (lo, hi), d in zip(record_parts(args.record_parts, args.record_growth), decs):
             bb = d.batch((pblob, soffs[lo:hi], ssizes[lo:hi]), cfg, out_kind)  # header parse + plan
             bb.upload()  # one H2D of the compressed bytes
             bb.decode()
