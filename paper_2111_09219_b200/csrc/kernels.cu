@@ -2652,8 +2652,12 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
 //     arithmetic on the decimal constants, ties replayed in FP64
 //     (pipeline.hpp:190-197).  Saturating byte packs, 3 x 32-bit stores per
 //     4 pixels.
-#ifndef PJG_K4_PAIRCOL
-#define PJG_K4_PAIRCOL 0
+// PJG_K4_SYM: lane = (unit, rows q and 7-q) and the even/odd split of both
+// passes (basis[u][7-x] = (-1)^u basis[u][x]): per nonzero column 4 FFMA2 on
+// (even u, odd u) pairs + 2 FADD, then 4 FFMA2 into the column-parity
+// accumulators; 0: rows q and q+4, 8 + 8 FFMA2 per column.
+#ifndef PJG_K4_SYM
+#define PJG_K4_SYM 1
 #endif
 constexpr float kM128 = 12583040.0f;  // 1.5 * 2^23 + 128: round(acc) + 128 in the low mantissa bits
 constexpr int kMagicBits = 0x4B400000;
@@ -3100,11 +3104,17 @@ __global__ void __launch_bounds__(K4Shape<CMP>::kThreads, K4Shape<CMP>::kMinBloc
     const uint32_t t_end = uint32_t(uint64_t(P.k4_tiles) * (gw + 1) / nw);
     if (t_begin >= t_end) return;
 
-    // IDCT lane constants: rows q and q+4 of the lane's unit
+    // IDCT lane constants: rows q and 7-q (SYM) or q and q+4 of the lane's unit
     const uint32_t q = lane & 3;
+#if PJG_K4_SYM
+    float2 bp[4];  // (b[2k][q], b[2k+1][q])
+#pragma unroll
+    for (int k = 0; k < 4; ++k) bp[k] = make_float2(s_b32[(2 * k) * 8 + q], s_b32[(2 * k + 1) * 8 + q]);
+#else
     float2 bq[8];  // (b[u][q], b[u][q+4])
 #pragma unroll
     for (int u = 0; u < 8; ++u) bq[u] = make_float2(s_b32[u * 8 + q], s_b32[u * 8 + q + 4]);
+#endif
 
     TileWalk& w = S.w;
     if (lane == 0) {
@@ -3398,8 +3408,8 @@ __global__ void __launch_bounds__(K4Shape<CMP>::kThreads, K4Shape<CMP>::kMinBloc
         // below; the syncs around the prefetch only run when a next tile exists
         __syncwarp();
 
-        // 3. IDCT of the AC units, eight per pass: lane = (unit a, rows q, q+4)
-        uint64_t pend = 0;  // per pass g: bit 16g + y (row q) / 16g + 8 + y (row q+4) need the FP64 replay
+        // 3. IDCT of the AC units, eight per pass: lane = (unit a, rows q, 7-q / q+4)
+        uint64_t pend = 0;  // per pass g: bit 16g + y (row q) / 16g + 8 + y (second row) need the FP64 replay
 #pragma unroll 1
         for (uint32_t g = 0; g * 8 < nac; ++g) {
             const uint32_t a = g * 8 + (lane >> 2);
@@ -3411,50 +3421,55 @@ __global__ void __launch_bounds__(K4Shape<CMP>::kThreads, K4Shape<CMP>::kMinBloc
             float2 acc[8];
 #pragma unroll
             for (int y = 0; y < 8; ++y) acc[y] = make_float2(0.f, 0.f);
-#if PJG_K4_PAIRCOL
-            // two columns per step: two independent column-sum chains (the
-            // 8-deep FFMA2 chain of one column was the kernel's top fixed-
-            // latency stall).  An odd count pairs the last column with one
-            // outside the union: zero in every unit of the pass, so its terms
-            // add exact zeros and the error bound is unchanged.
-            for (uint32_t m = ucols; m;) {
-                const uint32_t v = __ffs(m) - 1;
-                m &= m - 1;
-                const uint32_t w2 = m ? __ffs(m) - 1 : __ffs(~ucols) - 1;
-                m &= m - 1;
+#if PJG_K4_SYM
+            // x = q, 7-q: s(q) = E + O, s(7-q) = E - O with E / O the even / odd
+            // u terms of the column sum, one packed chain over (u, u+1) pairs;
+            // the row sums split the same way by the parity of v: out[x][y] =
+            // Ev[y] + Ov[y], out[x][7-y] = Ev[y] - Ov[y] (y < 4).  Each nonzero
+            // term still sees at most k (column) and m (row) roundings: a
+            // chain of j nonzero terms rounds each at most j times and the join
+            // adds one only when both halves are nonzero (j < k then).  The
+            // mirrored FP32 basis factor is -b32[u][x] for odd u, one FP32
+            // rounding of the reference's basis[u][7-x] up to its FP64 ulps
+            // (covered by the bound's slack).
+            float2 ae[4], ao[4];
+#pragma unroll
+            for (int y = 0; y < 4; ++y) ae[y] = ao[y] = make_float2(0.f, 0.f);
+            auto colsum = [&](uint32_t v) -> float2 {
                 const float4 f0 = *reinterpret_cast<const float4*>(F + v * 8);
-                const float4 f1 = *reinterpret_cast<const float4*>(F + v * 8 + 4);
-                const float4 g0 = *reinterpret_cast<const float4*>(F + w2 * 8);
-                const float4 g1 = *reinterpret_cast<const float4*>(F + w2 * 8 + 4);
-                // s = sum_u (b[u][q], b[u][q+4]) F[u][v]
-                float2 sv = __fmul2_rn(bq[0], f2(f0.x));
-                float2 sw = __fmul2_rn(bq[0], f2(g0.x));
-                sv = __ffma2_rn(bq[1], f2(f0.y), sv);
-                sw = __ffma2_rn(bq[1], f2(g0.y), sw);
-                sv = __ffma2_rn(bq[2], f2(f0.z), sv);
-                sw = __ffma2_rn(bq[2], f2(g0.z), sw);
-                sv = __ffma2_rn(bq[3], f2(f0.w), sv);
-                sw = __ffma2_rn(bq[3], f2(g0.w), sw);
-                sv = __ffma2_rn(bq[4], f2(f1.x), sv);
-                sw = __ffma2_rn(bq[4], f2(g1.x), sw);
-                sv = __ffma2_rn(bq[5], f2(f1.y), sv);
-                sw = __ffma2_rn(bq[5], f2(g1.y), sw);
-                sv = __ffma2_rn(bq[6], f2(f1.z), sv);
-                sw = __ffma2_rn(bq[6], f2(g1.z), sw);
-                sv = __ffma2_rn(bq[7], f2(f1.w), sv);
-                sw = __ffma2_rn(bq[7], f2(g1.w), sw);
+                float2 eo = __fmul2_rn(bp[0], make_float2(f0.x, f0.y));
+                eo = __ffma2_rn(bp[1], make_float2(f0.z, f0.w), eo);
+                if (urows_hi) {
+                    const float4 f1 = *reinterpret_cast<const float4*>(F + v * 8 + 4);
+                    eo = __ffma2_rn(bp[2], make_float2(f1.x, f1.y), eo);
+                    eo = __ffma2_rn(bp[3], make_float2(f1.z, f1.w), eo);
+                }
+                return make_float2(__fadd_rn(eo.x, eo.y), __fsub_rn(eo.x, eo.y));
+            };
+#pragma unroll 1
+            for (uint32_t m = ucols & 0x55u; m; m &= m - 1) {
+                const uint32_t v = __ffs(m) - 1;
+                const float2 sv = colsum(v);
                 const float4 b0 = *reinterpret_cast<const float4*>(s_b32 + v * 8);
-                const float4 b1 = *reinterpret_cast<const float4*>(s_b32 + v * 8 + 4);
-                const float4 c0 = *reinterpret_cast<const float4*>(s_b32 + w2 * 8);
-                const float4 c1 = *reinterpret_cast<const float4*>(s_b32 + w2 * 8 + 4);
-                acc[0] = __ffma2_rn(f2(c0.x), sw, __ffma2_rn(f2(b0.x), sv, acc[0]));
-                acc[1] = __ffma2_rn(f2(c0.y), sw, __ffma2_rn(f2(b0.y), sv, acc[1]));
-                acc[2] = __ffma2_rn(f2(c0.z), sw, __ffma2_rn(f2(b0.z), sv, acc[2]));
-                acc[3] = __ffma2_rn(f2(c0.w), sw, __ffma2_rn(f2(b0.w), sv, acc[3]));
-                acc[4] = __ffma2_rn(f2(c1.x), sw, __ffma2_rn(f2(b1.x), sv, acc[4]));
-                acc[5] = __ffma2_rn(f2(c1.y), sw, __ffma2_rn(f2(b1.y), sv, acc[5]));
-                acc[6] = __ffma2_rn(f2(c1.z), sw, __ffma2_rn(f2(b1.z), sv, acc[6]));
-                acc[7] = __ffma2_rn(f2(c1.w), sw, __ffma2_rn(f2(b1.w), sv, acc[7]));
+                ae[0] = __ffma2_rn(f2(b0.x), sv, ae[0]);
+                ae[1] = __ffma2_rn(f2(b0.y), sv, ae[1]);
+                ae[2] = __ffma2_rn(f2(b0.z), sv, ae[2]);
+                ae[3] = __ffma2_rn(f2(b0.w), sv, ae[3]);
+            }
+#pragma unroll 1
+            for (uint32_t m = ucols & 0xAAu; m; m &= m - 1) {
+                const uint32_t v = __ffs(m) - 1;
+                const float2 sv = colsum(v);
+                const float4 b0 = *reinterpret_cast<const float4*>(s_b32 + v * 8);
+                ao[0] = __ffma2_rn(f2(b0.x), sv, ao[0]);
+                ao[1] = __ffma2_rn(f2(b0.y), sv, ao[1]);
+                ao[2] = __ffma2_rn(f2(b0.z), sv, ao[2]);
+                ao[3] = __ffma2_rn(f2(b0.w), sv, ao[3]);
+            }
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+                acc[y] = __fadd2_rn(ae[y], ao[y]);
+                acc[7 - y] = fsub2(ae[y], ao[y]);
             }
 #else
             for (uint32_t m = ucols; m; m &= m - 1) {
@@ -3506,7 +3521,7 @@ __global__ void __launch_bounds__(K4Shape<CMP>::kThreads, K4Shape<CMP>::kMinBloc
                 uint8_t* pl = S.pl + I.boff[blk];
                 const uint32_t ps = I.bps[blk];
                 uint32_t* r0p = reinterpret_cast<uint32_t*>(pl + q * ps);
-                uint32_t* r1p = reinterpret_cast<uint32_t*>(pl + (q + 4) * ps);
+                uint32_t* r1p = reinterpret_cast<uint32_t*>(pl + (PJG_K4_SYM ? 7 - q : q + 4) * ps);
                 r0p[0] = pack4_sat(o0[0], o0[1], o0[2], o0[3]);
                 r0p[1] = pack4_sat(o0[4], o0[5], o0[6], o0[7]);
                 r1p[0] = pack4_sat(o1[0], o1[1], o1[2], o1[3]);
@@ -3548,7 +3563,8 @@ __global__ void __launch_bounds__(K4Shape<CMP>::kThreads, K4Shape<CMP>::kMinBloc
                         if (k < rb) continue;
                         if (k >= rb + 32) break;
                         const uint32_t bit = __ffsll(m) - 1;  // 16 g + 8 h + y
-                        const uint32_t a = (bit >> 4) * 8 + (lane >> 2), x = q + 4 * ((bit >> 3) & 1u);
+                        const uint32_t a = (bit >> 4) * 8 + (lane >> 2);
+                        const uint32_t x = ((bit >> 3) & 1u) ? (PJG_K4_SYM ? 7 - q : q + 4) : q;
                         S.rep[k - rb] = uint16_t((a << 6) | (x << 3) | (bit & 7u));
                     }
                 }
