@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kLayThreads) kp_counts(PlanParams P) {
                 }
                 if (!rejected) {
                     d.expected = m * h.dpm * 64;
-                    d.mcus_per_tile = uint16_t(64 / (8 * h.h_max));  // 64-pixel-wide K4 tiles
+                    d.mcus_per_tile = uint16_t(k4_mcus_per_tile(h.h_max, h.dpm));  // K4 warp tiles (<= 24 data units)
                     d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
                     c.sub = d.sub_count;
                     c.du = d.expected / 64;

@@ -2759,7 +2759,7 @@ struct WarpSmem {
     int32_t dcv[CMP ? kK4MaxBlocks : 1];    // compact: quantised DC of each unit
     uint32_t ud[CMP ? kK4MaxBlocks : 1];    // compact: per unit F offset (0xFFFF: DC-only) | qf offset << 16 | big << 24
     __align__(16) uint32_t win[CMP ? kK4Win : 1];  // compact: next tile's entries (cp.async window)
-    __align__(16) uint8_t pl[1664];             // sample planes (row stride padded by 4): 4:2:0 needs 68x16 + 2 x 36x8
+    __align__(16) uint8_t pl[1664];             // sample planes (row stride padded by 4): 4:2:0 needs 68x16 + 2 x 36x8, gray 196x8
     WarpImg img;
     float lim[kK4MaxBlocks];      // per AC unit: 0.5 - error bound
     uint32_t cm[kK4MaxBlocks];    // per AC unit: column mask | big << 8 | row mask << 16
@@ -3415,8 +3415,9 @@ __global__ void __launch_bounds__(K4Shape<CMP>::kThreads, K4Shape<CMP>::kMinBloc
             const uint32_t a = g * 8 + (lane >> 2);
             const bool act = a < nac;
             const uint32_t cmw = act ? S.cm[a] : 0u;
-            const uint32_t ucols = __reduce_or_sync(0xFFFFFFFFu, cmw & 0xFFu);
-            const bool urows_hi = __reduce_or_sync(0xFFFFFFFFu, cmw & 0xF00000u) != 0;
+            const uint32_t uor = __reduce_or_sync(0xFFFFFFFFu, cmw & 0xF000FFu);
+            const uint32_t ucols = uor & 0xFFu;
+            const bool urows_hi = (uor & 0xF00000u) != 0;
             const float* F = S.F + (act ? a : 0) * kFS;
             float2 acc[8];
 #pragma unroll
@@ -3611,19 +3612,33 @@ __global__ void __launch_bounds__(K4Shape<CMP>::kThreads, K4Shape<CMP>::kMinBloc
                 colour_tile<1, false>(I, S.pl, s_lut, P.out, X0, Y0, cols, rws, lane);
             }
         } else if (I.out_mode == 1) {
-            // grayscale RGB output (1 channel, the Y plane): 4 pixels per item
+            // grayscale RGB output (1 channel, the Y plane): item = 16 pixels of
+            // a row (16 slots per row, up to 192 pixels used), one 16-byte
+            // store when the destination is 16-byte aligned, else 4-byte words
             const uint32_t W = I.width;
-            const bool aligned = ((W & 3) == 0) && ((I.out_off & 3) == 0);
+            const bool al4 = ((W & 3) == 0) && ((I.out_off & 3) == 0);
+            const bool al16 = ((W & 15) == 0) && ((I.out_off & 15) == 0) && (X0 & 15) == 0;
             uint8_t* obase = P.out + I.out_off + uint64_t(Y0) * W + X0;
-            for (uint32_t it = lane; it < rws * kGroups; it += 32) {
-                const uint32_t r = it / kGroups, gx = (it % kGroups) * 4;
+            for (uint32_t it = lane; it < rws * 16; it += 32) {
+                const uint32_t r = it >> 4, gx = (it & 15u) * 16;
                 if (gx >= cols) continue;
-                const uint32_t y4 = *reinterpret_cast<const uint32_t*>(S.pl + I.poff[0] + r * I.pst[0] + gx);
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(S.pl + I.poff[0] + r * I.pst[0] + gx);
+                const uint4 y16 = make_uint4(src[0], src[1], src[2], src[3]);
                 uint8_t* dst = obase + uint64_t(r) * W + gx;
-                if (gx + 4 <= cols && aligned) {
-                    *reinterpret_cast<uint32_t*>(dst) = y4;
+                if (gx + 16 <= cols && al16) {
+                    *reinterpret_cast<uint4*>(dst) = y16;
                 } else {
-                    for (uint32_t i = 0; i < min(4u, cols - gx); ++i) dst[i] = uint8_t(y4 >> (8 * i));
+                    const uint32_t yw[4] = {y16.x, y16.y, y16.z, y16.w};
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k) {
+                        const uint32_t g4 = gx + 4 * k;
+                        if (g4 >= cols) break;
+                        if (g4 + 4 <= cols && al4) {
+                            *reinterpret_cast<uint32_t*>(dst + 4 * k) = yw[k];
+                        } else {
+                            for (uint32_t i = 0; i < min(4u, cols - g4); ++i) dst[4 * k + i] = uint8_t(yw[k] >> (8 * i));
+                        }
+                    }
                 }
             }
         } else {

@@ -718,7 +718,7 @@ int batch_create_impl(pjg_ctx* ctx, size_t n, const uint8_t* const* files, const
                 d.ri = h.restart_interval;
             }
             d.expected = h.total_dus() * 64;
-            d.mcus_per_tile = uint16_t(64 / (8 * h.h_max));  // 64-pixel-wide warp tiles (<= 24 data units)
+            d.mcus_per_tile = uint16_t(k4_mcus_per_tile(h.h_max, h.dpm));  // K4 warp tiles (<= 24 data units)
             d.tiles_x = (h.mcus_x + d.mcus_per_tile - 1) / d.mcus_per_tile;
         }
     };

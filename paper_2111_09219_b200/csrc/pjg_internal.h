@@ -219,6 +219,13 @@ constexpr int kK2Threads = 256;
 constexpr int kK3Threads = 128;
 constexpr int kK4Threads = 128;
 constexpr int kK4MaxBlocks = 24;                         // data units per K4 (warp) tile
+// K4 tile width in MCUs: 64-pixel-wide tiles (<= 24 data units), except
+// one-unit-per-MCU grayscale scans, whose 64-pixel tile held only 8 units (the
+// per-tile walk / classify / prefetch cost was paid per 8 units): 192 pixels,
+// 24 units, 1568 bytes of sample plane.
+PJG_HD uint32_t k4_mcus_per_tile(uint32_t h_max, uint32_t dpm) {
+    return dpm == 1 ? uint32_t(kK4MaxBlocks) : 64u / (8u * h_max);
+}
 
 struct Params {
     // batch
