@@ -2659,6 +2659,9 @@ __global__ void __launch_bounds__(kK3Threads, 5) k3_write(Params P) {
 #ifndef PJG_K4_SYM
 #define PJG_K4_SYM 1
 #endif
+#ifndef PJG_K4_COLSPLIT
+#define PJG_K4_COLSPLIT 0
+#endif
 constexpr float kM128 = 12583040.0f;  // 1.5 * 2^23 + 128: round(acc) + 128 in the low mantissa bits
 constexpr int kMagicBits = 0x4B400000;
 constexpr int kK4Warps = kK4Threads / 32;
@@ -3442,8 +3445,15 @@ __global__ void __launch_bounds__(K4Shape<CMP>::kThreads, K4Shape<CMP>::kMinBloc
                 eo = __ffma2_rn(bp[1], make_float2(f0.z, f0.w), eo);
                 if (urows_hi) {
                     const float4 f1 = *reinterpret_cast<const float4*>(F + v * 8 + 4);
+#if PJG_K4_COLSPLIT
+                    // u >= 4 as a second, independent 2-deep chain joined by one add
+                    float2 eh = __fmul2_rn(bp[2], make_float2(f1.x, f1.y));
+                    eh = __ffma2_rn(bp[3], make_float2(f1.z, f1.w), eh);
+                    eo = __fadd2_rn(eo, eh);
+#else
                     eo = __ffma2_rn(bp[2], make_float2(f1.x, f1.y), eo);
                     eo = __ffma2_rn(bp[3], make_float2(f1.z, f1.w), eo);
+#endif
                 }
                 return make_float2(__fadd_rn(eo.x, eo.y), __fsub_rn(eo.x, eo.y));
             };

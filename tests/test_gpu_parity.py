@@ -432,3 +432,27 @@ def test_alternating_density_batch(decoder, compact, monkeypatch):
             ref = Ref.decode(f, rgb=True)
             got = _rgb(outs[i], b.infos[i])
             assert np.array_equal(got, ref.data), (i, int((got != ref.data).sum()))
+
+
+@pytest.mark.parametrize("compact", ["1", "0"])
+def test_gray_wide_tile_store_paths(decoder, compact, monkeypatch):
+    """One-unit-per-MCU grayscale scans use 192-pixel K4 tiles with 16-byte Y
+    stores when the destination row is 16-byte aligned: widths that are a
+    multiple of 192, of 16 only, of 4 only, and odd, heights with a partial
+    last MCU row, in one batch (later images start at unaligned offsets) and
+    alone (offset 0) — RGB (1-channel) and planes equal the reference."""
+    monkeypatch.setenv("PJG_COMPACT", compact)
+    shapes = [(384, 40, 75), (208, 17, 90), (200, 9, 50), (201, 23, 95), (1000, 64, 85), (7, 5, 100)]
+    files = [ref_jpeg(w, h, 7100 + k, q, "gray") for k, (w, h, q) in enumerate(shapes)]
+    for batch in (files, files[:1], files[3:4]):
+        for mode in (pj.OutputColorspace.RGBInterleaved, pj.OutputColorspace.YCbCrPlanes,
+                     pj.OutputColorspace.Grayscale):
+            with decoder.batch(batch, pj.DecodeConfig(), mode) as b:
+                st = b.run()
+                assert (st == 0).all(), st
+                outs = b.download()
+                for i, f in enumerate(batch):
+                    ref = Ref.decode(f, rgb=mode == pj.OutputColorspace.RGBInterleaved)
+                    want = ref.data.reshape(-1)
+                    assert outs[i].size == want.size, (i, mode)
+                    assert np.array_equal(outs[i], want), (i, mode, int((outs[i] != want).sum()))
