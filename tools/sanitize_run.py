@@ -18,6 +18,7 @@ cases = [
     (1, 1024, 768, 7, 95, "444", 0, 256),        # one image, many K1 CTAs (inter-CTA chaining, K1c)
     (2, 640, 480, 9, 90, "420", 40, 512),        # restart intervals: K0 RST strip, K0b segments
     (3, 333, 211, 11, 60, "gray", 0, 128),       # ragged, gray
+    (2, 384, 64, 15, 80, "gray", 0, 1024),       # gray 192-pixel K4 tiles, 16-byte Y stores
     (1, 512, 384, 13, 100, "444", 0, 1024),      # > 128 scan bits per unit: the dense K3 -> K4 interface
 ]
 dec = pj.Decoder(0)
